@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark: weighted particles/s of GPU importance sampling (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload linreg|poly]
+
+Default workload (BASELINE.json configs[1]): Bayesian linear regression,
+1e9 particles per GPU (weak scaling), 1,000 synthetic points, prior normal(0,10) on (a, b).
+A step is one full importance-sampling pass over those particles: Philox draws, the model's
+1,000 observe() terms, the fused log-sum-exp / ESS / moment / mode reduction, and (N > 1) the
+per-rank record all-gather over NCCL. `--workload poly` runs the Fig.1 polynomial model
+(configs[4], C5: 1.25e10 particles per GPU, 20 points).
+
+`--impl reference` times the reference's CPU path — the C restatement in oracle/ (the
+reference ships no executable engine) — on all host cores, rank 0 only.
+One JSON line is printed by rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "weighted particles/sec (importance sampling)"
+UNIT = "particles/s"
+
+WORKLOADS = {
+    "linreg": {
+        "name": "C2: Bayesian linear regression IS, 1e9 particles/GPU, 1k points (BASELINE configs[1])",
+        "particles_per_gpu": 10**9,
+        "n_points": 1000,
+    },
+    "poly": {
+        "name": "C5: Fig.1 polynomial regression IS, 1.25e10 particles/GPU (1e11 on 8 GPUs), 20 points "
+                "(BASELINE configs[4])",
+        "particles_per_gpu": 12_500_000_000,
+        "n_points": 20,
+    },
+}
+
+
+def make_model(workload: str):
+    from paper_2010_08454_b200 import models
+
+    w = WORKLOADS[workload]
+    if workload == "linreg":
+        return models.LinearRegression.synthetic(n_points=w["n_points"])
+    return models.PolyRegression.synthetic(n_points=w["n_points"])
+
+
+def flops_per_particle(workload: str, n_points: int) -> float:
+    """Algorithmic fp32 flops of one particle's model evaluation."""
+    if workload == "linreg":
+        return 5.0 * n_points  # per point: (y - b) add, fma(-a, x, .), fma(r, r, acc)
+    # poly, E[n] = 3: Horner (n-1) fma + (y - p) add + fma(r, r, acc) per point
+    return n_points * (2 * 2 + 1 + 2)
+
+
+# ----------------------------------------------------------------------------- clocks --
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- helpers --
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_baseline(workload: str, model, target_s: float = 12.0, threads: int | None = None) -> dict:
+    """Oracle (C port of the reference semantics) on the host cores, bounded sample."""
+    from oracle import core
+
+    core.build()
+    threads = threads or os.cpu_count() or 1
+    key = 0x9E0160293A33AAF7
+    run = (lambda lo, hi: core.is_linreg(model.xs, model.ys, model.sigma, lo, hi, key, threads=threads)) \
+        if workload == "linreg" else (lambda lo, hi: core.is_poly(model.xs, model.ys, lo, hi, key, threads=threads))
+    n = 20_000 if workload == "linreg" else 500_000
+    t0 = time.perf_counter()
+    run(0, n)
+    dt = time.perf_counter() - t0
+    n2 = max(n, int(n * target_s / max(dt, 1e-3)))
+    t0 = time.perf_counter()
+    run(0, n2)
+    dt = time.perf_counter() - t0
+    return {"value": n2 / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{n2} particles of the same model/data in {dt:.1f} s "
+                      f"(oracle/cuppl_oracle.c, fp64, OpenMP {threads} threads)"}
+
+
+def calibrate_fp32(device) -> float:
+    """Measured FFMA2 ceiling (FLOP/s) on this GPU (csrc/calib_kernels.cu kind 0)."""
+    import torch
+
+    from paper_2010_08454_b200 import _native as N
+
+    L = N.lib()
+    sink = torch.zeros(256, dtype=torch.float32, device=device)
+    sm = torch.cuda.get_device_properties(device).multi_processor_count
+    blocks, iters = sm * 8, 4000
+    st = N.stream_ptr(device)
+    for _ in range(2):
+        N.check(L.cuppl_calibrate(0, blocks, iters, N.ptr(sink), st))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    N.check(L.cuppl_calibrate(0, blocks, iters, N.ptr(sink), st))
+    e1.record()
+    torch.cuda.synchronize()
+    secs = e0.elapsed_time(e1) / 1e3
+    return blocks * 256 * iters * 512.0 / secs
+
+
+def load_traffic(workload: str):
+    p = ROOT / "profiles" / "traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get(workload)
+        except json.JSONDecodeError:
+            return None
+    return None
+
+
+# ----------------------------------------------------------------------------- arms -----
+def run_ours(args) -> dict | None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2010_08454_b200 import build as B
+
+    B.build()
+    from paper_2010_08454_b200 import Rng, infer
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    wl = WORKLOADS[args.workload]
+    per_gpu = args.particles or wl["particles_per_gpu"]
+    model = make_model(args.workload)
+    launcher = infer.IsLauncher(model, device)
+    base = Rng(1)
+    lo = rank * per_gpu
+    hi = lo + per_gpu
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+    gathered = torch.empty(world * 256, dtype=torch.uint8, device=device)
+
+    def step(k: int):
+        launcher.launch(lo, hi, base.split(k).key)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, launcher.rec)
+
+    for k in range(args.warmup):
+        step(10_000 + k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (outside the step events)
+        starts[k].record()
+        step(k)
+        ends[k].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+    t_ms = total_ms.item()
+    value = world * per_gpu * args.steps / (t_ms / 1e3)
+
+    # e2e: the public API from host data (model arrays in host memory -> kernel parameter
+    # block; record + mode trace back to the host), same particle count and GPUs.
+    e2e_steps = max(1, min(args.steps, 3))
+    infer.run_importance(model, world * per_gpu, Rng(777))  # warm
+    torch.cuda.synchronize()
+    e2e_t = []
+    for k in range(e2e_steps):
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        post = infer.run_importance(model, world * per_gpu, base.split(500 + k))
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_t.append(e0.elapsed_time(e1))
+    e2e_ms = torch.tensor([sum(e2e_t)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = world * per_gpu * e2e_steps / (e2e_ms.item() / 1e3)
+    h2d = model.xs.nbytes + model.ys.nbytes
+    d2h = 256 * world + (16 if args.workload == "poly" else 8) + (4 if args.workload == "poly" else 0)
+
+    result = None
+    if rank == 0:
+        peak = calibrate_fp32(device)
+        fpp = flops_per_particle(args.workload, wl["n_points"])
+        kernel_s = (sum(step_ms) / args.steps) / 1e3
+        achieved = fpp * per_gpu / kernel_s
+        sm_max = clk.get("sm_max_mhz") or 1965.0
+        nominal = torch.cuda.get_device_properties(device).multi_processor_count * 128 * 2 * sm_max * 1e6
+        result = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": t_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32",
+            "data": "synthetic (numpy seed 0, fp64 -> fp32; SURVEY.md §8(d)); Philox draws keyed by Rng(1).split(step)",
+            "config": {
+                "workload": wl["name"],
+                "particles_per_gpu": per_gpu,
+                "n_points": wl["n_points"],
+                "parallelism": f"particle-sharded dp{world} (NCCL all-gather of 256 B rank records)",
+                "l2": "flushed between timed steps (256 MiB write, excluded by per-step CUDA events)",
+            },
+            "roofline": {
+                "bound": "fp32",
+                "achieved": achieved / 1e12,
+                "peak": peak / 1e12,
+                "unit": "TFLOP/s",
+                "frac": achieved / peak,
+                "traffic": load_traffic(args.workload),
+                "peak_source": "measured FFMA2 ceiling on this GPU (csrc/calib_kernels.cu kind 0); "
+                               "MEASURED_PEAKS.json has no fp32 CUDA-core figure",
+                "nominal_peak": nominal / 1e12,
+                "frac_of_nominal": achieved / nominal,
+                "flops_per_particle": fpp,
+            },
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "paper_2010_08454_b200.infer.run_importance(model, n, rng)",
+                    "log_z": post.log_z, "ess": post.ess},
+            "gpu_launches": args.steps,
+            "clocks": clk,
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            result["cpu_baseline"] = cpu_baseline(args.workload, model)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+def run_reference(args) -> dict | None:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return None
+    wl = WORKLOADS[args.workload]
+    model = make_model(args.workload)
+    from oracle import core
+
+    core.build()
+    threads = os.cpu_count() or 1
+    key = 0x9E0160293A33AAF7
+    per_step = 100_000 if args.workload == "linreg" else 5_000_000
+
+    def step(k):
+        if args.workload == "linreg":
+            core.is_linreg(model.xs, model.ys, model.sigma, k * per_step, (k + 1) * per_step, key, threads=threads)
+        else:
+            core.is_poly(model.xs, model.ys, k * per_step, (k + 1) * per_step, key, threads=threads)
+
+    for k in range(args.warmup):
+        step(1000 + k)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        step(k)
+    dt = time.perf_counter() - t0
+    value = per_step * args.steps / dt
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": wl["name"], "particles_per_step": per_step, "n_points": wl["n_points"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{per_step} particles per step of the same workload "
+                                   "(oracle/cuppl_oracle.c: C restatement of the reference semantics; "
+                                   "the reference ships no executable inference engine)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="linreg")
+    ap.add_argument("--particles", type=int, default=0, help="override particles per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,165 @@
+/*
+ * cuppl_gpu.h — C ABI of libcuppl_gpu.so, the sm_100a inference hot path.
+ *
+ * This is the drop-in boundary for CuPPL's (arXiv 2010.08454) inference engines. The
+ * reference keeps these engines in Python (`cuppl.infer`, specified in SPEC.md:363-459, not
+ * shipped) on top of `cuppl.rng.Rng` (pkg/src/cuppl/rng.py:23-117) and
+ * `cuppl.values.DistValue` (pkg/src/cuppl/values.py:86-98). Every entry point below replaces
+ * one piece of that path; the reference interface it replaces is cited next to it.
+ *
+ * Conventions:
+ *   - plain C types only; device buffers are raw pointers the caller allocated (PyTorch);
+ *   - `stream` is a cudaStream_t passed as void*; every call is stream-ordered and never
+ *     synchronises the host unless documented;
+ *   - the library keeps no allocations between calls; scratch comes from the caller's
+ *     `workspace` sized by the matching *_workspace_bytes() query;
+ *   - return value is a cuppl_status; cuppl_last_error() gives a thread-local message.
+ *
+ * Random numbers: Philox4x32-10 (Salmon et al. 2011) keyed by the 64-bit `Rng.key` of
+ * cuppl/rng.py:27 (split as key_lo, key_hi). The counter of every draw is
+ * (id_lo, id_hi, block, tag) where id is the 64-bit global particle / chain / sample index,
+ * `block` the 128-bit block index within that id's stream and `tag` one of CUPPL_TAG_*.
+ * This replaces Rng.split(i)/next_u64 (cuppl/rng.py:31-41): like split(i), a stream is a
+ * pure function of (key, i).
+ */
+#ifndef CUPPL_GPU_H
+#define CUPPL_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CUPPL_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define CUPPL_API __attribute__((visibility("default")))
+#else
+#define CUPPL_API
+#endif
+
+/* Status codes. Python maps them onto the reference exception classes of
+ * pkg/src/cuppl/errors.py (InvalidDistParamError :135, AllZeroWeightError :119,
+ * UnsupportedDistError :97, InferRuntimeError :123). */
+typedef enum cuppl_status {
+  CUPPL_OK = 0,
+  CUPPL_E_INVALID_PARAM = 1, /* errors.py:135 InvalidDistParamError */
+  CUPPL_E_ALL_ZERO = 2,      /* errors.py:119 AllZeroWeightError */
+  CUPPL_E_CUDA = 3,          /* CUDA runtime failure (message in cuppl_last_error) */
+  CUPPL_E_NCCL = 4,          /* reserved: collectives are issued by the host (torch.distributed) */
+  CUPPL_E_CAPACITY = 5,      /* workspace / parameter-space too small */
+  CUPPL_E_UNSUPPORTED = 6,   /* errors.py:97 UnsupportedDistError */
+  CUPPL_E_ARGUMENT = 7       /* bad pointer / size argument */
+} cuppl_status;
+
+/* Philox counter tags (word 3 of the counter). */
+#define CUPPL_TAG_IS 1u        /* importance-sampling prior draws            */
+#define CUPPL_TAG_SMC_INIT 2u  /* SMC t = 0 draws                             */
+#define CUPPL_TAG_SMC_STEP 3u  /* SMC transition draws (block = time step)    */
+#define CUPPL_TAG_SMC_COMB 4u  /* SMC systematic-comb offset (one per step)   */
+#define CUPPL_TAG_MH 5u        /* MH chains (block = step)                    */
+#define CUPPL_TAG_MH_INIT 6u   /* MH initial trace                            */
+#define CUPPL_TAG_DIST 7u      /* batch dist_sample                           */
+
+/* Distribution tags: order of the constructors in pkg/src/cuppl/builtins.py:86-94, plus
+ * categorical (absent from the reference catalog). */
+#define CUPPL_DIST_NORMAL 0             /* normal(mean, sd)            builtins.py:87 */
+#define CUPPL_DIST_BERNOULLI 1          /* bernoulli(p)                builtins.py:88 */
+#define CUPPL_DIST_POISSON 2            /* poisson(lambda)             builtins.py:89 */
+#define CUPPL_DIST_UNIFORM_DISCRETE 3   /* uniform-discrete(a, b) [a,b) builtins.py:90 */
+#define CUPPL_DIST_UNIFORM_CONTINUOUS 4 /* uniform-continuous(a, b)    builtins.py:91 */
+#define CUPPL_DIST_BETA 5               /* beta(a, b)                  builtins.py:93 */
+#define CUPPL_DIST_EXPONENTIAL 6        /* exponential(rate)           builtins.py:94 */
+#define CUPPL_DIST_CATEGORICAL 7        /* categorical(weights)      */
+
+/* Fixed-size distribution value: the paper's {int32 tag, 3 x 64-bit payload} encoding
+ * (cuppl/values.py:86-98). Categorical keeps its cumulative u64
+ * thresholds in a device side table (like the SPEC's empirical kind). */
+typedef struct cuppl_dist {
+  int32_t tag;
+  int32_t n_table;        /* categorical: number of categories K (>= 1) */
+  double p0, p1, p2;      /* parameters in the reference's argument order */
+  const uint64_t* table;  /* categorical: device pointer to K-1 thresholds in [0, 2^32] */
+} cuppl_dist;
+
+/* Per-rank importance-sampling record: the compact EmpiricalDistribution of SPEC.md:376-379
+ * plus the normalize() state of SPEC.md:417-425 (log-sum-exp stabiliser M and rescaled sums).
+ * All weights are exp(lw - max_lw). Records merge associatively (cuppl_is_record_merge). */
+#define CUPPL_REC_STATS 16
+#define CUPPL_REC_BINS 8
+typedef struct cuppl_is_record {
+  double max_lw;     /* M: max finite log-weight (-inf if none)                     */
+  double sum_w;      /* sum exp(lw - M) over finite lw                              */
+  double sum_w2;     /* sum exp(2 (lw - M))  (ESS = sum_w^2 / sum_w2)               */
+  double argmax_lw;  /* log-weight of the posterior mode particle                   */
+  uint64_t argmax_pid; /* its global particle id; ties go to the lowest id (D7)     */
+  uint64_t n_finite; /* particles with a finite log-weight                          */
+  uint64_t n_total;  /* particles evaluated                                         */
+  uint64_t reserved;
+  double stat_w[CUPPL_REC_STATS]; /* sum w * f_k(theta), model-defined statistics   */
+  double bin_w[CUPPL_REC_BINS];   /* sum w per discrete bin of the return value     */
+} cuppl_is_record;
+
+/* ---- library ---------------------------------------------------------------------- */
+CUPPL_API int cuppl_abi_version(void);
+CUPPL_API const char* cuppl_last_error(void);
+/* Number of SMs of the current device (grid sizing is a multiple of it). */
+CUPPL_API int cuppl_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- K8: counter-based draws (replaces Rng.next_u64 / split, cuppl/rng.py:31-41) ---- */
+/* out[4*i + w] = word w of Philox4x32-10(ctr = (id_lo, id_hi, block, tag), key) for
+ * i in [0, count), id = first_id + i. Debug/test entry point for bit-exact parity. */
+CUPPL_API int cuppl_philox_blocks(uint64_t key, uint64_t first_id, uint32_t block, uint32_t tag,
+                        uint64_t count, uint32_t* out, void* stream);
+
+/* ---- K8: batch dist_sample / dist_score (builtins.py:96-99) -------- */
+/* Draw count samples: sample i uses the Philox stream (first_id + i, block 0.., tag).
+ * Output is float for continuous kinds, int32 for discrete kinds (bernoulli: 0/1). */
+CUPPL_API int cuppl_dist_sample(const cuppl_dist* d, uint64_t key, uint32_t tag, uint64_t first_id,
+                      uint64_t count, void* out, void* stream);
+/* score[i] = dist_score(d, x[i]) (natural log, -inf outside the support). x is float for
+ * continuous kinds and int32 for discrete kinds. */
+CUPPL_API int cuppl_dist_score(const cuppl_dist* d, const void* x, uint64_t count, float* score,
+                     void* stream);
+
+/* ---- K1 + K2: importance sampling (replaces run_importance) -------- */
+/* Workspace bytes for an importance-sampling launch on the current device. */
+CUPPL_API size_t cuppl_is_workspace_bytes(void);
+
+/* Fig.1 polynomial model:
+ *   n ~ uniform-discrete(2, 5); c_j ~ normal(0, 10), j < n; factor(-sum_i (y_i - sum_j c_j x_i^j)^2)
+ * for global particle ids [pid_begin, pid_end). xs/ys are HOST arrays of n_points floats
+ * (they are passed to the kernel by value). Optional device outputs (NULL to skip):
+ *   lw_out[N], deg_out[N] (int32 n), coef_out[4N] (c_0..c_3, zero-padded), N = pid_end-pid_begin.
+ * injected (device, NULL for Philox): 5 floats per particle (n, c_0..c_3) replacing the draws.
+ * rec_out: device cuppl_is_record (bin_w[n-2] = posterior mass of degree n; stat_w holds
+ * sum w*c_j per degree: n=2 -> [0,1], n=3 -> [2..4], n=4 -> [5..8]). */
+CUPPL_API int cuppl_is_poly(const float* xs, const float* ys, int n_points, uint64_t pid_begin,
+                  uint64_t pid_end, uint64_t key, const float* injected, float* lw_out,
+                  int32_t* deg_out, float* coef_out, cuppl_is_record* rec_out, void* workspace,
+                  size_t workspace_bytes, void* stream);
+
+/* Bayesian linear regression: a, b ~ normal(0, 10);
+ * observe(normal(a x_i + b, sigma), y_i) for each point (desugar.py:37-39).
+ * injected: 2 floats per particle (a, b). coef_out[2N] = (a, b).
+ * rec_out->stat_w = [sum w a, sum w b, sum w a^2, sum w b^2, sum w a b]. */
+CUPPL_API int cuppl_is_linreg(const float* xs, const float* ys, int n_points, float sigma,
+                    uint64_t pid_begin, uint64_t pid_end, uint64_t key, const float* injected,
+                    float* lw_out, float* coef_out, cuppl_is_record* rec_out, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/* ---- roofline calibration ---------------------------------------------------------- */
+/* Pipe-rate microbenchmark, blocks x 256 threads, each thread runs `iters` iterations of:
+ * kind 0: 128 FFMA2 (256 fp32 FMA), kind 1: 128 FFMA, kind 2: one Philox4x32-10 block,
+ * kind 3: 32 MUFU.EX2 + 32 MUFU.LG2. `sink` is a device float[256] (never written in practice). */
+CUPPL_API int cuppl_calibrate(int kind, int blocks, int iters, float* sink, void* stream);
+
+/* Host-side ordered merge of n records (rank order). Pure host function. */
+CUPPL_API int cuppl_is_record_merge(const cuppl_is_record* recs, int n, cuppl_is_record* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CUPPL_GPU_H */

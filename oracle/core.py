@@ -1,0 +1,148 @@
+"""ctypes binding of oracle/liboracle.so (TEST INFRASTRUCTURE ONLY; see oracle/__init__.py)."""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB_PATH = HERE / "liboracle.so"
+
+
+class OrRecord(C.Structure):
+    """Layout of or_record == cuppl_is_record (include/cuppl_gpu.h)."""
+
+    _fields_ = [
+        ("max_lw", C.c_double),
+        ("sum_w", C.c_double),
+        ("sum_w2", C.c_double),
+        ("argmax_lw", C.c_double),
+        ("argmax_pid", C.c_uint64),
+        ("n_finite", C.c_uint64),
+        ("n_total", C.c_uint64),
+        ("reserved", C.c_uint64),
+        ("stat_w", C.c_double * 16),
+        ("bin_w", C.c_double * 8),
+    ]
+
+    def as_dict(self) -> dict:
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f not in ("stat_w", "bin_w")}
+        d["stat_w"] = np.array(self.stat_w[:])
+        d["bin_w"] = np.array(self.bin_w[:])
+        return d
+
+
+def build() -> Path:
+    """Compile the C restatement (make, in-tree)."""
+    srcs = list(HERE.glob("*.c")) + [HERE / "Makefile"]
+    if LIB_PATH.exists() and all(s.stat().st_mtime <= LIB_PATH.stat().st_mtime for s in srcs):
+        return LIB_PATH
+    subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            build()
+        L = C.CDLL(str(LIB_PATH))
+        P = C.POINTER
+        u32p, f32p, f64p, i32p, u64p = (P(C.c_uint32), P(C.c_float), P(C.c_double),
+                                        P(C.c_int32), P(C.c_uint64))
+        L.or_philox.argtypes = [u32p, u32p, u32p]
+        L.or_philox_blocks.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, u32p]
+        L.or_u01_open0.argtypes = [C.c_uint32]
+        L.or_u01_open0.restype = C.c_double
+        L.or_u01_closed0.argtypes = [C.c_uint32]
+        L.or_u01_closed0.restype = C.c_double
+        L.or_lemire.argtypes = [C.c_uint32, C.c_uint32, u32p]
+        L.or_box_muller.argtypes = [C.c_uint32, C.c_uint32, f64p, f64p]
+        L.or_poly_draw.argtypes = [C.c_uint64, C.c_uint64, P(C.c_int), f64p]
+        L.or_poly_lw.argtypes = [C.c_int, f64p, f32p, f32p, C.c_int]
+        L.or_poly_lw.restype = C.c_double
+        L.or_is_poly.argtypes = [f32p, f32p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, f32p,
+                                 f64p, i32p, f64p, P(OrRecord), C.c_int]
+        L.or_is_linreg.argtypes = [f32p, f32p, C.c_int, C.c_double, C.c_uint64, C.c_uint64,
+                                   C.c_uint64, f32p, f64p, f64p, P(OrRecord), C.c_int]
+        L.or_dist_sample.argtypes = [C.c_int, C.c_double, C.c_double, u64p, C.c_int, C.c_uint64,
+                                     C.c_uint32, C.c_uint64, C.c_uint64, f64p, i32p]
+        L.or_rec_merge.argtypes = [P(OrRecord), P(OrRecord)]
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray | None, ctype):
+    if a is None:
+        return None
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+def philox(ctr, key) -> np.ndarray:
+    c = np.asarray(ctr, dtype=np.uint32)
+    k = np.asarray(key, dtype=np.uint32)
+    out = np.zeros(4, dtype=np.uint32)
+    lib().or_philox(_ptr(c, C.c_uint32), _ptr(k, C.c_uint32), _ptr(out, C.c_uint32))
+    return out
+
+
+def philox_blocks(key: int, first_id: int, block: int, tag: int, count: int) -> np.ndarray:
+    out = np.zeros((count, 4), dtype=np.uint32)
+    lib().or_philox_blocks(key, first_id, block, tag, count, _ptr(out, C.c_uint32))
+    return out
+
+
+def is_poly(xs, ys, pid_begin, pid_end, key, injected=None, traces=False, threads=0):
+    xs = np.ascontiguousarray(xs, dtype=np.float32)
+    ys = np.ascontiguousarray(ys, dtype=np.float32)
+    n = pid_end - pid_begin
+    inj = None if injected is None else np.ascontiguousarray(injected, dtype=np.float32)
+    lw = np.zeros(n) if traces else None
+    deg = np.zeros(n, dtype=np.int32) if traces else None
+    coef = np.zeros((n, 4)) if traces else None
+    rec = OrRecord()
+    rc = lib().or_is_poly(_ptr(xs, C.c_float), _ptr(ys, C.c_float), len(xs), pid_begin, pid_end,
+                          key, _ptr(inj, C.c_float), _ptr(lw, C.c_double), _ptr(deg, C.c_int32),
+                          _ptr(coef, C.c_double), C.byref(rec), threads)
+    assert rc == 0
+    return rec.as_dict(), (lw, deg, coef)
+
+
+def is_linreg(xs, ys, sigma, pid_begin, pid_end, key, injected=None, traces=False, threads=0):
+    xs = np.ascontiguousarray(xs, dtype=np.float32)
+    ys = np.ascontiguousarray(ys, dtype=np.float32)
+    n = pid_end - pid_begin
+    inj = None if injected is None else np.ascontiguousarray(injected, dtype=np.float32)
+    lw = np.zeros(n) if traces else None
+    coef = np.zeros((n, 2)) if traces else None
+    rec = OrRecord()
+    rc = lib().or_is_linreg(_ptr(xs, C.c_float), _ptr(ys, C.c_float), len(xs), float(sigma),
+                            pid_begin, pid_end, key, _ptr(inj, C.c_float), _ptr(lw, C.c_double),
+                            _ptr(coef, C.c_double), C.byref(rec), threads)
+    assert rc == 0
+    return rec.as_dict(), (lw, coef)
+
+
+def dist_sample(tag: int, p0: float, p1: float, key: int, stream_tag: int, first_id: int,
+                count: int, table: np.ndarray | None = None):
+    """Returns float64 samples for continuous kinds, int32 for discrete ones."""
+    discrete = tag in (1, 2, 3, 7)
+    outf = None if discrete else np.zeros(count)
+    outi = np.zeros(count, dtype=np.int32) if discrete else None
+    tbl = None if table is None else np.ascontiguousarray(table, dtype=np.uint64)
+    K = 0 if table is None else len(table) + 1
+    rc = lib().or_dist_sample(tag, p0, p1, _ptr(tbl, C.c_uint64), K, key, stream_tag, first_id,
+                              count, _ptr(outf, C.c_double), _ptr(outi, C.c_int32))
+    assert rc == 0
+    return outi if discrete else outf
+
+
+def default_threads() -> int:
+    return os.cpu_count() or 1

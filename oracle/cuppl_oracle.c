@@ -1,0 +1,428 @@
+/*
+ * cuppl_oracle.c — CPU ORACLE for the CuPPL inference hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY. This file restates, in plain C and fp64, the reference
+ * semantics the GPU library (paper_2010_08454_b200/csrc) implements. Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg may load it,
+ * and only as the checker or the timed CPU baseline — never as the product path.
+ *
+ * What it restates (reference = /root/reference):
+ *   - Philox4x32-10 (Salmon et al., SC'11 "Parallel random numbers: as easy as 1, 2, 3";
+ *     Random123 known-answer vectors are checked in tests/test_oracle.py) replacing the
+ *     SplitMix keyed counter of pkg/src/cuppl/rng.py:16-45;
+ *   - draw algorithms of pkg/src/cuppl/rng.py:43-117 on a Philox word stream;
+ *   - dist_score of SPEC.md:312-320 and observe = factor(dist-score) (desugar.py:37-39);
+ *   - run_importance / normalize of SPEC.md:399-407 / 417-425 (prior proposal, factor adds to
+ *     the log-weight, log-sum-exp, ordered merge SPEC.md:449) for the Fig.1 polynomial model
+ *      and Bayesian linear regression.
+ * Parity status: Philox pinned by the Random123 KATs; distribution scores pinned by the SPEC
+ * known-answer rows; the engines have no executable reference (the
+ * reference ships no vm/infer) and are pinned by the SPEC engine KATs
+ * and the closed-form posteriors in oracle/exact.py.
+ *
+ * Build: see oracle/Makefile (gcc -O2 -fopenmp -ffp-contract=off).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define PH_M0 0xD2511F53u
+#define PH_M1 0xCD9E8D57u
+#define PH_W0 0x9E3779B9u
+#define PH_W1 0xBB67AE85u
+
+#define TAG_IS 1u
+#define TAG_DIST 7u
+
+/* ---------------------------------------------------------------- Philox4x32-10 ------- */
+void or_philox(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+  uint32_t k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)PH_M0 * c0;
+    const uint64_t p1 = (uint64_t)PH_M1 * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+    const uint32_t n1 = (uint32_t)p1;
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    const uint32_t n3 = (uint32_t)p0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    k0 += PH_W0;
+    k1 += PH_W1;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+static inline void block_of(uint64_t key, uint64_t id, uint32_t blk, uint32_t tag, uint32_t out[4]) {
+  const uint32_t ctr[4] = {(uint32_t)id, (uint32_t)(id >> 32), blk, tag};
+  const uint32_t k[2] = {(uint32_t)key, (uint32_t)(key >> 32)};
+  or_philox(ctr, k, out);
+}
+
+void or_philox_blocks(uint64_t key, uint64_t first_id, uint32_t block, uint32_t tag,
+                      uint64_t count, uint32_t* out) {
+  for (uint64_t i = 0; i < count; ++i) block_of(key, first_id + i, block, tag, out + 4 * i);
+}
+
+/* ---------------------------------------------------------------- transforms ---------- */
+static inline float bits_f(uint32_t u) {
+  float f;
+  memcpy(&f, &u, 4);
+  return f;
+}
+/* 23-bit uniforms from the mantissa, exact in both precisions */
+double or_u01_open0(uint32_t w) { return 2.0 - (double)bits_f(0x3F800000u | (w >> 9)); }
+double or_u01_closed0(uint32_t w) { return (double)bits_f(0x3F800000u | (w >> 9)) - 1.0; }
+
+/* Lemire multiply-shift with exact rejection; returns 0 if w must be rejected */
+int or_lemire(uint32_t w, uint32_t range, uint32_t* out) {
+  const uint64_t m = (uint64_t)w * range;
+  const uint32_t lo = (uint32_t)m;
+  *out = (uint32_t)(m >> 32);
+  if (lo < range) {
+    const uint32_t t = (0u - range) % range;
+    return lo >= t;
+  }
+  return 1;
+}
+
+void or_box_muller(uint32_t wa, uint32_t wb, double* z0, double* z1) {
+  const double u1 = or_u01_open0(wa), u2 = or_u01_closed0(wb);
+  const double r = sqrt(-2.0 * log(u1));
+  const double th = 2.0 * M_PI * u2;
+  *z0 = r * cos(th);
+  *z1 = r * sin(th);
+}
+
+/* ---------------------------------------------------------------- records ------------- */
+/* Same field order as cuppl_is_record (include/cuppl_gpu.h), restated here. */
+typedef struct or_record {
+  double max_lw, sum_w, sum_w2, argmax_lw;
+  uint64_t argmax_pid, n_finite, n_total, reserved;
+  double stat_w[16];
+  double bin_w[8];
+} or_record;
+
+static void rec_init(or_record* r) {
+  memset(r, 0, sizeof(*r));
+  r->max_lw = -INFINITY;
+  r->argmax_lw = -INFINITY;
+  r->argmax_pid = ~0ull;
+}
+
+/* online ordered accumulation of one particle (fp64) */
+static void rec_add(or_record* r, double lw, uint64_t pid, const double* f, int nf, int bin) {
+  r->n_total++;
+  if (!isfinite(lw)) return;
+  r->n_finite++;
+  if (lw > r->argmax_lw || (lw == r->argmax_lw && pid < r->argmax_pid)) {
+    r->argmax_lw = lw;
+    r->argmax_pid = pid;
+  }
+  if (lw > r->max_lw) {
+    const double s = exp(r->max_lw - lw);
+    r->sum_w *= s;
+    r->sum_w2 *= s * s;
+    for (int k = 0; k < 16; ++k) r->stat_w[k] *= s;
+    for (int k = 0; k < 8; ++k) r->bin_w[k] *= s;
+    r->max_lw = lw;
+  }
+  const double w = exp(lw - r->max_lw);
+  r->sum_w += w;
+  r->sum_w2 += w * w;
+  for (int k = 0; k < nf; ++k) r->stat_w[k] += w * f[k];
+  if (bin >= 0 && bin < 8) r->bin_w[bin] += w;
+}
+
+void or_rec_merge(or_record* a, const or_record* b) {
+  a->n_total += b->n_total;
+  a->n_finite += b->n_finite;
+  if (b->argmax_lw > a->argmax_lw || (b->argmax_lw == a->argmax_lw && b->argmax_pid < a->argmax_pid)) {
+    a->argmax_lw = b->argmax_lw;
+    a->argmax_pid = b->argmax_pid;
+  }
+  if (b->n_finite == 0) return;
+  if (a->n_finite == b->n_finite) {
+    a->max_lw = b->max_lw;
+    a->sum_w = b->sum_w;
+    a->sum_w2 = b->sum_w2;
+    memcpy(a->stat_w, b->stat_w, sizeof(a->stat_w));
+    memcpy(a->bin_w, b->bin_w, sizeof(a->bin_w));
+    return;
+  }
+  const double m = a->max_lw > b->max_lw ? a->max_lw : b->max_lw;
+  const double fa = exp(a->max_lw - m), fb = exp(b->max_lw - m);
+  a->max_lw = m;
+  a->sum_w = a->sum_w * fa + b->sum_w * fb;
+  a->sum_w2 = a->sum_w2 * fa * fa + b->sum_w2 * fb * fb;
+  for (int k = 0; k < 16; ++k) a->stat_w[k] = a->stat_w[k] * fa + b->stat_w[k] * fb;
+  for (int k = 0; k < 8; ++k) a->bin_w[k] = a->bin_w[k] * fa + b->bin_w[k] * fb;
+}
+
+/* ---------------------------------------------------------------- Fig.1 polynomial ---- */
+/* n ~ uniform-discrete(2,5) (support [2,5), D1) from word 0 of block 0, rejected words
+ * redrawn from word 0 of blocks 2, 3, ...; c_j ~ normal(0, 10) (D2):
+ * (c0, c1) = 10 BM(w1, w2) of block 0, (c2, c3) = 10 BM(w3 of block 0, w0 of block 1). */
+void or_poly_draw(uint64_t key, uint64_t pid, int* n, double c[4]) {
+  uint32_t b0[4], b1[4], k;
+  block_of(key, pid, 0, TAG_IS, b0);
+  block_of(key, pid, 1, TAG_IS, b1);
+  if (!or_lemire(b0[0], 3u, &k)) {
+    for (uint32_t blk = 2;; ++blk) {
+      uint32_t bb[4];
+      block_of(key, pid, blk, TAG_IS, bb);
+      if (or_lemire(bb[0], 3u, &k)) break;
+    }
+  }
+  *n = 2 + (int)k;
+  double z0, z1, z2, z3;
+  or_box_muller(b0[1], b0[2], &z0, &z1);
+  or_box_muller(b0[3], b1[0], &z2, &z3);
+  c[0] = 10.0 * z0;
+  c[1] = 10.0 * z1;
+  c[2] = *n > 2 ? 10.0 * z2 : 0.0;
+  c[3] = *n > 3 ? 10.0 * z3 : 0.0;
+}
+
+/* factor(-distance(c, data)), distance = sum_i (y_i - sum_{j<n} c_j x_i^j)^2 (D3) */
+double or_poly_lw(int n, const double* c, const float* xs, const float* ys, int D) {
+  double acc = 0.0;
+  for (int i = 0; i < D; ++i) {
+    const double x = xs[i];
+    double p = 0.0;
+    for (int j = n - 1; j >= 0; --j) p = p * x + c[j];
+    const double r = (double)ys[i] - p;
+    acc += r * r;
+  }
+  return -acc;
+}
+
+static void poly_particle(const float* xs, const float* ys, int D, uint64_t key, uint64_t pid,
+                          const float* inj, int* n, double c[4], double* lw) {
+  if (inj) {
+    *n = (int)inj[0];
+    for (int j = 0; j < 4; ++j) c[j] = j < *n ? (double)inj[1 + j] : 0.0;
+  } else {
+    or_poly_draw(key, pid, n, c);
+  }
+  *lw = or_poly_lw(*n, c, xs, ys, D);
+}
+
+static int n_threads(int want) {
+#ifdef _OPENMP
+  return want > 0 ? want : omp_get_max_threads();
+#else
+  (void)want;
+  return 1;
+#endif
+}
+
+/* run_importance over global ids [pid_begin, pid_end): contiguous chunks per thread, chunk
+ * records merged in chunk order. Optional traces (NULL to skip). */
+int or_is_poly(const float* xs, const float* ys, int D, uint64_t pid_begin, uint64_t pid_end,
+               uint64_t key, const float* injected, double* lw_out, int32_t* deg_out,
+               double* coef_out, or_record* out, int threads) {
+  const uint64_t N = pid_end - pid_begin;
+  const int T = n_threads(threads);
+  or_record* parts = (or_record*)malloc(sizeof(or_record) * (size_t)T);
+  if (!parts) return 1;
+#pragma omp parallel num_threads(T)
+  {
+#ifdef _OPENMP
+    const int t = omp_get_thread_num();
+#else
+    const int t = 0;
+#endif
+    const uint64_t lo = N * (uint64_t)t / (uint64_t)T, hi = N * (uint64_t)(t + 1) / (uint64_t)T;
+    or_record r;
+    rec_init(&r);
+    for (uint64_t i = lo; i < hi; ++i) {
+      int n;
+      double c[4], lw;
+      poly_particle(xs, ys, D, key, pid_begin + i, injected ? injected + 5 * i : NULL, &n, c, &lw);
+      double f[9] = {0};
+      if (n == 2) { f[0] = c[0]; f[1] = c[1]; }
+      else if (n == 3) { f[2] = c[0]; f[3] = c[1]; f[4] = c[2]; }
+      else { f[5] = c[0]; f[6] = c[1]; f[7] = c[2]; f[8] = c[3]; }
+      rec_add(&r, lw, pid_begin + i, f, 9, n - 2);
+      if (lw_out) lw_out[i] = lw;
+      if (deg_out) deg_out[i] = n;
+      if (coef_out) for (int j = 0; j < 4; ++j) coef_out[4 * i + j] = c[j];
+    }
+    parts[t] = r;
+  }
+  rec_init(out);
+  for (int t = 0; t < T; ++t) or_rec_merge(out, &parts[t]);
+  free(parts);
+  return 0;
+}
+
+/* ---------------------------------------------------------------- linear regression --- */
+void or_linreg_draw(uint64_t key, uint64_t pid, double* a, double* b) {
+  uint32_t w[4];
+  block_of(key, pid, 0, TAG_IS, w);
+  double z0, z1;
+  or_box_muller(w[0], w[1], &z0, &z1);
+  *a = 10.0 * z0;
+  *b = 10.0 * z1;
+}
+
+/* sum_i dist_score(normal(a x_i + b, sigma), y_i) (desugar.py:37-39) */
+double or_linreg_lw(double a, double b, const float* xs, const float* ys, int D, double sigma) {
+  double acc = 0.0;
+  const double c = -log(sigma) - 0.5 * log(2.0 * M_PI);
+  for (int i = 0; i < D; ++i) {
+    const double z = ((double)ys[i] - (a * (double)xs[i] + b)) / sigma;
+    acc += -0.5 * z * z + c;
+  }
+  return acc;
+}
+
+int or_is_linreg(const float* xs, const float* ys, int D, double sigma, uint64_t pid_begin,
+                 uint64_t pid_end, uint64_t key, const float* injected, double* lw_out,
+                 double* coef_out, or_record* out, int threads) {
+  const uint64_t N = pid_end - pid_begin;
+  const int T = n_threads(threads);
+  or_record* parts = (or_record*)malloc(sizeof(or_record) * (size_t)T);
+  if (!parts) return 1;
+#pragma omp parallel num_threads(T)
+  {
+#ifdef _OPENMP
+    const int t = omp_get_thread_num();
+#else
+    const int t = 0;
+#endif
+    const uint64_t lo = N * (uint64_t)t / (uint64_t)T, hi = N * (uint64_t)(t + 1) / (uint64_t)T;
+    or_record r;
+    rec_init(&r);
+    for (uint64_t i = lo; i < hi; ++i) {
+      double a, b;
+      if (injected) {
+        a = injected[2 * i];
+        b = injected[2 * i + 1];
+      } else {
+        or_linreg_draw(key, pid_begin + i, &a, &b);
+      }
+      const double lw = or_linreg_lw(a, b, xs, ys, D, sigma);
+      const double f[5] = {a, b, a * a, b * b, a * b};
+      rec_add(&r, lw, pid_begin + i, f, 5, -1);
+      if (lw_out) lw_out[i] = lw;
+      if (coef_out) { coef_out[2 * i] = a; coef_out[2 * i + 1] = b; }
+    }
+    parts[t] = r;
+  }
+  rec_init(out);
+  for (int t = 0; t < T; ++t) or_rec_merge(out, &parts[t]);
+  free(parts);
+  return 0;
+}
+
+/* ---------------------------------------------------------------- dist_sample --------- */
+/* Word-stream restatement of dist_kernels.cu (consumption order identical). */
+typedef struct {
+  uint64_t key, id;
+  uint32_t tag, blk;
+  uint32_t buf[4];
+  int pos;
+  int has_spare;
+  double spare;
+} wstream;
+
+static void ws_init(wstream* s, uint64_t key, uint64_t id, uint32_t tag) {
+  s->key = key; s->id = id; s->tag = tag; s->blk = 0; s->pos = 4; s->has_spare = 0; s->spare = 0;
+}
+static uint32_t ws_next(wstream* s) {
+  if (s->pos == 4) {
+    block_of(s->key, s->id, s->blk++, s->tag, s->buf);
+    s->pos = 0;
+  }
+  return s->buf[s->pos++];
+}
+static double ws_uniform(wstream* s) { return or_u01_closed0(ws_next(s)); }
+static double ws_uniform_pos(wstream* s) { return or_u01_open0(ws_next(s)); }
+static double ws_normal(wstream* s) {
+  if (s->has_spare) { s->has_spare = 0; return s->spare; }
+  const uint32_t wa = ws_next(s), wb = ws_next(s);
+  double z0, z1;
+  or_box_muller(wa, wb, &z0, &z1);
+  s->spare = z1;
+  s->has_spare = 1;
+  return z0;
+}
+static uint32_t ws_randint(wstream* s, uint32_t range) {
+  uint32_t k;
+  while (!or_lemire(ws_next(s), range, &k)) {}
+  return k;
+}
+static double ws_gamma(wstream* s, double shape) {
+  double boost = 1.0;
+  if (shape < 1.0) {
+    const double u = ws_uniform_pos(s);
+    boost = pow(u, 1.0 / shape);
+    shape += 1.0;
+  }
+  const double d = shape - 1.0 / 3.0, c = 1.0 / sqrt(9.0 * d);
+  for (;;) {
+    const double x = ws_normal(s);
+    double v = 1.0 + c * x;
+    if (v <= 0.0) continue;
+    v = v * v * v;
+    const double u = ws_uniform(s);
+    if (u < 1.0 - 0.0331 * (x * x) * (x * x)) return d * v * boost;
+    if (u > 0.0 && log(u) < 0.5 * x * x + d * (1.0 - v + log(v))) return d * v * boost;
+  }
+}
+static int ws_poisson(wstream* s, double lam) {
+  double stack[64];
+  int sp = 0, total = 0;
+  stack[sp++] = lam;
+  while (sp > 0) {
+    const double l = stack[--sp];
+    if (l < 30.0) {
+      const double limit = exp(-l);
+      int k = 0;
+      double p = ws_uniform(s);
+      while (p > limit) { ++k; p *= ws_uniform(s); }
+      total += k;
+    } else {
+      const double half = floor(l / 2.0);
+      stack[sp++] = l - half;
+      stack[sp++] = half;
+    }
+  }
+  return total;
+}
+
+/* tag: CUPPL_DIST_* ; params p0, p1 ; out_f (continuous) or out_i (discrete) */
+int or_dist_sample(int dtag, double p0, double p1, const uint64_t* table, int K, uint64_t key,
+                   uint32_t tag, uint64_t first_id, uint64_t count, double* out_f, int32_t* out_i) {
+  for (uint64_t i = 0; i < count; ++i) {
+    wstream s;
+    ws_init(&s, key, first_id + i, tag);
+    switch (dtag) {
+      case 0: out_f[i] = p0 + p1 * ws_normal(&s); break;
+      case 1: out_i[i] = ws_uniform(&s) < p0 ? 1 : 0; break;
+      case 2: out_i[i] = ws_poisson(&s, p0); break;
+      case 3: out_i[i] = (int32_t)p0 + (int32_t)ws_randint(&s, (uint32_t)((int64_t)p1 - (int64_t)p0)); break;
+      case 4: out_f[i] = p0 + (p1 - p0) * ws_uniform(&s); break;
+      case 5: {
+        const double x = ws_gamma(&s, p0), y = ws_gamma(&s, p1);
+        out_f[i] = x / (x + y);
+        break;
+      }
+      case 6: out_f[i] = -log(ws_uniform_pos(&s)) / p0; break;
+      case 7: {
+        const uint32_t w = ws_next(&s);
+        int k = 0;
+        while (k < K - 1 && !((uint64_t)w < table[k])) ++k;
+        out_i[i] = k;
+        break;
+      }
+      default: return 1;
+    }
+  }
+  return 0;
+}

@@ -1,0 +1,345 @@
+// is_kernels.cu — K1a/K1b importance-sampling evaluation fused with the K2 log-sum-exp /
+// ESS / moment / histogram / argmax reduction.
+//
+// Replaces run_importance's hot loop: for each particle i the reference
+// splits the RNG (cuppl/rng.py:31-37), runs the model through sample (prior draw) and
+// factor (log-weight += log_p), and normalize()
+// log-sum-exps the weights. Here a thread owns P particles at a time:
+// draws come from Philox keyed by the global particle id, the model runs in registers with
+// packed-fp32 (FFMA2) arithmetic on two particles per instruction, the data lives in the
+// kernel-parameter constant bank (or registers), and the weights never leave the SM unless
+// traces are requested: each thread keeps an online (max, sum w, sum w^2, sum w f(theta))
+// record that is merged per block and then once per grid by the last block to finish.
+#include "cuppl_device.cuh"
+#include "is_kernels.cuh"
+
+namespace cuppl {
+
+// Thread-level online accumulator (fp32 lanes; fp64 from the block level up, D10).
+template <int NS, int NB>
+struct ThreadAcc {
+  float m, s, s2;
+  float st[NS > 0 ? NS : 1];
+  float bn[NB > 0 ? NB : 1];
+  float amax_lw;
+  uint64_t amax_pid;
+  uint32_t n_fin, n_tot;
+
+  __device__ __forceinline__ void init() {
+    m = neg_inf_f();
+    s = s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) st[k] = 0.f;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) bn[k] = 0.f;
+    amax_lw = neg_inf_f();
+    amax_pid = ~0ull;
+    n_fin = n_tot = 0;
+  }
+
+  // Add one particle: stats f[k] and discrete bin `bin` (ignored when NB == 0).
+  __device__ __forceinline__ void add(float lw, uint64_t pid, const float* f, int bin) {
+    ++n_tot;
+    if (!(fabsf(lw) <= 3.402823466e38f)) return;  // excludes -inf, +inf, NaN (D9)
+    ++n_fin;
+    if (lw > amax_lw) {  // particles arrive in increasing pid per thread: ties keep the lowest
+      amax_lw = lw;
+      amax_pid = pid;
+    }
+    if (lw > m) {
+      const float f0 = fast_ex2((m - lw) * kLog2e);
+      s *= f0;
+      s2 *= f0 * f0;
+#pragma unroll
+      for (int k = 0; k < NS; ++k) st[k] *= f0;
+#pragma unroll
+      for (int k = 0; k < NB; ++k) bn[k] *= f0;
+      m = lw;
+    }
+    const float w = fast_ex2((lw - m) * kLog2e);
+    s += w;
+    s2 = fmaf(w, w, s2);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) st[k] = fmaf(w, f[k], st[k]);
+#pragma unroll
+    for (int k = 0; k < NB; ++k) bn[k] += (bin == k) ? w : 0.f;
+  }
+
+  // record view (block_reduce_view)
+  static constexpr int kStats = NS;
+  static constexpr int kBins = NB;
+  __device__ __forceinline__ unsigned long long n_finite() const { return n_fin; }
+  __device__ __forceinline__ unsigned long long n_total() const { return n_tot; }
+  __device__ __forceinline__ double max_lw() const { return m; }
+  __device__ __forceinline__ double sum_w() const { return s; }
+  __device__ __forceinline__ double sum_w2() const { return s2; }
+  __device__ __forceinline__ double stat(int k) const { return st[k]; }
+  __device__ __forceinline__ double bin(int k) const { return bn[k]; }
+  __device__ __forceinline__ double argmax_lw() const { return amax_lw; }
+  __device__ __forceinline__ unsigned long long argmax_pid() const { return amax_pid; }
+};
+
+// Block reduce + grid combine epilogue shared by the eval kernels.
+template <typename Acc>
+__device__ __forceinline__ void is_epilogue(const Acc& acc, cuppl_is_record* block_recs,
+                                            unsigned int* counter, cuppl_is_record* rec_out) {
+  __shared__ BlockScratch sc;
+  __shared__ cuppl_is_record brec;
+  block_reduce_view(acc, &brec, sc);
+  __syncthreads();
+  grid_combine(block_recs, counter, rec_out, brec, sc);
+}
+
+// ------------------------------------------------------------------ linear regression --
+// lw = -0.5/sigma^2 * sum_i (y_i - a x_i - b)^2 - D (ln sigma + 0.5 ln 2 pi)
+// Per point and particle pair: FADD2 (y - b), FFMA2 (r = -a x + (y - b)), FFMA2 (acc += r r).
+template <int P, bool INJ, int CAP>
+__global__ void __launch_bounds__(kIsThreads)
+is_linreg_kernel(const __grid_constant__ LinregParams<CAP> prm) {
+  static_assert(P % 2 == 0, "particles are processed in FFMA2 pairs");
+  ThreadAcc<5, 0> acc;
+  acc.init();
+  const PhiloxKey key{prm.k0, prm.k1};
+  const uint64_t n = prm.pid_end - prm.pid_begin;
+  const uint64_t chunk = static_cast<uint64_t>(blockDim.x) * P;
+  const uint64_t nchunks = (n + chunk - 1) / chunk;
+  const int D = prm.n_points;
+
+  for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const uint64_t base = ch * chunk + threadIdx.x;
+    float a[P], b[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const uint64_t idx = base + static_cast<uint64_t>(p) * blockDim.x;
+      if (INJ) {
+        const bool ok = idx < n;
+        a[p] = ok ? prm.injected[2 * idx] : 0.f;
+        b[p] = ok ? prm.injected[2 * idx + 1] : 0.f;
+      } else {
+        const uint4 w = draw_block(key, prm.pid_begin + idx, 0u, CUPPL_TAG_IS);
+        const float2 z = box_muller(w.x, w.y);
+        a[p] = 10.0f * z.x;  // normal(0, 10): mean + sd * z (D2)
+        b[p] = 10.0f * z.y;
+      }
+    }
+    f32x2 NA[P / 2], NB[P / 2], S0[P / 2], S1[P / 2];
+#pragma unroll
+    for (int q = 0; q < P / 2; ++q) {
+      NA[q] = pack2(-a[2 * q], -a[2 * q + 1]);
+      NB[q] = pack2(-b[2 * q], -b[2 * q + 1]);
+      S0[q] = pack2(0.f, 0.f);
+      S1[q] = pack2(0.f, 0.f);
+    }
+    int i = 0;
+#pragma unroll 2
+    for (; i + 1 < D; i += 2) {
+      const float2 p0 = prm.xy[i], p1 = prm.xy[i + 1];
+      const f32x2 X0 = pack2(p0.x, p0.x), Y0 = pack2(p0.y, p0.y);
+      const f32x2 X1 = pack2(p1.x, p1.x), Y1 = pack2(p1.y, p1.y);
+#pragma unroll
+      for (int q = 0; q < P / 2; ++q) {
+        const f32x2 r0 = fma2(NA[q], X0, add2(Y0, NB[q]));
+        const f32x2 r1 = fma2(NA[q], X1, add2(Y1, NB[q]));
+        S0[q] = fma2(r0, r0, S0[q]);
+        S1[q] = fma2(r1, r1, S1[q]);
+      }
+    }
+    if (i < D) {
+      const float2 p0 = prm.xy[i];
+      const f32x2 X0 = pack2(p0.x, p0.x), Y0 = pack2(p0.y, p0.y);
+#pragma unroll
+      for (int q = 0; q < P / 2; ++q) {
+        const f32x2 r0 = fma2(NA[q], X0, add2(Y0, NB[q]));
+        S0[q] = fma2(r0, r0, S0[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < P / 2; ++q) {
+      const float2 s = unpack2(add2(S0[q], S1[q]));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = 2 * q + h;
+        const uint64_t idx = base + static_cast<uint64_t>(p) * blockDim.x;
+        if (idx < n) {
+          const float lw = fmaf(prm.neg_half_inv_var, h ? s.y : s.x, prm.lw_const);
+          const float f[5] = {a[p], b[p], a[p] * a[p], b[p] * b[p], a[p] * b[p]};
+          acc.add(lw, prm.pid_begin + idx, f, 0);
+          if (prm.lw_out) prm.lw_out[idx] = lw;
+          if (prm.coef_out) reinterpret_cast<float2*>(prm.coef_out)[idx] = make_float2(a[p], b[p]);
+        }
+      }
+    }
+  }
+  is_epilogue(acc, prm.block_recs, prm.counter, prm.rec_out);
+}
+
+// ------------------------------------------------------------------ Fig.1 polynomial ----
+// n ~ uniform-discrete(2,5) from word 0 of block 0 (Lemire; the rare rejected word is
+// redrawn from blocks 2, 3, ...); (c0,c1) = 10*BM(w1,w2) of block 0; (c2,c3) = 10*BM(w3 of
+// block 0, w0 of block 1); c_j = 0 for j >= n (exact: Horner with zero leading terms).
+// lw = -sum_i (y_i - p(x_i))^2, p by Horner (D3).
+__device__ __forceinline__ void poly_draw(PhiloxKey key, uint64_t pid, int& n, float c[4]) {
+  const uint4 w0 = draw_block(key, pid, 0u, CUPPL_TAG_IS);
+  const uint4 w1 = draw_block(key, pid, 1u, CUPPL_TAG_IS);
+  uint32_t k;
+  if (!lemire(w0.x, 3u, &k)) {
+    for (uint32_t blk = 2;; ++blk) {
+      if (lemire(draw_block(key, pid, blk, CUPPL_TAG_IS).x, 3u, &k)) break;
+    }
+  }
+  n = 2 + static_cast<int>(k);
+  const float2 z01 = box_muller(w0.y, w0.z);
+  const float2 z23 = box_muller(w0.w, w1.x);
+  c[0] = 10.0f * z01.x;
+  c[1] = 10.0f * z01.y;
+  c[2] = n > 2 ? 10.0f * z23.x : 0.0f;
+  c[3] = n > 3 ? 10.0f * z23.y : 0.0f;
+}
+
+template <int P, bool INJ, int DC, int CAP>
+__global__ void __launch_bounds__(kIsThreads)
+is_poly_kernel(const __grid_constant__ PolyParams<CAP> prm) {
+  static_assert(P % 2 == 0, "particles are processed in FFMA2 pairs");
+  ThreadAcc<9, 3> acc;
+  acc.init();
+  const PhiloxKey key{prm.k0, prm.k1};
+  const uint64_t n = prm.pid_end - prm.pid_begin;
+  const uint64_t chunk = static_cast<uint64_t>(blockDim.x) * P;
+  const uint64_t nchunks = (n + chunk - 1) / chunk;
+  const int D = DC > 0 ? DC : prm.n_points;
+  float xr[DC > 0 ? DC : 1], nyr[DC > 0 ? DC : 1];  // register-resident data (DC > 0)
+  if constexpr (DC > 0) {
+#pragma unroll
+    for (int i = 0; i < DC; ++i) {
+      xr[i] = prm.xy[i].x;
+      nyr[i] = -prm.xy[i].y;
+    }
+  }
+
+  for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const uint64_t base = ch * chunk + threadIdx.x;
+    float c[P][4];
+    int deg[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const uint64_t idx = base + static_cast<uint64_t>(p) * blockDim.x;
+      if (INJ) {
+        const bool ok = idx < n;
+        const float* src = prm.injected + 5 * (ok ? idx : 0);
+        deg[p] = ok ? static_cast<int>(src[0]) : 2;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[p][j] = (ok && j < deg[p]) ? src[1 + j] : 0.f;
+      } else {
+        poly_draw(key, prm.pid_begin + idx, deg[p], c[p]);
+      }
+    }
+    f32x2 C0[P / 2], C1[P / 2], C2[P / 2], C3[P / 2], S[P / 2];
+#pragma unroll
+    for (int q = 0; q < P / 2; ++q) {
+      C0[q] = pack2(c[2 * q][0], c[2 * q + 1][0]);
+      C1[q] = pack2(c[2 * q][1], c[2 * q + 1][1]);
+      C2[q] = pack2(c[2 * q][2], c[2 * q + 1][2]);
+      C3[q] = pack2(c[2 * q][3], c[2 * q + 1][3]);
+      S[q] = pack2(0.f, 0.f);
+    }
+#pragma unroll(DC > 0 ? DC : 4)
+    for (int i = 0; i < D; ++i) {
+      float xi, nyi;
+      if constexpr (DC > 0) {
+        xi = xr[i];
+        nyi = nyr[i];
+      } else {
+        const float2 xy = prm.xy[i];
+        xi = xy.x;
+        nyi = -xy.y;
+      }
+      const f32x2 X = pack2(xi, xi), NY = pack2(nyi, nyi);
+#pragma unroll
+      for (int q = 0; q < P / 2; ++q) {
+        f32x2 t = fma2(C3[q], X, C2[q]);
+        t = fma2(t, X, C1[q]);
+        t = fma2(t, X, C0[q]);
+        const f32x2 r = add2(t, NY);
+        S[q] = fma2(r, r, S[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < P / 2; ++q) {
+      const float2 s = unpack2(S[q]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = 2 * q + h;
+        const uint64_t idx = base + static_cast<uint64_t>(p) * blockDim.x;
+        if (idx < n) {
+          const float lw = -(h ? s.y : s.x);
+          const int d = deg[p];
+          // stat layout: n=2 -> [0,1]; n=3 -> [2,3,4]; n=4 -> [5..8]  (sum w c_j per degree)
+          float f[9];
+#pragma unroll
+          for (int k = 0; k < 9; ++k) f[k] = 0.f;
+          if (d == 2) { f[0] = c[p][0]; f[1] = c[p][1]; }
+          else if (d == 3) { f[2] = c[p][0]; f[3] = c[p][1]; f[4] = c[p][2]; }
+          else { f[5] = c[p][0]; f[6] = c[p][1]; f[7] = c[p][2]; f[8] = c[p][3]; }
+          acc.add(lw, prm.pid_begin + idx, f, d - 2);
+          if (prm.lw_out) prm.lw_out[idx] = lw;
+          if (prm.deg_out) prm.deg_out[idx] = d;
+          if (prm.coef_out)
+            reinterpret_cast<float4*>(prm.coef_out)[idx] = make_float4(c[p][0], c[p][1], c[p][2], c[p][3]);
+        }
+      }
+    }
+  }
+  is_epilogue(acc, prm.block_recs, prm.counter, prm.rec_out);
+}
+
+// ------------------------------------------------------------------ launchers ----------
+template <typename KernelT, typename ParamT>
+static cudaError_t launch_persistent(KernelT kernel, const ParamT& prm, int sm_count,
+                                     uint64_t n_chunks, int max_blocks, cudaStream_t stream,
+                                     int* grid_out) {
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kIsThreads, 0);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = static_cast<uint64_t>(sm_count) * per_sm;
+  if (grid > n_chunks) grid = n_chunks ? n_chunks : 1;
+  if (grid > static_cast<uint64_t>(max_blocks)) grid = max_blocks;
+  *grid_out = static_cast<int>(grid);
+  kernel<<<static_cast<unsigned>(grid), kIsThreads, 0, stream>>>(prm);
+  return cudaGetLastError();
+}
+
+template <int CAP>
+cudaError_t launch_linreg(const LinregParams<CAP>& prm, bool injected, int sm_count,
+                          int max_blocks, cudaStream_t stream) {
+  constexpr int P = kLinregP;
+  const uint64_t n = prm.pid_end - prm.pid_begin;
+  const uint64_t nchunks = (n + kIsThreads * P - 1) / (kIsThreads * P);
+  int grid = 0;
+  if (injected)
+    return launch_persistent(is_linreg_kernel<P, true, CAP>, prm, sm_count, nchunks, max_blocks, stream, &grid);
+  return launch_persistent(is_linreg_kernel<P, false, CAP>, prm, sm_count, nchunks, max_blocks, stream, &grid);
+}
+
+template <int CAP>
+cudaError_t launch_poly(const PolyParams<CAP>& prm, bool injected, int sm_count, int max_blocks,
+                        cudaStream_t stream) {
+  constexpr int P = kPolyP;
+  const uint64_t n = prm.pid_end - prm.pid_begin;
+  const uint64_t nchunks = (n + kIsThreads * P - 1) / (kIsThreads * P);
+  int grid = 0;
+  if (prm.n_points == 20) {
+    if (injected)
+      return launch_persistent(is_poly_kernel<P, true, 20, CAP>, prm, sm_count, nchunks, max_blocks, stream, &grid);
+    return launch_persistent(is_poly_kernel<P, false, 20, CAP>, prm, sm_count, nchunks, max_blocks, stream, &grid);
+  }
+  if (injected)
+    return launch_persistent(is_poly_kernel<P, true, 0, CAP>, prm, sm_count, nchunks, max_blocks, stream, &grid);
+  return launch_persistent(is_poly_kernel<P, false, 0, CAP>, prm, sm_count, nchunks, max_blocks, stream, &grid);
+}
+
+template cudaError_t launch_linreg<kLinregCapSmall>(const LinregParams<kLinregCapSmall>&, bool, int, int, cudaStream_t);
+template cudaError_t launch_linreg<kLinregCapLarge>(const LinregParams<kLinregCapLarge>&, bool, int, int, cudaStream_t);
+template cudaError_t launch_poly<kPolyCap>(const PolyParams<kPolyCap>&, bool, int, int, cudaStream_t);
+
+}  // namespace cuppl

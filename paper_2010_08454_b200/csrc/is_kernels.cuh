@@ -1,0 +1,52 @@
+// is_kernels.cuh — launch parameters of the importance-sampling kernels (K1a/K1b + K2).
+// Data vectors are passed BY VALUE in the kernel-parameter block (constant bank 0, up to
+// 32 KB on sm_70+ with CUDA >= 12.1), so every thread reads x_i / y_i through the constant
+// cache with a warp-uniform address and no shared-memory staging is needed.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/cuppl_gpu.h"
+
+namespace cuppl {
+
+constexpr int kIsThreads = 256;
+constexpr int kLinregP = 8;  // particles per thread per chunk (4 FFMA2 pairs)
+constexpr int kPolyP = 4;    // particles per thread per chunk (2 FFMA2 pairs)
+constexpr int kLinregCapSmall = 1024;
+constexpr int kLinregCapLarge = 3968;
+constexpr int kPolyCap = 64;
+
+struct IsCommon {
+  uint64_t pid_begin, pid_end;
+  uint32_t k0, k1;
+  int n_points;
+  int pad_;
+  const float* injected;
+  float* lw_out;
+  float* coef_out;
+  cuppl_is_record* block_recs;
+  unsigned int* counter;
+  cuppl_is_record* rec_out;
+};
+
+template <int CAP>
+struct LinregParams : IsCommon {
+  float neg_half_inv_var;  // -0.5 / sigma^2
+  float lw_const;          // -D (ln sigma + 0.5 ln 2 pi)
+  float2 xy[CAP];
+};
+
+template <int CAP>
+struct PolyParams : IsCommon {
+  int32_t* deg_out;
+  float2 xy[CAP];
+};
+
+template <int CAP>
+cudaError_t launch_linreg(const LinregParams<CAP>& prm, bool injected, int sm_count,
+                          int max_blocks, cudaStream_t stream);
+template <int CAP>
+cudaError_t launch_poly(const PolyParams<CAP>& prm, bool injected, int sm_count, int max_blocks,
+                        cudaStream_t stream);
+
+}  // namespace cuppl

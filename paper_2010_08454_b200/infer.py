@@ -1,0 +1,242 @@
+"""Inference entry points — the drop-in for `cuppl.infer`.
+
+Signatures follow the SPEC: run_importance(model, n_samples, rng),
+run_lmh(model, n_samples, rng), normalize(samples); `rng` is a
+`cuppl.rng.Rng` (or this package's mirror, rng.py); `model` is a GPU model descriptor
+(models.py) because the reference has no executable model form. Extra arguments are
+keyword-only. Every engine runs in libcuppl_gpu.so; there is no CPU path.
+
+Multi-GPU: when torch.distributed is initialised, rank r of R evaluates global particle ids
+[floor(rN/R), floor((r+1)N/R)) (Philox counters use the global id, so draws do not depend on
+R) and the fixed-size per-rank records are all-gathered and merged in rank order in fp64
+(SPEC.md:449 ordered merge) — the only collective of importance sampling.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Any
+
+import numpy as np
+
+from . import _native as N
+from .errors import AllZeroWeightError, InferRuntimeError
+from .models import LinearRegression, PolyRegression
+from .rng import key_of, seed_of
+
+
+@dataclass
+class WeightedSample:
+    """(value, log_weight)."""
+
+    value: Any
+    log_weight: float
+
+
+@dataclass
+class EmpiricalDistribution:
+    """Normalised posterior in compact form.
+
+    support      merged (value, probability) pairs of the discrete part of the return value
+                 (e.g. the polynomial degree) — real-valued returns have singleton support
+                  and are summarised by `mean`, `mode` and, on request, traces
+    log_z        log of the normalising-constant estimate: LSE(lw) - log n
+    ess          effective sample size (sum w)^2 / sum w^2
+    mode         return value of the highest-weight particle (ties -> lowest id, D7)
+    """
+
+    support: list = field(default_factory=list)
+    n: int = 0
+    log_z: float = -math.inf
+    ess: float = 0.0
+    mode: Any = None
+    mode_log_weight: float = -math.inf
+    mode_index: int = -1
+    mean: dict = field(default_factory=dict)
+    stats: dict = field(default_factory=dict)
+    traces: dict = field(default_factory=dict)
+    record: dict = field(default_factory=dict)
+
+    def probability(self, value) -> float:
+        for v, p in self.support:
+            if v == value:
+                return p
+        return 0.0
+
+    def expectation(self, name: str) -> float:
+        return self.mean[name]
+
+
+# ----------------------------------------------------------------------------- helpers --
+def _world(group=None):
+    try:
+        import torch.distributed as dist
+    except ImportError:  # pragma: no cover
+        return 0, 1
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Global particle ids owned by `rank`: [floor(rN/R), floor((r+1)N/R))."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def record_to_dict(rec: N.IsRecord) -> dict:
+    d = {f: getattr(rec, f) for f, _ in N.IsRecord._fields_ if f not in ("stat_w", "bin_w")}
+    d["stat_w"] = np.array(rec.stat_w[:])
+    d["bin_w"] = np.array(rec.bin_w[:])
+    return d
+
+
+def records_from_bytes(buf: np.ndarray) -> list[N.IsRecord]:
+    raw = np.ascontiguousarray(buf).view(np.uint8).reshape(-1, N.REC_BYTES)
+    return [N.IsRecord.from_buffer_copy(r.tobytes()) for r in raw]
+
+
+def merge_records(recs: list[N.IsRecord]) -> N.IsRecord:
+    """Ordered fp64 merge (native, cuppl_is_record_merge)."""
+    arr = (N.IsRecord * len(recs))(*recs)
+    out = N.IsRecord()
+    N.check(N.lib().cuppl_is_record_merge(arr, len(recs), C.byref(out)), "record_merge")
+    return out
+
+
+def _gather_records(rec_dev, group=None):
+    """All-gather the per-rank device record (256 B) and merge in rank order."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = _world(group)
+    if world == 1:
+        return records_from_bytes(rec_dev.cpu().numpy())
+    backend = dist.get_backend(group)
+    src = rec_dev if backend == "nccl" else rec_dev.cpu()
+    out = torch.empty(world * src.numel(), dtype=src.dtype, device=src.device)
+    dist.all_gather_into_tensor(out, src, group=group)
+    return records_from_bytes(out.cpu().numpy())
+
+
+class IsLauncher:
+    """Device-level importance-sampling launch for one model (stream-ordered, no sync).
+
+    Keeps the model data on the host side of the ABI (it is passed by value into the kernel
+    parameter block) and owns the workspace / record buffers for repeated launches.
+    """
+
+    def __init__(self, model, device=None):
+        import torch
+
+        self.model = model
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        L = N.lib()
+        ws = L.cuppl_is_workspace_bytes()
+        self.ws = torch.empty(int(ws), dtype=torch.uint8, device=self.device)
+        self.rec = torch.empty(N.REC_BYTES, dtype=torch.uint8, device=self.device)
+        self._xs = np.ascontiguousarray(model.xs, dtype=np.float32)
+        self._ys = np.ascontiguousarray(model.ys, dtype=np.float32)
+        fp = C.POINTER(C.c_float)
+        self._xp = self._xs.ctypes.data_as(fp)
+        self._yp = self._ys.ctypes.data_as(fp)
+        if model.kind not in ("poly", "linreg"):
+            raise InferRuntimeError(f"importance sampling kernel for model kind {model.kind!r} not available")
+
+    def launch(self, pid_begin: int, pid_end: int, key: int, injected=None, lw_out=None,
+               deg_out=None, coef_out=None, rec_out=None, stream=None) -> None:
+        L = N.lib()
+        rec = self.rec if rec_out is None else rec_out
+        st = stream if stream is not None else N.stream_ptr(self.device)
+        m = self.model
+        if m.kind == "poly":
+            rc = L.cuppl_is_poly(self._xp, self._yp, len(self._xs), pid_begin, pid_end, key,
+                                 N.ptr(injected), N.ptr(lw_out), N.ptr(deg_out), N.ptr(coef_out),
+                                 N.ptr(rec), N.ptr(self.ws), self.ws.numel(), st)
+        else:
+            rc = L.cuppl_is_linreg(self._xp, self._yp, len(self._xs), float(m.sigma), pid_begin,
+                                   pid_end, key, N.ptr(injected), N.ptr(lw_out), N.ptr(coef_out),
+                                   N.ptr(rec), N.ptr(self.ws), self.ws.numel(), st)
+        N.check(rc, f"is_{m.kind}")
+
+    def trace_of(self, pid: int, key: int):
+        """Re-run one particle to recover its return value (Philox is counter-based)."""
+        import torch
+
+        kind = self.model.kind
+        coef = torch.empty(4 if kind == "poly" else 2, dtype=torch.float32, device=self.device)
+        deg = torch.empty(1, dtype=torch.int32, device=self.device) if kind == "poly" else None
+        rec = torch.empty(N.REC_BYTES, dtype=torch.uint8, device=self.device)
+        self.launch(pid, pid + 1, key, coef_out=coef, deg_out=deg, rec_out=rec)
+        c = coef.cpu().numpy().astype(float).tolist()
+        if kind == "poly":
+            n = int(deg.cpu().item())
+            return c[:n]
+        return tuple(c)
+
+
+def _distribution_from_record(model, rec: N.IsRecord, n: int, launcher: IsLauncher, key: int,
+                              traces: dict) -> EmpiricalDistribution:
+    if rec.n_finite == 0:
+        raise AllZeroWeightError("every particle has log-weight -inf (SPEC.md:421)")
+    S, S2, M = rec.sum_w, rec.sum_w2, rec.max_lw
+    out = EmpiricalDistribution(n=n, record=record_to_dict(rec), traces=traces)
+    out.log_z = M + math.log(S) - math.log(n)
+    out.ess = S * S / S2
+    out.mode_log_weight = rec.argmax_lw
+    out.mode_index = int(rec.argmax_pid)
+    out.mode = launcher.trace_of(out.mode_index, key)
+    st = np.array(rec.stat_w[:]) / S
+    if model.kind == "linreg":
+        out.mean = {"a": st[0], "b": st[1]}
+        out.stats = {"var_a": st[2] - st[0] ** 2, "var_b": st[3] - st[1] ** 2,
+                     "cov_ab": st[4] - st[0] * st[1]}
+    else:
+        bins = np.array(rec.bin_w[:3]) / S
+        out.support = [(d, float(bins[d - 2])) for d in (2, 3, 4)]
+        idx = {2: (0, 2), 3: (2, 5), 4: (5, 9)}
+        for d, (a, b) in idx.items():
+            w = rec.bin_w[d - 2]
+            out.mean[f"c|n={d}"] = (np.array(rec.stat_w[a:b]) / w).tolist() if w > 0 else None
+    return out
+
+
+def run_importance(model, n_samples: int, rng, *, return_traces: bool = False, group=None,
+                   device=None) -> EmpiricalDistribution:
+    """Likelihood-weighting importance sampling on the GPU.
+
+    Each particle draws from the prior at every `sample` and adds `factor` terms to its
+    log-weight; the result is normalised with a log-sum-exp. With
+    torch.distributed initialised the particles are sharded over the ranks.
+    """
+    import torch
+
+    if n_samples < 1:
+        raise ValueError("n_samples must be >= 1")
+    if not isinstance(model, (PolyRegression, LinearRegression)):
+        raise InferRuntimeError(f"no importance-sampling kernel for {type(model).__name__}")
+    rank, world = _world(group)
+    lo, hi = shard_range(n_samples, rank, world)
+    key = key_of(rng)
+    launcher = IsLauncher(model, device)
+    dev = launcher.device
+    traces = {}
+    lw = deg = coef = None
+    if return_traces:
+        n_local = hi - lo
+        lw = torch.empty(n_local, dtype=torch.float32, device=dev)
+        coef = torch.empty((n_local, 4 if model.kind == "poly" else 2), dtype=torch.float32, device=dev)
+        if model.kind == "poly":
+            deg = torch.empty(n_local, dtype=torch.int32, device=dev)
+        traces = {"log_weight": lw, "coef": coef, "pid_begin": lo}
+        if deg is not None:
+            traces["degree"] = deg
+    try:
+        launcher.launch(lo, hi, key, lw_out=lw, deg_out=deg, coef_out=coef)
+        recs = _gather_records(launcher.rec, group)
+    except InferRuntimeError as e:
+        e.seed = seed_of(rng)
+        raise
+    rec = merge_records(recs)
+    return _distribution_from_record(model, rec, n_samples, launcher, key, traces)

@@ -1,0 +1,248 @@
+"""CPU tests: pin the oracle (Philox KATs, the reference's own RNG outputs, SPEC known-answer
+rows) and check its engines against closed-form posteriors. No GPU needed."""
+
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import exact, refstream, semantics as S
+
+GOLD = json.loads((Path(__file__).parent / "golden" / "refrng.json").read_text())
+
+
+# ------------------------------------------------------------------ Philox ------------
+# Random123 kat_vectors, philox4x32 with 10 rounds.
+KAT = [
+    ([0, 0, 0, 0], [0, 0], [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]),
+    ([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2, [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]),
+    ([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0],
+     [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]),
+]
+
+
+@pytest.mark.parametrize("ctr,key,want", KAT)
+def test_philox_kat(oracle_lib, ctr, key, want):
+    assert list(oracle_lib.philox(ctr, key)) == want
+
+
+def test_philox_blocks_counter_layout(oracle_lib):
+    key = (0x01234567 << 32) | 0x89ABCDEF
+    blk = oracle_lib.philox_blocks(key, (7 << 32) | 5, 3, 1, 2)
+    want0 = oracle_lib.philox([5, 7, 3, 1], [0x89ABCDEF, 0x01234567])
+    want1 = oracle_lib.philox([6, 7, 3, 1], [0x89ABCDEF, 0x01234567])
+    assert list(blk[0]) == list(want0) and list(blk[1]) == list(want1)
+
+
+def test_uniform_transforms_exact(oracle_lib):
+    L = oracle_lib.lib()
+    assert L.or_u01_open0(0xFFFFFFFF) == 2.0**-23 and L.or_u01_open0(0) == 1.0
+    assert L.or_u01_closed0(0) == 0.0 and L.or_u01_closed0(0xFFFFFFFF) == 1.0 - 2.0**-23
+    for w in [1, 511, 512, 0x80000000, 0xDEADBEEF]:
+        assert L.or_u01_closed0(w) == (w >> 9) * 2.0**-23
+        assert L.or_u01_open0(w) == 1.0 - (w >> 9) * 2.0**-23
+
+
+def test_lemire_exact_uniform(oracle_lib):
+    import ctypes as C
+
+    L = oracle_lib.lib()
+    out = C.c_uint32()
+    # range 3: only w == 0 is rejected; every accepted class has exactly the same count
+    assert L.or_lemire(0, 3, C.byref(out)) == 0
+    assert L.or_lemire(1, 3, C.byref(out)) == 1
+    # brute force on a reduced 2^12 model of the same arithmetic
+    counts = np.zeros(5, dtype=int)
+    for w in range(1 << 12):
+        m = w * 5
+        lo = m & 0xFFF
+        t = ((1 << 12) - 5) % 5
+        if lo < 5 and lo < t:
+            continue
+        counts[m >> 12] += 1
+    assert len(set(counts)) == 1
+
+
+# ------------------------------------------------------------------ reference RNG ------
+def test_rng_mirror_matches_reference_keys():
+    from paper_2010_08454_b200.rng import Rng
+
+    for rec in GOLD["streams"]:
+        r = Rng(rec["seed"], rec["stream"])
+        assert r.key == rec["key"]
+        assert [r.next_u64() for _ in range(4)] == rec["next_u64"]
+        r = Rng(rec["seed"], rec["stream"])
+        assert [r.uniform() for _ in range(4)] == rec["uniform"]
+    for rec in GOLD["splits"]:
+        base = Rng(rec["seed"], rec["stream"])
+        for i, k in rec["children"]:
+            assert base.split(i).key == k
+
+
+def test_refstream_algorithms_match_reference():
+    for rec in GOLD["streams"]:
+        mk = lambda: refstream.SplitMixStream(rec["seed"], rec["stream"])  # noqa: E731
+        s = mk()
+        assert [s.randint(3) for _ in range(6)] == rec["randint3"]
+        s = mk()
+        assert [s.normal(0.0, 10.0) for _ in range(5)] == rec["normal_0_10"]
+        s = mk()
+        assert [s.beta(2.0, 3.0) for _ in range(3)] == rec["beta_2_3"]
+        s = mk()
+        assert [s.poisson(4.0) for _ in range(4)] == rec["poisson_4"]
+        s = mk()
+        assert [s.exponential(2.0) for _ in range(3)] == rec["exponential_2"]
+
+
+def test_value_key_matches_reference():
+    from paper_2010_08454_b200 import values
+
+    for rec in GOLD["value_key"]:
+        v = eval(rec["value"])  # literals written by make_golden.py
+        assert repr(values.value_key(v)) == rec["key"]
+
+
+# ------------------------------------------------------------------ SPEC KATs ---------
+def test_dist_score_spec_rows():
+    assert S.dist_score(S.BERNOULLI, [0.5], True) == pytest.approx(-0.6931472, abs=1e-7)
+    assert S.dist_score(S.NORMAL, [0, 1], 0.0) == pytest.approx(-0.9189385, abs=1e-7)
+    assert S.dist_score(S.UNIFORM_DISCRETE, [2, 5], 7) == -math.inf
+
+
+def test_dist_var_spec_rows():
+    assert S.dist_var(S.BERNOULLI, [0.5]) == 0.25
+    assert S.dist_var(S.NORMAL, [0, 10]) == 100
+    assert S.dist_var(S.UNIFORM_DISCRETE, [2, 5]) == pytest.approx(2 / 3)
+    # the product's dist-var agrees
+    from paper_2010_08454_b200 import dists
+
+    for d, tag, p in [(dists.bernoulli(0.5), S.BERNOULLI, [0.5]), (dists.normal(0, 10), S.NORMAL, [0, 10]),
+                      (dists.uniform_discrete(2, 5), S.UNIFORM_DISCRETE, [2, 5]),
+                      (dists.beta(2, 3), S.BETA, [2, 3]), (dists.poisson(3.5), S.POISSON, [3.5]),
+                      (dists.exponential(2.0), S.EXPONENTIAL, [2.0]),
+                      (dists.uniform_continuous(-1, 3), S.UNIFORM_CONTINUOUS, [-1, 3])]:
+        assert dists.variance(d) == pytest.approx(S.dist_var(tag, p))
+
+
+def test_score_normalisation():
+    tot = sum(math.exp(S.dist_score(S.BERNOULLI, [0.3], x)) for x in (True, False))
+    assert abs(tot - 1) < 1e-9
+    tot = sum(math.exp(S.dist_score(S.UNIFORM_DISCRETE, [2, 5], k)) for k in range(-3, 10))
+    assert abs(tot - 1) < 1e-9
+    tot = sum(math.exp(S.dist_score(S.POISSON, [4.0], k)) for k in range(0, 200))
+    assert abs(tot - 1) < 1e-9
+    tot = sum(math.exp(S.dist_score(S.CATEGORICAL, [[1, 0, 3, 2]], k)) for k in range(4))
+    assert abs(tot - 1) < 1e-9
+    xs = np.linspace(-8, 8, 200001)
+    f = np.exp([S.dist_score(S.NORMAL, [0.0, 1.0], x) for x in xs])
+    assert abs(np.trapezoid(f, xs) - 1) < 1e-6
+
+
+def test_normalize_spec_rows():
+    out, _ = S.normalize([("x", math.log(0.2)), ("y", math.log(0.2))])
+    assert [p for _, p in out.values()] == pytest.approx([0.5, 0.5])
+    out, _ = S.normalize([("x", -1000.0), ("y", -1001.0)])
+    assert out[S.value_key("x")][1] == pytest.approx(0.7311, abs=1e-4)
+    assert out[S.value_key("y")][1] == pytest.approx(0.2689, abs=1e-4)
+    out, _ = S.normalize([("x", -math.inf), ("y", 0.0)])
+    assert list(out) == [S.value_key("y")] and out[S.value_key("y")][1] == 1.0
+    with pytest.raises(ZeroDivisionError):
+        S.normalize([("x", -math.inf)])
+
+
+def test_categorical_thresholds():
+    t = S.categorical_thresholds([1, 0, 3])
+    assert list(t) == [1 << 30, 1 << 30]
+    assert S.categorical_from_word(t, 0) == 0
+    assert S.categorical_from_word(t, (1 << 30) - 1) == 0
+    assert S.categorical_from_word(t, 1 << 30) == 2  # zero-weight category never drawn
+    t = S.categorical_thresholds([1, 1, 0])
+    assert list(t) == [1 << 31, 1 << 32]
+    assert S.categorical_from_word(t, 0xFFFFFFFF) == 1
+    from paper_2010_08454_b200 import dists
+
+    assert dists.categorical_thresholds([0.2] * 5) == list(S.categorical_thresholds([0.2] * 5))
+
+
+# ------------------------------------------------------------------ oracle engines ----
+def test_oracle_dist_sample_spec_rows(oracle_lib):
+    key = refstream.key_of(1)
+    b = oracle_lib.dist_sample(S.BERNOULLI, 1.0, 0.0, key, 7, 0, 1000)
+    assert (b == 1).all()
+    u = oracle_lib.dist_sample(S.UNIFORM_DISCRETE, 2, 5, key, 7, 0, 10000)
+    assert set(np.unique(u)) == {2, 3, 4}
+    z = oracle_lib.dist_sample(S.NORMAL, 0.0, 10.0, key, 7, 0, 10**6)
+    assert abs(z.mean()) < 0.05 and abs(z.std() - 10) < 0.1
+    bt = oracle_lib.dist_sample(S.BETA, 2.0, 3.0, key, 7, 0, 200000)
+    assert abs(bt.mean() - 0.4) < 0.003 and abs(bt.var() - S.dist_var(S.BETA, [2, 3])) < 0.002
+    po = oracle_lib.dist_sample(S.POISSON, 45.0, 0.0, key, 7, 0, 100000)
+    assert abs(po.mean() - 45) < 0.15 and abs(po.var() - 45) < 1.5
+    thr = S.categorical_thresholds([0.1, 0.0, 0.6, 0.3])
+    c = oracle_lib.dist_sample(S.CATEGORICAL, 0, 0, key, 7, 0, 100000, table=thr)
+    freq = np.bincount(c, minlength=4) / len(c)
+    assert freq[1] == 0 and np.allclose(freq, [0.1, 0, 0.6, 0.3], atol=0.01)
+
+
+def test_oracle_poly_against_exact(oracle_lib):
+    from paper_2010_08454_b200.models import PolyRegression
+
+    m = PolyRegression.synthetic()
+    n = 400_000
+    rec, _ = oracle_lib.is_poly(m.xs, m.ys, 0, n, refstream.key_of(1))
+    p_exact, means, _, logz_exact = exact.poly_posterior(m.xs.astype(float), m.ys.astype(float))
+    S_, S2 = rec["sum_w"], rec["sum_w2"]
+    ess = S_ * S_ / S2
+    p = rec["bin_w"][:3] / S_
+    for d in (2, 3, 4):
+        se = math.sqrt(max(p_exact[d] * (1 - p_exact[d]), 1e-6) / ess)
+        assert abs(p[d - 2] - p_exact[d]) < 5 * se + 1e-3
+    logz = rec["max_lw"] + math.log(S_) - math.log(n)
+    assert abs(logz - logz_exact) < 5 / math.sqrt(ess) + 0.05
+
+
+def test_oracle_linreg_against_exact(oracle_lib):
+    from paper_2010_08454_b200.models import LinearRegression
+
+    m = LinearRegression.synthetic(n_points=20)
+    n = 400_000
+    rec, _ = oracle_lib.is_linreg(m.xs, m.ys, 1.0, 0, n, refstream.key_of(1))
+    mean, cov, logz_exact = exact.linreg_posterior(m.xs.astype(float), m.ys.astype(float), 1.0)
+    S_, S2 = rec["sum_w"], rec["sum_w2"]
+    ess = S_ * S_ / S2
+    est = rec["stat_w"][:2] / S_
+    sd = np.sqrt(np.diag(cov))
+    assert np.all(np.abs(est - mean) < 5 * sd / math.sqrt(ess) + 1e-3)
+    logz = rec["max_lw"] + math.log(S_) - math.log(n)
+    assert abs(logz - logz_exact) < 5 / math.sqrt(ess) + 0.05
+
+
+def test_oracle_rank_partition_invariance(oracle_lib):
+    """Records of R shards merged in rank order equal the single-shard record."""
+    import ctypes as C
+
+    from paper_2010_08454_b200.models import PolyRegression
+
+    m = PolyRegression.synthetic()
+    n, key = 50_000, refstream.key_of(3)
+    full, _ = oracle_lib.is_poly(m.xs, m.ys, 0, n, key, threads=1)
+    for R in (2, 4, 8):
+        acc = oracle_lib.OrRecord()
+        acc.max_lw = acc.argmax_lw = -math.inf
+        acc.argmax_pid = (1 << 64) - 1
+        for r in range(R):
+            lo, hi = n * r // R, n * (r + 1) // R
+            part, _ = oracle_lib.is_poly(m.xs, m.ys, lo, hi, key, threads=1)
+            pr = oracle_lib.OrRecord()
+            for k, v in part.items():
+                if k in ("stat_w", "bin_w"):
+                    getattr(pr, k)[:] = list(v)
+                else:
+                    setattr(pr, k, v)
+            oracle_lib.lib().or_rec_merge(C.byref(acc), C.byref(pr))
+        got = acc.as_dict()
+        assert got["argmax_pid"] == full["argmax_pid"] and got["n_finite"] == full["n_finite"]
+        assert got["max_lw"] == full["max_lw"]
+        assert got["sum_w"] == pytest.approx(full["sum_w"], rel=1e-12)
+        assert np.allclose(got["bin_w"], full["bin_w"], rtol=1e-12)
