@@ -153,7 +153,9 @@ CUPPL_API int cuppl_is_linreg(const float* xs, const float* ys, int n_points, fl
 /* ---- roofline calibration ---------------------------------------------------------- */
 /* Pipe-rate microbenchmark, blocks x 256 threads, each thread runs `iters` iterations of:
  * kind 0: 128 FFMA2 (256 fp32 FMA), kind 1: 128 FFMA, kind 2: one Philox4x32-10 block,
- * kind 3: 32 MUFU.EX2 + 32 MUFU.LG2. `sink` is a device float[256] (never written in practice). */
+ * kind 3: 32 MUFU.EX2 + 32 MUFU.LG2; kinds 4..8: 16 "points" of the linear-regression inner
+ * loop on 8 particles (4: FADD2+2 FFMA2, 5: 3 FFMA2, 6: scalar FADD+2 FFMA, 7: 2 FADD2 chain,
+ * 8: 2 FADD chain). `sink` is a device float[256] (never written in practice). */
 CUPPL_API int cuppl_calibrate(int kind, int blocks, int iters, float* sink, void* stream);
 
 /* Host-side ordered merge of n records (rank order). Pure host function. */

@@ -163,15 +163,19 @@ void or_rec_merge(or_record* a, const or_record* b) {
 }
 
 /* ---------------------------------------------------------------- Fig.1 polynomial ---- */
-/* n ~ uniform-discrete(2,5) (support [2,5), D1) from word 0 of block 0, rejected words
- * redrawn from word 0 of blocks 2, 3, ...; c_j ~ normal(0, 10) (D2):
- * (c0, c1) = 10 BM(w1, w2) of block 0, (c2, c3) = 10 BM(w3 of block 0, w0 of block 1). */
+/* One Philox block per particle (csrc/is_kernels.cu poly_draw): (c0, c1) = 10 BM(w0, w1),
+ * (c2, c3) = 10 BM(w2, w3) (normal(0, 10), D2); n ~ uniform-discrete(2,5) (support [2,5), D1)
+ * by Lemire on u = w0[8:0] | w1[8:0] << 9 | w2[8:0] << 18 | w3[4:0] << 27 (the bits the 23-bit
+ * Box-Muller uniforms do not use); a rejected u is redrawn from word 0 of blocks 1, 2, ... */
+uint32_t or_poly_degree_word(const uint32_t w[4]) {
+  return (w[0] & 0x1FFu) | ((w[1] & 0x1FFu) << 9) | ((w[2] & 0x1FFu) << 18) | ((w[3] & 0x1Fu) << 27);
+}
+
 void or_poly_draw(uint64_t key, uint64_t pid, int* n, double c[4]) {
-  uint32_t b0[4], b1[4], k;
+  uint32_t b0[4], k;
   block_of(key, pid, 0, TAG_IS, b0);
-  block_of(key, pid, 1, TAG_IS, b1);
-  if (!or_lemire(b0[0], 3u, &k)) {
-    for (uint32_t blk = 2;; ++blk) {
+  if (!or_lemire(or_poly_degree_word(b0), 3u, &k)) {
+    for (uint32_t blk = 1;; ++blk) {
       uint32_t bb[4];
       block_of(key, pid, blk, TAG_IS, bb);
       if (or_lemire(bb[0], 3u, &k)) break;
@@ -179,8 +183,8 @@ void or_poly_draw(uint64_t key, uint64_t pid, int* n, double c[4]) {
   }
   *n = 2 + (int)k;
   double z0, z1, z2, z3;
-  or_box_muller(b0[1], b0[2], &z0, &z1);
-  or_box_muller(b0[3], b1[0], &z2, &z3);
+  or_box_muller(b0[0], b0[1], &z0, &z1);
+  or_box_muller(b0[2], b0[3], &z2, &z3);
   c[0] = 10.0 * z0;
   c[1] = 10.0 * z1;
   c[2] = *n > 2 ? 10.0 * z2 : 0.0;

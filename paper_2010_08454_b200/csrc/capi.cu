@@ -3,6 +3,7 @@
 // no host synchronisation.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -56,6 +57,14 @@ using namespace cuppl;
 
 namespace {
 constexpr int kMaxBlocksPerSm = 32;
+
+int linreg_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("CUPPL_LINREG_VARIANT");
+    return e ? std::atoi(e) : kLinregVariant;
+  }();
+  return v;
+}
 
 size_t is_ws_bytes(int sm) {
   return 256 + static_cast<size_t>(sm) * kMaxBlocksPerSm * sizeof(cuppl_is_record);
@@ -230,8 +239,11 @@ int cuppl_is_linreg(const float* xs, const float* ys, int n_points, float sigma,
       return s;
     prm.neg_half_inv_var = nhiv;
     prm.lw_const = lwc;
-    return cuda_status(launch_linreg(prm, injected != nullptr, sm, sm * kMaxBlocksPerSm, st),
-                       "is_linreg");
+    prm.one = 1.0f;
+    prm.pad1_ = 0.f;
+    return cuda_status(
+        launch_linreg(prm, injected != nullptr, sm, sm * kMaxBlocksPerSm, st, linreg_variant()),
+        "is_linreg");
   }
   LinregParams<kLinregCapLarge> prm;
   if (int s = fill_common(prm, xs, ys, n_points, kLinregCapLarge, pid_begin, pid_end, key,
@@ -239,8 +251,11 @@ int cuppl_is_linreg(const float* xs, const float* ys, int n_points, float sigma,
     return s;
   prm.neg_half_inv_var = nhiv;
   prm.lw_const = lwc;
-  return cuda_status(launch_linreg(prm, injected != nullptr, sm, sm * kMaxBlocksPerSm, st),
-                     "is_linreg");
+  prm.one = 1.0f;
+  prm.pad1_ = 0.f;
+  return cuda_status(
+      launch_linreg(prm, injected != nullptr, sm, sm * kMaxBlocksPerSm, st, linreg_variant()),
+      "is_linreg");
 }
 
 int cuppl_is_poly(const float* xs, const float* ys, int n_points, uint64_t pid_begin,

@@ -93,7 +93,7 @@ __device__ __forceinline__ void is_epilogue(const Acc& acc, cuppl_is_record* blo
 // ------------------------------------------------------------------ linear regression --
 // lw = -0.5/sigma^2 * sum_i (y_i - a x_i - b)^2 - D (ln sigma + 0.5 ln 2 pi)
 // Per point and particle pair: FADD2 (y - b), FFMA2 (r = -a x + (y - b)), FFMA2 (acc += r r).
-template <int P, bool INJ, int CAP>
+template <int P, bool INJ, int CAP, int V>
 __global__ void __launch_bounds__(kIsThreads)
 is_linreg_kernel(const __grid_constant__ LinregParams<CAP> prm) {
   static_assert(P % 2 == 0, "particles are processed in FFMA2 pairs");
@@ -122,51 +122,90 @@ is_linreg_kernel(const __grid_constant__ LinregParams<CAP> prm) {
         b[p] = 10.0f * z.y;
       }
     }
-    f32x2 NA[P / 2], NB[P / 2], S0[P / 2], S1[P / 2];
+    // sum_i r_i^2 per particle, two accumulators per particle (even / odd points)
+    float ssum[P];
+    if constexpr (V == 2) {
+      // scalar: per point and particle FADD (y - b), FFMA (r), FFMA (acc); x_i, y_i read
+      // straight from the constant bank as instruction operands
+      float s0[P], s1[P];
 #pragma unroll
-    for (int q = 0; q < P / 2; ++q) {
-      NA[q] = pack2(-a[2 * q], -a[2 * q + 1]);
-      NB[q] = pack2(-b[2 * q], -b[2 * q + 1]);
-      S0[q] = pack2(0.f, 0.f);
-      S1[q] = pack2(0.f, 0.f);
-    }
-    int i = 0;
+      for (int p = 0; p < P; ++p) s0[p] = s1[p] = 0.f;
+      int i = 0;
 #pragma unroll 2
-    for (; i + 1 < D; i += 2) {
-      const float2 p0 = prm.xy[i], p1 = prm.xy[i + 1];
-      const f32x2 X0 = pack2(p0.x, p0.x), Y0 = pack2(p0.y, p0.y);
-      const f32x2 X1 = pack2(p1.x, p1.x), Y1 = pack2(p1.y, p1.y);
+      for (; i + 1 < D; i += 2) {
+        const float2 p0 = prm.xy[i], p1 = prm.xy[i + 1];
 #pragma unroll
-      for (int q = 0; q < P / 2; ++q) {
-        const f32x2 r0 = fma2(NA[q], X0, add2(Y0, NB[q]));
-        const f32x2 r1 = fma2(NA[q], X1, add2(Y1, NB[q]));
-        S0[q] = fma2(r0, r0, S0[q]);
-        S1[q] = fma2(r1, r1, S1[q]);
-      }
-    }
-    if (i < D) {
-      const float2 p0 = prm.xy[i];
-      const f32x2 X0 = pack2(p0.x, p0.x), Y0 = pack2(p0.y, p0.y);
-#pragma unroll
-      for (int q = 0; q < P / 2; ++q) {
-        const f32x2 r0 = fma2(NA[q], X0, add2(Y0, NB[q]));
-        S0[q] = fma2(r0, r0, S0[q]);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < P / 2; ++q) {
-      const float2 s = unpack2(add2(S0[q], S1[q]));
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int p = 2 * q + h;
-        const uint64_t idx = base + static_cast<uint64_t>(p) * blockDim.x;
-        if (idx < n) {
-          const float lw = fmaf(prm.neg_half_inv_var, h ? s.y : s.x, prm.lw_const);
-          const float f[5] = {a[p], b[p], a[p] * a[p], b[p] * b[p], a[p] * b[p]};
-          acc.add(lw, prm.pid_begin + idx, f, 0);
-          if (prm.lw_out) prm.lw_out[idx] = lw;
-          if (prm.coef_out) reinterpret_cast<float2*>(prm.coef_out)[idx] = make_float2(a[p], b[p]);
+        for (int p = 0; p < P; ++p) {
+          const float r0 = fmaf(-a[p], p0.x, p0.y - b[p]);
+          const float r1 = fmaf(-a[p], p1.x, p1.y - b[p]);
+          s0[p] = fmaf(r0, r0, s0[p]);
+          s1[p] = fmaf(r1, r1, s1[p]);
         }
+      }
+      if (i < D) {
+        const float2 p0 = prm.xy[i];
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const float r0 = fmaf(-a[p], p0.x, p0.y - b[p]);
+          s0[p] = fmaf(r0, r0, s0[p]);
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < P; ++p) ssum[p] = s0[p] + s1[p];
+    } else {
+      // packed: particle pairs share one FFMA2 / FADD2; V == 1 issues the (y - b) add as an
+      // FFMA2 with a runtime 1.0 so it can use both FMA sub-pipes
+      f32x2 NA[P / 2], NB[P / 2], S0[P / 2], S1[P / 2];
+      const f32x2 ONE = pack2(prm.one, prm.one);
+#pragma unroll
+      for (int q = 0; q < P / 2; ++q) {
+        NA[q] = pack2(-a[2 * q], -a[2 * q + 1]);
+        NB[q] = pack2(-b[2 * q], -b[2 * q + 1]);
+        S0[q] = pack2(0.f, 0.f);
+        S1[q] = pack2(0.f, 0.f);
+      }
+      int i = 0;
+#pragma unroll 2
+      for (; i + 1 < D; i += 2) {
+        const float2 p0 = prm.xy[i], p1 = prm.xy[i + 1];
+        const f32x2 X0 = pack2(p0.x, p0.x), Y0 = pack2(p0.y, p0.y);
+        const f32x2 X1 = pack2(p1.x, p1.x), Y1 = pack2(p1.y, p1.y);
+#pragma unroll
+        for (int q = 0; q < P / 2; ++q) {
+          const f32x2 c0 = V == 1 ? fma2(NB[q], ONE, Y0) : add2(Y0, NB[q]);
+          const f32x2 c1 = V == 1 ? fma2(NB[q], ONE, Y1) : add2(Y1, NB[q]);
+          const f32x2 r0 = fma2(NA[q], X0, c0);
+          const f32x2 r1 = fma2(NA[q], X1, c1);
+          S0[q] = fma2(r0, r0, S0[q]);
+          S1[q] = fma2(r1, r1, S1[q]);
+        }
+      }
+      if (i < D) {
+        const float2 p0 = prm.xy[i];
+        const f32x2 X0 = pack2(p0.x, p0.x), Y0 = pack2(p0.y, p0.y);
+#pragma unroll
+        for (int q = 0; q < P / 2; ++q) {
+          const f32x2 c0 = V == 1 ? fma2(NB[q], ONE, Y0) : add2(Y0, NB[q]);
+          const f32x2 r0 = fma2(NA[q], X0, c0);
+          S0[q] = fma2(r0, r0, S0[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < P / 2; ++q) {
+        const float2 t = unpack2(add2(S0[q], S1[q]));
+        ssum[2 * q] = t.x;
+        ssum[2 * q + 1] = t.y;
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const uint64_t idx = base + static_cast<uint64_t>(p) * blockDim.x;
+      if (idx < n) {
+        const float lw = fmaf(prm.neg_half_inv_var, ssum[p], prm.lw_const);
+        const float f[5] = {a[p], b[p], a[p] * a[p], b[p] * b[p], a[p] * b[p]};
+        acc.add(lw, prm.pid_begin + idx, f, 0);
+        if (prm.lw_out) prm.lw_out[idx] = lw;
+        if (prm.coef_out) reinterpret_cast<float2*>(prm.coef_out)[idx] = make_float2(a[p], b[p]);
       }
     }
   }
@@ -174,22 +213,26 @@ is_linreg_kernel(const __grid_constant__ LinregParams<CAP> prm) {
 }
 
 // ------------------------------------------------------------------ Fig.1 polynomial ----
-// n ~ uniform-discrete(2,5) from word 0 of block 0 (Lemire; the rare rejected word is
-// redrawn from blocks 2, 3, ...); (c0,c1) = 10*BM(w1,w2) of block 0; (c2,c3) = 10*BM(w3 of
-// block 0, w0 of block 1); c_j = 0 for j >= n (exact: Horner with zero leading terms).
-// lw = -sum_i (y_i - p(x_i))^2, p by Horner (D3).
+// One Philox block per particle: (c0, c1) = 10 BM(w0, w1), (c2, c3) = 10 BM(w2, w3); the
+// Box-Muller uniforms use the top 23 bits of each word, and n ~ uniform-discrete(2,5) (D1)
+// uses the otherwise unused low bits: u = w0[8:0] | w1[8:0] << 9 | w2[8:0] << 18 |
+// w3[4:0] << 27, Lemire on 3; a rejected u (u == 0) is redrawn from word 0 of blocks 1, 2, ...
+// c_j = 0 for j >= n (exact: Horner with zero leading terms). lw = -sum_i (y_i - p(x_i))^2 (D3).
+__device__ __forceinline__ uint32_t poly_degree_word(uint4 w) {
+  return (w.x & 0x1FFu) | ((w.y & 0x1FFu) << 9) | ((w.z & 0x1FFu) << 18) | ((w.w & 0x1Fu) << 27);
+}
+
 __device__ __forceinline__ void poly_draw(PhiloxKey key, uint64_t pid, int& n, float c[4]) {
-  const uint4 w0 = draw_block(key, pid, 0u, CUPPL_TAG_IS);
-  const uint4 w1 = draw_block(key, pid, 1u, CUPPL_TAG_IS);
+  const uint4 w = draw_block(key, pid, 0u, CUPPL_TAG_IS);
   uint32_t k;
-  if (!lemire(w0.x, 3u, &k)) {
-    for (uint32_t blk = 2;; ++blk) {
+  if (!lemire(poly_degree_word(w), 3u, &k)) {
+    for (uint32_t blk = 1;; ++blk) {
       if (lemire(draw_block(key, pid, blk, CUPPL_TAG_IS).x, 3u, &k)) break;
     }
   }
   n = 2 + static_cast<int>(k);
-  const float2 z01 = box_muller(w0.y, w0.z);
-  const float2 z23 = box_muller(w0.w, w1.x);
+  const float2 z01 = box_muller(w.x, w.y);
+  const float2 z23 = box_muller(w.z, w.w);
   c[0] = 10.0f * z01.x;
   c[1] = 10.0f * z01.y;
   c[2] = n > 2 ? 10.0f * z23.x : 0.0f;
@@ -207,14 +250,6 @@ is_poly_kernel(const __grid_constant__ PolyParams<CAP> prm) {
   const uint64_t chunk = static_cast<uint64_t>(blockDim.x) * P;
   const uint64_t nchunks = (n + chunk - 1) / chunk;
   const int D = DC > 0 ? DC : prm.n_points;
-  float xr[DC > 0 ? DC : 1], nyr[DC > 0 ? DC : 1];  // register-resident data (DC > 0)
-  if constexpr (DC > 0) {
-#pragma unroll
-    for (int i = 0; i < DC; ++i) {
-      xr[i] = prm.xy[i].x;
-      nyr[i] = -prm.xy[i].y;
-    }
-  }
 
   for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
     const uint64_t base = ch * chunk + threadIdx.x;
@@ -244,16 +279,8 @@ is_poly_kernel(const __grid_constant__ PolyParams<CAP> prm) {
     }
 #pragma unroll(DC > 0 ? DC : 4)
     for (int i = 0; i < D; ++i) {
-      float xi, nyi;
-      if constexpr (DC > 0) {
-        xi = xr[i];
-        nyi = nyr[i];
-      } else {
-        const float2 xy = prm.xy[i];
-        xi = xy.x;
-        nyi = -xy.y;
-      }
-      const f32x2 X = pack2(xi, xi), NY = pack2(nyi, nyi);
+      const float2 xy = prm.xy[i];  // warp-uniform constant-bank load (LDCU)
+      const f32x2 X = pack2(xy.x, xy.x), NY = pack2(-xy.y, -xy.y);
 #pragma unroll
       for (int q = 0; q < P / 2; ++q) {
         f32x2 t = fma2(C3[q], X, C2[q]);
@@ -309,16 +336,26 @@ static cudaError_t launch_persistent(KernelT kernel, const ParamT& prm, int sm_c
   return cudaGetLastError();
 }
 
-template <int CAP>
-cudaError_t launch_linreg(const LinregParams<CAP>& prm, bool injected, int sm_count,
-                          int max_blocks, cudaStream_t stream) {
+template <int CAP, int V>
+static cudaError_t launch_linreg_v(const LinregParams<CAP>& prm, bool injected, int sm_count,
+                                   int max_blocks, cudaStream_t stream) {
   constexpr int P = kLinregP;
   const uint64_t n = prm.pid_end - prm.pid_begin;
   const uint64_t nchunks = (n + kIsThreads * P - 1) / (kIsThreads * P);
   int grid = 0;
   if (injected)
-    return launch_persistent(is_linreg_kernel<P, true, CAP>, prm, sm_count, nchunks, max_blocks, stream, &grid);
-  return launch_persistent(is_linreg_kernel<P, false, CAP>, prm, sm_count, nchunks, max_blocks, stream, &grid);
+    return launch_persistent(is_linreg_kernel<P, true, CAP, V>, prm, sm_count, nchunks, max_blocks, stream, &grid);
+  return launch_persistent(is_linreg_kernel<P, false, CAP, V>, prm, sm_count, nchunks, max_blocks, stream, &grid);
+}
+
+template <int CAP>
+cudaError_t launch_linreg(const LinregParams<CAP>& prm, bool injected, int sm_count,
+                          int max_blocks, cudaStream_t stream, int variant) {
+  switch (variant) {
+    case 1: return launch_linreg_v<CAP, 1>(prm, injected, sm_count, max_blocks, stream);
+    case 2: return launch_linreg_v<CAP, 2>(prm, injected, sm_count, max_blocks, stream);
+    default: return launch_linreg_v<CAP, 0>(prm, injected, sm_count, max_blocks, stream);
+  }
 }
 
 template <int CAP>
@@ -338,8 +375,8 @@ cudaError_t launch_poly(const PolyParams<CAP>& prm, bool injected, int sm_count,
   return launch_persistent(is_poly_kernel<P, false, 0, CAP>, prm, sm_count, nchunks, max_blocks, stream, &grid);
 }
 
-template cudaError_t launch_linreg<kLinregCapSmall>(const LinregParams<kLinregCapSmall>&, bool, int, int, cudaStream_t);
-template cudaError_t launch_linreg<kLinregCapLarge>(const LinregParams<kLinregCapLarge>&, bool, int, int, cudaStream_t);
+template cudaError_t launch_linreg<kLinregCapSmall>(const LinregParams<kLinregCapSmall>&, bool, int, int, cudaStream_t, int);
+template cudaError_t launch_linreg<kLinregCapLarge>(const LinregParams<kLinregCapLarge>&, bool, int, int, cudaStream_t, int);
 template cudaError_t launch_poly<kPolyCap>(const PolyParams<kPolyCap>&, bool, int, int, cudaStream_t);
 
 }  // namespace cuppl

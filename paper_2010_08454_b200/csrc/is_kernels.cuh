@@ -33,6 +33,8 @@ template <int CAP>
 struct LinregParams : IsCommon {
   float neg_half_inv_var;  // -0.5 / sigma^2
   float lw_const;          // -D (ln sigma + 0.5 ln 2 pi)
+  float one;               // 1.0f at run time (operand of the FFMA2 form of the add, V == 1)
+  float pad1_;
   float2 xy[CAP];
 };
 
@@ -44,7 +46,11 @@ struct PolyParams : IsCommon {
 
 template <int CAP>
 cudaError_t launch_linreg(const LinregParams<CAP>& prm, bool injected, int sm_count,
-                          int max_blocks, cudaStream_t stream);
+                          int max_blocks, cudaStream_t stream, int variant);
+// Inner-loop formulation of the linear-regression kernel: 0 = FADD2 + 2 FFMA2 per point and
+// particle pair, 1 = 3 FFMA2, 2 = scalar with constant-bank operands. Default: kLinregVariant;
+// the CUPPL_LINREG_VARIANT environment variable overrides it (tuning only).
+constexpr int kLinregVariant = 1;
 template <int CAP>
 cudaError_t launch_poly(const PolyParams<CAP>& prm, bool injected, int sm_count, int max_blocks,
                         cudaStream_t stream);

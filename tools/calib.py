@@ -16,7 +16,11 @@ def main():
     sm = torch.cuda.get_device_properties(dev).multi_processor_count
     out = {"sm_count": sm}
     for kind, name, per_iter in [(0, "ffma2_flops", 512.0), (1, "ffma_flops", 256.0),
-                                 (2, "philox_blocks", 1.0), (3, "mufu_ops", 64.0)]:
+                                 (2, "philox_blocks", 1.0), (3, "mufu_ops", 64.0),
+                                 (4, "lr_fadd2_ffma2_particle_points", 128.0),
+                                 (5, "lr_3ffma2_particle_points", 128.0),
+                                 (6, "lr_scalar_particle_points", 128.0),
+                                 (7, "fadd2_lane_ops", 256.0), (8, "fadd_lane_ops", 256.0)]:
         for blocks_per_sm in (4, 8, 16):
             blocks, iters = sm * blocks_per_sm, 2000 if kind != 2 else 200
             for _ in range(2):
