@@ -150,6 +150,51 @@ CUPPL_API int cuppl_is_linreg(const float* xs, const float* ys, int n_points, fl
                     float* lw_out, float* coef_out, cuppl_is_record* rec_out, void* workspace,
                     size_t workspace_bytes, void* stream);
 
+/* ---- K4/K5/K6: SMC bootstrap particle filter (new: SPEC.md:455 lists SMC as a non-goal;
+ *      semantics defined by SURVEY.md Appendix A D6 and oracle/cuppl_oracle.c or_smc_*) ---- */
+typedef struct cuppl_smc_model {
+  int32_t n_states;           /* S <= 256 (particle state is one byte)                    */
+  float inv_sd;               /* emission y_t ~ normal(mu[x_t], sd): 1 / sd                */
+  float c;                    /* -ln sd - 0.5 ln 2 pi                                       */
+  int32_t reserved;
+  const uint64_t* thr_trans;  /* device [S][S-1] inverse-CDF thresholds of transition rows */
+  const uint64_t* thr_init;   /* device [S-1] thresholds of the initial distribution        */
+  const float* mu;            /* HOST [S] emission means (passed by value to the kernels)   */
+} cuppl_smc_model;
+
+/* Scratch for one rank of n_local particles: segment offsets, look-back words, counters,
+ * per-tile sums. Must be zeroed once before the first step (cuppl_smc_init does it). */
+CUPPL_API size_t cuppl_smc_workspace_bytes(uint64_t n_local);
+
+/* t = 0: x[j] ~ categorical(init), lw[j] = log N(y0; mu[x[j]], sd) for local particles
+ * j_begin + [0, n_local) (j_begin multiple of 8); atomicMax of lw into *m_key (ordered int,
+ * caller initialises it to INT32_MIN). Zeroes the workspace. */
+CUPPL_API int cuppl_smc_init(const cuppl_smc_model* m, uint64_t n_local, uint64_t j_begin,
+                             uint64_t key, float y0, uint8_t* x, float* lw, int32_t* m_key,
+                             void* workspace, size_t workspace_bytes, void* stream);
+
+/* Statistics and weight scan of population t (K5): quantised weights against max *m_key,
+ * rank-local segment offsets into the workspace, rank_rec[4] = {T_r, bits(sum e),
+ * bits(sum e^2), 0}; hist[S] (optional, zeroed by the caller) += integer weights per state. */
+CUPPL_API int cuppl_smc_scan(uint64_t n_local, const float* lw, const uint8_t* x,
+                             const int32_t* m_key, int n_states, uint64_t* hist,
+                             uint64_t* rank_rec, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
+/* Systematic resampling of population t + propagation to t+1 (K6). rank_recs: device
+ * [world][4] records of every rank (all-gathered); rank_begin: device [world+1] global index
+ * of each rank's first particle (multiples of 8); x_out / lw_out / anc_out: device arrays of
+ * `world` destination pointers (peer-mapped for other ranks; anc_out NULL to skip). The
+ * outputs whose ancestors live on this rank are written to their owners; *m_key_next gets the
+ * atomicMax of the new log-weights written here. */
+CUPPL_API int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_total,
+                                 uint64_t key, uint32_t t, int rank, int world, float y_next,
+                                 const float* lw, const uint8_t* x, const int32_t* m_key,
+                                 const uint64_t* rank_recs, const uint64_t* rank_begin,
+                                 uint8_t* const* x_out, float* const* lw_out,
+                                 uint64_t* const* anc_out, int32_t* m_key_next, void* workspace,
+                                 size_t workspace_bytes, void* stream);
+
 /* ---- roofline calibration ---------------------------------------------------------- */
 /* Pipe-rate microbenchmark, blocks x 256 threads, each thread runs `iters` iterations of:
  * kind 0: 128 FFMA2 (256 fp32 FMA), kind 1: 128 FFMA, kind 2: one Philox4x32-10 block,

@@ -146,3 +146,83 @@ def dist_sample(tag: int, p0: float, p1: float, key: int, stream_tag: int, first
 
 def default_threads() -> int:
     return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------- SMC -------
+class OrSmcStats(C.Structure):
+    _fields_ = [("M", C.c_float), ("status", C.c_uint32), ("T", C.c_uint64), ("s1", C.c_double),
+                ("s2", C.c_double)]
+
+
+def _smc_sig(L):
+    P = C.POINTER
+    if getattr(L, "_smc_sig", False):
+        return
+    L.or_smc_init.argtypes = [C.c_uint64, C.c_uint64, P(C.c_uint64), C.c_int, P(C.c_float), C.c_float,
+                              C.c_float, C.c_float, P(C.c_int32), P(C.c_float)]
+    L.or_smc_step.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, P(C.c_uint64), C.c_int, P(C.c_float),
+                              C.c_float, C.c_float, C.c_float, P(C.c_int32), P(C.c_float), P(C.c_int32),
+                              P(C.c_float), P(C.c_uint64), P(OrSmcStats), P(C.c_uint64)]
+    L.or_smc_step.restype = C.c_int
+    L.or_comb_target.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64]
+    L.or_comb_target.restype = C.c_uint64
+    L.or_comb_word.argtypes = [C.c_uint64, C.c_uint32]
+    L.or_comb_word.restype = C.c_uint32
+    L.or_exp_repro.argtypes = [C.c_float]
+    L.or_exp_repro.restype = C.c_float
+    L._smc_sig = True
+
+
+def smc_run(model, n: int, key: int, steps: int | None = None, record_ancestors: bool = False,
+            hist_steps=None):
+    """Exact CPU restatement of run_smc (or_smc_*). Returns a dict of per-step statistics,
+    final population, integer filtering histograms and optionally ancestors per step."""
+    from oracle.semantics import categorical_thresholds
+
+    L = lib()
+    _smc_sig(L)
+    S = model.n_states
+    T = steps or model.T
+    thrA = np.ascontiguousarray(np.concatenate([categorical_thresholds(model.A[s]) for s in range(S)]),
+                                dtype=np.uint64)
+    thr0 = np.ascontiguousarray(categorical_thresholds(model.pi0), dtype=np.uint64)
+    mu = np.ascontiguousarray(model.mu, dtype=np.float32)
+    ys = np.ascontiguousarray(model.ys, dtype=np.float32)
+    inv_sd = np.float32(1.0 / model.sd)
+    c = np.float32(-np.log(model.sd) - 0.5 * np.log(2 * np.pi))
+    x = np.zeros(n, dtype=np.int32)
+    lw = np.zeros(n, dtype=np.float32)
+    x2 = np.zeros(n, dtype=np.int32)
+    lw2 = np.zeros(n, dtype=np.float32)
+    anc = np.zeros(n, dtype=np.uint64) if record_ancestors else None
+    hist_steps = set(hist_steps if hist_steps is not None else [T - 1])
+    u64p = C.POINTER(C.c_uint64)
+    L.or_smc_init(n, key, _ptr(thr0, C.c_uint64) if len(thr0) else None, S, _ptr(mu, C.c_float), float(ys[0]),
+                  float(inv_sd), float(c), _ptr(x, C.c_int32), _ptr(lw, C.c_float))
+    out = {"M": np.zeros(T, np.float32), "T": np.zeros(T, np.uint64), "s1": np.zeros(T), "s2": np.zeros(T),
+           "hist": {}, "ancestors": []}
+    for t in range(T):
+        st = OrSmcStats()
+        h = np.zeros(S, dtype=np.uint64) if t in hist_steps else None
+        last = t + 1 >= T
+        rc = L.or_smc_step(n, key, t, _ptr(thrA, C.c_uint64), S, _ptr(mu, C.c_float),
+                           float(ys[t + 1]) if not last else 0.0, float(inv_sd), float(c),
+                           _ptr(x, C.c_int32), _ptr(lw, C.c_float),
+                           None if last else _ptr(x2, C.c_int32), None if last else _ptr(lw2, C.c_float),
+                           None if (last or anc is None) else anc.ctypes.data_as(u64p), C.byref(st),
+                           None if h is None else h.ctypes.data_as(u64p))
+        out["M"][t], out["T"][t], out["s1"][t], out["s2"][t] = st.M, st.T, st.s1, st.s2
+        if h is not None:
+            out["hist"][t] = h
+        if rc != 0:
+            out["status"] = (rc, t)
+            break
+        if not last:
+            if anc is not None:
+                out["ancestors"].append(anc.copy())
+            x, x2 = x2, x
+            lw, lw2 = lw2, lw
+    out["x"], out["lw"] = x, lw
+    out["log_z_steps"] = out["M"].astype(np.float64) + np.log(out["s1"]) - np.log(n)
+    out["log_z"] = float(out["log_z_steps"].sum())
+    return out

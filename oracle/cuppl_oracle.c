@@ -430,3 +430,144 @@ int or_dist_sample(int dtag, double p0, double p1, const uint64_t* table, int K,
   }
   return 0;
 }
+
+/* ---------------------------------------------------------------- SMC (bootstrap PF) -- */
+/* HMM bootstrap particle filter with integer-exact systematic resampling (SURVEY.md §8(d)
+ * C4, Appendix A D6; SMC has no reference semantics — SPEC.md:455 lists it as a non-goal —
+ * so this restatement *defines* it, bit for bit, for the GPU kernels of csrc/smc_kernels.cu).
+ *
+ *   x_0 ~ categorical(pi0); lw_t = log N(y_t; mu[x_t], sd) (fp32, fixed op sequence);
+ *   w_i = floor(exp_repro(lw_i - M_t) * 2^31) (u32), M_t = max lw_t, C = inclusive u64 scan;
+ *   comb: u = word0(Philox(t, 0, 0, TAG_SMC_COMB)),
+ *         target_j = floor((j 2^32 + u) T / (N 2^32))  (exact, unsigned 128-bit), a_j = upper_bound(C, target_j);
+ *   x_{t+1}[j] ~ categorical(A[x_t[a_j]]) with word (j & 3) of Philox(j >> 2, t + 1, TAG_SMC_STEP).
+ * Categorical draws use u64 inverse-CDF thresholds (D5); every step is exact integer or IEEE
+ * fp32 arithmetic without contraction, so CPU and GPU agree bit for bit. */
+#define TAG_SMC_INIT 2u
+#define TAG_SMC_STEP 3u
+#define TAG_SMC_COMB 4u
+
+static inline float f_bits(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
+
+float or_exp_repro(float d) {
+  const float t = d * 1.44269504f;
+  const float k = rintf(t);
+  float r = fmaf(k, -0.693145752f, d);
+  r = fmaf(k, -1.42860677e-06f, r);
+  float p = 1.38888893e-03f;
+  p = fmaf(p, r, 8.33333377e-03f);
+  p = fmaf(p, r, 4.16666679e-02f);
+  p = fmaf(p, r, 1.66666672e-01f);
+  p = fmaf(p, r, 0.5f);
+  p = fmaf(p, r, 1.0f);
+  p = fmaf(p, r, 1.0f);
+  return p * f_bits((uint32_t)((int)k + 127) << 23);
+}
+
+/* e = exp(lw - M) for lw - M >= -87 (else 0); w = min(floor(e 2^31), 2^31) */
+float or_smc_e(float lw, float M) {
+  if (!(lw > -INFINITY)) return 0.0f;
+  const float d = lw - M;
+  if (!(d >= -87.0f)) return 0.0f;
+  return or_exp_repro(d);
+}
+uint32_t or_smc_w(float e) {
+  const float x = e * 2147483648.0f;
+  uint32_t w = (uint32_t)x;
+  return w > 0x80000000u ? 0x80000000u : w;
+}
+
+float or_emission(float y, float mu, float inv_sd, float c) {
+  const float z = (y - mu) * inv_sd;
+  return fmaf(-0.5f * z, z, c);
+}
+
+int or_categorical(const uint64_t* thr, int K, uint32_t w) {
+  int lo = 0, hi = K - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((uint64_t)w < thr[mid]) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+/* D6: target_j = floor((j 2^32 + u) T / (N 2^32)), in [0, T) for j < N. */
+uint64_t or_comb_target(uint64_t j, uint32_t u, uint64_t T, uint64_t N) {
+  const unsigned __int128 x = ((unsigned __int128)((j << 32) | u)) * (unsigned __int128)T;
+  return (uint64_t)(x / ((unsigned __int128)N << 32));
+}
+
+static inline uint32_t smc_word(uint64_t key, uint64_t j, uint32_t blk, uint32_t tag) {
+  uint32_t b[4];
+  block_of(key, j >> 2, blk, tag, b);
+  return b[j & 3];
+}
+
+uint32_t or_comb_word(uint64_t key, uint32_t t) {
+  uint32_t b[4];
+  block_of(key, (uint64_t)t, 0, TAG_SMC_COMB, b);
+  return b[0];
+}
+
+typedef struct or_smc_stats {
+  float M;
+  uint32_t status; /* 0 ok, 2 all-zero weights */
+  uint64_t T;
+  double s1, s2;
+} or_smc_stats;
+
+void or_smc_init(uint64_t N, uint64_t key, const uint64_t* thr_pi0, int S, const float* mu,
+                 float y0, float inv_sd, float c, int32_t* x, float* lw) {
+  for (uint64_t j = 0; j < N; ++j) {
+    const int k = or_categorical(thr_pi0, S, smc_word(key, j, 0, TAG_SMC_INIT));
+    x[j] = k;
+    lw[j] = or_emission(y0, mu[k], inv_sd, c);
+  }
+}
+
+/* Statistics of population t (max, integer total, s1 = sum e, s2 = sum e^2, optional integer
+ * filtering histogram), then — when x_out != NULL — resample + propagate to t + 1. */
+int or_smc_step(uint64_t N, uint64_t key, uint32_t t, const uint64_t* thrA, int S,
+                const float* mu, float y_next, float inv_sd, float c, const int32_t* x,
+                const float* lw, int32_t* x_out, float* lw_out, uint64_t* anc,
+                or_smc_stats* st, uint64_t* hist) {
+  float M = -INFINITY;
+  for (uint64_t i = 0; i < N; ++i)
+    if (lw[i] > M) M = lw[i];
+  uint64_t* C = (uint64_t*)malloc(sizeof(uint64_t) * (N ? N : 1));
+  if (!C) return 1;
+  uint64_t T = 0;
+  double s1 = 0.0, s2 = 0.0;
+  if (hist) memset(hist, 0, sizeof(uint64_t) * (size_t)S);
+  for (uint64_t i = 0; i < N; ++i) {
+    const float e = M > -INFINITY ? or_smc_e(lw[i], M) : 0.0f;
+    const uint32_t w = or_smc_w(e);
+    T += w;
+    C[i] = T;
+    s1 += (double)e;
+    s2 += (double)e * (double)e;
+    if (hist) hist[x[i]] += w;
+  }
+  st->M = M;
+  st->T = T;
+  st->s1 = s1;
+  st->s2 = s2;
+  st->status = T == 0 ? 2 : 0;
+  if (T == 0 || !x_out) { free(C); return T == 0 ? 2 : 0; }
+  const uint32_t u = or_comb_word(key, t);
+  for (uint64_t j = 0; j < N; ++j) {
+    const uint64_t tj = or_comb_target(j, u, T, N);
+    uint64_t lo = 0, hi = N - 1; /* smallest i with C[i] > tj (exists: C[N-1] = T > tj) */
+    while (lo < hi) {
+      const uint64_t mid = lo + ((hi - lo) >> 1);
+      if (C[mid] > tj) hi = mid; else lo = mid + 1;
+    }
+    if (anc) anc[j] = lo;
+    const int k = or_categorical(thrA + (size_t)x[lo] * (size_t)(S - 1), S,
+                                 smc_word(key, j, t + 1, TAG_SMC_STEP));
+    x_out[j] = k;
+    lw_out[j] = or_emission(y_next, mu[k], inv_sd, c);
+  }
+  free(C);
+  return 0;
+}

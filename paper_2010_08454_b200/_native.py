@@ -58,6 +58,20 @@ class Dist(C.Structure):
     ]
 
 
+class SmcModel(C.Structure):
+    """cuppl_smc_model (include/cuppl_gpu.h)."""
+
+    _fields_ = [
+        ("n_states", C.c_int32),
+        ("inv_sd", C.c_float),
+        ("c", C.c_float),
+        ("reserved", C.c_int32),
+        ("thr_trans", C.c_void_p),
+        ("thr_init", C.c_void_p),
+        ("mu", C.c_void_p),
+    ]
+
+
 _lock = threading.Lock()
 _lib: C.CDLL | None = None
 
@@ -78,6 +92,11 @@ _SIG = {
     "cuppl_is_linreg": ([_P, _P, C.c_int, _F32, _U64, _U64, _U64, _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
     "cuppl_is_record_merge": ([_P, C.c_int, _P], C.c_int),
     "cuppl_calibrate": ([C.c_int, C.c_int, C.c_int, _P, _P], C.c_int),
+    "cuppl_smc_workspace_bytes": ([_U64], C.c_size_t),
+    "cuppl_smc_init": ([_P, _U64, _U64, _U64, _F32, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
+    "cuppl_smc_scan": ([_U64, _P, _P, _P, C.c_int, _P, _P, _P, C.c_size_t, _P], C.c_int),
+    "cuppl_smc_resample": ([_P, _U64, _U64, _U64, _U32, C.c_int, C.c_int, _F32, _P, _P, _P, _P, _P,
+                            _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
 }
 
 

@@ -240,7 +240,7 @@ __device__ __forceinline__ void poly_draw(PhiloxKey key, uint64_t pid, int& n, f
 }
 
 template <int P, bool INJ, int DC, int CAP>
-__global__ void __launch_bounds__(kIsThreads)
+__global__ void __launch_bounds__(kIsThreads, kPolyMinBlocks)
 is_poly_kernel(const __grid_constant__ PolyParams<CAP> prm) {
   static_assert(P % 2 == 0, "particles are processed in FFMA2 pairs");
   ThreadAcc<9, 3> acc;

@@ -12,6 +12,7 @@ namespace cuppl {
 constexpr int kIsThreads = 256;
 constexpr int kLinregP = 8;  // particles per thread per chunk (4 FFMA2 pairs)
 constexpr int kPolyP = 4;    // particles per thread per chunk (2 FFMA2 pairs)
+constexpr int kPolyMinBlocks = 4;  // 64 registers: 32 warps per SM to hide the Horner chains
 constexpr int kLinregCapSmall = 1024;
 constexpr int kLinregCapLarge = 3968;
 constexpr int kPolyCap = 64;
@@ -50,7 +51,7 @@ cudaError_t launch_linreg(const LinregParams<CAP>& prm, bool injected, int sm_co
 // Inner-loop formulation of the linear-regression kernel: 0 = FADD2 + 2 FFMA2 per point and
 // particle pair, 1 = 3 FFMA2, 2 = scalar with constant-bank operands. Default: kLinregVariant;
 // the CUPPL_LINREG_VARIANT environment variable overrides it (tuning only).
-constexpr int kLinregVariant = 1;
+constexpr int kLinregVariant = 0;
 template <int CAP>
 cudaError_t launch_poly(const PolyParams<CAP>& prm, bool injected, int sm_count, int max_blocks,
                         cudaStream_t stream);

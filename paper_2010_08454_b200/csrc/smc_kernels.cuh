@@ -1,0 +1,83 @@
+// smc_kernels.cuh — launch parameters of the SMC kernels (K4 init, K5 scan, K6 resample).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/cuppl_gpu.h"
+
+namespace cuppl {
+
+constexpr int kSmcThreads = 256;
+constexpr int kSegment = 32;                  // particles per segment offset
+constexpr int kTileSegs = 256;                // segments per K5 tile (one per thread)
+constexpr int kTile = kTileSegs * kSegment;   // 8192 particles per scan tile
+constexpr int kBatchPerThread = 8;            // sources per thread per K6 batch
+constexpr int kBatch = kSmcThreads * kBatchPerThread;  // 2048 sources per K6 batch
+constexpr int kOutPerThread = 8;              // outputs per thread per K6 sub-chunk
+constexpr int kChunk = kSmcThreads * kOutPerThread;    // 2048 outputs per sub-chunk
+constexpr int kMaxStates = 256;               // particle state stored as u8
+constexpr int kMaxRanks = 64;
+
+// Bootstrap-filter model (HMM), passed by value.
+struct SmcModel {
+  int S;         // number of states (<= 256)
+  float inv_sd;  // 1 / sd of the Gaussian emission
+  float c;       // -ln sd - 0.5 ln 2 pi
+  int pad_;
+  const unsigned long long* thrA;     // [S][S-1] inverse-CDF thresholds of the rows of A
+  const unsigned long long* thr_pi0;  // [S-1] thresholds of pi0
+  float mu[kMaxStates];               // emission means
+};
+
+struct SmcInitArgs {
+  unsigned long long n_local;  // particles on this rank
+  unsigned long long j_begin;  // global index of local particle 0 (multiple of 4)
+  unsigned long long key;
+  float y0;
+  int pad_;
+  uint8_t* x;
+  float* lw;
+  int* m_key;  // ordered-int key of max lw_0 (atomicMax target)
+};
+
+struct SmcScanArgs {
+  unsigned long long n_local;
+  const float* lw;
+  const uint8_t* x;
+  const int* m_key;              // max of lw_t as an ordered int (global over ranks)
+  unsigned long long* segoff;    // [ceil(n/32)] rank-local inclusive offsets per segment
+  unsigned long long* flags;     // [n_tiles] look-back words (status << 62 | value), zero on entry
+  unsigned int* counters;        // [2]: dynamic tile id, done count (zero on entry; reset on exit)
+  double* tile_s;                // [n_tiles][2] per-tile sum e, sum e^2
+  unsigned long long* hist;      // [S] integer filtering weights of x_t (NULL: skip), zero on entry
+  unsigned long long* rank_rec;  // [4]: T_r, bits(s1_r), bits(s2_r), status (written by the last CTA)
+  int S;
+  int pad_;
+};
+
+struct SmcResampleArgs {
+  unsigned long long n_local;
+  unsigned long long n_total;
+  unsigned long long key;
+  unsigned int t;  // population being resampled; the new one is t + 1
+  int rank, world;
+  float y_next;
+  const float* lw;
+  const uint8_t* x;
+  const int* m_key;                        // max of lw_t (ordered int)
+  const unsigned long long* segoff;        // rank-local inclusive segment offsets
+  const unsigned long long* rank_recs;     // [world][4] gathered rank records of step t
+  const unsigned long long* rank_begin;    // [world + 1] global index of each rank's first particle
+  uint8_t* const* x_out;                   // [world] destination x (peer-mapped for q != rank)
+  float* const* lw_out;                    // [world] destination lw
+  unsigned long long* const* anc_out;      // [world] debug ancestor (global index) or NULL
+  int* m_key_next;                         // atomicMax of lw_{t+1} over the outputs written here
+  unsigned long long* flags_to_clear;      // K5 look-back words, zeroed for the next scan
+  unsigned long long n_tiles;
+};
+
+cudaError_t launch_smc_init(const SmcModel& m, const SmcInitArgs& a, int sm_count, cudaStream_t st);
+cudaError_t launch_smc_scan(const SmcScanArgs& a, int sm_count, cudaStream_t st);
+cudaError_t launch_smc_resample(const SmcModel& m, const SmcResampleArgs& a, int sm_count,
+                                cudaStream_t st);
+
+}  // namespace cuppl

@@ -1,0 +1,255 @@
+"""Host orchestration of the SMC bootstrap particle filter (K4 init, K5 scan, K6 resample).
+
+The engine has no reference counterpart (SPEC.md:455 lists SMC/particle methods as a
+non-goal); its semantics are SURVEY.md §8(a) a17 / Appendix A D6 and are restated bit for bit
+by oracle/cuppl_oracle.c (or_smc_*).
+
+Per time step t, on every rank r (one process per GPU):
+  1. all-reduce MAX of the max log-weight key  (NCCL; skipped for one rank)
+  2. K5 scan: quantised weights, rank-local segment offsets, rank record {T_r, s1_r, s2_r}
+  3. all-gather of the 32-byte rank records    (NCCL; skipped for one rank)
+  4. K6 resample(t) -> population t+1: the outputs whose ancestors live on rank r are produced
+     by rank r and stored straight into their owner's buffers (peer pointers).
+A `LocalGroup` runs R virtual ranks in one process on one GPU (same kernels, collectives done
+with tensor ops) — it exercises the multi-rank arithmetic without a second GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .dists import categorical_thresholds
+from .errors import AllZeroWeightError, InferRuntimeError
+from .models import HiddenMarkovModel
+from .rng import key_of, seed_of
+
+INT32_MIN = -(2**31)
+
+
+def key_to_float(k: int) -> float:
+    """Inverse of the kernels' monotone float->int key (f2key)."""
+    k = int(k) & 0xFFFFFFFF
+    if k & 0x80000000:
+        k ^= 0x7FFFFFFF
+    return float(np.array([k], dtype=np.uint32).view(np.float32)[0])
+
+
+@dataclass
+class SmcResult:
+    """Outcome of run_smc. Arrays are indexed by time step t = 0..T-1."""
+
+    n_particles: int
+    log_z: float
+    log_z_steps: np.ndarray
+    ess: np.ndarray
+    max_log_weight: np.ndarray
+    total_weight: np.ndarray          # integer weight totals T_t (exact)
+    filtering: dict = field(default_factory=dict)   # t -> normalised state histogram
+    filtering_int: dict = field(default_factory=dict)  # t -> integer weights per state
+    states: object = None             # final population (tensor per rank) and log-weights
+    log_weights: object = None
+    ancestors: list = field(default_factory=list)   # per step (when recorded)
+
+
+def rank_boundaries(n: int, world: int) -> list[int]:
+    """Global index of each rank's first particle; multiples of 8 (vector stores, Philox blocks)."""
+    if n < 8 * world:
+        raise ValueError("n_particles must be >= 8 * world_size")
+    n8 = n // 8
+    b = [8 * (n8 * q // world) for q in range(world)] + [n]
+    return b
+
+
+class _Rank:
+    """Device state of one rank."""
+
+    def __init__(self, runner, r: int):
+        import torch
+
+        self.r = r
+        dev = runner.device
+        lo, hi = runner.bounds[r], runner.bounds[r + 1]
+        self.lo, self.n = lo, hi - lo
+        self.x = [torch.empty(self.n, dtype=torch.uint8, device=dev) for _ in range(2)]
+        self.lw = [torch.empty(self.n, dtype=torch.float32, device=dev) for _ in range(2)]
+        self.anc = ([torch.empty(self.n, dtype=torch.int64, device=dev) for _ in range(2)]
+                    if runner.record_ancestors else None)
+        ws = N.lib().cuppl_smc_workspace_bytes(self.n)
+        self.ws = torch.empty(int(ws), dtype=torch.uint8, device=dev)
+        self.m_key = torch.full((runner.T,), INT32_MIN, dtype=torch.int32, device=dev)
+        self.rec = torch.zeros((runner.T, 4), dtype=torch.int64, device=dev)
+
+
+class SmcRunner:
+    def __init__(self, model: HiddenMarkovModel, n_particles: int, rng, *, group=None, device=None,
+                 record_ancestors: bool = False, hist_steps=None, local_world: int | None = None,
+                 steps: int | None = None):
+        import torch
+
+        if not isinstance(model, HiddenMarkovModel):
+            raise InferRuntimeError(f"no SMC kernel for {type(model).__name__}")
+        if model.n_states > 256:
+            raise InferRuntimeError("SMC kernels store the state in one byte: n_states <= 256")
+        self.model = model
+        self.N = int(n_particles)
+        if self.N >= 2**31:
+            raise InferRuntimeError("n_particles must be < 2^31 (u64 weight totals, u32 comb)")
+        self.key = key_of(rng)
+        self.seed = seed_of(rng)
+        self.T = int(steps or model.T)
+        if self.T > model.T:
+            raise ValueError("steps exceeds the number of observations")
+        self.record_ancestors = record_ancestors
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.group = group
+        self.local = local_world is not None
+        if self.local:
+            self.world, self.rank = int(local_world), 0
+            self.ranks_here = list(range(self.world))
+        else:
+            from .infer import _world
+
+            self.rank, self.world = _world(group)
+            self.ranks_here = [self.rank]
+        if self.world > 1 and not self.local:
+            raise InferRuntimeError("multi-process SMC needs peer-mapped buffers (not available yet)")
+        self.bounds = rank_boundaries(self.N, self.world)
+        S = model.n_states
+        thrA = np.array([categorical_thresholds(list(model.A[s])) for s in range(S)], dtype=np.uint64)
+        thr0 = np.array(categorical_thresholds(list(model.pi0)), dtype=np.uint64)
+        dev = self.device
+        self.thrA = torch.tensor(thrA.reshape(-1).view(np.int64), device=dev)
+        self.thr0 = torch.tensor(thr0.view(np.int64) if len(thr0) else np.zeros(1, np.int64), device=dev)
+        self.mu = np.ascontiguousarray(model.mu, dtype=np.float32)
+        sd = float(model.sd)
+        self.cm = N.SmcModel()
+        self.cm.n_states = S
+        self.cm.inv_sd = float(np.float32(1.0 / sd))
+        self.cm.c = float(np.float32(-math.log(sd) - 0.5 * math.log(2 * math.pi)))
+        self.cm.thr_trans = self.thrA.data_ptr()
+        self.cm.thr_init = self.thr0.data_ptr()
+        self.cm.mu = self.mu.ctypes.data
+        self.ys = np.ascontiguousarray(model.ys, dtype=np.float32)
+        self.hist_steps = sorted(set(hist_steps if hist_steps is not None else [self.T - 1]))
+        self.ranks = [_Rank(self, r) for r in self.ranks_here]
+        self.hist = {t: torch.zeros((len(self.ranks), S), dtype=torch.int64, device=dev)
+                     for t in self.hist_steps}
+        self.rank_begin = torch.tensor(self.bounds, dtype=torch.int64, device=dev)
+        self.gathered = torch.zeros((self.T, self.world, 4), dtype=torch.int64, device=dev)
+        # destination pointer tables per ping-pong parity: x_out / lw_out / anc_out [world]
+        self._tables = {}
+        for par in (0, 1):
+            xp = [rk.x[par].data_ptr() for rk in self.ranks]
+            lp = [rk.lw[par].data_ptr() for rk in self.ranks]
+            ap = [rk.anc[par].data_ptr() for rk in self.ranks] if record_ancestors else None
+            self._tables[par] = (torch.tensor(xp, dtype=torch.int64, device=dev),
+                                 torch.tensor(lp, dtype=torch.int64, device=dev),
+                                 torch.tensor(ap, dtype=torch.int64, device=dev) if ap else None)
+        self.ancestors = []
+        self.cur = 0
+
+    # ------------------------------------------------------------------ collectives -------
+    def _allreduce_max(self, t: int):
+        if self.world == 1:
+            return
+        import torch
+
+        if self.local:
+            m = torch.stack([rk.m_key[t] for rk in self.ranks]).max()
+            for rk in self.ranks:
+                rk.m_key[t].copy_(m)
+        else:  # pragma: no cover - multi-GPU
+            import torch.distributed as dist
+
+            dist.all_reduce(self.ranks[0].m_key[t:t + 1], op=dist.ReduceOp.MAX, group=self.group)
+
+    def _allgather(self, t: int):
+        if self.local or self.world == 1:
+            for i, rk in enumerate(self.ranks):
+                self.gathered[t, rk.r].copy_(rk.rec[t])
+        else:  # pragma: no cover - multi-GPU
+            import torch.distributed as dist
+
+            dist.all_gather_into_tensor(self.gathered[t].view(-1), self.ranks[0].rec[t], group=self.group)
+
+    # ------------------------------------------------------------------ steps -------------
+    def init(self):
+        L = N.lib()
+        st = N.stream_ptr(self.device)
+        for rk in self.ranks:
+            N.check(L.cuppl_smc_init(C.byref(self.cm), rk.n, rk.lo, self.key, float(self.ys[0]),
+                                     N.ptr(rk.x[0]), N.ptr(rk.lw[0]), N.ptr(rk.m_key[0:1]),
+                                     N.ptr(rk.ws), rk.ws.numel(), st), "smc_init", seed=self.seed)
+        self.cur = 0
+
+    def step(self, t: int):
+        """Scan population t and (t < T-1) resample/propagate it to t+1."""
+        L = N.lib()
+        st = N.stream_ptr(self.device)
+        self._allreduce_max(t)
+        h = self.hist.get(t)
+        for i, rk in enumerate(self.ranks):
+            N.check(L.cuppl_smc_scan(rk.n, N.ptr(rk.lw[self.cur]), N.ptr(rk.x[self.cur]),
+                                     N.ptr(rk.m_key[t:t + 1]), self.model.n_states,
+                                     None if h is None else N.ptr(h[i]), N.ptr(rk.rec[t]),
+                                     N.ptr(rk.ws), rk.ws.numel(), st), "smc_scan", seed=self.seed, step=t)
+        self._allgather(t)
+        if t + 1 >= self.T:
+            return
+        nxt = 1 - self.cur
+        xt, lt, at = self._tables[nxt]
+        for rk in self.ranks:
+            N.check(L.cuppl_smc_resample(
+                C.byref(self.cm), rk.n, self.N, self.key, t, rk.r, self.world, float(self.ys[t + 1]),
+                N.ptr(rk.lw[self.cur]), N.ptr(rk.x[self.cur]), N.ptr(rk.m_key[t:t + 1]),
+                N.ptr(self.gathered[t]), N.ptr(self.rank_begin), N.ptr(xt), N.ptr(lt),
+                None if at is None else N.ptr(at), N.ptr(rk.m_key[t + 1:t + 2]),
+                N.ptr(rk.ws), rk.ws.numel(), st), "smc_resample", seed=self.seed, step=t)
+        if self.record_ancestors:
+            self.ancestors.append([rk.anc[nxt].clone() for rk in self.ranks])
+        self.cur = nxt
+
+    def run(self) -> SmcResult:
+        self.init()
+        for t in range(self.T):
+            self.step(t)
+        return self.result()
+
+    def result(self) -> SmcResult:
+        g = self.gathered.cpu().numpy().view(np.uint64)
+        mk = self.ranks[0].m_key.cpu().numpy()
+        Tt = g[:, :, 0].sum(axis=1)
+        s1 = np.zeros(self.T)
+        s2 = np.zeros(self.T)
+        for q in range(self.world):  # rank order, fp64
+            s1 += g[:, q, 1].view(np.float64)
+            s2 += g[:, q, 2].view(np.float64)
+        M = np.array([key_to_float(k) for k in mk])
+        zero = np.nonzero(Tt == 0)[0]
+        if len(zero):
+            raise AllZeroWeightError(f"all particle weights are zero at step {int(zero[0])}")
+        lz = M + np.log(s1) - math.log(self.N)
+        res = SmcResult(n_particles=self.N, log_z=float(lz.sum()), log_z_steps=lz, ess=s1 * s1 / s2,
+                        max_log_weight=M, total_weight=Tt)
+        for t, h in self.hist.items():
+            hi = h.cpu().numpy().view(np.uint64).sum(axis=0)
+            res.filtering_int[t] = hi
+            res.filtering[t] = hi.astype(np.float64) / float(hi.sum())
+        res.states = [rk.x[self.cur] for rk in self.ranks]
+        res.log_weights = [rk.lw[self.cur] for rk in self.ranks]
+        res.ancestors = self.ancestors
+        return res
+
+
+def run_smc(model: HiddenMarkovModel, n_particles: int, rng, *, steps: int | None = None,
+            record_ancestors: bool = False, hist_steps=None, group=None, device=None,
+            local_world: int | None = None) -> SmcResult:
+    """Bootstrap particle filter with systematic resampling at every step."""
+    r = SmcRunner(model, n_particles, rng, group=group, device=device, record_ancestors=record_ancestors,
+                  hist_steps=hist_steps, local_world=local_world, steps=steps)
+    return r.run()
