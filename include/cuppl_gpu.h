@@ -157,8 +157,9 @@ typedef struct cuppl_smc_model {
   float inv_sd;               /* emission y_t ~ normal(mu[x_t], sd): 1 / sd                */
   float c;                    /* -ln sd - 0.5 ln 2 pi                                       */
   int32_t reserved;
-  const uint64_t* thr_trans;  /* device [S][S-1] inverse-CDF thresholds of transition rows */
-  const uint64_t* thr_init;   /* device [S-1] thresholds of the initial distribution        */
+  const uint64_t* alias_trans; /* device [S][S] alias tables of the transition rows:      */
+                               /*   entry = thr (bits 0..32, in [0, 2^32]) | alias << 40    */
+  const uint64_t* alias_init;  /* device [S] alias table of the initial distribution       */
   const float* mu;            /* HOST [S] emission means (passed by value to the kernels)   */
 } cuppl_smc_model;
 

@@ -168,24 +168,41 @@ def _smc_sig(L):
     L.or_comb_target.restype = C.c_uint64
     L.or_comb_word.argtypes = [C.c_uint64, C.c_uint32]
     L.or_comb_word.restype = C.c_uint32
+    L.or_alias_build.argtypes = [P(C.c_double), C.c_int, P(C.c_uint64)]
+    L.or_alias_draw.argtypes = [P(C.c_uint64), C.c_int, C.c_uint32]
+    L.or_alias_draw.restype = C.c_int
     L.or_exp_repro.argtypes = [C.c_float]
     L.or_exp_repro.restype = C.c_float
     L._smc_sig = True
+
+
+def alias_table(weights) -> np.ndarray:
+    """or_alias_build: u64 entries thr | alias << 40."""
+    L = lib()
+    _smc_sig(L)
+    w = np.ascontiguousarray(weights, dtype=np.float64)
+    out = np.zeros(len(w), dtype=np.uint64)
+    L.or_alias_build(_ptr(w, C.c_double), len(w), _ptr(out, C.c_uint64))
+    return out
+
+
+def alias_draw(table: np.ndarray, w: int) -> int:
+    L = lib()
+    _smc_sig(L)
+    t = np.ascontiguousarray(table, dtype=np.uint64)
+    return L.or_alias_draw(_ptr(t, C.c_uint64), len(t), w)
 
 
 def smc_run(model, n: int, key: int, steps: int | None = None, record_ancestors: bool = False,
             hist_steps=None):
     """Exact CPU restatement of run_smc (or_smc_*). Returns a dict of per-step statistics,
     final population, integer filtering histograms and optionally ancestors per step."""
-    from oracle.semantics import categorical_thresholds
-
     L = lib()
     _smc_sig(L)
     S = model.n_states
     T = steps or model.T
-    thrA = np.ascontiguousarray(np.concatenate([categorical_thresholds(model.A[s]) for s in range(S)]),
-                                dtype=np.uint64)
-    thr0 = np.ascontiguousarray(categorical_thresholds(model.pi0), dtype=np.uint64)
+    thrA = np.ascontiguousarray(np.concatenate([alias_table(model.A[s]) for s in range(S)]), dtype=np.uint64)
+    thr0 = alias_table(model.pi0)
     mu = np.ascontiguousarray(model.mu, dtype=np.float32)
     ys = np.ascontiguousarray(model.ys, dtype=np.float32)
     inv_sd = np.float32(1.0 / model.sd)
@@ -197,7 +214,7 @@ def smc_run(model, n: int, key: int, steps: int | None = None, record_ancestors:
     anc = np.zeros(n, dtype=np.uint64) if record_ancestors else None
     hist_steps = set(hist_steps if hist_steps is not None else [T - 1])
     u64p = C.POINTER(C.c_uint64)
-    L.or_smc_init(n, key, _ptr(thr0, C.c_uint64) if len(thr0) else None, S, _ptr(mu, C.c_float), float(ys[0]),
+    L.or_smc_init(n, key, _ptr(thr0, C.c_uint64), S, _ptr(mu, C.c_float), float(ys[0]),
                   float(inv_sd), float(c), _ptr(x, C.c_int32), _ptr(lw, C.c_float))
     out = {"M": np.zeros(T, np.float32), "T": np.zeros(T, np.uint64), "s1": np.zeros(T), "s2": np.zeros(T),
            "hist": {}, "ancestors": []}

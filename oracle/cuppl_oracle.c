@@ -440,9 +440,11 @@ int or_dist_sample(int dtag, double p0, double p1, const uint64_t* table, int K,
  *   w_i = floor(exp_repro(lw_i - M_t) * 2^31) (u32), M_t = max lw_t, C = inclusive u64 scan;
  *   comb: u = word0(Philox(t, 0, 0, TAG_SMC_COMB)),
  *         target_j = floor((j 2^32 + u) T / (N 2^32))  (exact, unsigned 128-bit), a_j = upper_bound(C, target_j);
- *   x_{t+1}[j] ~ categorical(A[x_t[a_j]]) with word (j & 3) of Philox(j >> 2, t + 1, TAG_SMC_STEP).
- * Categorical draws use u64 inverse-CDF thresholds (D5); every step is exact integer or IEEE
- * fp32 arithmetic without contraction, so CPU and GPU agree bit for bit. */
+ *   x_{t+1}[j] ~ categorical(A[x_t[a_j]]) (alias draw) with word (j & 3) of
+ *                Philox(j >> 2, t + 1, TAG_SMC_STEP).
+ * Categorical draws of the filter use alias tables (or_alias_build / or_alias_draw: O(1) per
+ * draw); every step is exact integer or IEEE fp32 arithmetic without contraction, so CPU and
+ * GPU agree bit for bit. */
 #define TAG_SMC_INIT 2u
 #define TAG_SMC_STEP 3u
 #define TAG_SMC_COMB 4u
@@ -482,6 +484,55 @@ float or_emission(float y, float mu, float inv_sd, float c) {
   return fmaf(-0.5f * z, z, c);
 }
 
+/* Walker / Vose alias table with exact integer masses (SMC categorical draws): column k keeps
+ * k when the coin (low 32 bits of w K) is below thr_k in [0, 2^32], else yields alias_k.
+ * Entry layout: thr (bits 0..32) | alias << 40. Construction: m_k = floor(w_k / W * K * 2^32)
+ * (left-fold W), the rounding deficit added to the first largest m_k, then small / large stacks
+ * popped LIFO in index order — restated verbatim by paper_2010_08454_b200/dists.py. */
+void or_alias_build(const double* w, int K, uint64_t* out) {
+  if (K <= 0) return;
+  const uint64_t unit = 1ull << 32;
+  double total = 0.0;
+  for (int k = 0; k < K; ++k) total += w[k];
+  int64_t* m = (int64_t*)malloc(sizeof(int64_t) * K);
+  int* small = (int*)malloc(sizeof(int) * K);
+  int* large = (int*)malloc(sizeof(int) * K);
+  uint64_t* thr = (uint64_t*)malloc(sizeof(uint64_t) * K);
+  int* alias = (int*)malloc(sizeof(int) * K);
+  int64_t sum = 0;
+  int kmax = 0;
+  for (int k = 0; k < K; ++k) {
+    m[k] = (int64_t)floor(w[k] / total * K * 4294967296.0);
+    sum += m[k];
+  }
+  for (int k = 1; k < K; ++k)
+    if (m[k] > m[kmax]) kmax = k;
+  m[kmax] += (int64_t)K * (int64_t)unit - sum;
+  int ns = 0, nl = 0;
+  for (int k = 0; k < K; ++k) {
+    if (m[k] < (int64_t)unit) small[ns++] = k; else large[nl++] = k;
+  }
+  while (ns && nl) {
+    const int sm = small[--ns], lg = large[--nl];
+    thr[sm] = (uint64_t)m[sm];
+    alias[sm] = lg;
+    m[lg] -= (int64_t)unit - m[sm];
+    if (m[lg] < (int64_t)unit) small[ns++] = lg; else large[nl++] = lg;
+  }
+  while (nl) { const int k = large[--nl]; thr[k] = unit; alias[k] = k; }
+  while (ns) { const int k = small[--ns]; thr[k] = unit; alias[k] = k; }
+  for (int k = 0; k < K; ++k) out[k] = thr[k] | ((uint64_t)alias[k] << 40);
+  free(m); free(small); free(large); free(thr); free(alias);
+}
+
+int or_alias_draw(const uint64_t* tab, int K, uint32_t w) {
+  const uint64_t p = (uint64_t)w * (uint64_t)K;
+  const int col = (int)(p >> 32);
+  const uint32_t coin = (uint32_t)p;
+  const uint64_t e = tab[col];
+  return (uint64_t)coin < (e & 0x1FFFFFFFFull) ? col : (int)(e >> 40);
+}
+
 int or_categorical(const uint64_t* thr, int K, uint32_t w) {
   int lo = 0, hi = K - 1;
   while (lo < hi) {
@@ -516,10 +567,10 @@ typedef struct or_smc_stats {
   double s1, s2;
 } or_smc_stats;
 
-void or_smc_init(uint64_t N, uint64_t key, const uint64_t* thr_pi0, int S, const float* mu,
+void or_smc_init(uint64_t N, uint64_t key, const uint64_t* alias_pi0, int S, const float* mu,
                  float y0, float inv_sd, float c, int32_t* x, float* lw) {
   for (uint64_t j = 0; j < N; ++j) {
-    const int k = or_categorical(thr_pi0, S, smc_word(key, j, 0, TAG_SMC_INIT));
+    const int k = or_alias_draw(alias_pi0, S, smc_word(key, j, 0, TAG_SMC_INIT));
     x[j] = k;
     lw[j] = or_emission(y0, mu[k], inv_sd, c);
   }
@@ -527,7 +578,7 @@ void or_smc_init(uint64_t N, uint64_t key, const uint64_t* thr_pi0, int S, const
 
 /* Statistics of population t (max, integer total, s1 = sum e, s2 = sum e^2, optional integer
  * filtering histogram), then — when x_out != NULL — resample + propagate to t + 1. */
-int or_smc_step(uint64_t N, uint64_t key, uint32_t t, const uint64_t* thrA, int S,
+int or_smc_step(uint64_t N, uint64_t key, uint32_t t, const uint64_t* aliasA, int S,
                 const float* mu, float y_next, float inv_sd, float c, const int32_t* x,
                 const float* lw, int32_t* x_out, float* lw_out, uint64_t* anc,
                 or_smc_stats* st, uint64_t* hist) {
@@ -563,8 +614,8 @@ int or_smc_step(uint64_t N, uint64_t key, uint32_t t, const uint64_t* thrA, int 
       if (C[mid] > tj) hi = mid; else lo = mid + 1;
     }
     if (anc) anc[j] = lo;
-    const int k = or_categorical(thrA + (size_t)x[lo] * (size_t)(S - 1), S,
-                                 smc_word(key, j, t + 1, TAG_SMC_STEP));
+    const int k = or_alias_draw(aliasA + (size_t)x[lo] * (size_t)S, S,
+                                smc_word(key, j, t + 1, TAG_SMC_STEP));
     x_out[j] = k;
     lw_out[j] = or_emission(y_next, mu[k], inv_sd, c);
   }

@@ -66,8 +66,8 @@ class SmcModel(C.Structure):
         ("inv_sd", C.c_float),
         ("c", C.c_float),
         ("reserved", C.c_int32),
-        ("thr_trans", C.c_void_p),
-        ("thr_init", C.c_void_p),
+        ("alias_trans", C.c_void_p),
+        ("alias_init", C.c_void_p),
         ("mu", C.c_void_p),
     ]
 

@@ -49,14 +49,14 @@ int fill_model(const cuppl_smc_model* m, SmcModel* out) {
     return set_error(CUPPL_E_CAPACITY, "n_states=%d outside [1, %d]", m->n_states, kMaxStates);
   if (!(m->inv_sd > 0.f) || !std::isfinite(m->inv_sd))
     return set_error(CUPPL_E_INVALID_PARAM, "normal(mu, sd): sd must be > 0");
-  if (!m->mu || (m->n_states > 1 && (!m->thr_trans || !m->thr_init)))
+  if (!m->mu || !m->alias_trans || !m->alias_init)
     return set_error(CUPPL_E_ARGUMENT, "model tables are NULL");
   std::memset(out, 0, sizeof(*out));
   out->S = m->n_states;
   out->inv_sd = m->inv_sd;
   out->c = m->c;
-  out->thrA = reinterpret_cast<const unsigned long long*>(m->thr_trans);
-  out->thr_pi0 = reinterpret_cast<const unsigned long long*>(m->thr_init);
+  out->alias_trans = reinterpret_cast<const unsigned long long*>(m->alias_trans);
+  out->alias_init = reinterpret_cast<const unsigned long long*>(m->alias_init);
   for (int s = 0; s < m->n_states; ++s) out->mu[s] = m->mu[s];
   return CUPPL_OK;
 }

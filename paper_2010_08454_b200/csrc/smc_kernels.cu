@@ -1,4 +1,4 @@
-// smc_kernels.cu — K4 init, K5 quantise + tile scan (decoupled look-back), K6 fused
+// smc_kernels.cu — K4 init, K5 quantise + tile scan (single-pass decoupled look-back), K6 fused
 // systematic resampling + ancestor gather + propagate + reweight, for the bootstrap particle
 // filter. SMC has no reference semantics, so
 // oracle/cuppl_oracle.c (or_smc_*) *defines* every bit these kernels must reproduce:
@@ -7,7 +7,7 @@
 //   C        = inclusive u64 scan of w; T = C[N-1]
 //   target_j = floor((j 2^32 + u) T / (N 2^32)), u = word 0 of Philox(t, 0, 0, TAG_SMC_COMB)
 //   a_j      = min{i : C_i > target_j}
-//   x'_j     ~ categorical(A[x_{a_j}]) with word (j & 3) of Philox(j >> 2, t + 1, TAG_SMC_STEP)
+//   x'_j     ~ categorical(A[x_{a_j}]): alias draw with word (j & 3) of Philox(j >> 2, t+1, STEP)
 //   lw'_j    = log N(y_{t+1}; mu[x'_j], sd)
 //
 // Data layout per rank: x (u8, one byte per particle), lw (f32); segoff (u64 per 32
@@ -16,12 +16,13 @@
 // 1 + 4 (K6 writes x', lw') = 14 B per particle (+0.25 B of segment offsets each way).
 //
 // K6 is output-balanced and source-streaming: CTA b owns an even share of the rank's output
-// range, finds the ancestor of its first output once (warp-parallel 32-ary search on segoff),
+// range, finds the ancestor of its first output once (warp-parallel 33-ary search on segoff),
 // then streams its sources in order in batches of 2048. For each staged source with w_i > 0 it
 // computes f_i = min{j : target_j >= C_{i-1}} with an incremental integer recurrence; since
 // a_j = max{i : w_i > 0, f_i <= j}, a scatter of i into mark[f_i] followed by an inclusive
 // max-scan yields every ancestor of the batch's outputs with no per-output search, whatever the
-// offspring distribution.
+// offspring distribution. Outputs are then propagated in dense rounds of 1024 (4 consecutive
+// outputs per thread share one Philox block).
 #include "cuppl_device.cuh"
 #include "smc_kernels.cuh"
 
@@ -67,14 +68,12 @@ __device__ __forceinline__ int f2key(float f) {
 }
 __device__ __forceinline__ float key2f(int k) { return __int_as_float(k ^ ((k >> 31) & 0x7FFFFFFF)); }
 
-__device__ __forceinline__ int categorical_u64(const unsigned long long* thr, int K, uint32_t w) {
-  int lo = 0, hi = K - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (static_cast<unsigned long long>(w) < __ldg(thr + mid)) hi = mid;
-    else lo = mid + 1;
-  }
-  return lo;
+// Alias draw (oracle or_alias_draw): column = high word of w K, coin = low word.
+__device__ __forceinline__ int alias_draw(const unsigned long long* tab, int K, uint32_t w) {
+  const unsigned long long p = static_cast<unsigned long long>(w) * static_cast<unsigned>(K);
+  const int col = static_cast<int>(p >> 32);
+  const unsigned long long e = __ldg(tab + col);
+  return (p & 0xFFFFFFFFull) < (e & 0x1FFFFFFFFull) ? col : static_cast<int>(e >> 40);
 }
 
 // ------------------------------------------------------------------ K4: init ------------
@@ -97,7 +96,7 @@ __global__ void __launch_bounds__(kSmcThreads) smc_init_kernel(const __grid_cons
     for (int k = 0; k < 4; ++k) {
       const unsigned long long i = 4 * q + k;
       if (i < a.n_local) {
-        const int s = categorical_u64(m.thr_pi0, m.S, ws[k]);
+        const int s = alias_draw(m.alias_init, m.S, ws[k]);
         const float lw = emission(a.y0, s_mu[s], m.inv_sd, m.c);
         a.x[i] = static_cast<uint8_t>(s);
         a.lw[i] = lw;
@@ -115,13 +114,39 @@ constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagIncl = 2ull << 62;
 constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
-__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Warp-parallel decoupled look-back (Merrill & Garland): every lane inspects one predecessor
+// per round; the window contributes up to the nearest inclusive prefix. Returns the exclusive
+// prefix of `tile` (all lanes).
+__device__ __forceinline__ unsigned long long warp_lookback(const unsigned long long* flags,
+                                                            unsigned long long tile) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long prefix = 0;
+  long long k = static_cast<long long>(tile) - 1;
+  while (k >= 0) {
+    const long long idx = k - lane;
+    const unsigned long long f = idx >= 0 ? ld_relaxed_u64(flags + idx) : kFlagIncl;
+    const unsigned int st = static_cast<unsigned int>(f >> 62);
+    const unsigned int incl = __ballot_sync(0xffffffffu, st == 2u);
+    const int lim = incl ? __ffs(incl) - 1 : 31;  // lanes 0..lim contribute this round
+    const unsigned int lim_mask = lim == 31 ? 0xffffffffu : ((2u << lim) - 1u);
+    if (__ballot_sync(0xffffffffu, st == 0u) & lim_mask) continue;  // a predecessor is still running
+    unsigned long long v = lane <= lim ? (f & kValMask) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    prefix += v;
+    if (incl) break;
+    k -= 32;
+  }
+  return prefix;
 }
 
 template <bool HIST>
@@ -144,34 +169,50 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(SmcScanArgs a) {
   const unsigned long long tile = s_tile;
   const unsigned long long wbase = tile * kTile + static_cast<unsigned long long>(warp) * 1024;
   float s1 = 0.f, s2 = 0.f;
-#pragma unroll 2
+  // all 8 loads of the warp's 1024 particles in flight first
+  float4 v[8];
+  uchar4 xv[8];
+#pragma unroll
   for (int it = 0; it < 8; ++it) {
     const unsigned long long p0 = wbase + it * 128 + lane * 4;
-    float v[4];
-    uint8_t xv[4] = {0, 0, 0, 0};
     if (p0 + 3 < n) {
-      const float4 f = __ldcs(reinterpret_cast<const float4*>(a.lw + p0));
-      v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-      if (HIST) {
-        const uchar4 c = *reinterpret_cast<const uchar4*>(a.x + p0);
-        xv[0] = c.x; xv[1] = c.y; xv[2] = c.z; xv[3] = c.w;
-      }
+      v[it] = __ldcs(reinterpret_cast<const float4*>(a.lw + p0));
+      if (HIST) xv[it] = *reinterpret_cast<const uchar4*>(a.x + p0);
     } else {
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        v[k] = p0 + k < n ? a.lw[p0 + k] : neg_inf_f();
-        if (HIST) xv[k] = p0 + k < n ? a.x[p0 + k] : 0;
+      v[it].x = p0 < n ? a.lw[p0] : neg_inf_f();
+      v[it].y = p0 + 1 < n ? a.lw[p0 + 1] : neg_inf_f();
+      v[it].z = p0 + 2 < n ? a.lw[p0 + 2] : neg_inf_f();
+      v[it].w = p0 + 3 < n ? a.lw[p0 + 3] : neg_inf_f();
+      if (HIST) {
+        xv[it].x = p0 < n ? a.x[p0] : 0;
+        xv[it].y = p0 + 1 < n ? a.x[p0 + 1] : 0;
+        xv[it].z = p0 + 2 < n ? a.x[p0 + 2] : 0;
+        xv[it].w = p0 + 3 < n ? a.x[p0 + 3] : 0;
       }
     }
+  }
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const float vv[4] = {v[it].x, v[it].y, v[it].z, v[it].w};
+    const uint8_t xx[4] = {xv[it].x, xv[it].y, xv[it].z, xv[it].w};
     unsigned long long ws = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float e = smc_e(v[k], M);
+      const float e = smc_e(vv[k], M);
       const uint32_t w = smc_w(e);
       ws += w;
       s1 += e;
       s2 = fmaf(e, e, s2);
-      if (HIST && w) atomicAdd(&shist[xv[k]], static_cast<unsigned long long>(w));
+      if (HIST) {
+        // warp-aggregated histogram: one shared atomic per distinct state in the warp
+        const unsigned int grp = __match_any_sync(0xffffffffu, static_cast<unsigned int>(xx[k]));
+        const unsigned int lo = __reduce_add_sync(grp, w & 0xFFFFu);
+        const unsigned int hi = __reduce_add_sync(grp, w >> 16);
+        if (lane == __ffs(grp) - 1) {
+          const unsigned long long tot = (static_cast<unsigned long long>(hi) << 16) + lo;
+          if (tot) atomicAdd(&shist[xx[k]], tot);
+        }
+      }
     }
     ws += __shfl_xor_sync(0xffffffffu, ws, 1);
     ws += __shfl_xor_sync(0xffffffffu, ws, 2);
@@ -188,29 +229,20 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(SmcScanArgs a) {
   }
   if (lane == 31) wtot[warp] = incl;
   __syncthreads();
-  unsigned long long wpre = 0;
-  for (int w = 0; w < warp; ++w) wpre += wtot[w];
+  unsigned long long wpre = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < kSmcThreads / 32; ++w) {
+    if (w < warp) wpre += wtot[w];
+    agg += wtot[w];
+  }
   incl += wpre;
-  if (tid == 0) {
-    unsigned long long agg = 0;
-    for (int w = 0; w < kSmcThreads / 32; ++w) agg += wtot[w];
-    unsigned long long prefix = 0;
-    if (tile == 0) {
-      st_release_u64(a.flags, kFlagIncl | agg);
-    } else {
-      st_release_u64(a.flags + tile, kFlagAgg | agg);
-      long long k = static_cast<long long>(tile) - 1;
-      while (k >= 0) {
-        const unsigned long long f = ld_volatile_u64(a.flags + k);
-        const unsigned long long st = f >> 62;
-        if (st == 0) continue;  // predecessor not published yet
-        prefix += f & kValMask;
-        if (st == 2) break;
-        --k;
-      }
-      st_release_u64(a.flags + tile, kFlagIncl | (prefix + agg));
+  if (warp == 0) {
+    if (lane == 0) st_relaxed_u64(a.flags + tile, (tile == 0 ? kFlagIncl : kFlagAgg) | agg);
+    const unsigned long long prefix = tile == 0 ? 0ull : warp_lookback(a.flags, tile);
+    if (lane == 0) {
+      if (tile != 0) st_relaxed_u64(a.flags + tile, kFlagIncl | (prefix + agg));
+      s_prefix = prefix;
     }
-    s_prefix = prefix;
   }
   __syncthreads();
   const unsigned long long gs = tile * kTileSegs + tid;
@@ -240,7 +272,7 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(SmcScanArgs a) {
   f1 = block_sum_d(f1, sc);
   f2 = block_sum_d(f2, sc);
   if (tid == 0) {
-    const unsigned long long T = ld_volatile_u64(a.flags + n_tiles - 1) & kValMask;
+    const unsigned long long T = ld_relaxed_u64(a.flags + n_tiles - 1) & kValMask;
     a.rank_rec[0] = T;
     a.rank_rec[1] = static_cast<unsigned long long>(__double_as_longlong(f1));
     a.rank_rec[2] = static_cast<unsigned long long>(__double_as_longlong(f2));
@@ -253,38 +285,39 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(SmcScanArgs a) {
 // ------------------------------------------------------------------ K6: resample --------
 // Comb in integers (D6): with T = Q N + R0 and A = floor(u T / 2^32) = Qa N + Ra,
 // target_j = floor((j 2^32 + u) T / (N 2^32)) = j Q + Qa + floor((j R0 + Ra) / N),
-// where j R0 + Ra < N^2 < 2^64 (N < 2^32).
+// where j R0 + Ra < N^2 < 2^62 (N < 2^31); every per-index quantity fits 32 bits.
 struct Comb {
-  unsigned long long N, Q, R0, Qa, Ra;
-  double invN;
+  unsigned int N, Q, R0, Qa, Ra;
+  double invN, step_inv;  // 1/N, N/T
+  unsigned int u;
 };
 
-// floor(num / N) for num < 2^64: fp64 estimate, exact correction.
+// floor(num / N) for num < 2^62: fp64 estimate, exact correction.
 __device__ __forceinline__ unsigned long long div_n(unsigned long long num, const Comb& cb,
-                                                   unsigned long long* rem) {
-  unsigned long long q = static_cast<unsigned long long>(__dmul_rn(__ull2double_rn(num), cb.invN));
-  long long r = static_cast<long long>(num - q * cb.N);
+                                                   unsigned int* rem) {
+  long long q = static_cast<long long>(__dmul_rn(__ull2double_rn(num), cb.invN));
+  long long r = static_cast<long long>(num) - q * static_cast<long long>(cb.N);
   while (r < 0) {
     --q;
-    r += static_cast<long long>(cb.N);
+    r += cb.N;
   }
   while (r >= static_cast<long long>(cb.N)) {
     ++q;
-    r -= static_cast<long long>(cb.N);
+    r -= cb.N;
   }
-  *rem = static_cast<unsigned long long>(r);
-  return q;
+  *rem = static_cast<unsigned int>(r);
+  return static_cast<unsigned long long>(q);
 }
 
 // Cursor over consecutive targets: (j, target_j, (j R0 + Ra) mod N).
 struct CombCursor {
-  unsigned long long j, tgt, mod;
-  __device__ __forceinline__ void seek(unsigned long long jj, const Comb& cb) {
+  unsigned int j, mod;
+  unsigned long long tgt;
+  __device__ __forceinline__ void seek(unsigned int jj, const Comb& cb) {
     j = jj;
-    unsigned long long r;
-    const unsigned long long q = div_n(jj * cb.R0 + cb.Ra, cb, &r);
-    tgt = jj * cb.Q + cb.Qa + q;
-    mod = r;
+    const unsigned long long q =
+        div_n(static_cast<unsigned long long>(jj) * cb.R0 + cb.Ra, cb, &mod);
+    tgt = static_cast<unsigned long long>(jj) * cb.Q + cb.Qa + q;
   }
   __device__ __forceinline__ void next(const Comb& cb) {
     ++j;
@@ -295,48 +328,42 @@ struct CombCursor {
       ++tgt;
     }
   }
-  // advance to the smallest j' >= j with target_j' >= c (or N); big gaps jump by estimate
-  __device__ __forceinline__ void advance_to(unsigned long long c, const Comb& cb, double step_inv) {
+  // smallest j' >= j with target_j' >= c (N if none); long gaps re-seek from an estimate
+  __device__ __forceinline__ void advance_to(unsigned long long c, const Comb& cb) {
     if (j >= cb.N || tgt >= c) return;
-    const unsigned long long gap = c - tgt;
-    if (gap > 8 * (cb.Q + 1)) {
-      // estimate j' ~ j + gap N / T, then settle exactly from below
-      double est = __dmul_rn(__ull2double_rn(gap), step_inv);
-      unsigned long long jj = j + (est > 2.0 ? static_cast<unsigned long long>(est) - 2 : 0);
-      if (jj > cb.N) jj = cb.N;
+    if (c - tgt > 4ull * cb.Q + 4ull) {
+      // target_j ~ (j + u/2^32) T / N  =>  j ~ c N / T - u / 2^32 (error << 1)
+      const double e = __dmul_rn(__ull2double_rn(c), cb.step_inv) - 2.0;
+      const unsigned int jj = e <= static_cast<double>(j) ? j
+                             : e >= static_cast<double>(cb.N) ? cb.N - 1
+                                                              : static_cast<unsigned int>(e);
       if (jj > j) {
         seek(jj, cb);
-        // seek may overshoot only if the estimate was too large: back off exponentially
-        unsigned long long back = 1;
-        while (j > 0 && tgt >= c) {
-          const unsigned long long jn = j > back ? j - back : 0;
-          seek(jn, cb);
-          back <<= 1;
-        }
+        while (j > 0 && tgt >= c) seek(j - 1, cb);  // never taken unless the estimate was high
       }
     }
     while (j < cb.N && tgt < c) next(cb);
   }
 };
 
-__device__ __forceinline__ unsigned long long comb_target(unsigned long long j, const Comb& cb) {
-  unsigned long long r;
-  return j * cb.Q + cb.Qa + div_n(j * cb.R0 + cb.Ra, cb, &r);
+__device__ __forceinline__ unsigned long long comb_target(unsigned int j, const Comb& cb) {
+  CombCursor c;
+  c.seek(j, cb);
+  return c.tgt;
 }
 
 // smallest j in [0, N] with target_j >= c (N if none)
-__device__ unsigned long long first_j_at_least(unsigned long long c, const Comb& cb,
-                                               double step_inv) {
+__device__ __forceinline__ unsigned int first_j_at_least(unsigned long long c, const Comb& cb) {
   CombCursor cur;
   cur.seek(0, cb);
-  cur.advance_to(c, cb, step_inv);
+  cur.advance_to(c, cb);
   return cur.j;
 }
 
 // Warp-cooperative rank-local upper bound: smallest local i with C_i > t (C = inclusive scan
 // of the rank's weights, represented by segoff + the lw of one segment). Returns n_local if none.
-// The segment is found with a 33-way search (5 rounds of one coalesced-ish probe per lane for
-// 3e6 segments), then resolved inside the segment with a warp scan of its 32 weights.
+// The segment is found with a 33-ary search (5 rounds for 3e6 segments), then resolved inside
+// the segment with a warp scan of its 32 weights.
 __device__ unsigned long long warp_upper_bound(unsigned long long t, const SmcResampleArgs& a,
                                                float M) {
   const int lane = threadIdx.x & 31;
@@ -376,18 +403,21 @@ __device__ unsigned long long warp_upper_bound(unsigned long long t, const SmcRe
   return s * kSegment + (__ffs(bal) - 1);
 }
 
-__global__ void __launch_bounds__(kSmcThreads) smc_resample_kernel(const __grid_constant__ SmcModel m,
-                                                                   SmcResampleArgs a) {
+template <bool MULTI>
+__global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __grid_constant__ SmcModel m,
+                                                                      SmcResampleArgs a) {
   __shared__ unsigned int mark[kChunk];
   __shared__ uint8_t xs[kBatch];
   __shared__ unsigned long long wsum[kSmcThreads / 32];
   __shared__ unsigned int wmax[kSmcThreads / 32];
   __shared__ unsigned int s_carry;
   __shared__ unsigned long long s_u64[4];
-  __shared__ unsigned long long s_rank_begin[kMaxRanks + 1];
+  __shared__ unsigned long long s_rank_begin[MULTI ? kMaxRanks + 1 : 1];
   __shared__ float s_mu[kMaxStates];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int q = tid; q < m.S; q += kSmcThreads) s_mu[q] = m.mu[q];
+  if (MULTI)
+    for (int q = tid; q <= a.world; q += kSmcThreads) s_rank_begin[q] = a.rank_begin[q];
 
   // step constants (identical on every rank)
   unsigned long long T = 0, O = 0;
@@ -397,7 +427,6 @@ __global__ void __launch_bounds__(kSmcThreads) smc_resample_kernel(const __grid_
     T += Tq;
   }
   const unsigned long long Tr = a.rank_recs[4 * a.rank];
-  for (int q = tid; q <= a.world; q += kSmcThreads) s_rank_begin[q] = a.rank_begin[q];
   // clear the look-back words for the next scan
   for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(kSmcThreads) + tid;
        i < a.n_tiles; i += static_cast<unsigned long long>(gridDim.x) * kSmcThreads)
@@ -405,21 +434,21 @@ __global__ void __launch_bounds__(kSmcThreads) smc_resample_kernel(const __grid_
   if (T == 0) return;  // all weights zero: the host raises AllZeroWeightError
   const float M = key2f(*a.m_key);
   const PhiloxKey key = make_key(a.key);
-  const uint32_t u = draw_block(key, a.t, 0u, CUPPL_TAG_SMC_COMB).x;
   Comb cb;
-  cb.N = a.n_total;
-  cb.Q = T / cb.N;
-  cb.R0 = T % cb.N;
-  const unsigned long long A = __umul64hi(static_cast<unsigned long long>(u) << 32, T);  // floor(u T / 2^32)
-  cb.Qa = A / cb.N;
-  cb.Ra = A % cb.N;
+  cb.u = draw_block(key, a.t, 0u, CUPPL_TAG_SMC_COMB).x;
+  cb.N = static_cast<unsigned int>(a.n_total);
+  cb.Q = static_cast<unsigned int>(T / cb.N);
+  cb.R0 = static_cast<unsigned int>(T % cb.N);
+  const unsigned long long A = __umul64hi(static_cast<unsigned long long>(cb.u) << 32, T);  // floor(u T / 2^32)
+  cb.Qa = static_cast<unsigned int>(A / cb.N);
+  cb.Ra = static_cast<unsigned int>(A % cb.N);
   cb.invN = 1.0 / static_cast<double>(cb.N);
-  const double step_inv = static_cast<double>(cb.N) / static_cast<double>(T);
+  cb.step_inv = static_cast<double>(cb.N) / static_cast<double>(T);
 
   // this rank's outputs: J_r = {j : O <= target_j < O + Tr}; this CTA's even share of it
   if (tid == 0) {
-    s_u64[0] = a.rank == 0 ? 0ull : first_j_at_least(O, cb, step_inv);
-    s_u64[1] = a.rank == a.world - 1 ? cb.N : first_j_at_least(O + Tr, cb, step_inv);
+    s_u64[0] = a.rank == 0 ? 0ull : first_j_at_least(O, cb);
+    s_u64[1] = a.rank == a.world - 1 ? cb.N : first_j_at_least(O + Tr, cb);
   }
   __syncthreads();
   const unsigned long long jr_lo = s_u64[0], jr_hi = s_u64[1];
@@ -430,7 +459,7 @@ __global__ void __launch_bounds__(kSmcThreads) smc_resample_kernel(const __grid_
 
   // ancestor of the first output -> first batch starts at its segment boundary
   if (warp == 0) {
-    const unsigned long long tl = comb_target(jb_lo, cb) - O;
+    const unsigned long long tl = comb_target(static_cast<unsigned int>(jb_lo), cb) - O;
     const unsigned long long i0 = warp_upper_bound(tl, a, M);
     if (lane == 0) s_u64[2] = i0;
   }
@@ -439,6 +468,7 @@ __global__ void __launch_bounds__(kSmcThreads) smc_resample_kernel(const __grid_
   unsigned long long c_base = batch_base > 0 ? a.segoff[batch_base / kSegment - 1] : 0ull;
   unsigned long long j_cur = jb_lo;
   float bmax = neg_inf_f();
+  const unsigned int S = static_cast<unsigned int>(m.S);
 
   while (j_cur < jb_hi && batch_base < a.n_local) {
     // ---- stage 2048 sources: thread tid owns [batch_base + 8 tid, +8)
@@ -448,7 +478,7 @@ __global__ void __launch_bounds__(kSmcThreads) smc_resample_kernel(const __grid_
     if (i0 + kBatchPerThread <= a.n_local) {
       const float4 f0 = __ldcs(reinterpret_cast<const float4*>(a.lw + i0));
       const float4 f1 = __ldcs(reinterpret_cast<const float4*>(a.lw + i0) + 1);
-      const uint2 xx = *reinterpret_cast<const uint2*>(a.x + i0);
+      const uint2 xx = __ldcs(reinterpret_cast<const uint2*>(a.x + i0));
       const float v[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
 #pragma unroll
       for (int k = 0; k < kBatchPerThread; ++k) {
@@ -475,29 +505,26 @@ __global__ void __launch_bounds__(kSmcThreads) smc_resample_kernel(const __grid_
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
     unsigned long long wpre = 0, btot = 0;
+#pragma unroll
     for (int q = 0; q < kSmcThreads / 32; ++q) {
       if (q < warp) wpre += wsum[q];
       btot += wsum[q];
     }
-    const unsigned long long texcl = c_base + wpre + incl - tw;  // C_{i0 - 1} (local)
     // f_k for each positive-weight source (global target units), monotone per thread
-    unsigned long long f[kBatchPerThread];
+    unsigned int f[kBatchPerThread];
     {
       CombCursor cur;
       bool init = false;
-      unsigned long long c = texcl;
+      unsigned long long c = c_base + wpre + incl - tw;  // C_{i0 - 1} (local)
 #pragma unroll
       for (int k = 0; k < kBatchPerThread; ++k) {
-        f[k] = ~0ull;
+        f[k] = 0xFFFFFFFFu;
         if (w[k]) {
           if (!init) {
-            const unsigned long long jg = O + c == 0 ? 0 : first_j_at_least(O + c, cb, step_inv);
-            cur.seek(jg < cb.N ? jg : cb.N - 1, cb);
-            if (jg >= cb.N) cur.j = cb.N;
+            cur.seek(0, cb);
             init = true;
-          } else {
-            cur.advance_to(O + c, cb, step_inv);
           }
+          cur.advance_to(O + c, cb);
           f[k] = cur.j;
         }
         c += w[k];
@@ -506,35 +533,32 @@ __global__ void __launch_bounds__(kSmcThreads) smc_resample_kernel(const __grid_
     // outputs whose ancestors lie in this batch: [j_cur, j_next)
     if (tid == kSmcThreads - 1) {
       const unsigned long long c_end = c_base + btot;
-      unsigned long long jn = c_end >= Tr ? jb_hi : first_j_at_least(O + c_end, cb, step_inv);
+      const unsigned long long jn = c_end >= Tr ? jb_hi : first_j_at_least(O + c_end, cb);
       s_u64[3] = jn < jb_hi ? jn : jb_hi;
     }
     __syncthreads();
     const unsigned long long j_next = s_u64[3];
 
     for (unsigned long long j0 = j_cur; j0 < j_next;) {
-      const unsigned long long jbase = (j0 / kChunk) * kChunk;
+      const unsigned long long jbase = j0 & ~3ull;  // Philox blocks cover 4 outputs
       const unsigned long long j1 = jbase + kChunk < j_next ? jbase + kChunk : j_next;
 #pragma unroll
-      for (int k = 0; k < kOutPerThread; ++k) mark[kOutPerThread * tid + k] = 0u;
+      for (int k = 0; k < kChunk / kSmcThreads; ++k) mark[k * kSmcThreads + tid] = 0u;
       if (tid == 0) s_carry = 0u;
       __syncthreads();
 #pragma unroll
       for (int k = 0; k < kBatchPerThread; ++k) {
-        if (f[k] == ~0ull) continue;
+        if (f[k] == 0xFFFFFFFFu) continue;
         const unsigned int rel = kBatchPerThread * tid + k + 1;  // +1: 0 means "none"
         if (f[k] <= j0) atomicMax(&s_carry, rel);
         else if (f[k] < j1) atomicMax(&mark[f[k] - jbase], rel);
       }
       __syncthreads();
-      // inclusive max-scan over this thread's 8 marks, then across threads
-      unsigned int run[kOutPerThread];
+      // inclusive max-scan over mark[0, kChunk): thread tid owns kScanPer consecutive entries
+      constexpr int kScanPer = kChunk / kSmcThreads;
       unsigned int tm = 0;
 #pragma unroll
-      for (int k = 0; k < kOutPerThread; ++k) {
-        tm = max(tm, mark[kOutPerThread * tid + k]);
-        run[k] = tm;
-      }
+      for (int k = 0; k < kScanPer; ++k) tm = max(tm, mark[kScanPer * tid + k]);
       unsigned int im = tm;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -547,73 +571,76 @@ __global__ void __launch_bounds__(kSmcThreads) smc_resample_kernel(const __grid_
       for (int q = 0; q < warp; ++q) carry = max(carry, wmax[q]);
       const unsigned int prev = __shfl_up_sync(0xffffffffu, im, 1);
       if (lane > 0) carry = max(carry, prev);
-      // propagate my outputs
-      const unsigned long long jt = jbase + kOutPerThread * tid;
-      uint8_t xo[kOutPerThread];
-      float lo[kOutPerThread];
-      bool any = false, all = true;
 #pragma unroll
-      for (int h = 0; h < kOutPerThread / 4; ++h) {
-        const unsigned long long jq = jt + 4 * h;
-        const bool need = jq + 3 >= j0 && jq < j1;
-        uint4 wd = make_uint4(0, 0, 0, 0);
-        if (need) wd = draw_block(key, jq >> 2, a.t + 1, CUPPL_TAG_SMC_STEP);
+      for (int k = 0; k < kScanPer; ++k) {
+        carry = max(carry, mark[kScanPer * tid + k]);
+        mark[kScanPer * tid + k] = carry;  // now the ancestor (+1) of output jbase + index
+      }
+      __syncthreads();
+      // propagate in dense rounds of 1024 outputs: thread tid takes 4 consecutive outputs
+      for (unsigned long long jr = jbase; jr < j1; jr += 4 * kSmcThreads) {
+        const unsigned long long jq = jr + 4 * tid;
+        if (jq + 3 < j0 || jq >= j1) continue;
+        const uint4 wd = draw_block(key, jq >> 2, a.t + 1, CUPPL_TAG_SMC_STEP);
         const uint32_t wv[4] = {wd.x, wd.y, wd.z, wd.w};
+        uint8_t xo[4];
+        float lo[4];
+        bool all = true;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const int kk = 4 * h + k;
           const unsigned long long j = jq + k;
-          const bool valid = j >= j0 && j < j1;
-          xo[kk] = 0;
-          lo[kk] = 0.f;
-          if (valid) {
-            const unsigned int anc = max(carry, run[kk]) - 1;  // relative to batch_base
+          xo[k] = 0;
+          lo[k] = 0.f;
+          if (j >= j0 && j < j1) {
+            const unsigned int anc = mark[j - jbase] - 1;  // relative to batch_base
             const int xa = xs[anc];
-            const int s = categorical_u64(m.thrA + static_cast<size_t>(xa) * (m.S - 1), m.S, wv[k]);
+            const int s = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[k]);
             const float l = emission(a.y_next, s_mu[s], m.inv_sd, m.c);
-            xo[kk] = static_cast<uint8_t>(s);
-            lo[kk] = l;
+            xo[k] = static_cast<uint8_t>(s);
+            lo[k] = l;
             bmax = fmaxf(bmax, l);
             if (a.anc_out) {
               int q = 0;
-              while (q + 1 < a.world && s_rank_begin[q + 1] <= j) ++q;
-              a.anc_out[q][j - s_rank_begin[q]] = s_rank_begin[a.rank] + batch_base + anc;
+              if (MULTI)
+                while (q + 1 < a.world && s_rank_begin[q + 1] <= j) ++q;
+              const unsigned long long rb = MULTI ? s_rank_begin[q] : 0ull;
+              const unsigned long long my = MULTI ? s_rank_begin[a.rank] : 0ull;
+              a.anc_out[q][j - rb] = my + batch_base + anc;
             }
-            any = true;
           } else {
             all = false;
           }
         }
-      }
-      if (any) {
-        // owner rank of the first output of the run (ranks own contiguous index ranges)
         int q = 0;
-        const unsigned long long jfirst = jt > j0 ? jt : j0;
-        while (q + 1 < a.world && s_rank_begin[q + 1] <= jfirst) ++q;
-        const unsigned long long dest = jt - s_rank_begin[q];
-        const bool same_owner = q + 1 >= a.world || s_rank_begin[q + 1] >= jt + kOutPerThread;
-        if (all && same_owner && (dest % kOutPerThread) == 0 && jt >= s_rank_begin[q]) {
-          uint2 packed;
-          packed.x = xo[0] | (xo[1] << 8) | (xo[2] << 16) | (static_cast<uint32_t>(xo[3]) << 24);
-          packed.y = xo[4] | (xo[5] << 8) | (xo[6] << 16) | (static_cast<uint32_t>(xo[7]) << 24);
-          *reinterpret_cast<uint2*>(a.x_out[q] + dest) = packed;
-          float4* lp = reinterpret_cast<float4*>(a.lw_out[q] + dest);
-          __stcs(lp, make_float4(lo[0], lo[1], lo[2], lo[3]));
-          __stcs(lp + 1, make_float4(lo[4], lo[5], lo[6], lo[7]));
+        unsigned long long rb = 0;
+        bool same = true;
+        if (MULTI) {
+          const unsigned long long jf = jq > j0 ? jq : j0;
+          while (q + 1 < a.world && s_rank_begin[q + 1] <= jf) ++q;
+          rb = s_rank_begin[q];
+          same = q + 1 >= a.world || s_rank_begin[q + 1] >= jq + 4;
+        }
+        const unsigned long long dest = jq - rb;
+        if (all && same && jq >= rb && (dest & 3) == 0) {
+          const uint32_t packed = xo[0] | (xo[1] << 8) | (xo[2] << 16) | (static_cast<uint32_t>(xo[3]) << 24);
+          *reinterpret_cast<uint32_t*>(a.x_out[q] + dest) = packed;
+          __stcs(reinterpret_cast<float4*>(a.lw_out[q] + dest), make_float4(lo[0], lo[1], lo[2], lo[3]));
         } else {
 #pragma unroll
-          for (int k = 0; k < kOutPerThread; ++k) {
-            const unsigned long long j = jt + k;
+          for (int k = 0; k < 4; ++k) {
+            const unsigned long long j = jq + k;
             if (j >= j0 && j < j1) {
               int qq = 0;
-              while (qq + 1 < a.world && s_rank_begin[qq + 1] <= j) ++qq;
-              a.x_out[qq][j - s_rank_begin[qq]] = xo[k];
-              a.lw_out[qq][j - s_rank_begin[qq]] = lo[k];
+              if (MULTI)
+                while (qq + 1 < a.world && s_rank_begin[qq + 1] <= j) ++qq;
+              const unsigned long long rbb = MULTI ? s_rank_begin[qq] : 0ull;
+              a.x_out[qq][j - rbb] = xo[k];
+              a.lw_out[qq][j - rbb] = lo[k];
             }
           }
         }
       }
-      __syncthreads();  // mark / wmax reuse
+      __syncthreads();  // mark reuse
       j0 = j1;
     }
     j_cur = j_next;
@@ -647,18 +674,25 @@ cudaError_t launch_smc_scan(const SmcScanArgs& a, int sm_count, cudaStream_t st)
   return cudaGetLastError();
 }
 
-cudaError_t launch_smc_resample(const SmcModel& m, const SmcResampleArgs& a, int sm_count,
-                                cudaStream_t st) {
+template <bool MULTI>
+static cudaError_t launch_resample_t(const SmcModel& m, const SmcResampleArgs& a, int sm_count,
+                                     cudaStream_t st) {
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, smc_resample_kernel,
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, smc_resample_kernel<MULTI>,
                                                                 kSmcThreads, 0);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   unsigned long long g = static_cast<unsigned long long>(sm_count) * per_sm;
-  const unsigned long long want = (a.n_local + kBatch - 1) / kBatch;  // ~ one batch per CTA minimum
+  const unsigned long long want = (a.n_local + kBatch - 1) / kBatch;  // >= one batch per CTA
   if (g > want) g = want > 0 ? want : 1;
-  smc_resample_kernel<<<static_cast<unsigned>(g), kSmcThreads, 0, st>>>(m, a);
+  smc_resample_kernel<MULTI><<<static_cast<unsigned>(g), kSmcThreads, 0, st>>>(m, a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_smc_resample(const SmcModel& m, const SmcResampleArgs& a, int sm_count,
+                                cudaStream_t st) {
+  return a.world > 1 ? launch_resample_t<true>(m, a, sm_count, st)
+                     : launch_resample_t<false>(m, a, sm_count, st);
 }
 
 }  // namespace cuppl

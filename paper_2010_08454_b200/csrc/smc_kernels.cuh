@@ -12,7 +12,7 @@ constexpr int kTileSegs = 256;                // segments per K5 tile (one per t
 constexpr int kTile = kTileSegs * kSegment;   // 8192 particles per scan tile
 constexpr int kBatchPerThread = 8;            // sources per thread per K6 batch
 constexpr int kBatch = kSmcThreads * kBatchPerThread;  // 2048 sources per K6 batch
-constexpr int kOutPerThread = 8;              // outputs per thread per K6 sub-chunk
+constexpr int kOutPerThread = 16;             // ancestor slots per thread per K6 sub-chunk
 constexpr int kChunk = kSmcThreads * kOutPerThread;    // 2048 outputs per sub-chunk
 constexpr int kMaxStates = 256;               // particle state stored as u8
 constexpr int kMaxRanks = 64;
@@ -23,8 +23,8 @@ struct SmcModel {
   float inv_sd;  // 1 / sd of the Gaussian emission
   float c;       // -ln sd - 0.5 ln 2 pi
   int pad_;
-  const unsigned long long* thrA;     // [S][S-1] inverse-CDF thresholds of the rows of A
-  const unsigned long long* thr_pi0;  // [S-1] thresholds of pi0
+  const unsigned long long* alias_trans;  // [S][S] alias tables of the rows of A (thr | alias << 40)
+  const unsigned long long* alias_init;   // [S] alias table of pi0
   float mu[kMaxStates];               // emission means
 };
 

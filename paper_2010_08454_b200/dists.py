@@ -71,6 +71,39 @@ def categorical_thresholds(weights) -> list[int]:
     return out
 
 
+def alias_table(weights) -> list[int]:
+    """Walker / Vose alias table with exact integer masses (used by the SMC kernels).
+
+    Column k keeps k when the coin (low 32 bits of w*K for a u32 word w; the column is the high
+    32 bits) is below thr_k in [0, 2^32], else yields alias_k; entries are thr | alias << 40.
+    Masses m_k = floor(w_k / W * K * 2^32) sum to K * 2^32 after adding the rounding deficit to
+    the first largest m_k; small / large stacks are popped LIFO in index order (the oracle's
+    or_alias_build restates this exactly).
+    """
+    K = len(weights)
+    unit = 1 << 32
+    total = 0.0
+    for v in weights:
+        total += v
+    m = [int(math.floor(float(v) / total * K * 4294967296.0)) for v in weights]
+    kmax = 0
+    for k in range(K):
+        if m[k] > m[kmax]:
+            kmax = k
+    m[kmax] += K * unit - sum(m)
+    small = [k for k in range(K) if m[k] < unit]
+    large = [k for k in range(K) if m[k] >= unit]
+    thr, alias = [0] * K, [0] * K
+    while small and large:
+        s, lg = small.pop(), large.pop()
+        thr[s], alias[s] = m[s], lg
+        m[lg] -= unit - m[s]
+        (small if m[lg] < unit else large).append(lg)
+    for k in large + small:
+        thr[k], alias[k] = unit, k
+    return [thr[k] | (alias[k] << 40) for k in range(K)]
+
+
 def variance(d: DistValue) -> float:
     """dist-var (SPEC.md:321-329)."""
     t = d.tag

@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from .dists import categorical_thresholds
+from .dists import alias_table
 from .errors import AllZeroWeightError, InferRuntimeError
 from .models import HiddenMarkovModel
 from .rng import key_of, seed_of
@@ -120,19 +120,19 @@ class SmcRunner:
             raise InferRuntimeError("multi-process SMC needs peer-mapped buffers (not available yet)")
         self.bounds = rank_boundaries(self.N, self.world)
         S = model.n_states
-        thrA = np.array([categorical_thresholds(list(model.A[s])) for s in range(S)], dtype=np.uint64)
-        thr0 = np.array(categorical_thresholds(list(model.pi0)), dtype=np.uint64)
+        aliasA = np.array([alias_table(list(model.A[s])) for s in range(S)], dtype=np.uint64)
+        alias0 = np.array(alias_table(list(model.pi0)), dtype=np.uint64)
         dev = self.device
-        self.thrA = torch.tensor(thrA.reshape(-1).view(np.int64), device=dev)
-        self.thr0 = torch.tensor(thr0.view(np.int64) if len(thr0) else np.zeros(1, np.int64), device=dev)
+        self.aliasA = torch.tensor(aliasA.reshape(-1).view(np.int64), device=dev)
+        self.alias0 = torch.tensor(alias0.view(np.int64), device=dev)
         self.mu = np.ascontiguousarray(model.mu, dtype=np.float32)
         sd = float(model.sd)
         self.cm = N.SmcModel()
         self.cm.n_states = S
         self.cm.inv_sd = float(np.float32(1.0 / sd))
         self.cm.c = float(np.float32(-math.log(sd) - 0.5 * math.log(2 * math.pi)))
-        self.cm.thr_trans = self.thrA.data_ptr()
-        self.cm.thr_init = self.thr0.data_ptr()
+        self.cm.alias_trans = self.aliasA.data_ptr()
+        self.cm.alias_init = self.alias0.data_ptr()
         self.cm.mu = self.mu.ctypes.data
         self.ys = np.ascontiguousarray(model.ys, dtype=np.float32)
         self.hist_steps = sorted(set(hist_steps if hist_steps is not None else [self.T - 1]))

@@ -246,3 +246,61 @@ def test_oracle_rank_partition_invariance(oracle_lib):
         assert got["max_lw"] == full["max_lw"]
         assert got["sum_w"] == pytest.approx(full["sum_w"], rel=1e-12)
         assert np.allclose(got["bin_w"], full["bin_w"], rtol=1e-12)
+
+
+def test_alias_tables_match_and_are_exact(oracle_lib):
+    """Product (dists.alias_table) and oracle (or_alias_build) build identical tables whose
+    integer column masses reproduce the categorical probabilities to 2^-32."""
+    from oracle import core
+    from paper_2010_08454_b200 import dists
+
+    rs = np.random.default_rng(0)
+    unit = 1 << 32
+    for K in (1, 2, 3, 5, 50, 256):
+        for _ in range(10):
+            w = rs.random(K) ** 3
+            w[rs.random(K) < 0.2] = 0
+            if w.sum() == 0:
+                w[0] = 1
+            a = core.alias_table(w)
+            assert np.array_equal(a, np.array(dists.alias_table(list(w)), dtype=np.uint64))
+            p = np.zeros(K)
+            for col in range(K):
+                thr, al = int(a[col]) & 0x1FFFFFFFF, int(a[col]) >> 40
+                p[col] += thr / unit / K
+                p[al] += (unit - thr) / unit / K
+            assert np.allclose(p, w / w.sum(), atol=1e-8)
+            assert all(p[k] == 0 for k in range(K) if w[k] == 0)
+
+
+def test_comb_target_decomposition():
+    """The kernels' u64 decomposition of the D6 comb equals the 128-bit definition."""
+    from oracle import core
+
+    L = core.lib()
+    core._smc_sig(L)
+    rs = np.random.default_rng(1)
+    for _ in range(200):
+        N = int(rs.integers(8, 2**31 - 1))
+        T = int(rs.integers(1, N)) * int(rs.integers(1, 2**31))
+        u = int(rs.integers(0, 2**32))
+        Q, R0 = divmod(T, N)
+        Qa, Ra = divmod((u * T) >> 32, N)
+        for j in [0, 1, N // 3, N - 1] + list(rs.integers(0, N, 5)):
+            j = int(j)
+            want = ((j << 32) + u) * T // (N << 32)
+            assert L.or_comb_target(j, u, T, N) == want
+            assert j * Q + Qa + (j * R0 + Ra) // N == want
+            assert 0 <= want < T
+
+
+def test_smc_oracle_matches_forward_algorithm(oracle_lib):
+    from oracle import core, exact
+    from paper_2010_08454_b200 import models
+
+    m = models.HiddenMarkovModel.synthetic(S=50, T=40)
+    lz, filt = exact.hmm_forward(m.A, m.pi0, m.mu.astype(float), m.sd, m.ys.astype(float))
+    r = core.smc_run(m, 200_000, 99)
+    assert abs(r["log_z"] - lz) < 0.3
+    h = r["hist"][39]
+    assert np.abs(h / h.sum() - filt[39]).sum() < 0.05
