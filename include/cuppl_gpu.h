@@ -174,9 +174,10 @@ CUPPL_API int cuppl_smc_init(const cuppl_smc_model* m, uint64_t n_local, uint64_
                              uint64_t key, float y0, uint8_t* x, float* lw, int32_t* m_key,
                              void* workspace, size_t workspace_bytes, void* stream);
 
-/* Statistics and weight scan of population t (K5): quantised weights against max *m_key,
- * rank-local segment offsets into the workspace, rank_rec[4] = {T_r, bits(sum e),
- * bits(sum e^2), 0}; hist[S] (optional, zeroed by the caller) += integer weights per state. */
+/* Weight scan of population t (K5): quantised weights against max *m_key, segment offsets
+ * and tile prefixes (single-pass decoupled look-back) into the workspace, rank_rec[0] = T_r
+ * (integer weight total of this rank; rank_rec[1..3] untouched); hist[S] (optional, zeroed by
+ * the caller) += integer weights per state. */
 CUPPL_API int cuppl_smc_scan(uint64_t n_local, const float* lw, const uint8_t* x,
                              const int32_t* m_key, int n_states, uint64_t* hist,
                              uint64_t* rank_rec, void* workspace, size_t workspace_bytes,
@@ -187,14 +188,20 @@ CUPPL_API int cuppl_smc_scan(uint64_t n_local, const float* lw, const uint8_t* x
  * of each rank's first particle (multiples of 8); x_out / lw_out / anc_out: device arrays of
  * `world` destination pointers (peer-mapped for other ranks; anc_out NULL to skip). The
  * outputs whose ancestors live on this rank are written to their owners; *m_key_next gets the
- * atomicMax of the new log-weights written here. */
+ * atomicMax of the new log-weights written here; stats_out[2] (device doubles) receives this
+ * rank's (sum exp(lw - M), sum exp(2 (lw - M))) of population t, folded in fixed order. */
 CUPPL_API int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_total,
                                  uint64_t key, uint32_t t, int rank, int world, float y_next,
                                  const float* lw, const uint8_t* x, const int32_t* m_key,
                                  const uint64_t* rank_recs, const uint64_t* rank_begin,
                                  uint8_t* const* x_out, float* const* lw_out,
-                                 uint64_t* const* anc_out, int32_t* m_key_next, void* workspace,
-                                 size_t workspace_bytes, void* stream);
+                                 uint64_t* const* anc_out, int32_t* m_key_next, double* stats_out,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* Statistics of a population that is not resampled (the last step): stats_out[2] as in
+ * cuppl_smc_resample, from the per-tile sums of the preceding cuppl_smc_scan. */
+CUPPL_API int cuppl_smc_fold(uint64_t n_local, double* stats_out, void* workspace,
+                             size_t workspace_bytes, void* stream);
 
 /* ---- roofline calibration ---------------------------------------------------------- */
 /* Pipe-rate microbenchmark, blocks x 256 threads, each thread runs `iters` iterations of:

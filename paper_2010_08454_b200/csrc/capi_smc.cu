@@ -11,6 +11,7 @@ using namespace cuppl;
 namespace {
 struct SmcWs {
   unsigned long long* segoff;
+  unsigned long long* tile_prefix;
   unsigned long long* flags;
   unsigned int* counters;
   double* tile_s;
@@ -33,11 +34,14 @@ size_t ws_layout(uint64_t n, SmcWs* w, void* base) {
   off = align256(off + n_segs * 8);
   const size_t tiles_off = off;
   off = align256(off + n_tiles * 16);
+  const size_t prefix_off = off;
+  off = align256(off + n_tiles * 8);
   if (w) {
     w->flags = reinterpret_cast<unsigned long long*>(p + flags_off);
     w->counters = reinterpret_cast<unsigned int*>(p + counters_off);
     w->segoff = reinterpret_cast<unsigned long long*>(p + segoff_off);
     w->tile_s = reinterpret_cast<double*>(p + tiles_off);
+    w->tile_prefix = reinterpret_cast<unsigned long long*>(p + prefix_off);
     w->zero_bytes = zero_end;
   }
   return off;
@@ -116,6 +120,7 @@ int cuppl_smc_scan(uint64_t n_local, const float* lw, const uint8_t* x, const in
   a.x = x;
   a.m_key = m_key;
   a.segoff = w.segoff;
+  a.tile_prefix = w.tile_prefix;
   a.flags = w.flags;
   a.counters = w.counters;
   a.tile_s = w.tile_s;
@@ -129,8 +134,8 @@ int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_to
                        uint32_t t, int rank, int world, float y_next, const float* lw,
                        const uint8_t* x, const int32_t* m_key, const uint64_t* rank_recs,
                        const uint64_t* rank_begin, uint8_t* const* x_out, float* const* lw_out,
-                       uint64_t* const* anc_out, int32_t* m_key_next, void* workspace,
-                       size_t workspace_bytes, void* stream) {
+                       uint64_t* const* anc_out, int32_t* m_key_next, double* stats_out,
+                       void* workspace, size_t workspace_bytes, void* stream) {
   SmcModel sm;
   if (int s = fill_model(m, &sm)) return s;
   SmcWs w;
@@ -138,7 +143,7 @@ int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_to
   if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
     return set_error(CUPPL_E_ARGUMENT, "rank %d / world %d", rank, world);
   if (n_total < n_local || n_total >= (1ull << 32)) return set_error(CUPPL_E_CAPACITY, "n_total");
-  if (!lw || !x || !m_key || !rank_recs || !rank_begin || !x_out || !lw_out || !m_key_next)
+  if (!lw || !x || !m_key || !rank_recs || !rank_begin || !x_out || !lw_out || !m_key_next || !stats_out)
     return set_error(CUPPL_E_ARGUMENT, "NULL buffer");
   int sms = 0;
   if (int s = device_sm_count(&sms)) return s;
@@ -155,6 +160,10 @@ int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_to
   a.x = x;
   a.m_key = m_key;
   a.segoff = w.segoff;
+  a.tile_prefix = w.tile_prefix;
+  a.tile_s = w.tile_s;
+  a.stats_out = reinterpret_cast<double*>(stats_out);
+  a.counters = w.counters;
   a.rank_recs = reinterpret_cast<const unsigned long long*>(rank_recs);
   a.rank_begin = reinterpret_cast<const unsigned long long*>(rank_begin);
   a.x_out = x_out;
@@ -165,6 +174,16 @@ int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_to
   a.n_tiles = (n_local + kTile - 1) / kTile;
   return cuda_status(launch_smc_resample(sm, a, sms, static_cast<cudaStream_t>(stream)),
                      "smc_resample");
+}
+
+int cuppl_smc_fold(uint64_t n_local, double* stats_out, void* workspace, size_t workspace_bytes,
+                   void* stream) {
+  SmcWs w;
+  if (int s = check_ws(n_local, workspace, workspace_bytes, &w)) return s;
+  if (!stats_out) return set_error(CUPPL_E_ARGUMENT, "NULL buffer");
+  return cuda_status(launch_smc_fold(w.tile_s, (n_local + kTile - 1) / kTile, stats_out, w.counters,
+                                     static_cast<cudaStream_t>(stream)),
+                     "smc_fold");
 }
 
 }  // extern "C"

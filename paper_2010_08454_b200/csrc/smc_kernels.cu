@@ -16,13 +16,13 @@
 // 1 + 4 (K6 writes x', lw') = 14 B per particle (+0.25 B of segment offsets each way).
 //
 // K6 is output-balanced and source-streaming: CTA b owns an even share of the rank's output
-// range, finds the ancestor of its first output once (warp-parallel 33-ary search on segoff),
-// then streams its sources in order in batches of 2048. For each staged source with w_i > 0 it
-// computes f_i = min{j : target_j >= C_{i-1}} with an incremental integer recurrence; since
-// a_j = max{i : w_i > 0, f_i <= j}, a scatter of i into mark[f_i] followed by an inclusive
-// max-scan yields every ancestor of the batch's outputs with no per-output search, whatever the
-// offspring distribution. Outputs are then propagated in dense rounds of 1024 (4 consecutive
-// outputs per thread share one Philox block).
+// range, finds the ancestor of its first output once (warp-parallel 33-ary search over the
+// segment prefixes), then streams its sources in order in batches of 2048. Source i's children
+// are exactly the outputs [F(C_{i-1}), F(C_i)) with F(c) = min{j : target_j >= c}, which an
+// incremental integer cursor evaluates in O(1) amortised per source; each source writes its
+// state into its children's slots (long runs are filled by the whole CTA), so no per-output
+// search is needed whatever the offspring distribution. Outputs are then propagated in dense
+// rounds of 1024 (4 consecutive outputs per thread share one Philox block).
 #include "cuppl_device.cuh"
 #include "smc_kernels.cuh"
 
@@ -153,16 +153,14 @@ template <bool HIST>
 __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(SmcScanArgs a) {
   __shared__ unsigned long long seg_sum[kTileSegs];
   __shared__ unsigned long long wtot[kSmcThreads / 32];
-  __shared__ unsigned long long s_prefix;
+  __shared__ double wpart[kSmcThreads / 32][2];
   __shared__ unsigned int s_tile;
-  __shared__ bool s_last;
-  __shared__ BlockScratch sc;
   __shared__ unsigned long long shist[HIST ? kMaxStates : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long n = a.n_local;
   const unsigned long long n_tiles = (n + kTile - 1) / kTile;
   const float M = key2f(*a.m_key);
-  if (tid == 0) s_tile = atomicAdd(&a.counters[0], 1u);
+  if (tid == 0) s_tile = atomicAdd(&a.counters[0], 1u);  // launch-order tile ids: look-back is deadlock free
   if (HIST)
     for (int s = tid; s < a.S; s += kSmcThreads) shist[s] = 0;
   __syncthreads();
@@ -219,6 +217,16 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(SmcScanArgs a) {
     ws += __shfl_xor_sync(0xffffffffu, ws, 4);
     if ((lane & 7) == 0) seg_sum[warp * 32 + it * 4 + (lane >> 3)] = ws;
   }
+  double d1 = s1, d2 = s2;  // per-warp fp64 partials, fixed tree
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d1 += __shfl_down_sync(0xffffffffu, d1, o);
+    d2 += __shfl_down_sync(0xffffffffu, d2, o);
+  }
+  if (lane == 0) {
+    wpart[warp][0] = d1;
+    wpart[warp][1] = d2;
+  }
   __syncthreads();
   // inclusive scan of the tile's 256 segment sums (thread tid <-> segment tid)
   unsigned long long incl = seg_sum[tid];
@@ -235,50 +243,26 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(SmcScanArgs a) {
     if (w < warp) wpre += wtot[w];
     agg += wtot[w];
   }
-  incl += wpre;
-  if (warp == 0) {
-    if (lane == 0) st_relaxed_u64(a.flags + tile, (tile == 0 ? kFlagIncl : kFlagAgg) | agg);
-    const unsigned long long prefix = tile == 0 ? 0ull : warp_lookback(a.flags, tile);
-    if (lane == 0) {
-      if (tile != 0) st_relaxed_u64(a.flags + tile, kFlagIncl | (prefix + agg));
-      s_prefix = prefix;
-    }
-  }
-  __syncthreads();
   const unsigned long long gs = tile * kTileSegs + tid;
-  if (gs * kSegment < n) a.segoff[gs] = s_prefix + incl;
-  const double d1 = block_sum_d(static_cast<double>(s1), sc);
-  const double d2 = block_sum_d(static_cast<double>(s2), sc);
-  if (tid == 0) {
-    a.tile_s[2 * tile] = d1;
-    a.tile_s[2 * tile + 1] = d2;
-  }
+  if (gs * kSegment < n) a.segoff[gs] = incl + wpre;  // tile-local; K6 adds tile_prefix
   if (HIST) {
     for (int s = tid; s < a.S; s += kSmcThreads)
       if (shist[s]) atomicAdd(&a.hist[s], shist[s]);
   }
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = atomicAdd(&a.counters[1], 1u) == n_tiles - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  // last CTA: fixed-order fp64 fold of the tile sums -> rank record
-  double f1 = 0.0, f2 = 0.0;
-  for (unsigned long long tt = tid; tt < n_tiles; tt += kSmcThreads) {
-    f1 += a.tile_s[2 * tt];
-    f2 += a.tile_s[2 * tt + 1];
-  }
-  f1 = block_sum_d(f1, sc);
-  f2 = block_sum_d(f2, sc);
-  if (tid == 0) {
-    const unsigned long long T = ld_relaxed_u64(a.flags + n_tiles - 1) & kValMask;
-    a.rank_rec[0] = T;
-    a.rank_rec[1] = static_cast<unsigned long long>(__double_as_longlong(f1));
-    a.rank_rec[2] = static_cast<unsigned long long>(__double_as_longlong(f2));
-    a.rank_rec[3] = 0;
-    a.counters[0] = 0;
-    a.counters[1] = 0;
+  if (warp != 0) return;  // only warp 0 waits on the predecessors
+  if (lane == 0) st_relaxed_u64(a.flags + tile, (tile == 0 ? kFlagIncl : kFlagAgg) | agg);
+  const unsigned long long prefix = tile == 0 ? 0ull : warp_lookback(a.flags, tile);
+  if (lane == 0) {
+    if (tile != 0) st_relaxed_u64(a.flags + tile, kFlagIncl | (prefix + agg));
+    a.tile_prefix[tile] = prefix;
+    double t1 = 0.0, t2 = 0.0;
+    for (int w = 0; w < kSmcThreads / 32; ++w) {
+      t1 += wpart[w][0];
+      t2 += wpart[w][1];
+    }
+    a.tile_s[2 * tile] = t1;
+    a.tile_s[2 * tile + 1] = t2;
+    if (tile == n_tiles - 1) a.rank_rec[0] = prefix + agg;  // T_r
   }
 }
 
@@ -360,10 +344,15 @@ __device__ __forceinline__ unsigned int first_j_at_least(unsigned long long c, c
   return cur.j;
 }
 
+// Rank-local inclusive weight prefix at the end of segment s (K5 writes tile-local values).
+__device__ __forceinline__ unsigned long long seg_incl(const SmcResampleArgs& a, unsigned long long s) {
+  return __ldg(a.tile_prefix + s / kTileSegs) + __ldg(a.segoff + s);
+}
+
 // Warp-cooperative rank-local upper bound: smallest local i with C_i > t (C = inclusive scan
-// of the rank's weights, represented by segoff + the lw of one segment). Returns n_local if none.
-// The segment is found with a 33-ary search (5 rounds for 3e6 segments), then resolved inside
-// the segment with a warp scan of its 32 weights.
+// of the rank's weights, represented by the segment prefixes + the lw of one segment). Returns
+// n_local if none. The segment is found with a 33-ary search (5 rounds for 3e6 segments), then
+// resolved inside the segment with a warp scan of its 32 weights.
 __device__ unsigned long long warp_upper_bound(unsigned long long t, const SmcResampleArgs& a,
                                                float M) {
   const int lane = threadIdx.x & 31;
@@ -372,7 +361,7 @@ __device__ unsigned long long warp_upper_bound(unsigned long long t, const SmcRe
   while (hi - lo > 32) {
     const unsigned long long span = hi - lo;
     const unsigned long long p = lo + span * (lane + 1) / 33;  // strictly increasing, < hi
-    const unsigned int bal = __ballot_sync(0xffffffffu, a.segoff[p] > t);
+    const unsigned int bal = __ballot_sync(0xffffffffu, seg_incl(a, p) > t);
     if (!bal) {
       lo = lo + span * 32 / 33 + 1;
     } else {
@@ -384,12 +373,12 @@ __device__ unsigned long long warp_upper_bound(unsigned long long t, const SmcRe
   }
   {
     const unsigned long long p = lo + lane;
-    const unsigned int bal = __ballot_sync(0xffffffffu, p < hi && a.segoff[p] > t);
+    const unsigned int bal = __ballot_sync(0xffffffffu, p < hi && seg_incl(a, p) > t);
     hi = bal ? lo + (__ffs(bal) - 1) : hi;
   }
   const unsigned long long s = hi;
   if (s >= n_segs) return a.n_local;
-  const unsigned long long base = s > 0 ? a.segoff[s - 1] : 0ull;
+  const unsigned long long base = s > 0 ? seg_incl(a, s - 1) : 0ull;
   const unsigned long long i = s * kSegment + lane;
   const uint32_t w = i < a.n_local ? smc_w(smc_e(a.lw[i], M)) : 0u;
   unsigned long long incl = w;
@@ -403,21 +392,51 @@ __device__ unsigned long long warp_upper_bound(unsigned long long t, const SmcRe
   return s * kSegment + (__ffs(bal) - 1);
 }
 
+struct HeavyRange {
+  unsigned short lo, hi;  // slot range [lo, hi) relative to the sub-chunk base
+  unsigned short rel;     // source index relative to the batch (debug ancestors)
+  unsigned char x;        // ancestor state
+  unsigned char pad;
+};
+
 template <bool MULTI>
 __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __grid_constant__ SmcModel m,
                                                                       SmcResampleArgs a) {
-  __shared__ unsigned int mark[kChunk];
-  __shared__ uint8_t xs[kBatch];
+  __shared__ uint8_t ancx[kChunk];            // ancestor state of each output slot
+  __shared__ unsigned short ancr[kChunk];     // ancestor index (relative to the batch), debug only
+  __shared__ HeavyRange heavy[kHeavySlots];
+  __shared__ unsigned int s_nheavy;
   __shared__ unsigned long long wsum[kSmcThreads / 32];
-  __shared__ unsigned int wmax[kSmcThreads / 32];
-  __shared__ unsigned int s_carry;
   __shared__ unsigned long long s_u64[4];
   __shared__ unsigned long long s_rank_begin[MULTI ? kMaxRanks + 1 : 1];
   __shared__ float s_mu[kMaxStates];
+  __shared__ BlockScratch sc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int q = tid; q < m.S; q += kSmcThreads) s_mu[q] = m.mu[q];
   if (MULTI)
     for (int q = tid; q <= a.world; q += kSmcThreads) s_rank_begin[q] = a.rank_begin[q];
+  const bool debug_anc = a.anc_out != nullptr;
+  const unsigned long long n_tiles = a.n_tiles;
+
+  // CTA 0: fixed-order fp64 fold of K5's per-tile sums -> rank (sum e, sum e^2); reset K5's
+  // tile counter. Every CTA clears a slice of the look-back words for the next scan.
+  if (blockIdx.x == 0) {
+    double f1 = 0.0, f2 = 0.0;
+    for (unsigned long long tt = tid; tt < n_tiles; tt += kSmcThreads) {
+      f1 += a.tile_s[2 * tt];
+      f2 += a.tile_s[2 * tt + 1];
+    }
+    f1 = block_sum_d(f1, sc);
+    f2 = block_sum_d(f2, sc);
+    if (tid == 0) {
+      a.stats_out[0] = f1;
+      a.stats_out[1] = f2;
+      a.counters[0] = 0u;
+    }
+  }
+  for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(kSmcThreads) + tid; i < n_tiles;
+       i += static_cast<unsigned long long>(gridDim.x) * kSmcThreads)
+    a.flags_to_clear[i] = 0ull;
 
   // step constants (identical on every rank)
   unsigned long long T = 0, O = 0;
@@ -427,10 +446,6 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
     T += Tq;
   }
   const unsigned long long Tr = a.rank_recs[4 * a.rank];
-  // clear the look-back words for the next scan
-  for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(kSmcThreads) + tid;
-       i < a.n_tiles; i += static_cast<unsigned long long>(gridDim.x) * kSmcThreads)
-    a.flags_to_clear[i] = 0ull;
   if (T == 0) return;  // all weights zero: the host raises AllZeroWeightError
   const float M = key2f(*a.m_key);
   const PhiloxKey key = make_key(a.key);
@@ -465,15 +480,18 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
   }
   __syncthreads();
   unsigned long long batch_base = (s_u64[2] / kSegment) * kSegment;
-  unsigned long long c_base = batch_base > 0 ? a.segoff[batch_base / kSegment - 1] : 0ull;
+  unsigned long long c_base = batch_base > 0 ? seg_incl(a, batch_base / kSegment - 1) : 0ull;
   unsigned long long j_cur = jb_lo;
   float bmax = neg_inf_f();
   const unsigned int S = static_cast<unsigned int>(m.S);
+  CombCursor cur;
+  cur.seek(0, cb);
 
   while (j_cur < jb_hi && batch_base < a.n_local) {
     // ---- stage 2048 sources: thread tid owns [batch_base + 8 tid, +8)
     const unsigned long long i0 = batch_base + kBatchPerThread * tid;
     uint32_t w[kBatchPerThread];
+    uint8_t xk[kBatchPerThread];
     unsigned long long tw = 0;
     if (i0 + kBatchPerThread <= a.n_local) {
       const float4 f0 = __ldcs(reinterpret_cast<const float4*>(a.lw + i0));
@@ -484,14 +502,14 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
       for (int k = 0; k < kBatchPerThread; ++k) {
         w[k] = smc_w(smc_e(v[k], M));
         tw += w[k];
+        xk[k] = static_cast<uint8_t>((k < 4 ? xx.x : xx.y) >> (8 * (k & 3)));
       }
-      *reinterpret_cast<uint2*>(xs + kBatchPerThread * tid) = xx;
     } else {
 #pragma unroll
       for (int k = 0; k < kBatchPerThread; ++k) {
         const bool ok = i0 + k < a.n_local;
         w[k] = ok ? smc_w(smc_e(a.lw[i0 + k], M)) : 0u;
-        xs[kBatchPerThread * tid + k] = ok ? a.x[i0 + k] : 0;
+        xk[k] = ok ? a.x[i0 + k] : 0;
         tw += w[k];
       }
     }
@@ -510,31 +528,24 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
       if (q < warp) wpre += wsum[q];
       btot += wsum[q];
     }
-    // f_k for each positive-weight source (global target units), monotone per thread
-    unsigned int f[kBatchPerThread];
+    // children of source k: [F(C_{i-1}), F(C_i)), F(c) = min{j : target_j >= O + c}; one
+    // monotone integer cursor per thread (the previous batch's position is a lower bound)
+    unsigned int fk[kBatchPerThread + 1];
     {
-      CombCursor cur;
-      bool init = false;
       unsigned long long c = c_base + wpre + incl - tw;  // C_{i0 - 1} (local)
+      CombCursor cc = cur;
+      cc.advance_to(O + c, cb);
+      fk[0] = cc.j;
 #pragma unroll
       for (int k = 0; k < kBatchPerThread; ++k) {
-        f[k] = 0xFFFFFFFFu;
-        if (w[k]) {
-          if (!init) {
-            cur.seek(0, cb);
-            init = true;
-          }
-          cur.advance_to(O + c, cb);
-          f[k] = cur.j;
-        }
         c += w[k];
+        if (w[k]) cc.advance_to(O + c, cb);
+        fk[k + 1] = cc.j;
       }
-    }
-    // outputs whose ancestors lie in this batch: [j_cur, j_next)
-    if (tid == kSmcThreads - 1) {
-      const unsigned long long c_end = c_base + btot;
-      const unsigned long long jn = c_end >= Tr ? jb_hi : first_j_at_least(O + c_end, cb);
-      s_u64[3] = jn < jb_hi ? jn : jb_hi;
+      if (tid == kSmcThreads - 1) {
+        const unsigned long long jn = fk[kBatchPerThread];  // F(C at batch end)
+        s_u64[3] = jn < jb_hi ? jn : jb_hi;
+      }
     }
     __syncthreads();
     const unsigned long long j_next = s_u64[3];
@@ -542,41 +553,44 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
     for (unsigned long long j0 = j_cur; j0 < j_next;) {
       const unsigned long long jbase = j0 & ~3ull;  // Philox blocks cover 4 outputs
       const unsigned long long j1 = jbase + kChunk < j_next ? jbase + kChunk : j_next;
-#pragma unroll
-      for (int k = 0; k < kChunk / kSmcThreads; ++k) mark[k * kSmcThreads + tid] = 0u;
-      if (tid == 0) s_carry = 0u;
+      if (tid == 0) s_nheavy = 0u;
       __syncthreads();
+      // every source writes its ancestor state into its children's slots
 #pragma unroll
       for (int k = 0; k < kBatchPerThread; ++k) {
-        if (f[k] == 0xFFFFFFFFu) continue;
-        const unsigned int rel = kBatchPerThread * tid + k + 1;  // +1: 0 means "none"
-        if (f[k] <= j0) atomicMax(&s_carry, rel);
-        else if (f[k] < j1) atomicMax(&mark[f[k] - jbase], rel);
+        const unsigned long long lo = fk[k] > j0 ? fk[k] : j0;
+        const unsigned long long hi = fk[k + 1] < j1 ? fk[k + 1] : j1;
+        if (lo >= hi) continue;
+        const unsigned int rel = kBatchPerThread * tid + k;
+        if (hi - lo <= kHeavy) {
+          for (unsigned long long j = lo; j < hi; ++j) {
+            ancx[j - jbase] = xk[k];
+            if (debug_anc) ancr[j - jbase] = static_cast<unsigned short>(rel);
+          }
+        } else {
+          const unsigned int slot = atomicAdd(&s_nheavy, 1u);
+          if (slot < kHeavySlots) {
+            heavy[slot] = HeavyRange{static_cast<unsigned short>(lo - jbase),
+                                     static_cast<unsigned short>(hi - jbase),
+                                     static_cast<unsigned short>(rel), xk[k], 0};
+          } else {
+            for (unsigned long long j = lo; j < hi; ++j) {
+              ancx[j - jbase] = xk[k];
+              if (debug_anc) ancr[j - jbase] = static_cast<unsigned short>(rel);
+            }
+          }
+        }
       }
       __syncthreads();
-      // inclusive max-scan over mark[0, kChunk): thread tid owns kScanPer consecutive entries
-      constexpr int kScanPer = kChunk / kSmcThreads;
-      unsigned int tm = 0;
-#pragma unroll
-      for (int k = 0; k < kScanPer; ++k) tm = max(tm, mark[kScanPer * tid + k]);
-      unsigned int im = tm;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned int t2 = __shfl_up_sync(0xffffffffu, im, o);
-        if (lane >= o) im = max(im, t2);
+      const unsigned int nh = s_nheavy < kHeavySlots ? s_nheavy : kHeavySlots;
+      for (unsigned int h = 0; h < nh; ++h) {
+        const HeavyRange hr = heavy[h];
+        for (unsigned int j = hr.lo + tid; j < hr.hi; j += kSmcThreads) {
+          ancx[j] = hr.x;
+          if (debug_anc) ancr[j] = hr.rel;
+        }
       }
-      if (lane == 31) wmax[warp] = im;
-      __syncthreads();
-      unsigned int carry = s_carry;
-      for (int q = 0; q < warp; ++q) carry = max(carry, wmax[q]);
-      const unsigned int prev = __shfl_up_sync(0xffffffffu, im, 1);
-      if (lane > 0) carry = max(carry, prev);
-#pragma unroll
-      for (int k = 0; k < kScanPer; ++k) {
-        carry = max(carry, mark[kScanPer * tid + k]);
-        mark[kScanPer * tid + k] = carry;  // now the ancestor (+1) of output jbase + index
-      }
-      __syncthreads();
+      if (nh) __syncthreads();
       // propagate in dense rounds of 1024 outputs: thread tid takes 4 consecutive outputs
       for (unsigned long long jr = jbase; jr < j1; jr += 4 * kSmcThreads) {
         const unsigned long long jq = jr + 4 * tid;
@@ -592,20 +606,19 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
           xo[k] = 0;
           lo[k] = 0.f;
           if (j >= j0 && j < j1) {
-            const unsigned int anc = mark[j - jbase] - 1;  // relative to batch_base
-            const int xa = xs[anc];
+            const int xa = ancx[j - jbase];
             const int s = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[k]);
             const float l = emission(a.y_next, s_mu[s], m.inv_sd, m.c);
             xo[k] = static_cast<uint8_t>(s);
             lo[k] = l;
             bmax = fmaxf(bmax, l);
-            if (a.anc_out) {
+            if (debug_anc) {
               int q = 0;
               if (MULTI)
                 while (q + 1 < a.world && s_rank_begin[q + 1] <= j) ++q;
               const unsigned long long rb = MULTI ? s_rank_begin[q] : 0ull;
               const unsigned long long my = MULTI ? s_rank_begin[a.rank] : 0ull;
-              a.anc_out[q][j - rb] = my + batch_base + anc;
+              a.anc_out[q][j - rb] = my + batch_base + ancr[j - jbase];
             }
           } else {
             all = false;
@@ -640,17 +653,50 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
           }
         }
       }
-      __syncthreads();  // mark reuse
+      __syncthreads();  // slot reuse
       j0 = j1;
+    }
+    // carry the cursor of the last thread as the next batch's lower bound
+    if (tid == kSmcThreads - 1) s_u64[2] = fk[kBatchPerThread];
+    __syncthreads();
+    {
+      const unsigned int jl = static_cast<unsigned int>(s_u64[2]);
+      if (jl > cur.j && jl < cb.N) cur.seek(jl, cb);
     }
     j_cur = j_next;
     c_base += btot;
     batch_base += kBatch;
-    __syncthreads();  // xs / wsum / s_u64 reuse
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
   if (lane == 0 && bmax > neg_inf_f()) atomicMax(a.m_key_next, f2key(bmax));
+}
+
+// Fixed-order fold of K5's per-tile sums for a population that is not resampled (the last
+// step): same arithmetic as K6's CTA 0.
+__global__ void __launch_bounds__(kSmcThreads) smc_fold_kernel(const double* tile_s,
+                                                               unsigned long long n_tiles,
+                                                               double* stats_out,
+                                                               unsigned int* counters) {
+  __shared__ BlockScratch sc;
+  double f1 = 0.0, f2 = 0.0;
+  for (unsigned long long tt = threadIdx.x; tt < n_tiles; tt += kSmcThreads) {
+    f1 += tile_s[2 * tt];
+    f2 += tile_s[2 * tt + 1];
+  }
+  f1 = block_sum_d(f1, sc);
+  f2 = block_sum_d(f2, sc);
+  if (threadIdx.x == 0) {
+    stats_out[0] = f1;
+    stats_out[1] = f2;
+    counters[0] = 0u;
+  }
+}
+
+cudaError_t launch_smc_fold(const double* tile_s, unsigned long long n_tiles, double* stats_out,
+                            unsigned int* counters, cudaStream_t st) {
+  smc_fold_kernel<<<1, kSmcThreads, 0, st>>>(tile_s, n_tiles, stats_out, counters);
+  return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ launchers -----------

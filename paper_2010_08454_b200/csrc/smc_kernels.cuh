@@ -13,6 +13,8 @@ constexpr int kTile = kTileSegs * kSegment;   // 8192 particles per scan tile
 constexpr int kBatchPerThread = 8;            // sources per thread per K6 batch
 constexpr int kBatch = kSmcThreads * kBatchPerThread;  // 2048 sources per K6 batch
 constexpr int kOutPerThread = 16;             // ancestor slots per thread per K6 sub-chunk
+constexpr int kHeavy = 16;                    // children ranges longer than this are filled cooperatively
+constexpr int kHeavySlots = 512;
 constexpr int kChunk = kSmcThreads * kOutPerThread;    // 2048 outputs per sub-chunk
 constexpr int kMaxStates = 256;               // particle state stored as u8
 constexpr int kMaxRanks = 64;
@@ -44,12 +46,13 @@ struct SmcScanArgs {
   const float* lw;
   const uint8_t* x;
   const int* m_key;              // max of lw_t as an ordered int (global over ranks)
-  unsigned long long* segoff;    // [ceil(n/32)] rank-local inclusive offsets per segment
+  unsigned long long* segoff;    // [ceil(n/32)] TILE-local inclusive offsets per segment
+  unsigned long long* tile_prefix;  // [n_tiles] exclusive prefix of the tile sums (look-back)
   unsigned long long* flags;     // [n_tiles] look-back words (status << 62 | value), zero on entry
-  unsigned int* counters;        // [2]: dynamic tile id, done count (zero on entry; reset on exit)
+  unsigned int* counters;        // [2]: dynamic tile id (zero on entry; K6 resets it)
   double* tile_s;                // [n_tiles][2] per-tile sum e, sum e^2
   unsigned long long* hist;      // [S] integer filtering weights of x_t (NULL: skip), zero on entry
-  unsigned long long* rank_rec;  // [4]: T_r, bits(s1_r), bits(s2_r), status (written by the last CTA)
+  unsigned long long* rank_rec;  // [4]: T_r written by the last tile (other words untouched)
   int S;
   int pad_;
 };
@@ -64,7 +67,11 @@ struct SmcResampleArgs {
   const float* lw;
   const uint8_t* x;
   const int* m_key;                        // max of lw_t (ordered int)
-  const unsigned long long* segoff;        // rank-local inclusive segment offsets
+  const unsigned long long* segoff;        // tile-local inclusive segment offsets
+  const unsigned long long* tile_prefix;   // exclusive prefix of the tile sums
+  const double* tile_s;                    // [n_tiles][2] per-tile sum e, sum e^2 (folded by CTA 0)
+  double* stats_out;                       // [2]: rank sum e, sum e^2 of population t
+  unsigned int* counters;                  // K5 counters, reset here
   const unsigned long long* rank_recs;     // [world][4] gathered rank records of step t
   const unsigned long long* rank_begin;    // [world + 1] global index of each rank's first particle
   uint8_t* const* x_out;                   // [world] destination x (peer-mapped for q != rank)
@@ -77,6 +84,8 @@ struct SmcResampleArgs {
 
 cudaError_t launch_smc_init(const SmcModel& m, const SmcInitArgs& a, int sm_count, cudaStream_t st);
 cudaError_t launch_smc_scan(const SmcScanArgs& a, int sm_count, cudaStream_t st);
+cudaError_t launch_smc_fold(const double* tile_s, unsigned long long n_tiles, double* stats_out,
+                            unsigned int* counters, cudaStream_t st);
 cudaError_t launch_smc_resample(const SmcModel& m, const SmcResampleArgs& a, int sm_count,
                                 cudaStream_t st);
 

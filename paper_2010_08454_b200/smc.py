@@ -83,6 +83,7 @@ class _Rank:
         self.ws = torch.empty(int(ws), dtype=torch.uint8, device=dev)
         self.m_key = torch.full((runner.T,), INT32_MIN, dtype=torch.int32, device=dev)
         self.rec = torch.zeros((runner.T, 4), dtype=torch.int64, device=dev)
+        self.stats = torch.zeros((runner.T, 2), dtype=torch.float64, device=dev)
 
 
 class SmcRunner:
@@ -177,6 +178,17 @@ class SmcRunner:
 
             dist.all_gather_into_tensor(self.gathered[t].view(-1), self.ranks[0].rec[t], group=self.group)
 
+    def _gather_stats(self) -> np.ndarray:
+        import torch
+
+        if self.local or self.world == 1:
+            return torch.stack([rk.stats for rk in self.ranks]).cpu().numpy()
+        import torch.distributed as dist  # pragma: no cover - multi-GPU
+
+        out = torch.empty((self.world, self.T, 2), dtype=torch.float64, device=self.device)
+        dist.all_gather_into_tensor(out.view(-1), self.ranks[0].stats.view(-1), group=self.group)
+        return out.cpu().numpy()
+
     # ------------------------------------------------------------------ steps -------------
     def init(self):
         L = N.lib()
@@ -200,6 +212,9 @@ class SmcRunner:
                                      N.ptr(rk.ws), rk.ws.numel(), st), "smc_scan", seed=self.seed, step=t)
         self._allgather(t)
         if t + 1 >= self.T:
+            for rk in self.ranks:
+                N.check(L.cuppl_smc_fold(rk.n, N.ptr(rk.stats[t]), N.ptr(rk.ws), rk.ws.numel(), st),
+                        "smc_fold", seed=self.seed, step=t)
             return
         nxt = 1 - self.cur
         xt, lt, at = self._tables[nxt]
@@ -208,7 +223,7 @@ class SmcRunner:
                 C.byref(self.cm), rk.n, self.N, self.key, t, rk.r, self.world, float(self.ys[t + 1]),
                 N.ptr(rk.lw[self.cur]), N.ptr(rk.x[self.cur]), N.ptr(rk.m_key[t:t + 1]),
                 N.ptr(self.gathered[t]), N.ptr(self.rank_begin), N.ptr(xt), N.ptr(lt),
-                None if at is None else N.ptr(at), N.ptr(rk.m_key[t + 1:t + 2]),
+                None if at is None else N.ptr(at), N.ptr(rk.m_key[t + 1:t + 2]), N.ptr(rk.stats[t]),
                 N.ptr(rk.ws), rk.ws.numel(), st), "smc_resample", seed=self.seed, step=t)
         if self.record_ancestors:
             self.ancestors.append([rk.anc[nxt].clone() for rk in self.ranks])
@@ -224,11 +239,12 @@ class SmcRunner:
         g = self.gathered.cpu().numpy().view(np.uint64)
         mk = self.ranks[0].m_key.cpu().numpy()
         Tt = g[:, :, 0].sum(axis=1)
+        stats = self._gather_stats()  # [world, T, 2]
         s1 = np.zeros(self.T)
         s2 = np.zeros(self.T)
         for q in range(self.world):  # rank order, fp64
-            s1 += g[:, q, 1].view(np.float64)
-            s2 += g[:, q, 2].view(np.float64)
+            s1 += stats[q, :, 0]
+            s2 += stats[q, :, 1]
         M = np.array([key_to_float(k) for k in mk])
         zero = np.nonzero(Tt == 0)[0]
         if len(zero):

@@ -39,7 +39,8 @@ def test_smc_bit_exact_single_rank(cuda, oracle_lib, n, S, steps):
     assert np.array_equal(lw.view(np.uint32), ref["lw"].view(np.uint32))
     for t in range(steps):
         assert np.array_equal(res.filtering_int[t], ref["hist"][t])
-    assert np.allclose(res.log_z_steps, ref["log_z_steps"], rtol=1e-12, atol=1e-9)
+    # s1 is summed in fp32 per thread on the GPU, fp64 sequentially in the oracle
+    assert np.allclose(res.log_z_steps, ref["log_z_steps"], rtol=1e-7, atol=1e-7)
 
 
 @pytest.mark.parametrize("R", [2, 3, 8])
