@@ -17,12 +17,12 @@
 //
 // K6 is output-balanced and source-streaming: CTA b owns an even share of the rank's output
 // range, finds the ancestor of its first output once (warp-parallel 33-ary search over the
-// segment prefixes), then streams its sources in order in batches of 2048. Source i's children
-// are exactly the outputs [F(C_{i-1}), F(C_i)) with F(c) = min{j : target_j >= c}, which an
-// incremental integer cursor evaluates in O(1) amortised per source; each source writes its
-// state into its children's slots (long runs are filled by the whole CTA), so no per-output
-// search is needed whatever the offspring distribution. Outputs are then propagated in dense
-// rounds of 1024 (4 consecutive outputs per thread share one Philox block).
+// segment prefixes), then streams its sources in order in batches of 2048 staged in shared
+// memory with their batch-relative inclusive weight prefix. The batch's outputs are exactly
+// [F(C_start), F(C_end)) with F(c) = min{j : target_j >= c}; they are propagated in dense
+// rounds of 1024 (4 consecutive outputs per thread share one Philox block and one integer comb
+// cursor); each thread binary-searches the ancestor of its first output in shared memory and
+// steps to the next ones, so the work per output is uniform whatever the offspring counts.
 #include "cuppl_device.cuh"
 #include "smc_kernels.cuh"
 
@@ -392,20 +392,11 @@ __device__ unsigned long long warp_upper_bound(unsigned long long t, const SmcRe
   return s * kSegment + (__ffs(bal) - 1);
 }
 
-struct HeavyRange {
-  unsigned short lo, hi;  // slot range [lo, hi) relative to the sub-chunk base
-  unsigned short rel;     // source index relative to the batch (debug ancestors)
-  unsigned char x;        // ancestor state
-  unsigned char pad;
-};
-
 template <bool MULTI>
-__global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __grid_constant__ SmcModel m,
+__global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __grid_constant__ SmcModel m,
                                                                       SmcResampleArgs a) {
-  __shared__ uint8_t ancx[kChunk];            // ancestor state of each output slot
-  __shared__ unsigned short ancr[kChunk];     // ancestor index (relative to the batch), debug only
-  __shared__ HeavyRange heavy[kHeavySlots];
-  __shared__ unsigned int s_nheavy;
+  __shared__ unsigned long long cb_incl[kBatch];  // batch-relative inclusive weight prefix per source
+  __shared__ uint8_t xs[kBatch];                  // staged source states
   __shared__ unsigned long long wsum[kSmcThreads / 32];
   __shared__ unsigned long long s_u64[4];
   __shared__ unsigned long long s_rank_begin[MULTI ? kMaxRanks + 1 : 1];
@@ -484,36 +475,32 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
   unsigned long long j_cur = jb_lo;
   float bmax = neg_inf_f();
   const unsigned int S = static_cast<unsigned int>(m.S);
-  CombCursor cur;
-  cur.seek(0, cb);
 
   while (j_cur < jb_hi && batch_base < a.n_local) {
     // ---- stage 2048 sources: thread tid owns [batch_base + 8 tid, +8)
     const unsigned long long i0 = batch_base + kBatchPerThread * tid;
     uint32_t w[kBatchPerThread];
-    uint8_t xk[kBatchPerThread];
     unsigned long long tw = 0;
     if (i0 + kBatchPerThread <= a.n_local) {
       const float4 f0 = __ldcs(reinterpret_cast<const float4*>(a.lw + i0));
       const float4 f1 = __ldcs(reinterpret_cast<const float4*>(a.lw + i0) + 1);
-      const uint2 xx = __ldcs(reinterpret_cast<const uint2*>(a.x + i0));
+      *reinterpret_cast<uint2*>(xs + kBatchPerThread * tid) = __ldcs(reinterpret_cast<const uint2*>(a.x + i0));
       const float v[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
 #pragma unroll
       for (int k = 0; k < kBatchPerThread; ++k) {
         w[k] = smc_w(smc_e(v[k], M));
         tw += w[k];
-        xk[k] = static_cast<uint8_t>((k < 4 ? xx.x : xx.y) >> (8 * (k & 3)));
       }
     } else {
 #pragma unroll
       for (int k = 0; k < kBatchPerThread; ++k) {
         const bool ok = i0 + k < a.n_local;
         w[k] = ok ? smc_w(smc_e(a.lw[i0 + k], M)) : 0u;
-        xk[k] = ok ? a.x[i0 + k] : 0;
+        xs[kBatchPerThread * tid + k] = ok ? a.x[i0 + k] : 0;
         tw += w[k];
       }
     }
-    // block exclusive scan of the thread sums
+    // block exclusive scan of the thread sums -> batch-relative inclusive prefix per source
     unsigned long long incl = tw;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -522,147 +509,110 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
     }
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    unsigned long long wpre = 0, btot = 0;
+    unsigned long long run = 0, btot = 0;
 #pragma unroll
     for (int q = 0; q < kSmcThreads / 32; ++q) {
-      if (q < warp) wpre += wsum[q];
+      if (q < warp) run += wsum[q];
       btot += wsum[q];
     }
-    // children of source k: [F(C_{i-1}), F(C_i)), F(c) = min{j : target_j >= O + c}; one
-    // monotone integer cursor per thread (the previous batch's position is a lower bound)
-    unsigned int fk[kBatchPerThread + 1];
-    {
-      unsigned long long c = c_base + wpre + incl - tw;  // C_{i0 - 1} (local)
-      CombCursor cc = cur;
-      cc.advance_to(O + c, cb);
-      fk[0] = cc.j;
+    run += incl - tw;
 #pragma unroll
-      for (int k = 0; k < kBatchPerThread; ++k) {
-        c += w[k];
-        if (w[k]) cc.advance_to(O + c, cb);
-        fk[k + 1] = cc.j;
-      }
-      if (tid == kSmcThreads - 1) {
-        const unsigned long long jn = fk[kBatchPerThread];  // F(C at batch end)
-        s_u64[3] = jn < jb_hi ? jn : jb_hi;
-      }
+    for (int k = 0; k < kBatchPerThread; ++k) {
+      run += w[k];
+      cb_incl[kBatchPerThread * tid + k] = run;
+    }
+    // outputs whose ancestors lie in this batch: [j_cur, j_next), j_next = F(C at batch end)
+    if (tid == kSmcThreads - 1) {
+      const unsigned long long c_end = c_base + btot;
+      const unsigned long long jn = c_end >= Tr ? jb_hi : first_j_at_least(O + c_end, cb);
+      s_u64[3] = jn < jb_hi ? jn : jb_hi;
     }
     __syncthreads();
     const unsigned long long j_next = s_u64[3];
+    const unsigned long long off = O + c_base;  // global target of batch-relative weight 0
+    const unsigned long long jbase = j_cur & ~3ull;  // Philox blocks cover 4 outputs
 
-    for (unsigned long long j0 = j_cur; j0 < j_next;) {
-      const unsigned long long jbase = j0 & ~3ull;  // Philox blocks cover 4 outputs
-      const unsigned long long j1 = jbase + kChunk < j_next ? jbase + kChunk : j_next;
-      if (tid == 0) s_nheavy = 0u;
-      __syncthreads();
-      // every source writes its ancestor state into its children's slots
+    // propagate in dense rounds of 1024 outputs: thread tid takes 4 consecutive outputs, finds
+    // the first ancestor by binary search over the batch prefix, the others by stepping
+    for (unsigned long long jr = jbase; jr < j_next; jr += 4 * kSmcThreads) {
+      const unsigned long long jq = jr + 4 * tid;
+      if (jq + 3 < j_cur || jq >= j_next) continue;
+      CombCursor cc;
+      cc.seek(static_cast<unsigned int>(jq), cb);
+      const uint4 wd = draw_block(key, jq >> 2, a.t + 1, CUPPL_TAG_SMC_STEP);
+      const uint32_t wv[4] = {wd.x, wd.y, wd.z, wd.w};
+      uint8_t xo[4];
+      float lo[4];
+      bool all = true;
+      int k = -1;
 #pragma unroll
-      for (int k = 0; k < kBatchPerThread; ++k) {
-        const unsigned long long lo = fk[k] > j0 ? fk[k] : j0;
-        const unsigned long long hi = fk[k + 1] < j1 ? fk[k + 1] : j1;
-        if (lo >= hi) continue;
-        const unsigned int rel = kBatchPerThread * tid + k;
-        if (hi - lo <= kHeavy) {
-          for (unsigned long long j = lo; j < hi; ++j) {
-            ancx[j - jbase] = xk[k];
-            if (debug_anc) ancr[j - jbase] = static_cast<unsigned short>(rel);
+      for (int h = 0; h < 4; ++h) {
+        const unsigned long long j = jq + h;
+        xo[h] = 0;
+        lo[h] = 0.f;
+        if (j >= j_cur && j < j_next) {
+          const unsigned long long t = cc.tgt - off;  // batch-relative target, < btot
+          if (k < 0) {  // smallest k with cb_incl[k] > t
+            int lo2 = 0, hi2 = kBatch - 1;
+#pragma unroll 1
+            while (lo2 < hi2) {
+              const int mid = (lo2 + hi2) >> 1;
+              if (cb_incl[mid] > t) hi2 = mid;
+              else lo2 = mid + 1;
+            }
+            k = lo2;
+          } else {
+            while (cb_incl[k] <= t) ++k;
+          }
+          const int xa = xs[k];
+          const int s = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[h]);
+          const float l = emission(a.y_next, s_mu[s], m.inv_sd, m.c);
+          xo[h] = static_cast<uint8_t>(s);
+          lo[h] = l;
+          bmax = fmaxf(bmax, l);
+          if (debug_anc) {
+            int q = 0;
+            if (MULTI)
+              while (q + 1 < a.world && s_rank_begin[q + 1] <= j) ++q;
+            const unsigned long long rb = MULTI ? s_rank_begin[q] : 0ull;
+            const unsigned long long my = MULTI ? s_rank_begin[a.rank] : 0ull;
+            a.anc_out[q][j - rb] = my + batch_base + k;
           }
         } else {
-          const unsigned int slot = atomicAdd(&s_nheavy, 1u);
-          if (slot < kHeavySlots) {
-            heavy[slot] = HeavyRange{static_cast<unsigned short>(lo - jbase),
-                                     static_cast<unsigned short>(hi - jbase),
-                                     static_cast<unsigned short>(rel), xk[k], 0};
-          } else {
-            for (unsigned long long j = lo; j < hi; ++j) {
-              ancx[j - jbase] = xk[k];
-              if (debug_anc) ancr[j - jbase] = static_cast<unsigned short>(rel);
-            }
-          }
+          all = false;
         }
+        cc.next(cb);
       }
-      __syncthreads();
-      const unsigned int nh = s_nheavy < kHeavySlots ? s_nheavy : kHeavySlots;
-      for (unsigned int h = 0; h < nh; ++h) {
-        const HeavyRange hr = heavy[h];
-        for (unsigned int j = hr.lo + tid; j < hr.hi; j += kSmcThreads) {
-          ancx[j] = hr.x;
-          if (debug_anc) ancr[j] = hr.rel;
-        }
+      int q = 0;
+      unsigned long long rb = 0;
+      bool same = true;
+      if (MULTI) {
+        const unsigned long long jf = jq > j_cur ? jq : j_cur;
+        while (q + 1 < a.world && s_rank_begin[q + 1] <= jf) ++q;
+        rb = s_rank_begin[q];
+        same = q + 1 >= a.world || s_rank_begin[q + 1] >= jq + 4;
       }
-      if (nh) __syncthreads();
-      // propagate in dense rounds of 1024 outputs: thread tid takes 4 consecutive outputs
-      for (unsigned long long jr = jbase; jr < j1; jr += 4 * kSmcThreads) {
-        const unsigned long long jq = jr + 4 * tid;
-        if (jq + 3 < j0 || jq >= j1) continue;
-        const uint4 wd = draw_block(key, jq >> 2, a.t + 1, CUPPL_TAG_SMC_STEP);
-        const uint32_t wv[4] = {wd.x, wd.y, wd.z, wd.w};
-        uint8_t xo[4];
-        float lo[4];
-        bool all = true;
+      const unsigned long long dest = jq - rb;
+      if (all && same && jq >= rb && (dest & 3) == 0) {
+        const uint32_t packed = xo[0] | (xo[1] << 8) | (xo[2] << 16) | (static_cast<uint32_t>(xo[3]) << 24);
+        *reinterpret_cast<uint32_t*>(a.x_out[q] + dest) = packed;
+        __stcs(reinterpret_cast<float4*>(a.lw_out[q] + dest), make_float4(lo[0], lo[1], lo[2], lo[3]));
+      } else {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const unsigned long long j = jq + k;
-          xo[k] = 0;
-          lo[k] = 0.f;
-          if (j >= j0 && j < j1) {
-            const int xa = ancx[j - jbase];
-            const int s = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[k]);
-            const float l = emission(a.y_next, s_mu[s], m.inv_sd, m.c);
-            xo[k] = static_cast<uint8_t>(s);
-            lo[k] = l;
-            bmax = fmaxf(bmax, l);
-            if (debug_anc) {
-              int q = 0;
-              if (MULTI)
-                while (q + 1 < a.world && s_rank_begin[q + 1] <= j) ++q;
-              const unsigned long long rb = MULTI ? s_rank_begin[q] : 0ull;
-              const unsigned long long my = MULTI ? s_rank_begin[a.rank] : 0ull;
-              a.anc_out[q][j - rb] = my + batch_base + ancr[j - jbase];
-            }
-          } else {
-            all = false;
-          }
-        }
-        int q = 0;
-        unsigned long long rb = 0;
-        bool same = true;
-        if (MULTI) {
-          const unsigned long long jf = jq > j0 ? jq : j0;
-          while (q + 1 < a.world && s_rank_begin[q + 1] <= jf) ++q;
-          rb = s_rank_begin[q];
-          same = q + 1 >= a.world || s_rank_begin[q + 1] >= jq + 4;
-        }
-        const unsigned long long dest = jq - rb;
-        if (all && same && jq >= rb && (dest & 3) == 0) {
-          const uint32_t packed = xo[0] | (xo[1] << 8) | (xo[2] << 16) | (static_cast<uint32_t>(xo[3]) << 24);
-          *reinterpret_cast<uint32_t*>(a.x_out[q] + dest) = packed;
-          __stcs(reinterpret_cast<float4*>(a.lw_out[q] + dest), make_float4(lo[0], lo[1], lo[2], lo[3]));
-        } else {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const unsigned long long j = jq + k;
-            if (j >= j0 && j < j1) {
-              int qq = 0;
-              if (MULTI)
-                while (qq + 1 < a.world && s_rank_begin[qq + 1] <= j) ++qq;
-              const unsigned long long rbb = MULTI ? s_rank_begin[qq] : 0ull;
-              a.x_out[qq][j - rbb] = xo[k];
-              a.lw_out[qq][j - rbb] = lo[k];
-            }
+        for (int h = 0; h < 4; ++h) {
+          const unsigned long long j = jq + h;
+          if (j >= j_cur && j < j_next) {
+            int qq = 0;
+            if (MULTI)
+              while (qq + 1 < a.world && s_rank_begin[qq + 1] <= j) ++qq;
+            const unsigned long long rbb = MULTI ? s_rank_begin[qq] : 0ull;
+            a.x_out[qq][j - rbb] = xo[h];
+            a.lw_out[qq][j - rbb] = lo[h];
           }
         }
       }
-      __syncthreads();  // slot reuse
-      j0 = j1;
     }
-    // carry the cursor of the last thread as the next batch's lower bound
-    if (tid == kSmcThreads - 1) s_u64[2] = fk[kBatchPerThread];
-    __syncthreads();
-    {
-      const unsigned int jl = static_cast<unsigned int>(s_u64[2]);
-      if (jl > cur.j && jl < cb.N) cur.seek(jl, cb);
-    }
+    __syncthreads();  // cb_incl / xs / wsum / s_u64 reuse
     j_cur = j_next;
     c_base += btot;
     batch_base += kBatch;
