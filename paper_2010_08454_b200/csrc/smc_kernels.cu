@@ -21,8 +21,9 @@
 // memory with their batch-relative inclusive weight prefix. The batch's outputs are exactly
 // [F(C_start), F(C_end)) with F(c) = min{j : target_j >= c}; they are propagated in dense
 // rounds of 1024 (4 consecutive outputs per thread share one Philox block and one integer comb
-// cursor); each thread binary-searches the ancestor of its first output in shared memory and
-// steps to the next ones, so the work per output is uniform whatever the offspring counts.
+// cursor); each output's ancestor is a binary search over the staged prefix (zero-weight
+// sources make linear stepping divergent), so the work per output is uniform whatever the
+// offspring counts.
 #include "cuppl_device.cuh"
 #include "smc_kernels.cuh"
 
@@ -552,8 +553,8 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
         lo[h] = 0.f;
         if (j >= j_cur && j < j_next) {
           const unsigned long long t = cc.tgt - off;  // batch-relative target, < btot
-          if (k < 0) {  // smallest k with cb_incl[k] > t
-            int lo2 = 0, hi2 = kBatch - 1;
+          {  // smallest k with cb_incl[k] > t; targets increase, so search above the last hit
+            int lo2 = k < 0 ? 0 : k, hi2 = kBatch - 1;
 #pragma unroll 1
             while (lo2 < hi2) {
               const int mid = (lo2 + hi2) >> 1;
@@ -561,8 +562,6 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
               else lo2 = mid + 1;
             }
             k = lo2;
-          } else {
-            while (cb_incl[k] <= t) ++k;
           }
           const int xa = xs[k];
           const int s = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[h]);
