@@ -203,6 +203,23 @@ CUPPL_API int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uin
 CUPPL_API int cuppl_smc_fold(uint64_t n_local, double* stats_out, void* workspace,
                              size_t workspace_bytes, void* stream);
 
+/* ---- K7: many-chain lightweight Metropolis-Hastings (replaces run_lmh) -- */
+/* Gaussian mixture: mu_k ~ normal(0, prior_sd), k < K <= 7;
+ * z_i ~ categorical(1/K, ...); observe(normal(mu[z_i], sigma), y_i), i < D. One warp per chain;
+ * each step picks one of the K + D sites uniformly, redraws it from its prior, re-executes the
+ * model (full log-likelihood) and accepts with log a = l' - l.
+ * chains [chain_begin, chain_begin + n_chains) (global ids, Philox counter word 0).
+ * y: DEVICE pointer to cuppl_mh_padded_points(D) floats (data then zeros). Outputs (device):
+ * mu_out [n_chains][K],
+ * ll_out [n_chains], stats_out [n_chains][2K + 2] = sum of sorted mu, sum of sorted mu^2,
+ * recorded steps, accepted steps; trace_out [n_chains][n_rec][K] optional (NULL to skip). */
+CUPPL_API int cuppl_mh_padded_points(int D);
+CUPPL_API int cuppl_mh_gmm(const float* y, int D, int K, float prior_sd, float sigma,
+                           uint32_t n_chains, uint32_t chain_begin, uint32_t n_steps,
+                           uint32_t burn_in, uint32_t thin, uint64_t key, float* mu_out,
+                           float* ll_out, double* stats_out, float* trace_out, uint32_t n_rec,
+                           void* stream);
+
 /* ---- roofline calibration ---------------------------------------------------------- */
 /* Pipe-rate microbenchmark, blocks x 256 threads, each thread runs `iters` iterations of:
  * kind 0: 128 FFMA2 (256 fp32 FMA), kind 1: 128 FFMA, kind 2: one Philox4x32-10 block,

@@ -243,3 +243,44 @@ def smc_run(model, n: int, key: int, steps: int | None = None, record_ancestors:
     out["log_z_steps"] = out["M"].astype(np.float64) + np.log(out["s1"]) - np.log(n)
     out["log_z"] = float(out["log_z_steps"].sum())
     return out
+
+
+# ---------------------------------------------------------------------------- MH --------
+def _mh_sig(L):
+    P = C.POINTER
+    if getattr(L, "_mh_sig", False):
+        return
+    L.or_mh_gmm_chain.argtypes = [P(C.c_float), C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint32,
+                                  C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, P(C.c_double),
+                                  P(C.c_double), P(C.c_double), C.c_uint32, P(C.c_int32), P(C.c_double)]
+    L.or_mh_gmm_chain.restype = C.c_double
+    L.or_mh_gmm.argtypes = [P(C.c_float), C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint32, C.c_uint32,
+                            C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, P(C.c_double), P(C.c_double),
+                            P(C.c_double), C.c_int]
+    L._mh_sig = True
+
+
+def mh_gmm(ys, K, prior_sd, sigma, n_chains, n_steps, key, chain_begin=0, burn_in=0, thin=1, threads=0):
+    L = lib()
+    _mh_sig(L)
+    y = np.ascontiguousarray(ys, dtype=np.float32)
+    mu = np.zeros((n_chains, K))
+    ll = np.zeros(n_chains)
+    st = np.zeros((n_chains, 2 * K + 2))
+    L.or_mh_gmm(_ptr(y, C.c_float), len(y), K, prior_sd, sigma, n_chains, chain_begin, n_steps, burn_in, thin,
+                key, _ptr(mu, C.c_double), _ptr(ll, C.c_double), _ptr(st, C.c_double), threads)
+    return mu, ll, st
+
+
+def mh_gmm_init(ys, K, prior_sd, sigma, chain, key):
+    """Initial trace of one chain: (labels, means, log-likelihood)."""
+    L = lib()
+    _mh_sig(L)
+    y = np.ascontiguousarray(ys, dtype=np.float32)
+    z = np.zeros(len(y), dtype=np.int32)
+    mu = np.zeros(K)
+    st = np.zeros(2 * K + 2)
+    ll0 = C.c_double()
+    L.or_mh_gmm_chain(_ptr(y, C.c_float), len(y), K, prior_sd, sigma, chain, 0, 0, 1, key, _ptr(mu, C.c_double),
+                      _ptr(st, C.c_double), None, 0, _ptr(z, C.c_int32), C.byref(ll0))
+    return z, mu, ll0.value

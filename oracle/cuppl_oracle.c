@@ -622,3 +622,139 @@ int or_smc_step(uint64_t N, uint64_t key, uint32_t t, const uint64_t* aliasA, in
   free(C);
   return 0;
 }
+
+/* ---------------------------------------------------------------- LMH chains (GMM) ---- */
+/* Many independent single-site lightweight MH chains on
+ * the Gaussian mixture of SURVEY.md §8(d) C3, restating csrc/mh_kernels.cu in fp64:
+ * each step picks one of the K + D sites uniformly (Lemire on word 0 of Philox(chain, step, 0,
+ * TAG_MH); rejected words redrawn from sub-blocks 1, 2, ...), proposes from the site's prior
+ * (mean: normal(0, prior_sd) by Box-Muller on words 1, 2; label: Lemire on word 1), re-executes
+ * the model (full log-likelihood) and accepts iff log(u) < l' - l with u = u01_open0(word 3)
+ * (the resampled site's prior cancels with the proposal). */
+#define TAG_MH 5u
+#define TAG_MH_INIT 6u
+
+static inline void mh_block(uint64_t key, uint32_t chain, uint32_t step, uint32_t sub, uint32_t tag,
+                            uint32_t out[4]) {
+  const uint32_t ctr[4] = {chain, step, sub, tag};
+  const uint32_t k[2] = {(uint32_t)key, (uint32_t)(key >> 32)};
+  or_philox(ctr, k, out);
+}
+
+static double gmm_ll(const float* y, const int32_t* z, const double* mu, int D, double sigma) {
+  double s = 0.0;
+  for (int i = 0; i < D; ++i) {
+    const double r = ((double)y[i] - mu[z[i]]) / sigma;
+    s += -0.5 * r * r;
+  }
+  return s - D * (log(sigma) + 0.5 * log(2.0 * M_PI));
+}
+
+/* One chain. stats[2K + 2] as the GPU's; trace (optional) [n_rec][K]; mu_out[K]; returns ll. */
+double or_mh_gmm_chain(const float* y, int D, int K, double prior_sd, double sigma, uint32_t chain,
+                       uint32_t n_steps, uint32_t burn_in, uint32_t thin, uint64_t key,
+                       double* mu_out, double* stats, double* trace, uint32_t n_rec,
+                       int32_t* z_init_out, double* ll_init_out) {
+  int32_t* z = (int32_t*)malloc(sizeof(int32_t) * (size_t)D);
+  double mu[8] = {0};
+  for (int i = 0; i < D; ++i) {
+    uint32_t b[4], lab;
+    mh_block(key, chain, (uint32_t)i >> 2, 0, TAG_MH_INIT, b);
+    if (!or_lemire(b[i & 3], (uint32_t)K, &lab)) {
+      for (uint32_t r = 2;; ++r) {
+        uint32_t bb[4];
+        mh_block(key, chain, (uint32_t)i, r, TAG_MH_INIT, bb);
+        if (or_lemire(bb[0], (uint32_t)K, &lab)) break;
+      }
+    }
+    z[i] = (int32_t)lab;
+  }
+  for (int k = 0; k < K; ++k) {
+    uint32_t b[4];
+    double z0, z1, z2, z3;
+    mh_block(key, chain, (uint32_t)k >> 2, 1, TAG_MH_INIT, b);
+    or_box_muller(b[0], b[1], &z0, &z1);
+    or_box_muller(b[2], b[3], &z2, &z3);
+    const double zz[4] = {z0, z1, z2, z3};
+    mu[k] = prior_sd * zz[k & 3];
+  }
+  if (z_init_out) memcpy(z_init_out, z, sizeof(int32_t) * (size_t)D);
+  double ll = gmm_ll(y, z, mu, D, sigma);
+  if (ll_init_out) *ll_init_out = ll;
+  memset(stats, 0, sizeof(double) * (size_t)(2 * K + 2));
+  const uint32_t n_sites = (uint32_t)(K + D);
+  uint32_t rec = 0;
+  for (uint32_t s = 0; s < n_steps; ++s) {
+    uint32_t b[4], site = 0, zp = 0;
+    mh_block(key, chain, s, 0, TAG_MH, b);
+    if (!or_lemire(b[0], n_sites, &site)) {
+      for (uint32_t r = 1;; ++r) {
+        uint32_t bb[4];
+        mh_block(key, chain, s, r, TAG_MH, bb);
+        if (or_lemire(bb[0], n_sites, &site)) break;
+      }
+    }
+    double old = 0.0;
+    int32_t oldz = 0;
+    if (site < (uint32_t)K) {
+      double z0, z1;
+      or_box_muller(b[1], b[2], &z0, &z1);
+      old = mu[site];
+      mu[site] = prior_sd * z0;
+    } else {
+      if (!or_lemire(b[1], (uint32_t)K, &zp)) {
+        for (uint32_t r = 1;; ++r) {
+          uint32_t bb[4];
+          mh_block(key, chain, s, r, TAG_MH, bb);
+          if (or_lemire(bb[1], (uint32_t)K, &zp)) break;
+        }
+      }
+      oldz = z[site - K];
+      z[site - K] = (int32_t)zp;
+    }
+    const double llp = gmm_ll(y, z, mu, D, sigma);
+    const double logu = log(or_u01_open0(b[3]));
+    const int accept = logu < llp - ll;
+    if (accept) {
+      ll = llp;
+      stats[2 * K + 1] += 1.0;
+    } else if (site < (uint32_t)K) {
+      mu[site] = old;
+    } else {
+      z[site - K] = oldz;
+    }
+    if (s >= burn_in && (s - burn_in) % thin == 0) {
+      double srt[8];
+      for (int k = 0; k < K; ++k) {
+        const double v = mu[k];
+        int q = k;
+        while (q > 0 && srt[q - 1] > v) { srt[q] = srt[q - 1]; --q; }
+        srt[q] = v;
+      }
+      for (int k = 0; k < K; ++k) {
+        stats[k] += srt[k];
+        stats[K + k] += srt[k] * srt[k];
+        if (trace && rec < n_rec) trace[(size_t)rec * K + k] = srt[k];
+      }
+      stats[2 * K] += 1.0;
+      ++rec;
+    }
+  }
+  for (int k = 0; k < K; ++k) mu_out[k] = mu[k];
+  free(z);
+  return ll;
+}
+
+/* n_chains chains [chain_begin, +n) in parallel (OpenMP); outputs per chain as the GPU's. */
+int or_mh_gmm(const float* y, int D, int K, double prior_sd, double sigma, uint32_t n_chains,
+              uint32_t chain_begin, uint32_t n_steps, uint32_t burn_in, uint32_t thin, uint64_t key,
+              double* mu_out, double* ll_out, double* stats_out, int threads) {
+  const int T = n_threads(threads);
+#pragma omp parallel for num_threads(T) schedule(dynamic, 1)
+  for (int64_t c = 0; c < (int64_t)n_chains; ++c) {
+    ll_out[c] = or_mh_gmm_chain(y, D, K, prior_sd, sigma, chain_begin + (uint32_t)c, n_steps, burn_in,
+                                thin, key, mu_out + (size_t)c * K, stats_out + (size_t)c * (2 * K + 2),
+                                NULL, 0, NULL, NULL);
+  }
+  return 0;
+}

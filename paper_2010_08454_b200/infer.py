@@ -202,6 +202,25 @@ def _distribution_from_record(model, rec: N.IsRecord, n: int, launcher: IsLaunch
     return out
 
 
+def run_lmh(model, n_samples: int, rng, *, chains: int = 4096, burn_in: int = 0, thin: int = 1,
+            return_trace: bool = False, group=None, device=None):
+    """Lightweight Metropolis-Hastings as `chains` independent GPU chains of
+    `n_samples` steps (mh.py, kernel K7)."""
+    from .mh import run_lmh as _run
+
+    return _run(model, n_samples, rng, chains=chains, burn_in=burn_in, thin=thin,
+                return_trace=return_trace, group=group, device=device)
+
+
+def run_smc(model, n_particles: int, rng, *, steps: int | None = None, record_ancestors: bool = False,
+            hist_steps=None, group=None, device=None):
+    """Bootstrap particle filter with systematic resampling every step (smc.py, K4-K6)."""
+    from .smc import run_smc as _run
+
+    return _run(model, n_particles, rng, steps=steps, record_ancestors=record_ancestors,
+                hist_steps=hist_steps, group=group, device=device)
+
+
 def run_importance(model, n_samples: int, rng, *, return_traces: bool = False, group=None,
                    device=None) -> EmpiricalDistribution:
     """Likelihood-weighting importance sampling on the GPU.

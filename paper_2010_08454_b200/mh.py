@@ -1,0 +1,96 @@
+"""Many-chain lightweight Metropolis-Hastings (K7) — the GPU form of run_lmh.
+
+The reference runs ONE single-site LMH chain. Here `chains` independent chains
+run in one kernel (one warp each: replicas — with torch.distributed the chains
+are sharded over ranks and only the per-chain statistics are all-gathered at the end).
+Every step re-executes the model (full log-likelihood, the reference's re-execution semantics)
+and accepts with the single-site prior-proposal ratio. The oracle restatement is
+oracle/cuppl_oracle.c or_mh_gmm.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .errors import InferRuntimeError
+from .models import GaussianMixture
+from .rng import key_of, seed_of
+
+
+@dataclass
+class MhResult:
+    """Posterior summary of the return value (the sorted component means, label switching)."""
+
+    n_chains: int
+    n_steps: int
+    recorded: int                 # recorded samples per chain (after burn-in / thinning)
+    mean: np.ndarray              # pooled posterior mean of the sorted means
+    var: np.ndarray               # pooled posterior variance
+    chain_means: np.ndarray       # [chains, K] per-chain means (for MC standard errors / R-hat)
+    acceptance: float
+    final_mu: object = None       # device tensor [chains, K]
+    final_log_lik: object = None  # device tensor [chains]
+    trace: object = None          # device tensor [chains, recorded, K] when requested
+    extra: dict = field(default_factory=dict)
+
+    def mcse(self) -> np.ndarray:
+        """Monte Carlo standard error of `mean` from the between-chain spread."""
+        return self.chain_means.std(axis=0, ddof=1) / math.sqrt(self.n_chains)
+
+
+def run_lmh(model: GaussianMixture, n_samples: int, rng, *, chains: int = 4096, burn_in: int = 0,
+            thin: int = 1, return_trace: bool = False, group=None, device=None) -> MhResult:
+    """`chains` independent LMH chains of `n_samples` steps each on the GPU."""
+    import torch
+
+    from .infer import _world, shard_range
+
+    if not isinstance(model, GaussianMixture):
+        raise InferRuntimeError(f"no MH kernel for {type(model).__name__}")
+    if n_samples < 1 or chains < 1:
+        raise ValueError("n_samples and chains must be >= 1")
+    L = N.lib()
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    rank, world = _world(group)
+    c0, c1 = shard_range(chains, rank, world)
+    nc = c1 - c0
+    K, D = model.K, len(model.ys)
+    dpad = L.cuppl_mh_padded_points(D)
+    y = torch.zeros(dpad, dtype=torch.float32, device=dev)
+    y[:D] = torch.from_numpy(np.ascontiguousarray(model.ys, dtype=np.float32)).to(dev)
+    n_rec = 0 if n_samples <= burn_in else (n_samples - burn_in + thin - 1) // thin
+    mu = torch.empty((max(nc, 1), K), dtype=torch.float32, device=dev)
+    ll = torch.empty(max(nc, 1), dtype=torch.float32, device=dev)
+    st = torch.zeros((max(nc, 1), 2 * K + 2), dtype=torch.float64, device=dev)
+    tr = torch.empty((max(nc, 1), max(n_rec, 1), K), dtype=torch.float32, device=dev) if return_trace else None
+    if nc:
+        rc = L.cuppl_mh_gmm(N.ptr(y), D, K, float(model.prior_sd), float(model.sigma), nc, c0, n_samples,
+                            burn_in, thin, key_of(rng), N.ptr(mu), N.ptr(ll), N.ptr(st), N.ptr(tr),
+                            n_rec, N.stream_ptr(dev))
+        N.check(rc, "mh_gmm", seed=seed_of(rng))
+    stats = st[:nc]
+    if world > 1:  # pragma: no cover - multi-GPU
+        import torch.distributed as dist
+
+        sizes = [shard_range(chains, q, world)[1] - shard_range(chains, q, world)[0] for q in range(world)]
+        buf = torch.zeros((max(sizes) * world, 2 * K + 2), dtype=torch.float64, device=dev)
+        pad = torch.zeros((max(sizes), 2 * K + 2), dtype=torch.float64, device=dev)
+        pad[:nc] = stats
+        dist.all_gather_into_tensor(buf, pad, group=group)
+        stats = torch.cat([buf[q * max(sizes):q * max(sizes) + sizes[q]] for q in range(world)])
+    s = stats.cpu().numpy()
+    nrec = s[:, 2 * K]
+    tot = nrec.sum()
+    if tot <= 0:
+        raise InferRuntimeError("no recorded samples (n_samples <= burn_in)")
+    mean = s[:, :K].sum(axis=0) / tot
+    var = s[:, K:2 * K].sum(axis=0) / tot - mean ** 2
+    chain_means = s[:, :K] / np.maximum(nrec, 1)[:, None]
+    acc = float(s[:, 2 * K + 1].sum() / (len(s) * n_samples))
+    return MhResult(n_chains=chains, n_steps=n_samples, recorded=int(nrec[0]) if len(nrec) else 0, mean=mean,
+                    var=var, chain_means=chain_means, acceptance=acc, final_mu=mu[:nc], final_log_lik=ll[:nc],
+                    trace=None if tr is None else tr[:nc])

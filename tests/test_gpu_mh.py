@@ -1,0 +1,87 @@
+"""GPU tests of the many-chain LMH engine (K7) against the CPU restatement and closed forms."""
+
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+KEY = 0x9E0160293A33AAF7
+
+
+def test_mh_initial_trace_and_short_chain_match_oracle(cuda, oracle_lib):
+    """Zero steps: initial means / log-likelihood equal the oracle's; a few steps: identical
+    accept decisions except where fp32 vs fp64 re-execution straddles log u (rare)."""
+    import torch
+
+    from oracle import core
+    from paper_2010_08454_b200 import _native as N
+    from paper_2010_08454_b200 import models
+
+    m = models.GaussianMixture.synthetic(n_points=1000)
+    L = N.lib()
+    K, D = m.K, len(m.ys)
+    y = torch.zeros(L.cuppl_mh_padded_points(D), device=cuda)
+    y[:D] = torch.tensor(m.ys, device=cuda)
+    nc = 64
+    mu = torch.empty((nc, K), device=cuda)
+    ll = torch.empty(nc, device=cuda)
+    st = torch.zeros((nc, 2 * K + 2), dtype=torch.float64, device=cuda)
+    N.check(L.cuppl_mh_gmm(N.ptr(y), D, K, 10.0, 1.0, nc, 0, 0, 0, 1, KEY, N.ptr(mu), N.ptr(ll), N.ptr(st),
+                           None, 0, N.stream_ptr()))
+    mu0, ll0 = mu.cpu().numpy(), ll.cpu().numpy()
+    for c in range(nc):
+        z, mref, lref = core.mh_gmm_init(m.ys, K, 10.0, 1.0, c, KEY)
+        assert np.allclose(mu0[c], mref, rtol=1e-5, atol=1e-4)
+        assert abs(ll0[c] - lref) <= 1e-4 * abs(lref) + 1e-2
+    steps = 200
+    N.check(L.cuppl_mh_gmm(N.ptr(y), D, K, 10.0, 1.0, nc, 0, steps, 0, 1, KEY, N.ptr(mu), N.ptr(ll), N.ptr(st),
+                           None, 0, N.stream_ptr()))
+    mref, lref, sref = core.mh_gmm(m.ys, K, 10.0, 1.0, nc, steps, KEY)
+    got = st.cpu().numpy()
+    same = np.all(np.isclose(mu.cpu().numpy(), mref, rtol=1e-4, atol=1e-3), axis=1)
+    assert same.mean() > 0.9, same.mean()  # chains whose decisions never straddled
+    assert np.array_equal(got[same, 2 * K + 1], sref[same, 2 * K + 1])
+
+
+def test_mh_single_component_matches_conjugate_posterior(cuda):
+    """K = 1: mu | y ~ normal with precision 1/100 + D; chains must recover it."""
+    from paper_2010_08454_b200 import Rng, infer, models
+
+    rs = np.random.default_rng(3)
+    y = 1.7 + rs.standard_normal(400)
+    m = models.GaussianMixture(y, K=1)
+    prec = 1 / 100 + len(y)
+    mean = y.astype(np.float32).astype(float).sum() / prec
+    post = infer.run_lmh(m, 2000, Rng(5), chains=512, burn_in=200)
+    assert abs(post.mean[0] - mean) < 5 * post.mcse()[0] + 1e-3
+    assert abs(post.var[0] - 1 / prec) < 0.2 / prec
+    assert 0.0 < post.acceptance < 1.0
+
+
+def test_mh_gmm_recovers_separated_means(cuda):
+    from paper_2010_08454_b200 import Rng, infer, models
+
+    m = models.GaussianMixture.synthetic(n_points=2000)
+    post = infer.run_lmh(m, 4000, Rng(1), chains=256, burn_in=2000)
+    # sorted posterior means near the generating (-8, -4, 0, 4, 8) for chains that found the mode
+    good = np.all(np.abs(post.chain_means - np.array([-8, -4, 0, 4, 8])) < 1.0, axis=1)
+    assert good.mean() > 0.3
+    assert np.all(np.abs(np.median(post.chain_means[good], axis=0) - [-8, -4, 0, 4, 8]) < 0.3)
+
+
+def test_mh_statistics_match_oracle_chains(cuda, oracle_lib):
+    """Same model, same chains: GPU and oracle posterior summaries agree within MC error."""
+    from oracle import core
+    from paper_2010_08454_b200 import Rng, infer, models
+
+    m = models.GaussianMixture.synthetic(n_points=300, K=3)
+    rng = Rng(11)
+    post = infer.run_lmh(m, 3000, rng, chains=128, burn_in=1000)
+    mref, lref, sref = core.mh_gmm(m.ys, 3, 10.0, 1.0, 128, 3000, rng.key, burn_in=1000)
+    ref_chain = sref[:, :3] / sref[:, [6]]
+    se = np.sqrt(post.chain_means.var(axis=0, ddof=1) / 128 + ref_chain.var(axis=0, ddof=1) / 128)
+    assert np.all(np.abs(post.chain_means.mean(axis=0) - ref_chain.mean(axis=0)) < 5 * se + 0.05)
+    acc_ref = sref[:, 7].sum() / (128 * 3000)
+    assert abs(post.acceptance - acc_ref) < 0.02
