@@ -203,6 +203,21 @@ CUPPL_API int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uin
 CUPPL_API int cuppl_smc_fold(uint64_t n_local, double* stats_out, void* workspace,
                              size_t workspace_bytes, void* stream);
 
+/* ---- K3: normalize / empirical-posterior histogram and mode ------------ */
+/* lw[n] (device, fp64 or fp32) and bin[n] (device int32 value ids, NULL = all 0) ->
+ *   bins[n_bins] (device u64): sum over the bin of floor(exp(lw - M) 2^s), s = *scale_bits
+ *     (host int, set by the call: 62 - ceil(log2 n), so sums never overflow);
+ *   out[6] (device fp64): M = max finite lw (-inf if none), sum exp(2 (lw - M)), argmax lw,
+ *     argmax index (u64 bits), number of finite lw (u64 bits), 0.
+ * Integer bin sums make the result independent of the reduction order. */
+CUPPL_API size_t cuppl_normalize_workspace_bytes(void);
+CUPPL_API int cuppl_normalize_f64(const double* lw, const int32_t* bin, uint64_t n, int n_bins,
+                                  uint64_t* bins, double* out, int* scale_bits, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+CUPPL_API int cuppl_normalize_f32(const float* lw, const int32_t* bin, uint64_t n, int n_bins,
+                                  uint64_t* bins, double* out, int* scale_bits, void* workspace,
+                                  size_t workspace_bytes, void* stream);
+
 /* ---- K7: many-chain lightweight Metropolis-Hastings (replaces run_lmh) -- */
 /* Gaussian mixture: mu_k ~ normal(0, prior_sd), k < K <= 7;
  * z_i ~ categorical(1/K, ...); observe(normal(mu[z_i], sigma), y_i), i < D. One warp per chain;

@@ -91,6 +91,9 @@ _SIG = {
     "cuppl_is_poly": ([_P, _P, C.c_int, _U64, _U64, _U64, _P, _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
     "cuppl_is_linreg": ([_P, _P, C.c_int, _F32, _U64, _U64, _U64, _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
     "cuppl_is_record_merge": ([_P, C.c_int, _P], C.c_int),
+    "cuppl_normalize_workspace_bytes": ([], C.c_size_t),
+    "cuppl_normalize_f64": ([_P, _P, _U64, C.c_int, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
+    "cuppl_normalize_f32": ([_P, _P, _U64, C.c_int, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
     "cuppl_mh_padded_points": ([C.c_int], C.c_int),
     "cuppl_mh_gmm": ([_P, C.c_int, C.c_int, _F32, _F32, _U32, _U32, _U32, _U32, _U32, _U64, _P, _P, _P, _P,
                       _U32, _P], C.c_int),

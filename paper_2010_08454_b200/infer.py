@@ -202,6 +202,74 @@ def _distribution_from_record(model, rec: N.IsRecord, n: int, launcher: IsLaunch
     return out
 
 
+def normalize_tensors(lw, bins=None, n_bins: int = 1) -> dict:
+    """K3 on device tensors: lw (fp32/fp64 CUDA tensor), bins (int32 value ids or None).
+
+    Returns {"max_lw", "probs" (np.ndarray [n_bins]), "log_z", "ess", "argmax", "argmax_lw",
+    "n_finite"}; raises AllZeroWeightError when every weight is -inf."""
+    import torch
+
+    L = N.lib()
+    dev = lw.device
+    lw = lw.contiguous()
+    n = lw.numel()
+    if bins is not None:
+        bins = bins.to(torch.int32).contiguous()
+    out_bins = torch.empty(n_bins, dtype=torch.int64, device=dev)
+    out = torch.empty(6, dtype=torch.float64, device=dev)
+    ws = torch.empty(int(L.cuppl_normalize_workspace_bytes()), dtype=torch.uint8, device=dev)
+    sb = C.c_int(0)
+    fn = L.cuppl_normalize_f64 if lw.dtype == torch.float64 else L.cuppl_normalize_f32
+    if lw.dtype not in (torch.float64, torch.float32):
+        lw = lw.to(torch.float64)
+        fn = L.cuppl_normalize_f64
+    N.check(fn(N.ptr(lw), N.ptr(bins), n, n_bins, N.ptr(out_bins), N.ptr(out), C.byref(sb), N.ptr(ws),
+               ws.numel(), N.stream_ptr(dev)), "normalize")
+    o = out.cpu().numpy()
+    b = out_bins.cpu().numpy().view(np.uint64)
+    nf = int(o[4:5].view(np.uint64)[0])
+    if nf == 0:
+        raise AllZeroWeightError("every weight is -inf (SPEC.md:421)")
+    total = int(b.sum(dtype=np.uint64)) if n_bins > 1 else int(b[0])
+    total_f = float(total) * 2.0 ** -sb.value
+    M = float(o[0])
+    probs = b.astype(np.float64) / float(total) if total > 0 else np.zeros(n_bins)
+    return {"max_lw": M, "probs": probs, "log_z": M + math.log(total_f) - math.log(n),
+            "ess": total_f * total_f / float(o[1]), "argmax": int(o[3:4].view(np.uint64)[0]),
+            "argmax_lw": float(o[2]), "n_finite": nf, "scale_bits": sb.value}
+
+
+def normalize(samples, *, device=None) -> EmpiricalDistribution:
+    """normalize(samples): WeightedSample list (or (value, log_weight) pairs)
+    -> EmpiricalDistribution. Support is merged by structural equality (value_key,
+    cuppl/values.py:101-122) on the host; the log-sum-exp and the per-value masses run in K3."""
+    import torch
+
+    from .values import value_key
+
+    if not samples:
+        raise AllZeroWeightError("normalize of an empty sample")
+    ids, values, lws = {}, [], []
+    idx = []
+    for s in samples:
+        v, lw = (s.value, s.log_weight) if isinstance(s, WeightedSample) else s
+        k = value_key(v)
+        if k not in ids:
+            ids[k] = len(values)
+            values.append(v)
+        idx.append(ids[k])
+        lws.append(float(lw))
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    lw_t = torch.tensor(lws, dtype=torch.float64, device=dev)
+    b_t = torch.tensor(idx, dtype=torch.int32, device=dev)
+    r = normalize_tensors(lw_t, b_t, len(values))
+    support = [(v, float(p)) for v, p in zip(values, r["probs"]) if p > 0]
+    return EmpiricalDistribution(support=support, n=len(samples), log_z=r["log_z"], ess=r["ess"],
+                                 mode=samples[r["argmax"]].value if isinstance(samples[r["argmax"]], WeightedSample)
+                                 else samples[r["argmax"]][0],
+                                 mode_log_weight=r["argmax_lw"], mode_index=r["argmax"], record=r)
+
+
 def run_lmh(model, n_samples: int, rng, *, chains: int = 4096, burn_in: int = 0, thin: int = 1,
             return_trace: bool = False, group=None, device=None):
     """Lightweight Metropolis-Hastings as `chains` independent GPU chains of

@@ -240,3 +240,53 @@ def test_all_zero_weights_raise(cuda):
     m = models.LinearRegression([0.0, 1.0], [np.inf, 0.0])
     with pytest.raises(errors.AllZeroWeightError):
         infer.run_importance(m, 1000, Rng(1))
+
+
+def test_normalize_spec_rows(cuda):
+    from paper_2010_08454_b200 import errors, infer
+
+    d = infer.normalize([("x", math.log(0.2)), ("y", math.log(0.2))])
+    assert d.support == [("x", 0.5), ("y", 0.5)]
+    d = infer.normalize([infer.WeightedSample("x", -1000.0), infer.WeightedSample("y", -1001.0)])
+    assert d.probability("x") == pytest.approx(math.e / (math.e + 1), abs=1e-9)
+    assert d.probability("y") == pytest.approx(1 / (math.e + 1), abs=1e-9)
+    d = infer.normalize([("x", -math.inf), ("y", 0.0)])
+    assert d.support == [("y", 1.0)]
+    with pytest.raises(errors.AllZeroWeightError):
+        infer.normalize([("x", -math.inf), ("y", -math.inf)])
+
+
+def test_normalize_merges_support_and_is_permutation_invariant(cuda, oracle_lib):
+    from oracle import semantics as S
+    from paper_2010_08454_b200 import infer
+
+    rs = np.random.default_rng(0)
+    vals = [int(v) for v in rs.integers(0, 20, 5000)] + [(1, 2.0), True, None]
+    lws = list(rs.normal(-3, 2, len(vals)))
+    samples = list(zip(vals, lws))
+    d = infer.normalize(samples)
+    ref, lz = S.normalize(samples)
+    assert abs(sum(p for _, p in d.support) - 1) < 1e-12
+    for v, p in d.support:
+        assert p == pytest.approx(ref[S.value_key(v)][1], abs=1e-9)
+    assert d.log_z == pytest.approx(lz, abs=1e-9)
+    perm = rs.permutation(len(samples))
+    d2 = infer.normalize([samples[i] for i in perm])
+    assert sorted(d.support, key=repr) == sorted(d2.support, key=repr)  # identical bytes
+
+
+def test_normalize_tensors_matches_is_record(cuda):
+    """K3 over IS traces reproduces the fused K2 record (degree histogram, log Z, mode)."""
+    import torch
+
+    from paper_2010_08454_b200 import Rng, infer, models
+
+    m = models.PolyRegression.synthetic()
+    post = infer.run_importance(m, 2_000_000, Rng(4), return_traces=True)
+    lw = post.traces["log_weight"]
+    deg = post.traces["degree"] - 2
+    r = infer.normalize_tensors(lw, deg, 3)
+    for d, p in post.support:
+        assert r["probs"][d - 2] == pytest.approx(p, rel=1e-4, abs=1e-7)
+    assert r["log_z"] == pytest.approx(post.log_z, abs=1e-4)
+    assert r["argmax"] == post.mode_index
