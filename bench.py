@@ -2,14 +2,16 @@
 """Benchmark: weighted particles/s of GPU importance sampling (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload linreg|poly]
+                    [--workload linreg|poly|smc|mh]
 
 Default workload (BASELINE.json configs[1]): Bayesian linear regression,
 1e9 particles per GPU (weak scaling), 1,000 synthetic points, prior normal(0,10) on (a, b).
 A step is one full importance-sampling pass over those particles: Philox draws, the model's
 1,000 observe() terms, the fused log-sum-exp / ESS / moment / mode reduction, and (N > 1) the
 per-rank record all-gather over NCCL. `--workload poly` runs the Fig.1 polynomial model
-(configs[4], C5: 1.25e10 particles per GPU, 20 points).
+(configs[4], C5: 1.25e10 particles per GPU, 20 points); `--workload smc` the HMM particle
+filter (configs[3], SMC time-steps/s on 1e8 particles) and `--workload mh` the 4096-chain LMH
+sampler (configs[2], chain-steps/s).
 
 `--impl reference` times the reference's CPU path — the C restatement in oracle/ (the
 reference ships no executable engine) — on all host cores, rank 0 only.
@@ -47,6 +49,23 @@ WORKLOADS = {
         "particles_per_gpu": 12_500_000_000,
         "n_points": 20,
     },
+    "smc": {
+        "name": "C4: HMM S=50 bootstrap particle filter, 1e8 particles, T=1000, systematic resampling "
+                "every step (BASELINE configs[3], single GPU)",
+        "particles_per_gpu": 100_000_000,
+        "n_points": 1000,
+    },
+    "mh": {
+        "name": "C3: GMM K=5, 10k points, 4096 LMH chains x 10k steps (BASELINE configs[2])",
+        "particles_per_gpu": 4096,
+        "n_points": 10_000,
+    },
+}
+METRICS = {
+    "linreg": (METRIC, UNIT),
+    "poly": (METRIC, UNIT),
+    "smc": ("SMC steps/sec", "time-steps/s"),
+    "mh": ("MH chain-steps/sec", "chain-steps/s"),
 }
 
 
@@ -56,6 +75,10 @@ def make_model(workload: str):
     w = WORKLOADS[workload]
     if workload == "linreg":
         return models.LinearRegression.synthetic(n_points=w["n_points"])
+    if workload == "smc":
+        return models.HiddenMarkovModel.synthetic(S=50, T=w["n_points"])
+    if workload == "mh":
+        return models.GaussianMixture.synthetic(n_points=w["n_points"])
     return models.PolyRegression.synthetic(n_points=w["n_points"])
 
 
@@ -313,43 +336,197 @@ def run_ours(args) -> dict | None:
     return result
 
 
+def _hbm_peak() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+        except (KeyError, ValueError, json.JSONDecodeError):
+            pass
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def run_ours_engine(args) -> dict | None:
+    """SMC (C4) and many-chain MH (C3) workloads on one GPU."""
+    import torch
+
+    from paper_2010_08454_b200 import build as B
+
+    B.build()
+    from paper_2010_08454_b200 import Rng, infer, smc
+
+    rank, world, local = dist_env()
+    if world > 1:
+        if rank == 0:
+            print(json.dumps({"metric": METRICS[args.workload][0], "unavailable":
+                              "multi-process SMC/MH bench not wired yet (single-GPU workloads)"}))
+        return None
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    wl = WORKLOADS[args.workload]
+    model = make_model(args.workload)
+    metric, unit = METRICS[args.workload]
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+    if args.workload == "smc":
+        n = args.particles or wl["particles_per_gpu"]
+        T = model.T
+
+        def step(k):
+            r = smc.SmcRunner(model, n, Rng(1).split(k), steps=T, device=device)
+            r.init()
+            for t in range(T):
+                r.step(t)
+            return r
+        units_per_step = T
+    else:
+        chains = args.particles or wl["particles_per_gpu"]
+        n_steps = args.mh_steps
+
+        def step(k):
+            return infer.run_lmh(model, n_steps, Rng(1).split(k), chains=chains, device=device)
+        units_per_step = chains * n_steps
+    for k in range(args.warmup):
+        step(10_000 + k)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    last = None
+    for k in range(args.steps):
+        flush.zero_()
+        starts[k].record()
+        last = step(k)
+        ends[k].record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    t_ms = sum(step_ms)
+    value = units_per_step * args.steps / (t_ms / 1e3)
+    res = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+           "scaling": "strong" if args.workload == "smc" else "weak", "vs_baseline": None,
+           "dtype": "f32", "data": "synthetic (numpy seed 0; SURVEY.md §8(d))",
+           "config": {"workload": wl["name"], "l2": "flushed between timed steps (256 MiB write)"},
+           "clocks": clk}
+    if args.workload == "smc":
+        peak, src = _hbm_peak()
+        bytes_step = 14.0 * n  # K5 reads lw; K6 reads lw + x, writes x' + lw' (u8 state)
+        achieved = bytes_step * units_per_step / (t_ms / args.steps / 1e3) / 1e9
+        res["config"].update({"particles": n, "time_steps": T, "state": "u8", "resampling": "systematic every step"})
+        res["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                           "frac": achieved / peak, "traffic": load_traffic("smc"), "peak_source": src,
+                           "bytes_per_particle_step": 14}
+        res["particle_steps_per_s"] = n * units_per_step * args.steps / (t_ms / 1e3)
+        res["gpu_launches"] = args.steps * (1 + 2 * T)
+        # e2e: public API from host data (model arrays host -> device tables), result to host
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = infer.run_smc(model, n, Rng(99))
+        e1.record()
+        torch.cuda.synchronize()
+        res["e2e"] = {"value": T / (e0.elapsed_time(e1) / 1e3), "unit": unit,
+                      "h2d_bytes_per_step": int(model.A.nbytes + model.ys.nbytes + model.mu.nbytes),
+                      "d2h_bytes_per_step": int(T * 4 * 8 + T * 16 + T * 4 + 50 * 8),
+                      "api": "paper_2010_08454_b200.infer.run_smc(model, n, rng)", "log_z": out.log_z}
+    else:
+        peak = calibrate_fp32(device)
+        fl = 3.0 * wl["n_points"]  # per chain-step: per point (y - mu) add + fma(r, r, acc)
+        achieved = fl * units_per_step / (t_ms / args.steps / 1e3)
+        res["config"].update({"chains": units_per_step // args.mh_steps, "steps_per_chain": args.mh_steps,
+                              "semantics": "full re-execution per step (reference LMH)"})
+        res["roofline"] = {"bound": "fp32", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+                           "frac": achieved / peak, "traffic": load_traffic("mh"),
+                           "peak_source": "measured FFMA2 ceiling (csrc/calib_kernels.cu kind 0)",
+                           "flops_per_chain_step": fl}
+        res["gpu_launches"] = args.steps
+        res["acceptance"] = last.acceptance
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = infer.run_lmh(model, args.mh_steps, Rng(99), chains=units_per_step // args.mh_steps)
+        e1.record()
+        torch.cuda.synchronize()
+        res["e2e"] = {"value": units_per_step / (e0.elapsed_time(e1) / 1e3), "unit": unit,
+                      "h2d_bytes_per_step": int(model.ys.nbytes), "d2h_bytes_per_step": int(units_per_step // args.mh_steps * 12 * 8),
+                      "api": "paper_2010_08454_b200.infer.run_lmh(model, n, rng, chains=...)"}
+    if not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline_engine(args, model)
+    return res
+
+
+def cpu_baseline_engine(args, model) -> dict:
+    from oracle import core
+
+    core.build()
+    threads = os.cpu_count() or 1
+    if args.workload == "smc":
+        n, T = 100_000, 200
+        t0 = time.perf_counter()
+        core.smc_run(model, n, 0x9E0160293A33AAF7, steps=T)
+        dt = time.perf_counter() - t0
+        return {"value": T / dt, "unit": "time-steps/s", "cores": 1, "kind": "port",
+                "sample": f"{n} particles x {T} steps, oracle/cuppl_oracle.c or_smc_step (scalar, 1 thread); "
+                          f"{n * T / dt:.3g} particle-steps/s"}
+    chains, steps = 64, 2000
+    t0 = time.perf_counter()
+    core.mh_gmm(model.ys, model.K, model.prior_sd, model.sigma, chains, steps, 0x9E0160293A33AAF7, threads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": chains * steps / dt, "unit": "chain-steps/s", "cores": threads, "kind": "port",
+            "sample": f"{chains} chains x {steps} steps, oracle/cuppl_oracle.c or_mh_gmm (fp64, OpenMP {threads})"}
+
+
 def run_reference(args) -> dict | None:
     rank, world, _ = dist_env()
     if rank != 0:
         return None
     wl = WORKLOADS[args.workload]
     model = make_model(args.workload)
+    metric, unit = METRICS[args.workload]
     from oracle import core
 
     core.build()
     threads = os.cpu_count() or 1
     key = 0x9E0160293A33AAF7
-    per_step = 100_000 if args.workload == "linreg" else 5_000_000
+    if args.workload == "smc":
+        per_step, cores = 20_000, 1
+        sample = f"{per_step} particles x 50 time steps per step (or_smc_step, scalar)"
 
-    def step(k):
-        if args.workload == "linreg":
-            core.is_linreg(model.xs, model.ys, model.sigma, k * per_step, (k + 1) * per_step, key, threads=threads)
-        else:
-            core.is_poly(model.xs, model.ys, k * per_step, (k + 1) * per_step, key, threads=threads)
+        def step(k):
+            core.smc_run(model, per_step, key + k, steps=50)
+        units = 50
+    elif args.workload == "mh":
+        per_step, cores = 64, threads
+        sample = f"{per_step} chains x 200 steps per step (or_mh_gmm, fp64, OpenMP {threads})"
 
+        def step(k):
+            core.mh_gmm(model.ys, model.K, model.prior_sd, model.sigma, per_step, 200, key + k, threads=threads)
+        units = per_step * 200
+    else:
+        per_step, cores = (1_000_000 if args.workload == "linreg" else 20_000_000), threads
+        sample = (f"{per_step} particles per step of the same workload (oracle/cuppl_oracle.c: C restatement of "
+                  "the reference semantics; the reference ships no executable inference engine)")
+
+        def step(k):
+            if args.workload == "linreg":
+                core.is_linreg(model.xs, model.ys, model.sigma, k * per_step, (k + 1) * per_step, key, threads=threads)
+            else:
+                core.is_poly(model.xs, model.ys, k * per_step, (k + 1) * per_step, key, threads=threads)
+        units = per_step
     for k in range(args.warmup):
         step(1000 + k)
     t0 = time.perf_counter()
     for k in range(args.steps):
         step(k)
     dt = time.perf_counter() - t0
-    value = per_step * args.steps / dt
+    value = units * args.steps / dt
     return {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": wl["name"], "particles_per_step": per_step, "n_points": wl["n_points"]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{per_step} particles per step of the same workload "
-                                   "(oracle/cuppl_oracle.c: C restatement of the reference semantics; "
-                                   "the reference ships no executable inference engine)"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "config": {"workload": wl["name"], "units_per_step": units, "n_points": wl["n_points"]},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
@@ -362,10 +539,16 @@ def main():
     ap.add_argument("--workload", choices=tuple(WORKLOADS), default="linreg")
     ap.add_argument("--particles", type=int, default=0, help="override particles per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mh-steps", type=int, default=10_000, help="MH steps per chain (workload mh)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
-    res = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if args.impl == "reference":
+        res = run_reference(args)
+    elif args.workload in ("smc", "mh"):
+        res = run_ours_engine(args)
+    else:
+        res = run_ours(args)
     if res is not None:
         print(json.dumps(res), flush=True)
 
