@@ -10,9 +10,12 @@
 // oracle/cuppl_oracle.c (same Philox words; fp64).
 //
 // Layout: y (fp32, zero padded to 256 points) is staged once per CTA in shared memory and shared
-// by its chains; each chain keeps its labels packed two per byte (3 bits each, code 7 = padding)
-// and a 64-entry table of (-mu_a, -mu_b) pairs, so one byte of labels and one LDS.64 feed one
-// FADD2 + FFMA2 for two points: ~2.4 instructions per point per re-execution.
+// by its chains; each chain keeps one byte per pair of points, code = a W + b (W = K + 1, label
+// K = padding with mu = 0), and two 64-entry tables TA[code] = -mu_a, TB[code] = -mu_b. Lane l
+// handles float4 l + 32 j (points 4f..4f+3, pair codes read as one u16), so the y loads, the
+// code loads and the table lookups are all bank-conflict free; each pair of points costs two
+// LDS.32 + one FADD2 + one FFMA2. The kernel is bound by shared-memory bandwidth (about 8.5 B
+// per point per re-execution).
 //
 // Philox counters: (chain, step, sub, TAG_MH) per step (sub > 0 only for Lemire redraws);
 // initial trace: labels from (chain, i >> 2, 0, TAG_MH_INIT) word i & 3, means from
@@ -25,8 +28,9 @@ namespace cuppl {
 namespace {
 
 struct ChainSmem {
-  uint8_t* z;     // [D_pad / 2] packed label pairs (a << 3 | b)
-  float2* tab;    // [64] (-mu_a, -mu_b)
+  uint8_t* z;     // [D_pad / 2] pair codes a W + b
+  float* ta;      // [64] -mu_a of each code
+  float* tb;      // [64] -mu_b of each code
   float* mu;      // [8]
   double* stats;  // [2 * kMhMaxK + 2]
 };
@@ -34,7 +38,7 @@ struct ChainSmem {
 __host__ __device__ inline size_t align16(size_t v) { return (v + 15) & ~static_cast<size_t>(15); }
 
 __host__ __device__ inline size_t chain_bytes(int D_pad) {
-  return align16(D_pad / 2) + 64 * sizeof(float2) + 8 * sizeof(float) +
+  return align16(D_pad / 2) + 2 * 64 * sizeof(float) + 8 * sizeof(float) +
          (2 * kMhMaxK + 2) * sizeof(double);
 }
 
@@ -43,28 +47,28 @@ __device__ __forceinline__ uint4 mh_block(PhiloxKey k, unsigned int chain, unsig
   return philox4x32_10(make_uint4(chain, step, sub, tag), k.k0, k.k1);
 }
 
-__device__ __forceinline__ void rebuild_table(const ChainSmem& c, int lane) {
-  for (int e = lane; e < 64; e += 32) c.tab[e] = make_float2(-c.mu[e >> 3], -c.mu[e & 7]);
+__device__ __forceinline__ void rebuild_table(const ChainSmem& c, int lane, int W) {
+  for (int e = lane; e < 64; e += 32) {
+    const int a = e / W, b = e - a * W;
+    c.ta[e] = a < 8 ? -c.mu[a] : 0.f;
+    c.tb[e] = -c.mu[b];
+  }
 }
 
 // Full re-execution: sum_i -0.5 ((y_i - mu_{z_i}) / sigma)^2 + const, fixed reduction order.
-__device__ __forceinline__ float ll_pass(const float4* y4, const uint32_t* z4, const float2* tab,
-                                         int nwords, float nhiv, float ll_const, int lane) {
+__device__ __forceinline__ float ll_pass(const float4* y4, const unsigned short* z2, const float* ta,
+                                         const float* tb, int nf4, float nhiv, float ll_const,
+                                         int lane) {
   f32x2 acc0 = pack2(0.f, 0.f), acc1 = pack2(0.f, 0.f);
 #pragma unroll 4
-  for (int wi = lane; wi < nwords; wi += 32) {
-    const uint32_t zw = z4[wi];
-    const float4 ya = y4[2 * wi], yb = y4[2 * wi + 1];
-    const float2 m0 = tab[zw & 0xFFu], m1 = tab[(zw >> 8) & 0xFFu];
-    const float2 m2 = tab[(zw >> 16) & 0xFFu], m3 = tab[zw >> 24];
-    const f32x2 r0 = add2(pack2(ya.x, ya.y), pack2(m0.x, m0.y));
-    const f32x2 r1 = add2(pack2(ya.z, ya.w), pack2(m1.x, m1.y));
-    const f32x2 r2 = add2(pack2(yb.x, yb.y), pack2(m2.x, m2.y));
-    const f32x2 r3 = add2(pack2(yb.z, yb.w), pack2(m3.x, m3.y));
+  for (int f = lane; f < nf4; f += 32) {
+    const unsigned int zz = z2[f];  // codes of pairs 2f, 2f + 1
+    const float4 y = y4[f];
+    const unsigned int c0 = zz & 0xFFu, c1 = zz >> 8;
+    const f32x2 r0 = add2(pack2(y.x, y.y), pack2(ta[c0], tb[c0]));
+    const f32x2 r1 = add2(pack2(y.z, y.w), pack2(ta[c1], tb[c1]));
     acc0 = fma2(r0, r0, acc0);
     acc1 = fma2(r1, r1, acc1);
-    acc0 = fma2(r2, r2, acc0);
-    acc1 = fma2(r3, r3, acc1);
   }
   const float2 s0 = unpack2(acc0), s1 = unpack2(acc1);
   float s = (s0.x + s0.y) + (s1.x + s1.y);
@@ -93,12 +97,14 @@ __global__ void __launch_bounds__(kMhMaxChainsPerCta * 32, 1) mh_gmm_kernel(cons
   uint8_t* base = smem + align16(static_cast<size_t>(a.D_pad) * sizeof(float)) + warp * chain_bytes(a.D_pad);
   ChainSmem c;
   c.z = base;
-  c.tab = reinterpret_cast<float2*>(base + align16(a.D_pad / 2));
-  c.mu = reinterpret_cast<float*>(c.tab + 64);
+  c.ta = reinterpret_cast<float*>(base + align16(a.D_pad / 2));
+  c.tb = c.ta + 64;
+  c.mu = c.tb + 64;
   c.stats = reinterpret_cast<double*>(c.mu + 8);
   const PhiloxKey key = make_key(a.key);
   const int K = a.K, D = a.D;
   const unsigned int n_sites = static_cast<unsigned int>(K + D);
+  const int W = K + 1;  // label K = padding
 
   // ---- initial trace from the prior
   for (int p = lane; p < a.D_pad / 2; p += 32) {
@@ -106,7 +112,7 @@ __global__ void __launch_bounds__(kMhMaxChainsPerCta * 32, 1) mh_gmm_kernel(cons
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int i = 2 * p + h;
-      uint32_t lab = 7;  // padding
+      uint32_t lab = static_cast<uint32_t>(K);  // padding
       if (i < D) {
         const uint4 b = mh_block(key, chain, static_cast<unsigned int>(i) >> 2, 0u, CUPPL_TAG_MH_INIT);
         const uint32_t wv[4] = {b.x, b.y, b.z, b.w};
@@ -117,7 +123,7 @@ __global__ void __launch_bounds__(kMhMaxChainsPerCta * 32, 1) mh_gmm_kernel(cons
               break;
         }
       }
-      code = (code << 3) | lab;
+      code = code * W + lab;
     }
     c.z[p] = static_cast<uint8_t>(code);
   }
@@ -133,13 +139,38 @@ __global__ void __launch_bounds__(kMhMaxChainsPerCta * 32, 1) mh_gmm_kernel(cons
   }
   if (lane < 2 * kMhMaxK + 2) c.stats[lane] = 0.0;
   __syncwarp();
-  rebuild_table(c, lane);
+  rebuild_table(c, lane, W);
   __syncwarp();
   const float4* y4 = reinterpret_cast<const float4*>(ys);
-  const uint32_t* z4 = reinterpret_cast<const uint32_t*>(c.z);
-  const int nwords = a.D_pad / 8;
-  float ll = ll_pass(y4, z4, c.tab, nwords, a.neg_half_inv_var, a.ll_const, lane);
+  const unsigned short* z2 = reinterpret_cast<const unsigned short*>(c.z);
+  const int nf4 = a.D_pad / 4;
+  float ll = ll_pass(y4, z2, c.ta, c.tb, nf4, a.neg_half_inv_var, a.ll_const, lane);
   unsigned int rec = 0;
+  // run-length statistics: the sorted means change only when a mean proposal is accepted
+  float srt[kMhMaxK];
+  unsigned int run = 0;  // recorded steps since the sorted means last changed
+  auto sort_means = [&]() {
+    for (int k = 0; k < K; ++k) {  // insertion sort (label switching: compare sorted means)
+      const float v = c.mu[k];
+      int q = k;
+      while (q > 0 && srt[q - 1] > v) {
+        srt[q] = srt[q - 1];
+        --q;
+      }
+      srt[q] = v;
+    }
+  };
+  auto flush_run = [&]() {
+    if (run) {
+      for (int k = 0; k < K; ++k) {
+        c.stats[k] += static_cast<double>(srt[k]) * run;
+        c.stats[kMhMaxK + k] += static_cast<double>(srt[k]) * srt[k] * run;
+      }
+      c.stats[2 * kMhMaxK] += run;
+      run = 0;
+    }
+  };
+  if (lane == 0) sort_means();
 
   for (unsigned int s = 0; s < a.n_steps; ++s) {
     // lane 0 draws the site, the proposal and the acceptance uniform; broadcast
@@ -170,18 +201,19 @@ __global__ void __launch_bounds__(kMhMaxChainsPerCta * 32, 1) mh_gmm_kernel(cons
         c.mu[site] = muprop;
       }
       __syncwarp();
-      rebuild_table(c, lane);
+      rebuild_table(c, lane, W);
     } else {
       const int i = static_cast<int>(site) - K;
       p = i >> 1;
       if (lane == 0) {
         old_byte = c.z[p];
-        c.z[p] = (i & 1) ? static_cast<uint8_t>((old_byte & 0x38u) | zprop)
-                         : static_cast<uint8_t>((old_byte & 0x07u) | (zprop << 3));
+        const int ca = old_byte / W, cbb = old_byte - ca * W;
+        c.z[p] = (i & 1) ? static_cast<uint8_t>(ca * W + static_cast<int>(zprop))
+                         : static_cast<uint8_t>(static_cast<int>(zprop) * W + cbb);
       }
     }
     __syncwarp();
-    const float llp = ll_pass(y4, z4, c.tab, nwords, a.neg_half_inv_var, a.ll_const, lane);
+    const float llp = ll_pass(y4, z2, c.ta, c.tb, nf4, a.neg_half_inv_var, a.ll_const, lane);
     logu = __shfl_sync(0xffffffffu, logu, 0);
     const bool accept = logu < llp - ll;
     if (accept) {
@@ -192,32 +224,26 @@ __global__ void __launch_bounds__(kMhMaxChainsPerCta * 32, 1) mh_gmm_kernel(cons
         else c.z[p] = old_byte;
       }
       __syncwarp();
-      if (mu_site) rebuild_table(c, lane);
+      if (mu_site) rebuild_table(c, lane, W);
     }
     __syncwarp();
-    if (s >= a.burn_in && (s - a.burn_in) % a.thin == 0) {
-      if (lane == 0) {
-        float srt[kMhMaxK];
-        for (int k = 0; k < K; ++k) {  // insertion sort (label switching: compare sorted means)
-          const float v = c.mu[k];
-          int q = k;
-          while (q > 0 && srt[q - 1] > v) {
-            srt[q] = srt[q - 1];
-            --q;
-          }
-          srt[q] = v;
+    if (lane == 0) {
+      if (accept) {
+        c.stats[2 * kMhMaxK + 1] += 1.0;
+        if (mu_site) {
+          flush_run();
+          sort_means();
         }
-        for (int k = 0; k < K; ++k) {
-          c.stats[k] += srt[k];
-          c.stats[kMhMaxK + k] += static_cast<double>(srt[k]) * srt[k];
-          if (a.trace_out && rec < a.n_rec) a.trace_out[(static_cast<size_t>(local) * a.n_rec + rec) * K + k] = srt[k];
-        }
-        c.stats[2 * kMhMaxK] += 1.0;
       }
-      ++rec;
+      if (s >= a.burn_in && (s - a.burn_in) % a.thin == 0) {
+        ++run;
+        if (a.trace_out && rec < a.n_rec)
+          for (int k = 0; k < K; ++k) a.trace_out[(static_cast<size_t>(local) * a.n_rec + rec) * K + k] = srt[k];
+      }
     }
-    if (lane == 0 && accept) c.stats[2 * kMhMaxK + 1] += 1.0;
+    if (s >= a.burn_in && (s - a.burn_in) % a.thin == 0) ++rec;
   }
+  if (lane == 0) flush_run();
   __syncwarp();
   if (lane < K) a.mu_out[static_cast<size_t>(local) * K + lane] = c.mu[lane];
   if (lane == 0) a.ll_out[local] = ll;
