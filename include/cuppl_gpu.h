@@ -235,6 +235,17 @@ CUPPL_API int cuppl_mh_gmm(const float* y, int D, int K, float prior_sd, float s
                            float* ll_out, double* stats_out, float* trace_out, uint32_t n_rec,
                            void* stream);
 
+/* ---- shareable device arenas (multi-process SMC peer stores) ----------------------------- */
+/* cudaMalloc'd arena owned by the caller (free with cuppl_arena_free); its 64-byte IPC handle
+ * (cuppl_ipc_handle) is exchanged between ranks, which map it with cuppl_ipc_open (NVLink peer
+ * access enabled lazily) and unmap it with cuppl_ipc_close. */
+#define CUPPL_IPC_HANDLE_BYTES 64
+CUPPL_API int cuppl_arena_alloc(size_t bytes, void** ptr);
+CUPPL_API int cuppl_arena_free(void* ptr);
+CUPPL_API int cuppl_ipc_handle(const void* arena, void* handle_out);
+CUPPL_API int cuppl_ipc_open(const void* handle, void** ptr);
+CUPPL_API int cuppl_ipc_close(void* ptr);
+
 /* ---- roofline calibration ---------------------------------------------------------- */
 /* Pipe-rate microbenchmark, blocks x 256 threads, each thread runs `iters` iterations of:
  * kind 0: 128 FFMA2 (256 fp32 FMA), kind 1: 128 FFMA, kind 2: one Philox4x32-10 block,

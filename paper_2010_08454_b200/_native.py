@@ -97,6 +97,11 @@ _SIG = {
     "cuppl_mh_padded_points": ([C.c_int], C.c_int),
     "cuppl_mh_gmm": ([_P, C.c_int, C.c_int, _F32, _F32, _U32, _U32, _U32, _U32, _U32, _U64, _P, _P, _P, _P,
                       _U32, _P], C.c_int),
+    "cuppl_arena_alloc": ([C.c_size_t, _P], C.c_int),
+    "cuppl_arena_free": ([_P], C.c_int),
+    "cuppl_ipc_handle": ([_P, _P], C.c_int),
+    "cuppl_ipc_open": ([_P, _P], C.c_int),
+    "cuppl_ipc_close": ([_P], C.c_int),
     "cuppl_calibrate": ([C.c_int, C.c_int, C.c_int, _P, _P], C.c_int),
     "cuppl_smc_workspace_bytes": ([_U64], C.c_size_t),
     "cuppl_smc_init": ([_P, _U64, _U64, _U64, _F32, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),

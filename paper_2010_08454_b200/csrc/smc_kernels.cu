@@ -616,6 +616,7 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
     c_base += btot;
     batch_base += kBatch;
   }
+  if (MULTI) __threadfence_system();  // peer stores performed before the next collective
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
   if (lane == 0 && bmax > neg_inf_f()) atomicMax(a.m_key_next, f2key(bmax));

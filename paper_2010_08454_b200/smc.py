@@ -10,7 +10,9 @@ Per time step t, on every rank r (one process per GPU):
   3. all-gather of the 32-byte rank records    (NCCL; skipped for one rank)
   4. K6 resample(t) -> population t+1: the outputs whose ancestors live on rank r are produced
      by rank r and stored straight into their owner's buffers (peer pointers).
-A `LocalGroup` runs R virtual ranks in one process on one GPU (same kernels, collectives done
+With several processes the x / lw buffers live in cudaMalloc'd arenas whose CUDA-IPC handles are
+all-gathered once, so every rank holds a table of the peers' buffers (NVLink peer stores).
+`local_world=R` runs R virtual ranks in one process on one GPU (same kernels, collectives done
 with tensor ops) — it exercises the multi-rank arithmetic without a second GPU.
 """
 
@@ -65,6 +67,55 @@ def rank_boundaries(n: int, world: int) -> list[int]:
     return b
 
 
+class _DevArray:
+    """Zero-copy torch view of library-allocated device memory (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _align(v: int) -> int:
+    return (v + 255) & ~255
+
+
+class _Arena:
+    """x[2], lw[2] (and anc[2]) of one rank in one cudaMalloc'd arena shareable by CUDA IPC."""
+
+    def __init__(self, n: int, with_anc: bool, device):
+        import torch
+
+        self.n = n
+        self.off = {}
+        o = 0
+        for name, size in (("x0", n), ("x1", n), ("lw0", 4 * n), ("lw1", 4 * n)) + (
+                (("anc0", 8 * n), ("anc1", 8 * n)) if with_anc else ()):
+            self.off[name] = o
+            o += _align(size)
+        self.bytes = o
+        p = C.c_void_p()
+        N.check(N.lib().cuppl_arena_alloc(o, C.byref(p)), "arena_alloc")
+        self.base = p.value
+        with torch.cuda.device(device):
+            self.x = [torch.as_tensor(_DevArray(self.base + self.off[f"x{i}"], n, "|u1"), device=device)
+                      for i in range(2)]
+            self.lw = [torch.as_tensor(_DevArray(self.base + self.off[f"lw{i}"], n, "<f4"), device=device)
+                       for i in range(2)]
+            self.anc = ([torch.as_tensor(_DevArray(self.base + self.off[f"anc{i}"], n, "<i8"), device=device)
+                         for i in range(2)] if with_anc else None)
+
+    def handle(self) -> bytes:
+        h = (C.c_char * 64)()
+        N.check(N.lib().cuppl_ipc_handle(C.c_void_p(self.base), h), "ipc_handle")
+        return bytes(h)
+
+    def __del__(self):  # pragma: no cover - interpreter teardown order
+        try:
+            N.lib().cuppl_arena_free(C.c_void_p(self.base))
+        except Exception:
+            pass
+
+
 class _Rank:
     """Device state of one rank."""
 
@@ -75,10 +126,15 @@ class _Rank:
         dev = runner.device
         lo, hi = runner.bounds[r], runner.bounds[r + 1]
         self.lo, self.n = lo, hi - lo
-        self.x = [torch.empty(self.n, dtype=torch.uint8, device=dev) for _ in range(2)]
-        self.lw = [torch.empty(self.n, dtype=torch.float32, device=dev) for _ in range(2)]
-        self.anc = ([torch.empty(self.n, dtype=torch.int64, device=dev) for _ in range(2)]
-                    if runner.record_ancestors else None)
+        if runner.multiprocess:
+            self.arena = _Arena(self.n, runner.record_ancestors, dev)
+            self.x, self.lw, self.anc = self.arena.x, self.arena.lw, self.arena.anc
+        else:
+            self.arena = None
+            self.x = [torch.empty(self.n, dtype=torch.uint8, device=dev) for _ in range(2)]
+            self.lw = [torch.empty(self.n, dtype=torch.float32, device=dev) for _ in range(2)]
+            self.anc = ([torch.empty(self.n, dtype=torch.int64, device=dev) for _ in range(2)]
+                        if runner.record_ancestors else None)
         ws = N.lib().cuppl_smc_workspace_bytes(self.n)
         self.ws = torch.empty(int(ws), dtype=torch.uint8, device=dev)
         self.m_key = torch.full((runner.T,), INT32_MIN, dtype=torch.int32, device=dev)
@@ -117,8 +173,7 @@ class SmcRunner:
 
             self.rank, self.world = _world(group)
             self.ranks_here = [self.rank]
-        if self.world > 1 and not self.local:
-            raise InferRuntimeError("multi-process SMC needs peer-mapped buffers (not available yet)")
+        self.multiprocess = self.world > 1 and not self.local
         self.bounds = rank_boundaries(self.N, self.world)
         S = model.n_states
         aliasA = np.array([alias_table(list(model.A[s])) for s in range(S)], dtype=np.uint64)
@@ -143,11 +198,18 @@ class SmcRunner:
         self.rank_begin = torch.tensor(self.bounds, dtype=torch.int64, device=dev)
         self.gathered = torch.zeros((self.T, self.world, 4), dtype=torch.int64, device=dev)
         # destination pointer tables per ping-pong parity: x_out / lw_out / anc_out [world]
+        self._peers = []
+        if self.multiprocess:
+            xps, lps, aps = self._exchange_arenas()
         self._tables = {}
         for par in (0, 1):
-            xp = [rk.x[par].data_ptr() for rk in self.ranks]
-            lp = [rk.lw[par].data_ptr() for rk in self.ranks]
-            ap = [rk.anc[par].data_ptr() for rk in self.ranks] if record_ancestors else None
+            if self.multiprocess:
+                xp, lp = xps[par], lps[par]
+                ap = aps[par] if record_ancestors else None
+            else:
+                xp = [rk.x[par].data_ptr() for rk in self.ranks]
+                lp = [rk.lw[par].data_ptr() for rk in self.ranks]
+                ap = [rk.anc[par].data_ptr() for rk in self.ranks] if record_ancestors else None
             self._tables[par] = (torch.tensor(xp, dtype=torch.int64, device=dev),
                                  torch.tensor(lp, dtype=torch.int64, device=dev),
                                  torch.tensor(ap, dtype=torch.int64, device=dev) if ap else None)
@@ -155,6 +217,40 @@ class SmcRunner:
         self.cur = 0
 
     # ------------------------------------------------------------------ collectives -------
+    def _exchange_arenas(self):
+        """All-gather (IPC handle, offsets) of every rank's arena and map the peers'."""
+        import torch.distributed as dist
+
+        me = self.ranks[0].arena
+        info = (me.handle(), me.off)
+        allinfo = [None] * self.world
+        dist.all_gather_object(allinfo, info, group=self.group)
+        bases = []
+        for q, (h, off) in enumerate(allinfo):
+            if q == self.rank:
+                bases.append((me.base, off))
+                continue
+            p = C.c_void_p()
+            hb = (C.c_char * 64).from_buffer_copy(h)
+            N.check(N.lib().cuppl_ipc_open(hb, C.byref(p)), "ipc_open")
+            self._peers.append(p.value)
+            bases.append((p.value, off))
+        xs = [[b + o[f"x{par}"] for b, o in bases] for par in (0, 1)]
+        ls = [[b + o[f"lw{par}"] for b, o in bases] for par in (0, 1)]
+        an = ([[b + o[f"anc{par}"] for b, o in bases] for par in (0, 1)] if self.record_ancestors else None)
+        return xs, ls, an
+
+    def close(self):
+        """Unmap peer arenas (the local arena is freed with the runner)."""
+        for p in self._peers:
+            N.lib().cuppl_ipc_close(C.c_void_p(p))
+        self._peers = []
+
+    def _backend(self) -> str:
+        import torch.distributed as dist
+
+        return dist.get_backend(self.group)
+
     def _allreduce_max(self, t: int):
         if self.world == 1:
             return
@@ -164,29 +260,46 @@ class SmcRunner:
             m = torch.stack([rk.m_key[t] for rk in self.ranks]).max()
             for rk in self.ranks:
                 rk.m_key[t].copy_(m)
-        else:  # pragma: no cover - multi-GPU
+        else:
             import torch.distributed as dist
 
-            dist.all_reduce(self.ranks[0].m_key[t:t + 1], op=dist.ReduceOp.MAX, group=self.group)
+            v = self.ranks[0].m_key[t:t + 1]
+            if self._backend() == "nccl":
+                dist.all_reduce(v, op=dist.ReduceOp.MAX, group=self.group)
+            else:  # gloo (tests): host round trip, also a barrier after this rank's K6
+                h = v.cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.MAX, group=self.group)
+                v.copy_(h)
 
     def _allgather(self, t: int):
+        import torch
+
         if self.local or self.world == 1:
             for i, rk in enumerate(self.ranks):
                 self.gathered[t, rk.r].copy_(rk.rec[t])
-        else:  # pragma: no cover - multi-GPU
+        else:
             import torch.distributed as dist
 
-            dist.all_gather_into_tensor(self.gathered[t].view(-1), self.ranks[0].rec[t], group=self.group)
+            if self._backend() == "nccl":
+                dist.all_gather_into_tensor(self.gathered[t].view(-1), self.ranks[0].rec[t], group=self.group)
+            else:
+                h = torch.empty(self.world * 4, dtype=torch.int64)
+                dist.all_gather_into_tensor(h, self.ranks[0].rec[t].cpu(), group=self.group)
+                self.gathered[t].view(-1).copy_(h)
 
     def _gather_stats(self) -> np.ndarray:
         import torch
 
         if self.local or self.world == 1:
             return torch.stack([rk.stats for rk in self.ranks]).cpu().numpy()
-        import torch.distributed as dist  # pragma: no cover - multi-GPU
+        import torch.distributed as dist
 
-        out = torch.empty((self.world, self.T, 2), dtype=torch.float64, device=self.device)
-        dist.all_gather_into_tensor(out.view(-1), self.ranks[0].stats.view(-1), group=self.group)
+        if self._backend() == "nccl":
+            out = torch.empty((self.world, self.T, 2), dtype=torch.float64, device=self.device)
+            dist.all_gather_into_tensor(out.view(-1), self.ranks[0].stats.view(-1), group=self.group)
+        else:
+            out = torch.empty((self.world, self.T, 2), dtype=torch.float64)
+            dist.all_gather_into_tensor(out.view(-1), self.ranks[0].stats.view(-1).cpu(), group=self.group)
         return out.cpu().numpy()
 
     # ------------------------------------------------------------------ steps -------------

@@ -94,3 +94,62 @@ def test_smc_deterministic(cuda):
     _, x1, lw1, _ = _gpu_run(m, 300_000, 8, record_ancestors=False)
     _, x2, lw2, _ = _gpu_run(m, 300_000, 8, record_ancestors=False)
     assert np.array_equal(x1, x2) and np.array_equal(lw1.view(np.uint32), lw2.view(np.uint32))
+
+
+def _mp_worker(rank, world, port, n, steps, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)  # both ranks share the one GPU of the test box; peers via CUDA IPC
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2010_08454_b200 import models, smc
+
+        m = models.HiddenMarkovModel.synthetic(S=50, T=steps, seed=5)
+        r = smc.SmcRunner(m, n, KEY, record_ancestors=True, steps=steps)
+        res = r.run()
+        torch.cuda.synchronize()
+        q.put((rank, r.bounds[rank], res.states[0].cpu().numpy(), res.log_weights[0].cpu().numpy(),
+               [a[0].cpu().numpy() for a in res.ancestors], res.total_weight, res.log_z))
+        dist.barrier()
+        r.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_smc_multiprocess_ipc_matches_oracle(cuda, oracle_lib):
+    """Two processes (gloo for the tiny collectives, CUDA-IPC peer stores for the particles):
+    the same bits as the single-rank oracle."""
+    import multiprocessing as mp
+    import socket
+
+    from paper_2010_08454_b200 import models
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    n, steps = 40_000, 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_mp_worker, args=(r, 2, port, n, steps, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    m = models.HiddenMarkovModel.synthetic(S=50, T=steps, seed=5)
+    ref = oracle_lib.smc_run(m, n, KEY, record_ancestors=True)
+    x = np.concatenate([o[2] for o in out]).astype(np.int32)
+    lw = np.concatenate([o[3] for o in out])
+    assert np.array_equal(out[0][5], ref["T"]) and np.array_equal(out[1][5], ref["T"])
+    for t in range(steps - 1):
+        anc = np.concatenate([o[4][t] for o in out]).astype(np.uint64)
+        assert np.array_equal(anc, ref["ancestors"][t]), f"ancestors differ at step {t}"
+    assert np.array_equal(x, ref["x"]) and np.array_equal(lw.view(np.uint32), ref["lw"].view(np.uint32))
+    assert out[0][6] == out[1][6]
