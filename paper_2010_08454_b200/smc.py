@@ -214,6 +214,7 @@ class SmcRunner:
                                  torch.tensor(lp, dtype=torch.int64, device=dev),
                                  torch.tensor(ap, dtype=torch.int64, device=dev) if ap else None)
         self.ancestors = []
+        self._pending_anc = None
         self.cur = 0
 
     # ------------------------------------------------------------------ collectives -------
@@ -316,7 +317,8 @@ class SmcRunner:
         """Scan population t and (t < T-1) resample/propagate it to t+1."""
         L = N.lib()
         st = N.stream_ptr(self.device)
-        self._allreduce_max(t)
+        self._allreduce_max(t)  # also the barrier after every rank's K6(t - 1) peer stores
+        self._snapshot_ancestors()
         h = self.hist.get(t)
         for i, rk in enumerate(self.ranks):
             N.check(L.cuppl_smc_scan(rk.n, N.ptr(rk.lw[self.cur]), N.ptr(rk.x[self.cur]),
@@ -339,13 +341,19 @@ class SmcRunner:
                 None if at is None else N.ptr(at), N.ptr(rk.m_key[t + 1:t + 2]), N.ptr(rk.stats[t]),
                 N.ptr(rk.ws), rk.ws.numel(), st), "smc_resample", seed=self.seed, step=t)
         if self.record_ancestors:
-            self.ancestors.append([rk.anc[nxt].clone() for rk in self.ranks])
+            self._pending_anc = nxt  # complete only after the next collective (peer stores)
         self.cur = nxt
+
+    def _snapshot_ancestors(self):
+        if self._pending_anc is not None:
+            self.ancestors.append([rk.anc[self._pending_anc].clone() for rk in self.ranks])
+            self._pending_anc = None
 
     def run(self) -> SmcResult:
         self.init()
         for t in range(self.T):
             self.step(t)
+        self._snapshot_ancestors()
         return self.result()
 
     def result(self) -> SmcResult:
