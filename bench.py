@@ -171,6 +171,26 @@ def cpu_baseline(workload: str, model, target_s: float = 12.0, threads: int | No
                       f"(oracle/cuppl_oracle.c, fp64, OpenMP {threads} threads)"}
 
 
+def calibrate_philox(device) -> float:
+    """Measured Philox4x32-10 blocks/s on this GPU (csrc/calib_kernels.cu kind 2)."""
+    import torch
+
+    from paper_2010_08454_b200 import _native as N
+
+    L = N.lib()
+    sink = torch.zeros(256, dtype=torch.float32, device=device)
+    sm = torch.cuda.get_device_properties(device).multi_processor_count
+    blocks, iters = sm * 16, 400
+    st = N.stream_ptr(device)
+    N.check(L.cuppl_calibrate(2, blocks, iters, N.ptr(sink), st))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    N.check(L.cuppl_calibrate(2, blocks, iters, N.ptr(sink), st))
+    e1.record()
+    torch.cuda.synchronize()
+    return blocks * 256 * iters / (e0.elapsed_time(e1) / 1e3)
+
+
 def calibrate_fp32(device) -> float:
     """Measured FFMA2 ceiling (FLOP/s) on this GPU (csrc/calib_kernels.cu kind 0)."""
     import torch
@@ -289,6 +309,32 @@ def run_ours(args) -> dict | None:
         achieved = fpp * per_gpu / kernel_s
         sm_max = clk.get("sm_max_mhz") or 1965.0
         nominal = torch.cuda.get_device_properties(device).multi_processor_count * 128 * 2 * sm_max * 1e6
+        roof = {
+            "bound": "fp32",
+            "achieved": achieved / 1e12,
+            "peak": peak / 1e12,
+            "unit": "TFLOP/s",
+            "frac": achieved / peak,
+            "traffic": load_traffic(args.workload),
+            "peak_source": "measured FFMA2 ceiling on this GPU (csrc/calib_kernels.cu kind 0); "
+                           "MEASURED_PEAKS.json has no fp32 CUDA-core figure",
+            "nominal_peak": nominal / 1e12,
+            "frac_of_nominal": achieved / nominal,
+            "flops_per_particle": fpp,
+        }
+        if args.workload == "poly":
+            # issue-bound: one Philox block (IMAD.WIDE on the fma pipe) + the fp32 Horner work
+            # share the fma pipe; roof = 1 / (t_philox + t_fp32) with both rates measured here
+            ph = calibrate_philox(device)
+            t_part = 1.0 / ph + fpp / peak
+            roof_rate = 1.0 / t_part
+            rate = per_gpu / kernel_s
+            roof = {"bound": "issue (fma pipe: Philox IMAD.WIDE + fp32 FFMA2)", "achieved": rate,
+                    "peak": roof_rate, "unit": "particles/s", "frac": rate / roof_rate,
+                    "traffic": load_traffic(args.workload),
+                    "peak_source": f"measured: Philox {ph:.3g} blocks/s (calib kind 2) + FFMA2 {peak / 1e12:.1f} "
+                                   "TFLOP/s (kind 0), 1 block + {fpp:.0f} flops per particle".replace("{fpp:.0f}", f"{fpp:.0f}"),
+                    "flops_per_particle": fpp}
         result = {
             "metric": METRIC,
             "value": value,
@@ -309,19 +355,7 @@ def run_ours(args) -> dict | None:
                 "parallelism": f"particle-sharded dp{world} (NCCL all-gather of 256 B rank records)",
                 "l2": "flushed between timed steps (256 MiB write, excluded by per-step CUDA events)",
             },
-            "roofline": {
-                "bound": "fp32",
-                "achieved": achieved / 1e12,
-                "peak": peak / 1e12,
-                "unit": "TFLOP/s",
-                "frac": achieved / peak,
-                "traffic": load_traffic(args.workload),
-                "peak_source": "measured FFMA2 ceiling on this GPU (csrc/calib_kernels.cu kind 0); "
-                               "MEASURED_PEAKS.json has no fp32 CUDA-core figure",
-                "nominal_peak": nominal / 1e12,
-                "frac_of_nominal": achieved / nominal,
-                "flops_per_particle": fpp,
-            },
+            "roofline": roof,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "paper_2010_08454_b200.infer.run_importance(model, n, rng)",
                     "log_z": post.log_z, "ess": post.ess},
@@ -355,14 +389,13 @@ def run_ours_engine(args) -> dict | None:
     B.build()
     from paper_2010_08454_b200 import Rng, infer, smc
 
+    import torch.distributed as dist
+
     rank, world, local = dist_env()
-    if world > 1:
-        if rank == 0:
-            print(json.dumps({"metric": METRICS[args.workload][0], "unavailable":
-                              "multi-process SMC/MH bench not wired yet (single-GPU workloads)"}))
-        return None
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
     wl = WORKLOADS[args.workload]
     model = make_model(args.workload)
     metric, unit = METRICS[args.workload]
@@ -377,17 +410,19 @@ def run_ours_engine(args) -> dict | None:
             for t in range(T):
                 r.step(t)
             return r
-        units_per_step = T
+        units_per_step = T  # time steps of the whole (strong-scaled) population
     else:
         chains = args.particles or wl["particles_per_gpu"]
         n_steps = args.mh_steps
 
-        def step(k):
-            return infer.run_lmh(model, n_steps, Rng(1).split(k), chains=chains, device=device)
-        units_per_step = chains * n_steps
+        def step(k):  # weak scaling: `chains` chains per GPU, sharded by rank inside run_lmh
+            return infer.run_lmh(model, n_steps, Rng(1).split(k), chains=chains * world, device=device)
+        units_per_step = chains * n_steps * world
     for k in range(args.warmup):
         step(10_000 + k)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     clocks = ClockSampler(local)
@@ -399,10 +434,23 @@ def run_ours_engine(args) -> dict | None:
         last = step(k)
         ends[k].record()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
-    t_ms = sum(step_ms)
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    t_ms = tot.item()
     value = units_per_step * args.steps / (t_ms / 1e3)
+    if rank != 0:
+        if args.workload == "smc":
+            infer.run_smc(model, n, Rng(99))  # e2e leg is collective
+        else:
+            infer.run_lmh(model, args.mh_steps, Rng(99), chains=units_per_step // args.mh_steps)
+        dist.barrier()
+        dist.destroy_process_group()
+        return None
     res = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
            "scaling": "strong" if args.workload == "smc" else "weak", "vs_baseline": None,
@@ -411,9 +459,11 @@ def run_ours_engine(args) -> dict | None:
            "clocks": clk}
     if args.workload == "smc":
         peak, src = _hbm_peak()
-        bytes_step = 14.0 * n  # K5 reads lw; K6 reads lw + x, writes x' + lw' (u8 state)
+        bytes_step = 14.0 * n / world  # per GPU: K5 reads lw; K6 reads lw + x, writes x' + lw' (u8 state)
         achieved = bytes_step * units_per_step / (t_ms / args.steps / 1e3) / 1e9
-        res["config"].update({"particles": n, "time_steps": T, "state": "u8", "resampling": "systematic every step"})
+        res["config"].update({"particles": n, "time_steps": T, "state": "u8", "resampling": "systematic every step",
+                              "parallelism": f"particle-partitioned dp{world} (NCCL max all-reduce + 32-B "
+                                             "record all-gather per step, CUDA-IPC peer stores)"})
         res["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                            "frac": achieved / peak, "traffic": load_traffic("smc"), "peak_source": src,
                            "bytes_per_particle_step": 14}
@@ -449,8 +499,11 @@ def run_ours_engine(args) -> dict | None:
         res["e2e"] = {"value": units_per_step / (e0.elapsed_time(e1) / 1e3), "unit": unit,
                       "h2d_bytes_per_step": int(model.ys.nbytes), "d2h_bytes_per_step": int(units_per_step // args.mh_steps * 12 * 8),
                       "api": "paper_2010_08454_b200.infer.run_lmh(model, n, rng, chains=...)"}
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         res["cpu_baseline"] = cpu_baseline_engine(args, model)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
     return res
 
 
