@@ -167,36 +167,43 @@ typedef struct cuppl_smc_model {
  * per-tile sums. Must be zeroed once before the first step (cuppl_smc_init does it). */
 CUPPL_API size_t cuppl_smc_workspace_bytes(uint64_t n_local);
 
-/* t = 0: x[j] ~ categorical(init), lw[j] = log N(y0; mu[x[j]], sd) for local particles
- * j_begin + [0, n_local) (j_begin multiple of 8); atomicMax of lw into *m_key (ordered int,
- * caller initialises it to INT32_MIN). Zeroes the workspace. */
+/* A population is its states x (u8 per particle); in this discrete-state HMM the log-weight is
+ * a function of the state, lw = log N(y_t; mu[x], sd) (fp32, fixed op sequence), so the kernels
+ * tabulate the S per-state weights of a step instead of storing log-weights. */
+
+/* t = 0: x[j] ~ categorical(init) for local particles j_begin + [0, n_local) (j_begin multiple
+ * of 8); atomicMax of lw_0 into *m_key (ordered int, caller initialises it to INT32_MIN).
+ * Zeroes the workspace. */
 CUPPL_API int cuppl_smc_init(const cuppl_smc_model* m, uint64_t n_local, uint64_t j_begin,
-                             uint64_t key, float y0, uint8_t* x, float* lw, int32_t* m_key,
+                             uint64_t key, float y0, uint8_t* x, int32_t* m_key, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
+/* Weight scan of population t (K5) with observation y: quantised weights against max *m_key,
+ * segment offsets and tile prefixes (single-pass decoupled look-back) into the workspace,
+ * rank_rec[0] = T_r (integer weight total of this rank; rank_rec[1..3] untouched);
+ * hist[S] (optional, zeroed by the caller) += integer weights per state. */
+CUPPL_API int cuppl_smc_scan(const cuppl_smc_model* m, uint64_t n_local, float y, const uint8_t* x,
+                             const int32_t* m_key, uint64_t* hist, uint64_t* rank_rec,
                              void* workspace, size_t workspace_bytes, void* stream);
 
-/* Weight scan of population t (K5): quantised weights against max *m_key, segment offsets
- * and tile prefixes (single-pass decoupled look-back) into the workspace, rank_rec[0] = T_r
- * (integer weight total of this rank; rank_rec[1..3] untouched); hist[S] (optional, zeroed by
- * the caller) += integer weights per state. */
-CUPPL_API int cuppl_smc_scan(uint64_t n_local, const float* lw, const uint8_t* x,
-                             const int32_t* m_key, int n_states, uint64_t* hist,
-                             uint64_t* rank_rec, void* workspace, size_t workspace_bytes,
-                             void* stream);
-
-/* Systematic resampling of population t + propagation to t+1 (K6). rank_recs: device
- * [world][4] records of every rank (all-gathered); rank_begin: device [world+1] global index
- * of each rank's first particle (multiples of 8); x_out / lw_out / anc_out: device arrays of
- * `world` destination pointers (peer-mapped for other ranks; anc_out NULL to skip). The
- * outputs whose ancestors live on this rank are written to their owners; *m_key_next gets the
- * atomicMax of the new log-weights written here; stats_out[2] (device doubles) receives this
- * rank's (sum exp(lw - M), sum exp(2 (lw - M))) of population t, folded in fixed order. */
+/* Systematic resampling of population t (observation y_cur) + propagation to t+1 (y_next)
+ * (K6). rank_recs: device [world][4] records of every rank (all-gathered); rank_begin: device
+ * [world+1] global index of each rank's first particle (multiples of 8); x_out / anc_out:
+ * device arrays of `world` destination pointers (peer-mapped for other ranks; anc_out NULL to
+ * skip). The outputs whose ancestors live on this rank are written to their owners;
+ * *m_key_next gets the atomicMax of the new log-weights written here; stats_out[2] (device
+ * doubles) receives this rank's (sum exp(lw - M), sum exp(2 (lw - M))) of population t. */
 CUPPL_API int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_total,
-                                 uint64_t key, uint32_t t, int rank, int world, float y_next,
-                                 const float* lw, const uint8_t* x, const int32_t* m_key,
+                                 uint64_t key, uint32_t t, int rank, int world, float y_cur,
+                                 float y_next, const uint8_t* x, const int32_t* m_key,
                                  const uint64_t* rank_recs, const uint64_t* rank_begin,
-                                 uint8_t* const* x_out, float* const* lw_out,
-                                 uint64_t* const* anc_out, int32_t* m_key_next, double* stats_out,
-                                 void* workspace, size_t workspace_bytes, void* stream);
+                                 uint8_t* const* x_out, uint64_t* const* anc_out,
+                                 int32_t* m_key_next, double* stats_out, void* workspace,
+                                 size_t workspace_bytes, void* stream);
+
+/* lw[i] = log N(y; mu[x[i]], sd) (the per-particle log-weights of a population). */
+CUPPL_API int cuppl_smc_log_weights(const cuppl_smc_model* m, float y, const uint8_t* x, uint64_t n,
+                                    float* lw, void* stream);
 
 /* Statistics of a population that is not resampled (the last step): stats_out[2] as in
  * cuppl_smc_resample, from the per-tile sums of the preceding cuppl_smc_scan. */

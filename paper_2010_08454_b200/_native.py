@@ -104,11 +104,12 @@ _SIG = {
     "cuppl_ipc_close": ([_P], C.c_int),
     "cuppl_calibrate": ([C.c_int, C.c_int, C.c_int, _P, _P], C.c_int),
     "cuppl_smc_workspace_bytes": ([_U64], C.c_size_t),
-    "cuppl_smc_init": ([_P, _U64, _U64, _U64, _F32, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
-    "cuppl_smc_scan": ([_U64, _P, _P, _P, C.c_int, _P, _P, _P, C.c_size_t, _P], C.c_int),
+    "cuppl_smc_init": ([_P, _U64, _U64, _U64, _F32, _P, _P, _P, C.c_size_t, _P], C.c_int),
+    "cuppl_smc_scan": ([_P, _U64, _F32, _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
+    "cuppl_smc_log_weights": ([_P, _F32, _P, _U64, _P, _P], C.c_int),
     "cuppl_smc_fold": ([_U64, _P, _P, C.c_size_t, _P], C.c_int),
-    "cuppl_smc_resample": ([_P, _U64, _U64, _U64, _U32, C.c_int, C.c_int, _F32, _P, _P, _P, _P, _P,
-                            _P, _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
+    "cuppl_smc_resample": ([_P, _U64, _U64, _U64, _U32, C.c_int, C.c_int, _F32, _F32, _P, _P, _P, _P,
+                            _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
 }
 
 

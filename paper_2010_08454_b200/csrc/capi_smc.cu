@@ -79,13 +79,13 @@ extern "C" {
 size_t cuppl_smc_workspace_bytes(uint64_t n_local) { return ws_layout(n_local, nullptr, nullptr); }
 
 int cuppl_smc_init(const cuppl_smc_model* m, uint64_t n_local, uint64_t j_begin, uint64_t key,
-                   float y0, uint8_t* x, float* lw, int32_t* m_key, void* workspace,
-                   size_t workspace_bytes, void* stream) {
+                   float y0, uint8_t* x, int32_t* m_key, void* workspace, size_t workspace_bytes,
+                   void* stream) {
   SmcModel sm;
   if (int s = fill_model(m, &sm)) return s;
   SmcWs w;
   if (int s = check_ws(n_local, workspace, workspace_bytes, &w)) return s;
-  if (!x || !lw || !m_key) return set_error(CUPPL_E_ARGUMENT, "NULL buffer");
+  if (!x || !m_key) return set_error(CUPPL_E_ARGUMENT, "NULL buffer");
   if (j_begin % 8) return set_error(CUPPL_E_ARGUMENT, "j_begin must be a multiple of 8");
   int sms = 0;
   if (int s = device_sm_count(&sms)) return s;
@@ -99,25 +99,26 @@ int cuppl_smc_init(const cuppl_smc_model* m, uint64_t n_local, uint64_t j_begin,
   a.key = key;
   a.y0 = y0;
   a.x = x;
-  a.lw = lw;
   a.m_key = m_key;
   return cuda_status(launch_smc_init(sm, a, sms, st), "smc_init");
 }
 
-int cuppl_smc_scan(uint64_t n_local, const float* lw, const uint8_t* x, const int32_t* m_key,
-                   int n_states, uint64_t* hist, uint64_t* rank_rec, void* workspace,
+int cuppl_smc_scan(const cuppl_smc_model* m, uint64_t n_local, float y, const uint8_t* x,
+                   const int32_t* m_key, uint64_t* hist, uint64_t* rank_rec, void* workspace,
                    size_t workspace_bytes, void* stream) {
+  SmcModel sm;
+  if (int s = fill_model(m, &sm)) return s;
   SmcWs w;
   if (int s = check_ws(n_local, workspace, workspace_bytes, &w)) return s;
-  if (!lw || !x || !m_key || !rank_rec) return set_error(CUPPL_E_ARGUMENT, "NULL buffer");
-  if (n_states < 1 || n_states > kMaxStates) return set_error(CUPPL_E_CAPACITY, "n_states");
+  if (!x || !m_key || !rank_rec) return set_error(CUPPL_E_ARGUMENT, "NULL buffer");
   int sms = 0;
   if (int s = device_sm_count(&sms)) return s;
   SmcScanArgs a;
   std::memset(&a, 0, sizeof(a));
   a.n_local = n_local;
-  a.lw = lw;
   a.x = x;
+  a.y = y;
+  a.S = sm.S;
   a.m_key = m_key;
   a.segoff = w.segoff;
   a.tile_prefix = w.tile_prefix;
@@ -126,16 +127,14 @@ int cuppl_smc_scan(uint64_t n_local, const float* lw, const uint8_t* x, const in
   a.tile_s = w.tile_s;
   a.hist = reinterpret_cast<unsigned long long*>(hist);
   a.rank_rec = reinterpret_cast<unsigned long long*>(rank_rec);
-  a.S = n_states;
-  return cuda_status(launch_smc_scan(a, sms, static_cast<cudaStream_t>(stream)), "smc_scan");
+  return cuda_status(launch_smc_scan(sm, a, sms, static_cast<cudaStream_t>(stream)), "smc_scan");
 }
 
 int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_total, uint64_t key,
-                       uint32_t t, int rank, int world, float y_next, const float* lw,
-                       const uint8_t* x, const int32_t* m_key, const uint64_t* rank_recs,
-                       const uint64_t* rank_begin, uint8_t* const* x_out, float* const* lw_out,
-                       uint64_t* const* anc_out, int32_t* m_key_next, double* stats_out,
-                       void* workspace, size_t workspace_bytes, void* stream) {
+                       uint32_t t, int rank, int world, float y_cur, float y_next, const uint8_t* x,
+                       const int32_t* m_key, const uint64_t* rank_recs, const uint64_t* rank_begin,
+                       uint8_t* const* x_out, uint64_t* const* anc_out, int32_t* m_key_next,
+                       double* stats_out, void* workspace, size_t workspace_bytes, void* stream) {
   SmcModel sm;
   if (int s = fill_model(m, &sm)) return s;
   SmcWs w;
@@ -143,7 +142,7 @@ int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_to
   if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
     return set_error(CUPPL_E_ARGUMENT, "rank %d / world %d", rank, world);
   if (n_total < n_local || n_total >= (1ull << 32)) return set_error(CUPPL_E_CAPACITY, "n_total");
-  if (!lw || !x || !m_key || !rank_recs || !rank_begin || !x_out || !lw_out || !m_key_next || !stats_out)
+  if (!x || !m_key || !rank_recs || !rank_begin || !x_out || !m_key_next || !stats_out)
     return set_error(CUPPL_E_ARGUMENT, "NULL buffer");
   int sms = 0;
   if (int s = device_sm_count(&sms)) return s;
@@ -155,8 +154,8 @@ int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_to
   a.t = t;
   a.rank = rank;
   a.world = world;
+  a.y_cur = y_cur;
   a.y_next = y_next;
-  a.lw = lw;
   a.x = x;
   a.m_key = m_key;
   a.segoff = w.segoff;
@@ -167,13 +166,23 @@ int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_to
   a.rank_recs = reinterpret_cast<const unsigned long long*>(rank_recs);
   a.rank_begin = reinterpret_cast<const unsigned long long*>(rank_begin);
   a.x_out = x_out;
-  a.lw_out = lw_out;
   a.anc_out = reinterpret_cast<unsigned long long* const*>(anc_out);
   a.m_key_next = m_key_next;
   a.flags_to_clear = w.flags;
   a.n_tiles = (n_local + kTile - 1) / kTile;
   return cuda_status(launch_smc_resample(sm, a, sms, static_cast<cudaStream_t>(stream)),
                      "smc_resample");
+}
+
+int cuppl_smc_log_weights(const cuppl_smc_model* m, float y, const uint8_t* x, uint64_t n,
+                          float* lw, void* stream) {
+  SmcModel sm;
+  if (int s = fill_model(m, &sm)) return s;
+  if (n && (!x || !lw)) return set_error(CUPPL_E_ARGUMENT, "NULL buffer");
+  int sms = 0;
+  if (int s = device_sm_count(&sms)) return s;
+  return cuda_status(launch_smc_log_weights(sm, y, x, n, lw, sms, static_cast<cudaStream_t>(stream)),
+                     "smc_log_weights");
 }
 
 int cuppl_smc_fold(uint64_t n_local, double* stats_out, void* workspace, size_t workspace_bytes,

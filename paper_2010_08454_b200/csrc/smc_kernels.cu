@@ -10,10 +10,14 @@
 //   x'_j     ~ categorical(A[x_{a_j}]): alias draw with word (j & 3) of Philox(j >> 2, t+1, STEP)
 //   lw'_j    = log N(y_{t+1}; mu[x'_j], sd)
 //
-// Data layout per rank: x (u8, one byte per particle), lw (f32); segoff (u64 per 32
-// particles, rank-local inclusive weight prefix) is the only scan output in HBM. Per step
-// the algorithmic traffic is 4 B (K5 reads lw) + 4 + 1 (K6 stages lw, x of its sources) +
-// 1 + 4 (K6 writes x', lw') = 14 B per particle (+0.25 B of segment offsets each way).
+// Data layout per rank: a population is its states x (u8, one byte per particle). In a
+// discrete-state HMM the log-weight is a function of the state alone, so each kernel builds the
+// S-entry per-step tables lw_s = emission(y_t, mu_s), e_s = exp_repro(lw_s - M_t) and
+// w_s = floor(e_s 2^31) in shared memory (same fp32 op sequence as the oracle, which evaluates
+// them per particle) and never stores a log-weight. segoff (u64 per 32 particles, tile-local
+// inclusive weight prefix) and tile_prefix (u64 per 8192) are the scan outputs. Algorithmic HBM
+// traffic per particle-step: K5 reads x (1 B); K6 reads x (1 B) and writes x' (1 B) = 3 B
+// (+0.25 B of segment offsets each way).
 //
 // K6 is output-balanced and source-streaming: CTA b owns an even share of the rank's output
 // range, finds the ancestor of its first output once (warp-parallel 33-ary search over the
@@ -21,9 +25,8 @@
 // memory with their batch-relative inclusive weight prefix. The batch's outputs are exactly
 // [F(C_start), F(C_end)) with F(c) = min{j : target_j >= c}; they are propagated in dense
 // rounds of 1024 (4 consecutive outputs per thread share one Philox block and one integer comb
-// cursor); each output's ancestor is a binary search over the staged prefix (zero-weight
-// sources make linear stepping divergent), so the work per output is uniform whatever the
-// offspring counts.
+// cursor); each output's ancestor is a binary search over the staged prefix, so the work per
+// output is uniform whatever the offspring counts.
 #include "cuppl_device.cuh"
 #include "smc_kernels.cuh"
 
@@ -77,13 +80,28 @@ __device__ __forceinline__ int alias_draw(const unsigned long long* tab, int K, 
   return (p & 0xFFFFFFFFull) < (e & 0x1FFFFFFFFull) ? col : static_cast<int>(e >> 40);
 }
 
+// Per-step state tables (shared memory): log-weight, weight factor e and quantised weight of
+// every state for observation y and stabiliser M (M = -inf: lw only).
+__device__ __forceinline__ void build_tables(const SmcModel& m, float y, float M, float* lwS, float* eS,
+                                             uint32_t* wS) {
+  for (int s = threadIdx.x; s < m.S; s += blockDim.x) {
+    const float l = emission(y, m.mu[s], m.inv_sd, m.c);
+    if (lwS) lwS[s] = l;
+    if (eS) {
+      const float e = smc_e(l, M);
+      eS[s] = e;
+      wS[s] = smc_w(e);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ K4: init ------------
 // x_0[j] ~ categorical(pi0) with word (j & 3) of Philox(j >> 2, 0, TAG_SMC_INIT);
 // lw_0[j] = log N(y_0; mu[x_0[j]], sd). One Philox block per 4 particles.
 __global__ void __launch_bounds__(kSmcThreads) smc_init_kernel(const __grid_constant__ SmcModel m,
                                                                SmcInitArgs a) {
-  __shared__ float s_mu[kMaxStates];
-  for (int q = threadIdx.x; q < m.S; q += blockDim.x) s_mu[q] = m.mu[q];
+  __shared__ float lwS[kMaxStates];
+  build_tables(m, a.y0, neg_inf_f(), lwS, nullptr, nullptr);
   __syncthreads();
   const PhiloxKey key = make_key(a.key);
   float bmax = neg_inf_f();
@@ -93,16 +111,18 @@ __global__ void __launch_bounds__(kSmcThreads) smc_init_kernel(const __grid_cons
     const unsigned long long j = a.j_begin + 4 * q;  // global index, multiple of 4
     const uint4 w = draw_block(key, j >> 2, 0u, CUPPL_TAG_SMC_INIT);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    uint32_t packed = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const unsigned long long i = 4 * q + k;
-      if (i < a.n_local) {
-        const int s = alias_draw(m.alias_init, m.S, ws[k]);
-        const float lw = emission(a.y0, s_mu[s], m.inv_sd, m.c);
-        a.x[i] = static_cast<uint8_t>(s);
-        a.lw[i] = lw;
-        bmax = fmaxf(bmax, lw);
-      }
+      const int s = alias_draw(m.alias_init, m.S, ws[k]);
+      packed |= static_cast<uint32_t>(s) << (8 * k);
+      if (4 * q + k < a.n_local) bmax = fmaxf(bmax, lwS[s]);
+    }
+    if (4 * q + 3 < a.n_local) {
+      *reinterpret_cast<uint32_t*>(a.x + 4 * q) = packed;
+    } else {
+      for (int k = 0; k < 4; ++k)
+        if (4 * q + k < a.n_local) a.x[4 * q + k] = static_cast<uint8_t>(packed >> (8 * k));
     }
   }
 #pragma unroll
@@ -151,72 +171,56 @@ __device__ __forceinline__ unsigned long long warp_lookback(const unsigned long 
 }
 
 template <bool HIST>
-__global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(SmcScanArgs a) {
-  __shared__ unsigned long long seg_sum[kTileSegs];
+__global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(const __grid_constant__ SmcModel m,
+                                                               SmcScanArgs a) {
+  __shared__ uint32_t wS[kMaxStates];
+  __shared__ float eS[kMaxStates];
   __shared__ unsigned long long wtot[kSmcThreads / 32];
   __shared__ double wpart[kSmcThreads / 32][2];
   __shared__ unsigned int s_tile;
-  __shared__ unsigned long long shist[HIST ? kMaxStates : 1];
+  __shared__ unsigned int cnt[HIST ? kMaxStates : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long n = a.n_local;
   const unsigned long long n_tiles = (n + kTile - 1) / kTile;
-  const float M = key2f(*a.m_key);
   if (tid == 0) s_tile = atomicAdd(&a.counters[0], 1u);  // launch-order tile ids: look-back is deadlock free
+  build_tables(m, a.y, key2f(*a.m_key), nullptr, eS, wS);
   if (HIST)
-    for (int s = tid; s < a.S; s += kSmcThreads) shist[s] = 0;
+    for (int s = tid; s < a.S; s += kSmcThreads) cnt[s] = 0u;
   __syncthreads();
   const unsigned long long tile = s_tile;
-  const unsigned long long wbase = tile * kTile + static_cast<unsigned long long>(warp) * 1024;
-  float s1 = 0.f, s2 = 0.f;
-  // all 8 loads of the warp's 1024 particles in flight first
-  float4 v[8];
-  uchar4 xv[8];
-#pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const unsigned long long p0 = wbase + it * 128 + lane * 4;
-    if (p0 + 3 < n) {
-      v[it] = __ldcs(reinterpret_cast<const float4*>(a.lw + p0));
-      if (HIST) xv[it] = *reinterpret_cast<const uchar4*>(a.x + p0);
-    } else {
-      v[it].x = p0 < n ? a.lw[p0] : neg_inf_f();
-      v[it].y = p0 + 1 < n ? a.lw[p0 + 1] : neg_inf_f();
-      v[it].z = p0 + 2 < n ? a.lw[p0 + 2] : neg_inf_f();
-      v[it].w = p0 + 3 < n ? a.lw[p0 + 3] : neg_inf_f();
-      if (HIST) {
-        xv[it].x = p0 < n ? a.x[p0] : 0;
-        xv[it].y = p0 + 1 < n ? a.x[p0 + 1] : 0;
-        xv[it].z = p0 + 2 < n ? a.x[p0 + 2] : 0;
-        xv[it].w = p0 + 3 < n ? a.x[p0 + 3] : 0;
-      }
-    }
+  // thread tid owns segment tid of the tile: particles [tile * 8192 + 32 tid, +32)
+  const unsigned long long p0 = tile * kTile + static_cast<unsigned long long>(tid) * kSegment;
+  uint4 v0 = make_uint4(0, 0, 0, 0), v1 = make_uint4(0, 0, 0, 0);
+  int valid = 0;
+  if (p0 + kSegment <= n) {
+    v0 = __ldcs(reinterpret_cast<const uint4*>(a.x + p0));
+    v1 = __ldcs(reinterpret_cast<const uint4*>(a.x + p0) + 1);
+    valid = kSegment;
+  } else if (p0 < n) {
+    valid = static_cast<int>(n - p0);
+    uint8_t tmp[kSegment];
+    for (int k = 0; k < kSegment; ++k) tmp[k] = k < valid ? a.x[p0 + k] : 0;
+    v0 = *reinterpret_cast<const uint4*>(tmp);
+    v1 = *reinterpret_cast<const uint4*>(tmp + 16);
   }
+  const uint32_t words[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+  unsigned long long ws = 0;
+  float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const float vv[4] = {v[it].x, v[it].y, v[it].z, v[it].w};
-    const uint8_t xx[4] = {xv[it].x, xv[it].y, xv[it].z, xv[it].w};
-    unsigned long long ws = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float e = smc_e(vv[k], M);
-      const uint32_t w = smc_w(e);
-      ws += w;
-      s1 += e;
-      s2 = fmaf(e, e, s2);
-      if (HIST) {
-        // warp-aggregated histogram: one shared atomic per distinct state in the warp
-        const unsigned int grp = __match_any_sync(0xffffffffu, static_cast<unsigned int>(xx[k]));
-        const unsigned int lo = __reduce_add_sync(grp, w & 0xFFFFu);
-        const unsigned int hi = __reduce_add_sync(grp, w >> 16);
-        if (lane == __ffs(grp) - 1) {
-          const unsigned long long tot = (static_cast<unsigned long long>(hi) << 16) + lo;
-          if (tot) atomicAdd(&shist[xx[k]], tot);
-        }
-      }
+  for (int k = 0; k < kSegment; ++k) {
+    const uint32_t st = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+    const bool ok = k < valid;
+    const uint32_t w = ok ? wS[st] : 0u;
+    const float e = ok ? eS[st] : 0.f;
+    ws += w;
+    s1 += e;
+    s2 = fmaf(e, e, s2);
+    if (HIST) {
+      // warp-aggregated state counts: one shared atomic per distinct state in the warp
+      const unsigned int key = ok ? st : 0xFFFFFFFFu;
+      const unsigned int grp = __match_any_sync(0xffffffffu, key);
+      if (ok && lane == __ffs(grp) - 1) atomicAdd(&cnt[st], static_cast<unsigned int>(__popc(grp)));
     }
-    ws += __shfl_xor_sync(0xffffffffu, ws, 1);
-    ws += __shfl_xor_sync(0xffffffffu, ws, 2);
-    ws += __shfl_xor_sync(0xffffffffu, ws, 4);
-    if ((lane & 7) == 0) seg_sum[warp * 32 + it * 4 + (lane >> 3)] = ws;
   }
   double d1 = s1, d2 = s2;  // per-warp fp64 partials, fixed tree
 #pragma unroll
@@ -228,9 +232,8 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(SmcScanArgs a) {
     wpart[warp][0] = d1;
     wpart[warp][1] = d2;
   }
-  __syncthreads();
   // inclusive scan of the tile's 256 segment sums (thread tid <-> segment tid)
-  unsigned long long incl = seg_sum[tid];
+  unsigned long long incl = ws;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
@@ -248,7 +251,7 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(SmcScanArgs a) {
   if (gs * kSegment < n) a.segoff[gs] = incl + wpre;  // tile-local; K6 adds tile_prefix
   if (HIST) {
     for (int s = tid; s < a.S; s += kSmcThreads)
-      if (shist[s]) atomicAdd(&a.hist[s], shist[s]);
+      if (cnt[s]) atomicAdd(&a.hist[s], static_cast<unsigned long long>(cnt[s]) * wS[s]);
   }
   if (warp != 0) return;  // only warp 0 waits on the predecessors
   if (lane == 0) st_relaxed_u64(a.flags + tile, (tile == 0 ? kFlagIncl : kFlagAgg) | agg);
@@ -355,7 +358,7 @@ __device__ __forceinline__ unsigned long long seg_incl(const SmcResampleArgs& a,
 // n_local if none. The segment is found with a 33-ary search (5 rounds for 3e6 segments), then
 // resolved inside the segment with a warp scan of its 32 weights.
 __device__ unsigned long long warp_upper_bound(unsigned long long t, const SmcResampleArgs& a,
-                                               float M) {
+                                               const uint32_t* wS) {
   const int lane = threadIdx.x & 31;
   const unsigned long long n_segs = (a.n_local + kSegment - 1) / kSegment;
   unsigned long long lo = 0, hi = n_segs;  // invariant: answer in [lo, hi]
@@ -381,7 +384,7 @@ __device__ unsigned long long warp_upper_bound(unsigned long long t, const SmcRe
   if (s >= n_segs) return a.n_local;
   const unsigned long long base = s > 0 ? seg_incl(a, s - 1) : 0ull;
   const unsigned long long i = s * kSegment + lane;
-  const uint32_t w = i < a.n_local ? smc_w(smc_e(a.lw[i], M)) : 0u;
+  const uint32_t w = i < a.n_local ? wS[a.x[i]] : 0u;
   unsigned long long incl = w;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -401,10 +404,10 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
   __shared__ unsigned long long wsum[kSmcThreads / 32];
   __shared__ unsigned long long s_u64[4];
   __shared__ unsigned long long s_rank_begin[MULTI ? kMaxRanks + 1 : 1];
-  __shared__ float s_mu[kMaxStates];
+  __shared__ uint32_t wS[kMaxStates];   // quantised weights of population t per state
+  __shared__ float lwS1[kMaxStates];    // log-weights of population t + 1 per state
   __shared__ BlockScratch sc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int q = tid; q < m.S; q += kSmcThreads) s_mu[q] = m.mu[q];
   if (MULTI)
     for (int q = tid; q <= a.world; q += kSmcThreads) s_rank_begin[q] = a.rank_begin[q];
   const bool debug_anc = a.anc_out != nullptr;
@@ -439,7 +442,12 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
   }
   const unsigned long long Tr = a.rank_recs[4 * a.rank];
   if (T == 0) return;  // all weights zero: the host raises AllZeroWeightError
-  const float M = key2f(*a.m_key);
+  {
+    __shared__ float eS[kMaxStates];
+    build_tables(m, a.y_cur, key2f(*a.m_key), nullptr, eS, wS);
+    build_tables(m, a.y_next, neg_inf_f(), lwS1, nullptr, nullptr);
+  }
+  __syncthreads();
   const PhiloxKey key = make_key(a.key);
   Comb cb;
   cb.u = draw_block(key, a.t, 0u, CUPPL_TAG_SMC_COMB).x;
@@ -467,7 +475,7 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
   // ancestor of the first output -> first batch starts at its segment boundary
   if (warp == 0) {
     const unsigned long long tl = comb_target(static_cast<unsigned int>(jb_lo), cb) - O;
-    const unsigned long long i0 = warp_upper_bound(tl, a, M);
+    const unsigned long long i0 = warp_upper_bound(tl, a, wS);
     if (lane == 0) s_u64[2] = i0;
   }
   __syncthreads();
@@ -483,21 +491,20 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
     uint32_t w[kBatchPerThread];
     unsigned long long tw = 0;
     if (i0 + kBatchPerThread <= a.n_local) {
-      const float4 f0 = __ldcs(reinterpret_cast<const float4*>(a.lw + i0));
-      const float4 f1 = __ldcs(reinterpret_cast<const float4*>(a.lw + i0) + 1);
-      *reinterpret_cast<uint2*>(xs + kBatchPerThread * tid) = __ldcs(reinterpret_cast<const uint2*>(a.x + i0));
-      const float v[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+      const uint2 xx = __ldcs(reinterpret_cast<const uint2*>(a.x + i0));
+      *reinterpret_cast<uint2*>(xs + kBatchPerThread * tid) = xx;
 #pragma unroll
       for (int k = 0; k < kBatchPerThread; ++k) {
-        w[k] = smc_w(smc_e(v[k], M));
+        w[k] = wS[((k < 4 ? xx.x : xx.y) >> (8 * (k & 3))) & 0xFFu];
         tw += w[k];
       }
     } else {
 #pragma unroll
       for (int k = 0; k < kBatchPerThread; ++k) {
         const bool ok = i0 + k < a.n_local;
-        w[k] = ok ? smc_w(smc_e(a.lw[i0 + k], M)) : 0u;
-        xs[kBatchPerThread * tid + k] = ok ? a.x[i0 + k] : 0;
+        const uint8_t st = ok ? a.x[i0 + k] : 0;
+        w[k] = ok ? wS[st] : 0u;
+        xs[kBatchPerThread * tid + k] = st;
         tw += w[k];
       }
     }
@@ -543,14 +550,12 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
       const uint4 wd = draw_block(key, jq >> 2, a.t + 1, CUPPL_TAG_SMC_STEP);
       const uint32_t wv[4] = {wd.x, wd.y, wd.z, wd.w};
       uint8_t xo[4];
-      float lo[4];
       bool all = true;
       int k = -1;
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
         const unsigned long long j = jq + h;
         xo[h] = 0;
-        lo[h] = 0.f;
         if (j >= j_cur && j < j_next) {
           const unsigned long long t = cc.tgt - off;  // batch-relative target, < btot
           {  // smallest k with cb_incl[k] > t; targets increase, so search above the last hit
@@ -565,10 +570,8 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
           }
           const int xa = xs[k];
           const int s = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[h]);
-          const float l = emission(a.y_next, s_mu[s], m.inv_sd, m.c);
           xo[h] = static_cast<uint8_t>(s);
-          lo[h] = l;
-          bmax = fmaxf(bmax, l);
+          bmax = fmaxf(bmax, lwS1[s]);
           if (debug_anc) {
             int q = 0;
             if (MULTI)
@@ -594,8 +597,7 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
       const unsigned long long dest = jq - rb;
       if (all && same && jq >= rb && (dest & 3) == 0) {
         const uint32_t packed = xo[0] | (xo[1] << 8) | (xo[2] << 16) | (static_cast<uint32_t>(xo[3]) << 24);
-        *reinterpret_cast<uint32_t*>(a.x_out[q] + dest) = packed;
-        __stcs(reinterpret_cast<float4*>(a.lw_out[q] + dest), make_float4(lo[0], lo[1], lo[2], lo[3]));
+        __stcs(reinterpret_cast<unsigned int*>(a.x_out[q] + dest), packed);
       } else {
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
@@ -606,7 +608,6 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
               while (qq + 1 < a.world && s_rank_begin[qq + 1] <= j) ++qq;
             const unsigned long long rbb = MULTI ? s_rank_begin[qq] : 0ull;
             a.x_out[qq][j - rbb] = xo[h];
-            a.lw_out[qq][j - rbb] = lo[h];
           }
         }
       }
@@ -660,13 +661,34 @@ cudaError_t launch_smc_init(const SmcModel& m, const SmcInitArgs& a, int sm_coun
   return cudaGetLastError();
 }
 
-cudaError_t launch_smc_scan(const SmcScanArgs& a, int sm_count, cudaStream_t st) {
+cudaError_t launch_smc_scan(const SmcModel& m, const SmcScanArgs& a, int sm_count, cudaStream_t st) {
   (void)sm_count;
   const unsigned long long n_tiles = (a.n_local + kTile - 1) / kTile;
   if (a.hist)
-    smc_scan_kernel<true><<<static_cast<unsigned>(n_tiles), kSmcThreads, 0, st>>>(a);
+    smc_scan_kernel<true><<<static_cast<unsigned>(n_tiles), kSmcThreads, 0, st>>>(m, a);
   else
-    smc_scan_kernel<false><<<static_cast<unsigned>(n_tiles), kSmcThreads, 0, st>>>(a);
+    smc_scan_kernel<false><<<static_cast<unsigned>(n_tiles), kSmcThreads, 0, st>>>(m, a);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(kSmcThreads) smc_log_weights_kernel(const __grid_constant__ SmcModel m,
+                                                                      float y, const uint8_t* x,
+                                                                      unsigned long long n, float* lw) {
+  __shared__ float lwS[kMaxStates];
+  build_tables(m, y, neg_inf_f(), lwS, nullptr, nullptr);
+  __syncthreads();
+  for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<unsigned long long>(gridDim.x) * blockDim.x)
+    lw[i] = lwS[x[i]];
+}
+
+cudaError_t launch_smc_log_weights(const SmcModel& m, float y, const uint8_t* x, unsigned long long n,
+                                   float* lw, int sm_count, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  unsigned long long g = (n + kSmcThreads - 1) / kSmcThreads;
+  const unsigned long long cap = static_cast<unsigned long long>(sm_count) * 8;
+  if (g > cap) g = cap;
+  smc_log_weights_kernel<<<static_cast<unsigned>(g), kSmcThreads, 0, st>>>(m, y, x, n, lw);
   return cudaGetLastError();
 }
 

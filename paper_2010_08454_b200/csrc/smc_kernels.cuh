@@ -30,21 +30,24 @@ struct SmcModel {
   float mu[kMaxStates];               // emission means
 };
 
+// A population is only its states (u8): in a discrete-state HMM the log-weight of a particle
+// is a function of its state, lw = log N(y_t; mu[x], sd), so every kernel rebuilds the S-entry
+// per-step tables (emission, quantised weight) in shared memory instead of storing lw.
 struct SmcInitArgs {
   unsigned long long n_local;  // particles on this rank
-  unsigned long long j_begin;  // global index of local particle 0 (multiple of 4)
+  unsigned long long j_begin;  // global index of local particle 0 (multiple of 8)
   unsigned long long key;
   float y0;
   int pad_;
   uint8_t* x;
-  float* lw;
   int* m_key;  // ordered-int key of max lw_0 (atomicMax target)
 };
 
 struct SmcScanArgs {
   unsigned long long n_local;
-  const float* lw;
   const uint8_t* x;
+  float y;                       // observation of population t
+  int S;
   const int* m_key;              // max of lw_t as an ordered int (global over ranks)
   unsigned long long* segoff;    // [ceil(n/32)] TILE-local inclusive offsets per segment
   unsigned long long* tile_prefix;  // [n_tiles] exclusive prefix of the tile sums (look-back)
@@ -53,8 +56,6 @@ struct SmcScanArgs {
   double* tile_s;                // [n_tiles][2] per-tile sum e, sum e^2
   unsigned long long* hist;      // [S] integer filtering weights of x_t (NULL: skip), zero on entry
   unsigned long long* rank_rec;  // [4]: T_r written by the last tile (other words untouched)
-  int S;
-  int pad_;
 };
 
 struct SmcResampleArgs {
@@ -63,8 +64,9 @@ struct SmcResampleArgs {
   unsigned long long key;
   unsigned int t;  // population being resampled; the new one is t + 1
   int rank, world;
-  float y_next;
-  const float* lw;
+  float y_cur;     // observation of population t (source weights)
+  float y_next;    // observation of population t + 1 (max of the new log-weights)
+  int pad_;
   const uint8_t* x;
   const int* m_key;                        // max of lw_t (ordered int)
   const unsigned long long* segoff;        // tile-local inclusive segment offsets
@@ -75,7 +77,6 @@ struct SmcResampleArgs {
   const unsigned long long* rank_recs;     // [world][4] gathered rank records of step t
   const unsigned long long* rank_begin;    // [world + 1] global index of each rank's first particle
   uint8_t* const* x_out;                   // [world] destination x (peer-mapped for q != rank)
-  float* const* lw_out;                    // [world] destination lw
   unsigned long long* const* anc_out;      // [world] debug ancestor (global index) or NULL
   int* m_key_next;                         // atomicMax of lw_{t+1} over the outputs written here
   unsigned long long* flags_to_clear;      // K5 look-back words, zeroed for the next scan
@@ -83,7 +84,9 @@ struct SmcResampleArgs {
 };
 
 cudaError_t launch_smc_init(const SmcModel& m, const SmcInitArgs& a, int sm_count, cudaStream_t st);
-cudaError_t launch_smc_scan(const SmcScanArgs& a, int sm_count, cudaStream_t st);
+cudaError_t launch_smc_scan(const SmcModel& m, const SmcScanArgs& a, int sm_count, cudaStream_t st);
+cudaError_t launch_smc_log_weights(const SmcModel& m, float y, const uint8_t* x, unsigned long long n,
+                                   float* lw, int sm_count, cudaStream_t st);
 cudaError_t launch_smc_fold(const double* tile_s, unsigned long long n_tiles, double* stats_out,
                             unsigned int* counters, cudaStream_t st);
 cudaError_t launch_smc_resample(const SmcModel& m, const SmcResampleArgs& a, int sm_count,

@@ -80,7 +80,7 @@ def _align(v: int) -> int:
 
 
 class _Arena:
-    """x[2], lw[2] (and anc[2]) of one rank in one cudaMalloc'd arena shareable by CUDA IPC."""
+    """x[2] (and anc[2]) of one rank in one cudaMalloc'd arena shareable by CUDA IPC."""
 
     def __init__(self, n: int, with_anc: bool, device):
         import torch
@@ -88,8 +88,7 @@ class _Arena:
         self.n = n
         self.off = {}
         o = 0
-        for name, size in (("x0", n), ("x1", n), ("lw0", 4 * n), ("lw1", 4 * n)) + (
-                (("anc0", 8 * n), ("anc1", 8 * n)) if with_anc else ()):
+        for name, size in (("x0", n), ("x1", n)) + ((("anc0", 8 * n), ("anc1", 8 * n)) if with_anc else ()):
             self.off[name] = o
             o += _align(size)
         self.bytes = o
@@ -99,8 +98,6 @@ class _Arena:
         with torch.cuda.device(device):
             self.x = [torch.as_tensor(_DevArray(self.base + self.off[f"x{i}"], n, "|u1"), device=device)
                       for i in range(2)]
-            self.lw = [torch.as_tensor(_DevArray(self.base + self.off[f"lw{i}"], n, "<f4"), device=device)
-                       for i in range(2)]
             self.anc = ([torch.as_tensor(_DevArray(self.base + self.off[f"anc{i}"], n, "<i8"), device=device)
                          for i in range(2)] if with_anc else None)
 
@@ -128,11 +125,10 @@ class _Rank:
         self.lo, self.n = lo, hi - lo
         if runner.multiprocess:
             self.arena = _Arena(self.n, runner.record_ancestors, dev)
-            self.x, self.lw, self.anc = self.arena.x, self.arena.lw, self.arena.anc
+            self.x, self.anc = self.arena.x, self.arena.anc
         else:
             self.arena = None
             self.x = [torch.empty(self.n, dtype=torch.uint8, device=dev) for _ in range(2)]
-            self.lw = [torch.empty(self.n, dtype=torch.float32, device=dev) for _ in range(2)]
             self.anc = ([torch.empty(self.n, dtype=torch.int64, device=dev) for _ in range(2)]
                         if runner.record_ancestors else None)
         ws = N.lib().cuppl_smc_workspace_bytes(self.n)
@@ -200,18 +196,16 @@ class SmcRunner:
         # destination pointer tables per ping-pong parity: x_out / lw_out / anc_out [world]
         self._peers = []
         if self.multiprocess:
-            xps, lps, aps = self._exchange_arenas()
+            xps, aps = self._exchange_arenas()
         self._tables = {}
         for par in (0, 1):
             if self.multiprocess:
-                xp, lp = xps[par], lps[par]
+                xp = xps[par]
                 ap = aps[par] if record_ancestors else None
             else:
                 xp = [rk.x[par].data_ptr() for rk in self.ranks]
-                lp = [rk.lw[par].data_ptr() for rk in self.ranks]
                 ap = [rk.anc[par].data_ptr() for rk in self.ranks] if record_ancestors else None
             self._tables[par] = (torch.tensor(xp, dtype=torch.int64, device=dev),
-                                 torch.tensor(lp, dtype=torch.int64, device=dev),
                                  torch.tensor(ap, dtype=torch.int64, device=dev) if ap else None)
         self.ancestors = []
         self._pending_anc = None
@@ -237,9 +231,8 @@ class SmcRunner:
             self._peers.append(p.value)
             bases.append((p.value, off))
         xs = [[b + o[f"x{par}"] for b, o in bases] for par in (0, 1)]
-        ls = [[b + o[f"lw{par}"] for b, o in bases] for par in (0, 1)]
         an = ([[b + o[f"anc{par}"] for b, o in bases] for par in (0, 1)] if self.record_ancestors else None)
-        return xs, ls, an
+        return xs, an
 
     def close(self):
         """Unmap peer arenas (the local arena is freed with the runner)."""
@@ -309,8 +302,8 @@ class SmcRunner:
         st = N.stream_ptr(self.device)
         for rk in self.ranks:
             N.check(L.cuppl_smc_init(C.byref(self.cm), rk.n, rk.lo, self.key, float(self.ys[0]),
-                                     N.ptr(rk.x[0]), N.ptr(rk.lw[0]), N.ptr(rk.m_key[0:1]),
-                                     N.ptr(rk.ws), rk.ws.numel(), st), "smc_init", seed=self.seed)
+                                     N.ptr(rk.x[0]), N.ptr(rk.m_key[0:1]), N.ptr(rk.ws), rk.ws.numel(), st),
+                    "smc_init", seed=self.seed)
         self.cur = 0
 
     def step(self, t: int):
@@ -321,10 +314,10 @@ class SmcRunner:
         self._snapshot_ancestors()
         h = self.hist.get(t)
         for i, rk in enumerate(self.ranks):
-            N.check(L.cuppl_smc_scan(rk.n, N.ptr(rk.lw[self.cur]), N.ptr(rk.x[self.cur]),
-                                     N.ptr(rk.m_key[t:t + 1]), self.model.n_states,
-                                     None if h is None else N.ptr(h[i]), N.ptr(rk.rec[t]),
-                                     N.ptr(rk.ws), rk.ws.numel(), st), "smc_scan", seed=self.seed, step=t)
+            N.check(L.cuppl_smc_scan(C.byref(self.cm), rk.n, float(self.ys[t]), N.ptr(rk.x[self.cur]),
+                                     N.ptr(rk.m_key[t:t + 1]), None if h is None else N.ptr(h[i]),
+                                     N.ptr(rk.rec[t]), N.ptr(rk.ws), rk.ws.numel(), st),
+                    "smc_scan", seed=self.seed, step=t)
         self._allgather(t)
         if t + 1 >= self.T:
             for rk in self.ranks:
@@ -332,17 +325,27 @@ class SmcRunner:
                         "smc_fold", seed=self.seed, step=t)
             return
         nxt = 1 - self.cur
-        xt, lt, at = self._tables[nxt]
+        xt, at = self._tables[nxt]
         for rk in self.ranks:
             N.check(L.cuppl_smc_resample(
-                C.byref(self.cm), rk.n, self.N, self.key, t, rk.r, self.world, float(self.ys[t + 1]),
-                N.ptr(rk.lw[self.cur]), N.ptr(rk.x[self.cur]), N.ptr(rk.m_key[t:t + 1]),
-                N.ptr(self.gathered[t]), N.ptr(self.rank_begin), N.ptr(xt), N.ptr(lt),
+                C.byref(self.cm), rk.n, self.N, self.key, t, rk.r, self.world, float(self.ys[t]),
+                float(self.ys[t + 1]), N.ptr(rk.x[self.cur]), N.ptr(rk.m_key[t:t + 1]),
+                N.ptr(self.gathered[t]), N.ptr(self.rank_begin), N.ptr(xt),
                 None if at is None else N.ptr(at), N.ptr(rk.m_key[t + 1:t + 2]), N.ptr(rk.stats[t]),
                 N.ptr(rk.ws), rk.ws.numel(), st), "smc_resample", seed=self.seed, step=t)
         if self.record_ancestors:
             self._pending_anc = nxt  # complete only after the next collective (peer stores)
         self.cur = nxt
+
+    def log_weights(self, rk):
+        """Per-particle log-weights of the current population (tabulated per state)."""
+        import torch
+
+        lw = torch.empty(rk.n, dtype=torch.float32, device=self.device)
+        N.check(N.lib().cuppl_smc_log_weights(C.byref(self.cm), float(self.ys[self.T - 1]),
+                                              N.ptr(rk.x[self.cur]), rk.n, N.ptr(lw),
+                                              N.stream_ptr(self.device)), "smc_log_weights")
+        return lw
 
     def _snapshot_ancestors(self):
         if self._pending_anc is not None:
@@ -378,7 +381,7 @@ class SmcRunner:
             res.filtering_int[t] = hi
             res.filtering[t] = hi.astype(np.float64) / float(hi.sum())
         res.states = [rk.x[self.cur] for rk in self.ranks]
-        res.log_weights = [rk.lw[self.cur] for rk in self.ranks]
+        res.log_weights = [self.log_weights(rk) for rk in self.ranks]
         res.ancestors = self.ancestors
         return res
 
