@@ -175,6 +175,7 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(const __grid_cons
                                                                SmcScanArgs a) {
   __shared__ uint32_t wS[kMaxStates];
   __shared__ float eS[kMaxStates];
+  __shared__ uint2 wes[kMaxStates];  // (w, bits(e)) in one 64-bit entry: one LDS per particle
   __shared__ unsigned long long wtot[kSmcThreads / 32];
   __shared__ double wpart[kSmcThreads / 32][2];
   __shared__ unsigned int s_tile;
@@ -184,8 +185,10 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(const __grid_cons
   const unsigned long long n_tiles = (n + kTile - 1) / kTile;
   if (tid == 0) s_tile = atomicAdd(&a.counters[0], 1u);  // launch-order tile ids: look-back is deadlock free
   build_tables(m, a.y, key2f(*a.m_key), nullptr, eS, wS);
-  if (HIST)
-    for (int s = tid; s < a.S; s += kSmcThreads) cnt[s] = 0u;
+  for (int s = tid; s < a.S; s += kSmcThreads) {
+    wes[s] = make_uint2(wS[s], __float_as_uint(eS[s]));
+    if (HIST) cnt[s] = 0u;
+  }
   __syncthreads();
   const unsigned long long tile = s_tile;
   // thread tid owns segment tid of the tile: particles [tile * 8192 + 32 tid, +32)
@@ -206,12 +209,26 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(const __grid_cons
   const uint32_t words[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
   unsigned long long ws = 0;
   float s1 = 0.f, s2 = 0.f;
+  if (!HIST && valid == kSegment) {  // fast path: a full segment, no per-particle checks
+    uint32_t wsum_lo = 0, wsum_hi = 0;  // two u32 halves of 16 weights each never overflow 2^36
+#pragma unroll
+    for (int k = 0; k < kSegment; ++k) {
+      const uint2 te = wes[(words[k >> 2] >> (8 * (k & 3))) & 0xFFu];
+      const float e = __uint_as_float(te.y);
+      if (k < 16) wsum_lo += te.x >> 4; else wsum_hi += te.x >> 4;
+      ws += te.x & 15u;
+      s1 += e;
+      s2 = fmaf(e, e, s2);
+    }
+    ws += (static_cast<unsigned long long>(wsum_lo) + wsum_hi) << 4;
+  } else {
 #pragma unroll
   for (int k = 0; k < kSegment; ++k) {
     const uint32_t st = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
     const bool ok = k < valid;
-    const uint32_t w = ok ? wS[st] : 0u;
-    const float e = ok ? eS[st] : 0.f;
+    const uint2 te = wes[st];
+    const uint32_t w = ok ? te.x : 0u;
+    const float e = ok ? __uint_as_float(te.y) : 0.f;
     ws += w;
     s1 += e;
     s2 = fmaf(e, e, s2);
@@ -221,6 +238,7 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(const __grid_cons
       const unsigned int grp = __match_any_sync(0xffffffffu, key);
       if (ok && lane == __ffs(grp) - 1) atomicAdd(&cnt[st], static_cast<unsigned int>(__popc(grp)));
     }
+  }
   }
   double d1 = s1, d2 = s2;  // per-warp fp64 partials, fixed tree
 #pragma unroll
@@ -276,7 +294,7 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(const __grid_cons
 // where j R0 + Ra < N^2 < 2^62 (N < 2^31); every per-index quantity fits 32 bits.
 struct Comb {
   unsigned int N, Q, R0, Qa, Ra;
-  double invN, step_inv;  // 1/N, N/T
+  double invN, step_inv, a_over_t;  // 1/N, N/T, A/T
   unsigned int u;
 };
 
@@ -340,12 +358,15 @@ __device__ __forceinline__ unsigned long long comb_target(unsigned int j, const 
   return c.tgt;
 }
 
-// smallest j in [0, N] with target_j >= c (N if none)
+// smallest j in [0, N] with target_j >= c (N if none). target_j >= c <=> j T + A >= c N, so
+// F(c) = ceil((c N - A) / T): fp64 estimate, then exact fix-up on the integer targets.
 __device__ __forceinline__ unsigned int first_j_at_least(unsigned long long c, const Comb& cb) {
-  CombCursor cur;
-  cur.seek(0, cb);
-  cur.advance_to(c, cb);
-  return cur.j;
+  if (c == 0) return 0u;
+  const double est = __dmul_rn(__ull2double_rn(c), cb.step_inv) - cb.a_over_t;
+  unsigned int j = est <= 0.0 ? 0u : est >= static_cast<double>(cb.N) ? cb.N : static_cast<unsigned int>(ceil(est));
+  while (j > 0 && comb_target(j - 1, cb) >= c) --j;
+  while (j < cb.N && comb_target(j, cb) < c) ++j;
+  return j;
 }
 
 // Rank-local inclusive weight prefix at the end of segment s (K5 writes tile-local values).
@@ -396,7 +417,7 @@ __device__ unsigned long long warp_upper_bound(unsigned long long t, const SmcRe
   return s * kSegment + (__ffs(bal) - 1);
 }
 
-template <bool MULTI>
+template <bool MULTI, bool DEBUG>
 __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __grid_constant__ SmcModel m,
                                                                       SmcResampleArgs a) {
   __shared__ unsigned long long cb_incl[kBatch];  // batch-relative inclusive weight prefix per source
@@ -410,7 +431,7 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (MULTI)
     for (int q = tid; q <= a.world; q += kSmcThreads) s_rank_begin[q] = a.rank_begin[q];
-  const bool debug_anc = a.anc_out != nullptr;
+  constexpr bool debug_anc = DEBUG;
   const unsigned long long n_tiles = a.n_tiles;
 
   // CTA 0: fixed-order fp64 fold of K5's per-tile sums -> rank (sum e, sum e^2); reset K5's
@@ -459,6 +480,7 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
   cb.Ra = static_cast<unsigned int>(A % cb.N);
   cb.invN = 1.0 / static_cast<double>(cb.N);
   cb.step_inv = static_cast<double>(cb.N) / static_cast<double>(T);
+  cb.a_over_t = static_cast<double>(A) / static_cast<double>(T);
 
   // this rank's outputs: J_r = {j : O <= target_j < O + Tr}; this CTA's even share of it
   if (tid == 0) {
@@ -558,15 +580,12 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
         xo[h] = 0;
         if (j >= j_cur && j < j_next) {
           const unsigned long long t = cc.tgt - off;  // batch-relative target, < btot
-          {  // smallest k with cb_incl[k] > t; targets increase, so search above the last hit
-            int lo2 = k < 0 ? 0 : k, hi2 = kBatch - 1;
-#pragma unroll 1
-            while (lo2 < hi2) {
-              const int mid = (lo2 + hi2) >> 1;
-              if (cb_incl[mid] > t) hi2 = mid;
-              else lo2 = mid + 1;
-            }
-            k = lo2;
+          {  // smallest k with cb_incl[k] > t (exists: t < batch total): branchless, 11 steps
+            int kk = 0;
+#pragma unroll
+            for (int step = kBatch / 2; step >= 1; step >>= 1)
+              kk += (cb_incl[kk + step - 1] <= t) ? step : 0;
+            k = kk;
           }
           const int xa = xs[k];
           const int s = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[h]);
@@ -692,25 +711,28 @@ cudaError_t launch_smc_log_weights(const SmcModel& m, float y, const uint8_t* x,
   return cudaGetLastError();
 }
 
-template <bool MULTI>
+template <bool MULTI, bool DEBUG>
 static cudaError_t launch_resample_t(const SmcModel& m, const SmcResampleArgs& a, int sm_count,
                                      cudaStream_t st) {
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, smc_resample_kernel<MULTI>,
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, smc_resample_kernel<MULTI, DEBUG>,
                                                                 kSmcThreads, 0);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   unsigned long long g = static_cast<unsigned long long>(sm_count) * per_sm;
   const unsigned long long want = (a.n_local + kBatch - 1) / kBatch;  // >= one batch per CTA
   if (g > want) g = want > 0 ? want : 1;
-  smc_resample_kernel<MULTI><<<static_cast<unsigned>(g), kSmcThreads, 0, st>>>(m, a);
+  smc_resample_kernel<MULTI, DEBUG><<<static_cast<unsigned>(g), kSmcThreads, 0, st>>>(m, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_smc_resample(const SmcModel& m, const SmcResampleArgs& a, int sm_count,
                                 cudaStream_t st) {
-  return a.world > 1 ? launch_resample_t<true>(m, a, sm_count, st)
-                     : launch_resample_t<false>(m, a, sm_count, st);
+  if (a.anc_out)
+    return a.world > 1 ? launch_resample_t<true, true>(m, a, sm_count, st)
+                       : launch_resample_t<false, true>(m, a, sm_count, st);
+  return a.world > 1 ? launch_resample_t<true, false>(m, a, sm_count, st)
+                     : launch_resample_t<false, false>(m, a, sm_count, st);
 }
 
 }  // namespace cuppl
