@@ -172,7 +172,7 @@ CUPPL_API size_t cuppl_smc_workspace_bytes(uint64_t n_local);
  * tabulate the S per-state weights of a step instead of storing log-weights. */
 
 /* t = 0: x[j] ~ categorical(init) for local particles j_begin + [0, n_local) (j_begin multiple
- * of 8); atomicMax of lw_0 into *m_key (ordered int, caller initialises it to INT32_MIN).
+ * of 16); atomicMax of lw_0 into *m_key (ordered int, caller initialises it to INT32_MIN).
  * Zeroes the workspace. */
 CUPPL_API int cuppl_smc_init(const cuppl_smc_model* m, uint64_t n_local, uint64_t j_begin,
                              uint64_t key, float y0, uint8_t* x, int32_t* m_key, void* workspace,
@@ -188,7 +188,7 @@ CUPPL_API int cuppl_smc_scan(const cuppl_smc_model* m, uint64_t n_local, float y
 
 /* Systematic resampling of population t (observation y_cur) + propagation to t+1 (y_next)
  * (K6). rank_recs: device [world][4] records of every rank (all-gathered); rank_begin: device
- * [world+1] global index of each rank's first particle (multiples of 8); x_out / anc_out:
+ * [world+1] global index of each rank's first particle (multiples of 16); x_out / anc_out:
  * device arrays of `world` destination pointers (peer-mapped for other ranks; anc_out NULL to
  * skip). The outputs whose ancestors live on this rank are written to their owners;
  * *m_key_next gets the atomicMax of the new log-weights written here; stats_out[2] (device

@@ -86,7 +86,7 @@ int cuppl_smc_init(const cuppl_smc_model* m, uint64_t n_local, uint64_t j_begin,
   SmcWs w;
   if (int s = check_ws(n_local, workspace, workspace_bytes, &w)) return s;
   if (!x || !m_key) return set_error(CUPPL_E_ARGUMENT, "NULL buffer");
-  if (j_begin % 8) return set_error(CUPPL_E_ARGUMENT, "j_begin must be a multiple of 8");
+  if (j_begin % 16) return set_error(CUPPL_E_ARGUMENT, "j_begin must be a multiple of 16");
   int sms = 0;
   if (int s = device_sm_count(&sms)) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

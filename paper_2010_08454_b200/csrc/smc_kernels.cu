@@ -513,11 +513,12 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
     uint32_t w[kBatchPerThread];
     unsigned long long tw = 0;
     if (i0 + kBatchPerThread <= a.n_local) {
-      const uint2 xx = __ldcs(reinterpret_cast<const uint2*>(a.x + i0));
-      *reinterpret_cast<uint2*>(xs + kBatchPerThread * tid) = xx;
+      const uint4 xx = __ldcs(reinterpret_cast<const uint4*>(a.x + i0));
+      *reinterpret_cast<uint4*>(xs + kBatchPerThread * tid) = xx;
+      const uint32_t xw[4] = {xx.x, xx.y, xx.z, xx.w};
 #pragma unroll
       for (int k = 0; k < kBatchPerThread; ++k) {
-        w[k] = wS[((k < 4 ? xx.x : xx.y) >> (8 * (k & 3))) & 0xFFu];
+        w[k] = wS[(xw[k >> 2] >> (8 * (k & 3))) & 0xFFu];
         tw += w[k];
       }
     } else {
@@ -560,73 +561,82 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
     __syncthreads();
     const unsigned long long j_next = s_u64[3];
     const unsigned long long off = O + c_base;  // global target of batch-relative weight 0
-    const unsigned long long jbase = j_cur & ~3ull;  // Philox blocks cover 4 outputs
+    const unsigned long long jbase = j_cur & ~15ull;  // 16-output thread slots (4 Philox blocks)
 
-    // propagate in dense rounds of 1024 outputs: thread tid takes 4 consecutive outputs, finds
-    // the first ancestor by binary search over the batch prefix, the others by stepping
-    for (unsigned long long jr = jbase; jr < j_next; jr += 4 * kSmcThreads) {
-      const unsigned long long jq = jr + 4 * tid;
-      if (jq + 3 < j_cur || jq >= j_next) continue;
+    // propagate in rounds of 4096 outputs: thread tid takes 16 consecutive outputs (4 Philox
+    // blocks); the ancestor of its first output is a binary search over the staged prefix, the
+    // next ones follow by a monotone merge pointer (targets increase with j)
+    for (unsigned long long jr = jbase; jr < j_next; jr += kChunk) {
+      const unsigned long long jq = jr + kOutPerThread * static_cast<unsigned long long>(tid);
+      if (jq + kOutPerThread <= j_cur || jq >= j_next) continue;
+      const unsigned long long jf = jq > j_cur ? jq : j_cur;
       CombCursor cc;
-      cc.seek(static_cast<unsigned int>(jq), cb);
-      const uint4 wd = draw_block(key, jq >> 2, a.t + 1, CUPPL_TAG_SMC_STEP);
-      const uint32_t wv[4] = {wd.x, wd.y, wd.z, wd.w};
-      uint8_t xo[4];
+      cc.seek(static_cast<unsigned int>(jf), cb);
+      int k;
+      {  // smallest k with cb_incl[k] > t (exists: t < batch total): branchless, 12 steps
+        const unsigned long long t = cc.tgt - off;
+        int kk = 0;
+#pragma unroll
+        for (int step = kBatch / 2; step >= 1; step >>= 1)
+          kk += (cb_incl[kk + step - 1] <= t) ? step : 0;
+        k = kk;
+      }
+      uint32_t xo[kOutPerThread / 4] = {0, 0, 0, 0};
       bool all = true;
-      int k = -1;
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const unsigned long long j = jq + h;
-        xo[h] = 0;
-        if (j >= j_cur && j < j_next) {
-          const unsigned long long t = cc.tgt - off;  // batch-relative target, < btot
-          {  // smallest k with cb_incl[k] > t (exists: t < batch total): branchless, 11 steps
-            int kk = 0;
-#pragma unroll
-            for (int step = kBatch / 2; step >= 1; step >>= 1)
-              kk += (cb_incl[kk + step - 1] <= t) ? step : 0;
-            k = kk;
-          }
-          const int xa = xs[k];
-          const int s = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[h]);
-          xo[h] = static_cast<uint8_t>(s);
-          bmax = fmaxf(bmax, lwS1[s]);
-          if (debug_anc) {
-            int q = 0;
-            if (MULTI)
-              while (q + 1 < a.world && s_rank_begin[q + 1] <= j) ++q;
-            const unsigned long long rb = MULTI ? s_rank_begin[q] : 0ull;
-            const unsigned long long my = MULTI ? s_rank_begin[a.rank] : 0ull;
-            a.anc_out[q][j - rb] = my + batch_base + k;
-          }
-        } else {
+      for (int g = 0; g < kOutPerThread / 4; ++g) {
+        const unsigned long long jg = jq + 4 * g;
+        if (jg + 3 < j_cur || jg >= j_next) {
           all = false;
+          continue;
         }
-        cc.next(cb);
+        const uint4 wd = draw_block(key, jg >> 2, a.t + 1, CUPPL_TAG_SMC_STEP);
+        const uint32_t wv[4] = {wd.x, wd.y, wd.z, wd.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const unsigned long long j = jg + h;
+          if (j >= j_cur && j < j_next) {
+            const unsigned long long t = cc.tgt - off;  // batch-relative target, < btot
+            while (cb_incl[k] <= t) ++k;
+            const int xa = xs[k];
+            const int s = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[h]);
+            xo[g] |= static_cast<uint32_t>(s) << (8 * h);
+            bmax = fmaxf(bmax, lwS1[s]);
+            if (debug_anc) {
+              int q = 0;
+              if (MULTI)
+                while (q + 1 < a.world && s_rank_begin[q + 1] <= j) ++q;
+              const unsigned long long rb = MULTI ? s_rank_begin[q] : 0ull;
+              const unsigned long long my = MULTI ? s_rank_begin[a.rank] : 0ull;
+              a.anc_out[q][j - rb] = my + batch_base + k;
+            }
+            cc.next(cb);
+          } else {
+            all = false;
+          }
+        }
       }
       int q = 0;
       unsigned long long rb = 0;
       bool same = true;
       if (MULTI) {
-        const unsigned long long jf = jq > j_cur ? jq : j_cur;
         while (q + 1 < a.world && s_rank_begin[q + 1] <= jf) ++q;
         rb = s_rank_begin[q];
-        same = q + 1 >= a.world || s_rank_begin[q + 1] >= jq + 4;
+        same = q + 1 >= a.world || s_rank_begin[q + 1] >= jq + kOutPerThread;
       }
       const unsigned long long dest = jq - rb;
-      if (all && same && jq >= rb && (dest & 3) == 0) {
-        const uint32_t packed = xo[0] | (xo[1] << 8) | (xo[2] << 16) | (static_cast<uint32_t>(xo[3]) << 24);
-        __stcs(reinterpret_cast<unsigned int*>(a.x_out[q] + dest), packed);
+      if (all && same && jq >= rb && (dest & 15) == 0) {
+        __stcs(reinterpret_cast<uint4*>(a.x_out[q] + dest), make_uint4(xo[0], xo[1], xo[2], xo[3]));
       } else {
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
+        for (int h = 0; h < kOutPerThread; ++h) {
           const unsigned long long j = jq + h;
           if (j >= j_cur && j < j_next) {
             int qq = 0;
             if (MULTI)
               while (qq + 1 < a.world && s_rank_begin[qq + 1] <= j) ++qq;
             const unsigned long long rbb = MULTI ? s_rank_begin[qq] : 0ull;
-            a.x_out[qq][j - rbb] = xo[h];
+            a.x_out[qq][j - rbb] = static_cast<uint8_t>(xo[h >> 2] >> (8 * (h & 3)));
           }
         }
       }

@@ -10,12 +10,12 @@ constexpr int kSmcThreads = 256;
 constexpr int kSegment = 32;                  // particles per segment offset
 constexpr int kTileSegs = 256;                // segments per K5 tile (one per thread)
 constexpr int kTile = kTileSegs * kSegment;   // 8192 particles per scan tile
-constexpr int kBatchPerThread = 8;            // sources per thread per K6 batch
-constexpr int kBatch = kSmcThreads * kBatchPerThread;  // 2048 sources per K6 batch
-constexpr int kOutPerThread = 16;             // ancestor slots per thread per K6 sub-chunk
+constexpr int kBatchPerThread = 16;           // sources per thread per K6 batch
+constexpr int kBatch = kSmcThreads * kBatchPerThread;  // 4096 sources per K6 batch
+constexpr int kOutPerThread = 16;             // consecutive outputs per thread per K6 round
 constexpr int kHeavy = 16;                    // children ranges longer than this are filled cooperatively
 constexpr int kHeavySlots = 512;
-constexpr int kChunk = kSmcThreads * kOutPerThread;    // 2048 outputs per sub-chunk
+constexpr int kChunk = kSmcThreads * kOutPerThread;    // 4096 outputs per round
 constexpr int kMaxStates = 256;               // particle state stored as u8
 constexpr int kMaxRanks = 64;
 

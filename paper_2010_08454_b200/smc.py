@@ -59,12 +59,12 @@ class SmcResult:
 
 
 def rank_boundaries(n: int, world: int) -> list[int]:
-    """Global index of each rank's first particle; multiples of 8 (vector stores, Philox blocks)."""
-    if n < 8 * world:
-        raise ValueError("n_particles must be >= 8 * world_size")
-    n8 = n // 8
-    b = [8 * (n8 * q // world) for q in range(world)] + [n]
-    return b
+    """Global index of each rank's first particle; multiples of 16 (16-byte state stores,
+    Philox blocks of 4 outputs)."""
+    if n < 16 * world:
+        raise ValueError("n_particles must be >= 16 * world_size")
+    n16 = n // 16
+    return [16 * (n16 * q // world) for q in range(world)] + [n]
 
 
 class _DevArray:
