@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
                                                                       SmcResampleArgs a) {
   __shared__ unsigned long long cb_incl[kBatch];  // batch-relative inclusive weight prefix per source
   __shared__ uint8_t xs[kBatch];                  // staged source states
+  __shared__ __align__(16) uint8_t obuf[kOutBuf + 16];  // new states, indexed from o0 & ~15
   __shared__ unsigned long long wsum[kSmcThreads / 32];
   __shared__ unsigned long long s_u64[4];
   __shared__ unsigned long long s_rank_begin[MULTI ? kMaxRanks + 1 : 1];
@@ -561,85 +562,82 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
     __syncthreads();
     const unsigned long long j_next = s_u64[3];
     const unsigned long long off = O + c_base;  // global target of batch-relative weight 0
-    const unsigned long long jbase = j_cur & ~15ull;  // 16-output thread slots (4 Philox blocks)
 
-    // propagate in rounds of 4096 outputs: thread tid takes 16 consecutive outputs (4 Philox
-    // blocks); the ancestor of its first output is a binary search over the staged prefix, the
-    // next ones follow by a monotone merge pointer (targets increase with j)
-    for (unsigned long long jr = jbase; jr < j_next; jr += kChunk) {
-      const unsigned long long jq = jr + kOutPerThread * static_cast<unsigned long long>(tid);
-      if (jq + kOutPerThread <= j_cur || jq >= j_next) continue;
-      const unsigned long long jf = jq > j_cur ? jq : j_cur;
-      CombCursor cc;
-      cc.seek(static_cast<unsigned int>(jf), cb);
-      int k;
-      {  // smallest k with cb_incl[k] > t (exists: t < batch total): branchless, 12 steps
-        const unsigned long long t = cc.tgt - off;
-        int kk = 0;
+    // propagate [j_cur, j_next) in sub-rounds of at most kOutBuf outputs; thread tid takes an
+    // equal slice of consecutive outputs, finds the ancestor of its first by a branchless binary
+    // search over the staged prefix and the rest with a monotone merge pointer (targets increase
+    // with j); the new states are staged in shared memory and written out coalesced.
+    for (unsigned long long o0 = j_cur; o0 < j_next; o0 += kOutBuf) {
+      const unsigned long long o1 = o0 + kOutBuf < j_next ? o0 + kOutBuf : j_next;
+      const unsigned int n_out = static_cast<unsigned int>(o1 - o0);
+      const unsigned long long ob = o0 & ~15ull;  // obuf[j - ob]: same 16-byte phase as the owners' x
+      const unsigned int per = (n_out + kSmcThreads - 1) / kSmcThreads;
+      const unsigned int s0 = tid * per < n_out ? tid * per : n_out;
+      const unsigned int s1 = s0 + per < n_out ? s0 + per : n_out;
+      if (s0 < s1) {
+        CombCursor cc;
+        cc.seek(static_cast<unsigned int>(o0 + s0), cb);
+        int k;
+        {  // smallest k with cb_incl[k] > t (exists: t < batch total): branchless, 12 steps
+          const unsigned long long t = cc.tgt - off;
+          int kk = 0;
 #pragma unroll
-        for (int step = kBatch / 2; step >= 1; step >>= 1)
-          kk += (cb_incl[kk + step - 1] <= t) ? step : 0;
-        k = kk;
-      }
-      uint32_t xo[kOutPerThread / 4] = {0, 0, 0, 0};
-      bool all = true;
-#pragma unroll
-      for (int g = 0; g < kOutPerThread / 4; ++g) {
-        const unsigned long long jg = jq + 4 * g;
-        if (jg + 3 < j_cur || jg >= j_next) {
-          all = false;
-          continue;
+          for (int step = kBatch / 2; step >= 1; step >>= 1)
+            kk += (cb_incl[kk + step - 1] <= t) ? step : 0;
+          k = kk;
         }
-        const uint4 wd = draw_block(key, jg >> 2, a.t + 1, CUPPL_TAG_SMC_STEP);
-        const uint32_t wv[4] = {wd.x, wd.y, wd.z, wd.w};
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const unsigned long long j = jg + h;
-          if (j >= j_cur && j < j_next) {
-            const unsigned long long t = cc.tgt - off;  // batch-relative target, < btot
-            while (cb_incl[k] <= t) ++k;
-            const int xa = xs[k];
-            const int s = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[h]);
-            xo[g] |= static_cast<uint32_t>(s) << (8 * h);
-            bmax = fmaxf(bmax, lwS1[s]);
-            if (debug_anc) {
-              int q = 0;
-              if (MULTI)
-                while (q + 1 < a.world && s_rank_begin[q + 1] <= j) ++q;
-              const unsigned long long rb = MULTI ? s_rank_begin[q] : 0ull;
-              const unsigned long long my = MULTI ? s_rank_begin[a.rank] : 0ull;
-              a.anc_out[q][j - rb] = my + batch_base + k;
-            }
-            cc.next(cb);
-          } else {
-            all = false;
+        uint4 wd = make_uint4(0, 0, 0, 0);
+        unsigned long long blk = ~0ull;
+        for (unsigned int q = s0; q < s1; ++q) {
+          const unsigned long long j = o0 + q;
+          const unsigned long long t = cc.tgt - off;  // batch-relative target, < btot
+          while (cb_incl[k] <= t) ++k;
+          if ((j >> 2) != blk) {
+            blk = j >> 2;
+            wd = draw_block(key, blk, a.t + 1, CUPPL_TAG_SMC_STEP);
           }
-        }
-      }
-      int q = 0;
-      unsigned long long rb = 0;
-      bool same = true;
-      if (MULTI) {
-        while (q + 1 < a.world && s_rank_begin[q + 1] <= jf) ++q;
-        rb = s_rank_begin[q];
-        same = q + 1 >= a.world || s_rank_begin[q + 1] >= jq + kOutPerThread;
-      }
-      const unsigned long long dest = jq - rb;
-      if (all && same && jq >= rb && (dest & 15) == 0) {
-        __stcs(reinterpret_cast<uint4*>(a.x_out[q] + dest), make_uint4(xo[0], xo[1], xo[2], xo[3]));
-      } else {
-#pragma unroll
-        for (int h = 0; h < kOutPerThread; ++h) {
-          const unsigned long long j = jq + h;
-          if (j >= j_cur && j < j_next) {
-            int qq = 0;
+          const uint32_t h = static_cast<uint32_t>(j & 3);
+          const uint32_t wj = h == 0 ? wd.x : h == 1 ? wd.y : h == 2 ? wd.z : wd.w;
+          const int xa = xs[k];
+          const int st = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wj);
+          obuf[j - ob] = static_cast<uint8_t>(st);
+          bmax = fmaxf(bmax, lwS1[st]);
+          if (debug_anc) {
+            int r = 0;
             if (MULTI)
-              while (qq + 1 < a.world && s_rank_begin[qq + 1] <= j) ++qq;
-            const unsigned long long rbb = MULTI ? s_rank_begin[qq] : 0ull;
-            a.x_out[qq][j - rbb] = static_cast<uint8_t>(xo[h >> 2] >> (8 * (h & 3)));
+              while (r + 1 < a.world && s_rank_begin[r + 1] <= j) ++r;
+            const unsigned long long rb = MULTI ? s_rank_begin[r] : 0ull;
+            const unsigned long long my = MULTI ? s_rank_begin[a.rank] : 0ull;
+            a.anc_out[r][j - rb] = my + batch_base + k;
           }
+          cc.next(cb);
         }
       }
+      __syncthreads();
+      // coalesced copy-out of obuf[0, n_out) -> owners' x at global index o0 + i
+      int r = 0;
+      if (MULTI)
+        while (r + 1 < a.world && s_rank_begin[r + 1] <= o0) ++r;
+      unsigned long long g = o0;
+      while (g < o1) {
+        const unsigned long long rb = MULTI ? s_rank_begin[r] : 0ull;
+        const unsigned long long re = MULTI ? (r + 1 < a.world ? s_rank_begin[r + 1] : cb.N) : o1;
+        const unsigned long long e = re < o1 ? re : o1;
+        uint8_t* dst = a.x_out[r] + (g - rb);
+        const uint8_t* src = obuf + (g - ob);  // 16-byte phase of src == phase of dst
+        const unsigned int len = static_cast<unsigned int>(e - g);
+        // head bytes up to 16-byte alignment of dst, then uint4 chunks, then tail bytes
+        const unsigned int head = static_cast<unsigned int>((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15);
+        const unsigned int hb = head < len ? head : len;
+        if (tid < hb) dst[tid] = src[tid];
+        const unsigned int nv = (len - hb) / 16;
+        for (unsigned int v = tid; v < nv; v += kSmcThreads)
+          __stcs(reinterpret_cast<uint4*>(dst + hb) + v, reinterpret_cast<const uint4*>(src + hb)[v]);
+        for (unsigned int i = hb + 16 * nv + tid; i < len; i += kSmcThreads) dst[i] = src[i];
+        g = e;
+        ++r;
+      }
+      __syncthreads();  // obuf reuse
     }
     __syncthreads();  // cb_incl / xs / wsum / s_u64 reuse
     j_cur = j_next;

@@ -12,10 +12,7 @@ constexpr int kTileSegs = 256;                // segments per K5 tile (one per t
 constexpr int kTile = kTileSegs * kSegment;   // 8192 particles per scan tile
 constexpr int kBatchPerThread = 16;           // sources per thread per K6 batch
 constexpr int kBatch = kSmcThreads * kBatchPerThread;  // 4096 sources per K6 batch
-constexpr int kOutPerThread = 16;             // consecutive outputs per thread per K6 round
-constexpr int kHeavy = 16;                    // children ranges longer than this are filled cooperatively
-constexpr int kHeavySlots = 512;
-constexpr int kChunk = kSmcThreads * kOutPerThread;    // 4096 outputs per round
+constexpr int kOutBuf = 8192;                 // K6 output staging buffer (bytes = outputs)
 constexpr int kMaxStates = 256;               // particle state stored as u8
 constexpr int kMaxRanks = 64;
 
