@@ -571,12 +571,17 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
       const unsigned long long o1 = o0 + kOutBuf < j_next ? o0 + kOutBuf : j_next;
       const unsigned int n_out = static_cast<unsigned int>(o1 - o0);
       const unsigned long long ob = o0 & ~15ull;  // obuf[j - ob]: same 16-byte phase as the owners' x
-      const unsigned int per = (n_out + kSmcThreads - 1) / kSmcThreads;
-      const unsigned int s0 = tid * per < n_out ? tid * per : n_out;
-      const unsigned int s1 = s0 + per < n_out ? s0 + per : n_out;
-      if (s0 < s1) {
+      // slices of consecutive outputs, 4-aligned in j so a thread's Philox blocks (4 outputs
+      // each) are drawn at the same iteration by every lane
+      const unsigned long long a4 = o0 & ~3ull;
+      const unsigned int span4 = static_cast<unsigned int>(o1 - a4);
+      const unsigned int per = ((span4 + kSmcThreads - 1) / kSmcThreads + 3) & ~3u;
+      const unsigned long long q0 = a4 + static_cast<unsigned long long>(tid) * per;
+      const unsigned long long q1 = q0 + per < o1 ? q0 + per : o1;
+      const unsigned long long qs = q0 > o0 ? q0 : o0;
+      if (qs < q1) {
         CombCursor cc;
-        cc.seek(static_cast<unsigned int>(o0 + s0), cb);
+        cc.seek(static_cast<unsigned int>(qs), cb);
         int k;
         {  // smallest k with cb_incl[k] > t (exists: t < batch total): branchless, 12 steps
           const unsigned long long t = cc.tgt - off;
@@ -586,33 +591,32 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
             kk += (cb_incl[kk + step - 1] <= t) ? step : 0;
           k = kk;
         }
-        uint4 wd = make_uint4(0, 0, 0, 0);
-        unsigned long long blk = ~0ull;
-        for (unsigned int q = s0; q < s1; ++q) {
-          const unsigned long long j = o0 + q;
-          const unsigned long long t = cc.tgt - off;  // batch-relative target, < btot
-          while (cb_incl[k] <= t) ++k;
-          if ((j >> 2) != blk) {
-            blk = j >> 2;
-            wd = draw_block(key, blk, a.t + 1, CUPPL_TAG_SMC_STEP);
+        for (unsigned long long jg = q0; jg < q1; jg += 4) {
+          const uint4 wd = draw_block(key, jg >> 2, a.t + 1, CUPPL_TAG_SMC_STEP);
+          const uint32_t wv[4] = {wd.x, wd.y, wd.z, wd.w};
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const unsigned long long j = jg + h;
+            if (j < qs || j >= q1) continue;
+            const unsigned long long t = cc.tgt - off;  // batch-relative target, < btot
+            while (cb_incl[k] <= t) ++k;
+            const int xa = xs[k];
+            const int st = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[h]);
+            obuf[j - ob] = static_cast<uint8_t>(st);
+            bmax = fmaxf(bmax, lwS1[st]);
+            if (debug_anc) {
+              int r = 0;
+              if (MULTI)
+                while (r + 1 < a.world && s_rank_begin[r + 1] <= j) ++r;
+              const unsigned long long rb = MULTI ? s_rank_begin[r] : 0ull;
+              const unsigned long long my = MULTI ? s_rank_begin[a.rank] : 0ull;
+              a.anc_out[r][j - rb] = my + batch_base + k;
+            }
+            cc.next(cb);
           }
-          const uint32_t h = static_cast<uint32_t>(j & 3);
-          const uint32_t wj = h == 0 ? wd.x : h == 1 ? wd.y : h == 2 ? wd.z : wd.w;
-          const int xa = xs[k];
-          const int st = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wj);
-          obuf[j - ob] = static_cast<uint8_t>(st);
-          bmax = fmaxf(bmax, lwS1[st]);
-          if (debug_anc) {
-            int r = 0;
-            if (MULTI)
-              while (r + 1 < a.world && s_rank_begin[r + 1] <= j) ++r;
-            const unsigned long long rb = MULTI ? s_rank_begin[r] : 0ull;
-            const unsigned long long my = MULTI ? s_rank_begin[a.rank] : 0ull;
-            a.anc_out[r][j - rb] = my + batch_base + k;
-          }
-          cc.next(cb);
         }
       }
+      (void)n_out;
       __syncthreads();
       // coalesced copy-out of obuf[0, n_out) -> owners' x at global index o0 + i
       int r = 0;
