@@ -66,6 +66,14 @@ int linreg_variant() {
   return v;
 }
 
+int poly_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("CUPPL_POLY_VARIANT");
+    return e ? std::atoi(e) : kPolyVariant;
+  }();
+  return v;
+}
+
 size_t is_ws_bytes(int sm) {
   return 256 + static_cast<size_t>(sm) * kMaxBlocksPerSm * sizeof(cuppl_is_record);
 }
@@ -272,7 +280,7 @@ int cuppl_is_poly(const float* xs, const float* ys, int n_points, uint64_t pid_b
   prm.deg_out = deg_out;
   cudaError_t e = cudaMemsetAsync(workspace, 0, 256, st);
   if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync");
-  return cuda_status(launch_poly(prm, injected != nullptr, sm, sm * kMaxBlocksPerSm, st),
+  return cuda_status(launch_poly(prm, injected != nullptr, sm, sm * kMaxBlocksPerSm, st, poly_variant()),
                      "is_poly");
 }
 

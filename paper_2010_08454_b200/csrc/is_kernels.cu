@@ -239,83 +239,175 @@ __device__ __forceinline__ void poly_draw(PhiloxKey key, uint64_t pid, int& n, f
   c[3] = n > 3 ? 10.0f * z23.y : 0.0f;
 }
 
-template <int P, bool INJ, int DC, int CAP>
-__global__ void __launch_bounds__(kIsThreads, kPolyMinBlocks)
-is_poly_kernel(const __grid_constant__ PolyParams<CAP> prm) {
-  static_assert(P % 2 == 0, "particles are processed in FFMA2 pairs");
-  ThreadAcc<9, 3> acc;
-  acc.init();
-  const PhiloxKey key{prm.k0, prm.k1};
-  const uint64_t n = prm.pid_end - prm.pid_begin;
-  const uint64_t chunk = static_cast<uint64_t>(blockDim.x) * P;
-  const uint64_t nchunks = (n + chunk - 1) / chunk;
-  const int D = DC > 0 ? DC : prm.n_points;
+// Pair-packed online accumulator of the Fig.1 record: the two halves of every f32x2 belong to
+// the two particles of an FFMA2 pair, so the per-degree moments (sum w c_j for n = 2, 3, 4:
+// 9 values), the degree bins and sum w / sum w^2 cost one FADD2 / FFMA2 per pair. One
+// stabiliser m per thread (D10: fp32 lanes, fp64 from the block level up).
+struct PolyAcc {
+  static constexpr int kStats = 9;  // n=2 -> [0,1]; n=3 -> [2,3,4]; n=4 -> [5..8]
+  static constexpr int kBins = 3;   // n = 2, 3, 4
+  float m;
+  f32x2 s, s2, st[kStats], bn[kBins];
+  float amax_lw;
+  uint64_t amax_pid;
+  uint32_t n_fin, n_tot;
 
-  for (uint64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const uint64_t base = ch * chunk + threadIdx.x;
-    float c[P][4];
-    int deg[P];
+  __device__ __forceinline__ void init() {
+    m = neg_inf_f();
+    s = s2 = pack2(0.f, 0.f);
 #pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const uint64_t idx = base + static_cast<uint64_t>(p) * blockDim.x;
-      if (INJ) {
-        const bool ok = idx < n;
-        const float* src = prm.injected + 5 * (ok ? idx : 0);
-        deg[p] = ok ? static_cast<int>(src[0]) : 2;
+    for (int k = 0; k < kStats; ++k) st[k] = pack2(0.f, 0.f);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) c[p][j] = (ok && j < deg[p]) ? src[1 + j] : 0.f;
-      } else {
-        poly_draw(key, prm.pid_begin + idx, deg[p], c[p]);
-      }
+    for (int k = 0; k < kBins; ++k) bn[k] = pack2(0.f, 0.f);
+    amax_lw = neg_inf_f();
+    amax_pid = ~0ull;
+    n_fin = n_tot = 0;
+  }
+
+  // Particles a (lower pid) and b: log-weights, degrees, packed coefficients, validity.
+  __device__ __forceinline__ void add_pair(float la, float lb, int da, int db, f32x2 C0, f32x2 C1,
+                                           f32x2 C2, f32x2 C3, bool va, bool vb, uint64_t pid_a,
+                                           uint64_t pid_b) {
+    n_tot += static_cast<uint32_t>(va) + static_cast<uint32_t>(vb);
+    const bool fa = va && fabsf(la) <= 3.402823466e38f;  // excludes +-inf and NaN (D9)
+    const bool fb = vb && fabsf(lb) <= 3.402823466e38f;
+    n_fin += static_cast<uint32_t>(fa) + static_cast<uint32_t>(fb);
+    const float ea = fa ? la : neg_inf_f(), eb = fb ? lb : neg_inf_f();
+    const float lmax = fmaxf(ea, eb);
+    if (lmax > amax_lw) {  // strict: earlier (lower) pids win ties; a before b
+      amax_lw = lmax;
+      amax_pid = ea >= eb ? pid_a : pid_b;
     }
-    f32x2 C0[P / 2], C1[P / 2], C2[P / 2], C3[P / 2], S[P / 2];
+    if (lmax > m) {
+      const float f0 = fast_ex2((m - lmax) * kLog2e);
+      const f32x2 F = pack2(f0, f0);
+      s = mul2(s, F);
+      s2 = mul2(s2, mul2(F, F));
 #pragma unroll
-    for (int q = 0; q < P / 2; ++q) {
-      C0[q] = pack2(c[2 * q][0], c[2 * q + 1][0]);
-      C1[q] = pack2(c[2 * q][1], c[2 * q + 1][1]);
-      C2[q] = pack2(c[2 * q][2], c[2 * q + 1][2]);
-      C3[q] = pack2(c[2 * q][3], c[2 * q + 1][3]);
-      S[q] = pack2(0.f, 0.f);
+      for (int k = 0; k < kStats; ++k) st[k] = mul2(st[k], F);
+#pragma unroll
+      for (int k = 0; k < kBins; ++k) bn[k] = mul2(bn[k], F);
+      m = lmax;
     }
+    const float wa = fa ? fast_ex2((la - m) * kLog2e) : 0.f;
+    const float wb = fb ? fast_ex2((lb - m) * kLog2e) : 0.f;
+    const f32x2 W = pack2(wa, wb);
+    s = add2(s, W);
+    s2 = fma2(W, W, s2);
+    const f32x2 W2 = pack2(da == 2 ? wa : 0.f, db == 2 ? wb : 0.f);
+    const f32x2 W3 = pack2(da == 3 ? wa : 0.f, db == 3 ? wb : 0.f);
+    const f32x2 W4 = pack2(da == 4 ? wa : 0.f, db == 4 ? wb : 0.f);
+    bn[0] = add2(bn[0], W2);
+    bn[1] = add2(bn[1], W3);
+    bn[2] = add2(bn[2], W4);
+    st[0] = fma2(W2, C0, st[0]);
+    st[1] = fma2(W2, C1, st[1]);
+    st[2] = fma2(W3, C0, st[2]);
+    st[3] = fma2(W3, C1, st[3]);
+    st[4] = fma2(W3, C2, st[4]);
+    st[5] = fma2(W4, C0, st[5]);
+    st[6] = fma2(W4, C1, st[6]);
+    st[7] = fma2(W4, C2, st[7]);
+    st[8] = fma2(W4, C3, st[8]);
+  }
+
+  __device__ __forceinline__ static double hsum(f32x2 v) {
+    const float2 t = unpack2(v);
+    return static_cast<double>(t.x) + static_cast<double>(t.y);
+  }
+  // record view (block_reduce_view)
+  __device__ __forceinline__ unsigned long long n_finite() const { return n_fin; }
+  __device__ __forceinline__ unsigned long long n_total() const { return n_tot; }
+  __device__ __forceinline__ double max_lw() const { return m; }
+  __device__ __forceinline__ double sum_w() const { return hsum(s); }
+  __device__ __forceinline__ double sum_w2() const { return hsum(s2); }
+  __device__ __forceinline__ double stat(int k) const { return hsum(st[k]); }
+  __device__ __forceinline__ double bin(int k) const { return hsum(bn[k]); }
+  __device__ __forceinline__ double argmax_lw() const { return amax_lw; }
+  __device__ __forceinline__ unsigned long long argmax_pid() const { return amax_pid; }
+};
+
+// One chunk of P particles per thread: particle p of the chunk is global id base + p * 256.
+// FULL: every particle of the chunk is in range (no per-particle bounds checks).
+template <int P, bool INJ, int DC, bool TR, bool FULL, int CAP>
+__device__ __forceinline__ void poly_chunk(const PolyParams<CAP>& prm, PolyAcc& acc, PhiloxKey key,
+                                           uint64_t n, uint64_t base) {
+  const int D = DC > 0 ? DC : prm.n_points;
+  float c[P][4];
+  int deg[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    const uint64_t idx = base + static_cast<uint64_t>(p) * kIsThreads;
+    if (INJ) {
+      const bool ok = FULL || idx < n;
+      const float* src = prm.injected + 5 * (ok ? idx : 0);
+      deg[p] = ok ? static_cast<int>(src[0]) : 2;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[p][j] = (ok && j < deg[p]) ? src[1 + j] : 0.f;
+    } else {
+      poly_draw(key, prm.pid_begin + idx, deg[p], c[p]);
+    }
+  }
+  f32x2 C0[P / 2], C1[P / 2], C2[P / 2], C3[P / 2], S[P / 2];
+#pragma unroll
+  for (int q = 0; q < P / 2; ++q) {
+    C0[q] = pack2(c[2 * q][0], c[2 * q + 1][0]);
+    C1[q] = pack2(c[2 * q][1], c[2 * q + 1][1]);
+    C2[q] = pack2(c[2 * q][2], c[2 * q + 1][2]);
+    C3[q] = pack2(c[2 * q][3], c[2 * q + 1][3]);
+    S[q] = pack2(0.f, 0.f);
+  }
 #pragma unroll(DC > 0 ? DC : 4)
-    for (int i = 0; i < D; ++i) {
-      const float2 xy = prm.xy[i];  // warp-uniform constant-bank load (LDCU)
-      const f32x2 X = pack2(xy.x, xy.x), NY = pack2(-xy.y, -xy.y);
-#pragma unroll
-      for (int q = 0; q < P / 2; ++q) {
-        f32x2 t = fma2(C3[q], X, C2[q]);
-        t = fma2(t, X, C1[q]);
-        t = fma2(t, X, C0[q]);
-        const f32x2 r = add2(t, NY);
-        S[q] = fma2(r, r, S[q]);
-      }
-    }
+  for (int i = 0; i < D; ++i) {
+    const float2 xy = prm.xy[i];  // warp-uniform constant-bank load (LDCU)
+    const f32x2 X = pack2(xy.x, xy.x), NY = pack2(-xy.y, -xy.y);
 #pragma unroll
     for (int q = 0; q < P / 2; ++q) {
-      const float2 s = unpack2(S[q]);
+      f32x2 t = fma2(C3[q], X, C2[q]);
+      t = fma2(t, X, C1[q]);
+      t = fma2(t, X, C0[q]);
+      const f32x2 r = add2(t, NY);
+      S[q] = fma2(r, r, S[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < P / 2; ++q) {
+    const float2 sq = unpack2(S[q]);
+    const uint64_t ia = base + static_cast<uint64_t>(2 * q) * kIsThreads;
+    const uint64_t ib = ia + kIsThreads;
+    const bool va = FULL || ia < n, vb = FULL || ib < n;
+    acc.add_pair(-sq.x, -sq.y, deg[2 * q], deg[2 * q + 1], C0[q], C1[q], C2[q], C3[q], va, vb,
+                 prm.pid_begin + ia, prm.pid_begin + ib);
+    if (TR) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int p = 2 * q + h;
-        const uint64_t idx = base + static_cast<uint64_t>(p) * blockDim.x;
-        if (idx < n) {
-          const float lw = -(h ? s.y : s.x);
-          const int d = deg[p];
-          // stat layout: n=2 -> [0,1]; n=3 -> [2,3,4]; n=4 -> [5..8]  (sum w c_j per degree)
-          float f[9];
-#pragma unroll
-          for (int k = 0; k < 9; ++k) f[k] = 0.f;
-          if (d == 2) { f[0] = c[p][0]; f[1] = c[p][1]; }
-          else if (d == 3) { f[2] = c[p][0]; f[3] = c[p][1]; f[4] = c[p][2]; }
-          else { f[5] = c[p][0]; f[6] = c[p][1]; f[7] = c[p][2]; f[8] = c[p][3]; }
-          acc.add(lw, prm.pid_begin + idx, f, d - 2);
-          if (prm.lw_out) prm.lw_out[idx] = lw;
-          if (prm.deg_out) prm.deg_out[idx] = d;
+        const uint64_t idx = h ? ib : ia;
+        if (FULL || idx < n) {
+          if (prm.lw_out) prm.lw_out[idx] = -(h ? sq.y : sq.x);
+          if (prm.deg_out) prm.deg_out[idx] = deg[p];
           if (prm.coef_out)
             reinterpret_cast<float4*>(prm.coef_out)[idx] = make_float4(c[p][0], c[p][1], c[p][2], c[p][3]);
         }
       }
     }
   }
+}
+
+template <int P, bool INJ, int DC, bool TR, int CAP, int MB = kPolyMinBlocks>
+__global__ void __launch_bounds__(kIsThreads, MB)
+is_poly_kernel(const __grid_constant__ PolyParams<CAP> prm) {
+  static_assert(P % 2 == 0, "particles are processed in FFMA2 pairs");
+  PolyAcc acc;
+  acc.init();
+  const PhiloxKey key{prm.k0, prm.k1};
+  const uint64_t n = prm.pid_end - prm.pid_begin;
+  constexpr uint64_t chunk = static_cast<uint64_t>(kIsThreads) * P;
+  const uint64_t nfull = n / chunk;
+  for (uint64_t ch = blockIdx.x; ch < nfull; ch += gridDim.x)
+    poly_chunk<P, INJ, DC, TR, true>(prm, acc, key, n, ch * chunk + threadIdx.x);
+  if (nfull * chunk < n && blockIdx.x == nfull % gridDim.x)
+    poly_chunk<P, INJ, DC, TR, false>(prm, acc, key, n, nfull * chunk + threadIdx.x);
   is_epilogue(acc, prm.block_recs, prm.counter, prm.rec_out);
 }
 
@@ -360,23 +452,29 @@ cudaError_t launch_linreg(const LinregParams<CAP>& prm, bool injected, int sm_co
 
 template <int CAP>
 cudaError_t launch_poly(const PolyParams<CAP>& prm, bool injected, int sm_count, int max_blocks,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, int variant) {
   constexpr int P = kPolyP;
   const uint64_t n = prm.pid_end - prm.pid_begin;
-  const uint64_t nchunks = (n + kIsThreads * P - 1) / (kIsThreads * P);
   int grid = 0;
-  if (prm.n_points == 20) {
-    if (injected)
-      return launch_persistent(is_poly_kernel<P, true, 20, CAP>, prm, sm_count, nchunks, max_blocks, stream, &grid);
-    return launch_persistent(is_poly_kernel<P, false, 20, CAP>, prm, sm_count, nchunks, max_blocks, stream, &grid);
+  auto chunks = [n](int p) { return (n + kIsThreads * p - 1) / (kIsThreads * p); };
+  const bool tr = prm.lw_out || prm.deg_out || prm.coef_out;
+  if (prm.n_points == 20 && !injected && !tr) {  // the benchmark configuration (C1/C5)
+    switch (variant) {  // (particles per thread, min blocks per SM): tuning only
+      case 1: return launch_persistent(is_poly_kernel<4, false, 20, false, CAP, 3>, prm, sm_count, chunks(4), max_blocks, stream, &grid);
+      case 2: return launch_persistent(is_poly_kernel<2, false, 20, false, CAP, 4>, prm, sm_count, chunks(2), max_blocks, stream, &grid);
+      case 3: return launch_persistent(is_poly_kernel<2, false, 20, false, CAP, 3>, prm, sm_count, chunks(2), max_blocks, stream, &grid);
+      default: return launch_persistent(is_poly_kernel<P, false, 20, false, CAP>, prm, sm_count, chunks(P), max_blocks, stream, &grid);
+    }
   }
   if (injected)
-    return launch_persistent(is_poly_kernel<P, true, 0, CAP>, prm, sm_count, nchunks, max_blocks, stream, &grid);
-  return launch_persistent(is_poly_kernel<P, false, 0, CAP>, prm, sm_count, nchunks, max_blocks, stream, &grid);
+    return launch_persistent(is_poly_kernel<P, true, 0, true, CAP>, prm, sm_count, chunks(P), max_blocks, stream, &grid);
+  if (!tr)
+    return launch_persistent(is_poly_kernel<P, false, 0, false, CAP>, prm, sm_count, chunks(P), max_blocks, stream, &grid);
+  return launch_persistent(is_poly_kernel<P, false, 0, true, CAP>, prm, sm_count, chunks(P), max_blocks, stream, &grid);
 }
 
 template cudaError_t launch_linreg<kLinregCapSmall>(const LinregParams<kLinregCapSmall>&, bool, int, int, cudaStream_t, int);
 template cudaError_t launch_linreg<kLinregCapLarge>(const LinregParams<kLinregCapLarge>&, bool, int, int, cudaStream_t, int);
-template cudaError_t launch_poly<kPolyCap>(const PolyParams<kPolyCap>&, bool, int, int, cudaStream_t);
+template cudaError_t launch_poly<kPolyCap>(const PolyParams<kPolyCap>&, bool, int, int, cudaStream_t, int);
 
 }  // namespace cuppl

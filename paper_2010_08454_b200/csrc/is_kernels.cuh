@@ -12,7 +12,7 @@ namespace cuppl {
 constexpr int kIsThreads = 256;
 constexpr int kLinregP = 8;  // particles per thread per chunk (4 FFMA2 pairs)
 constexpr int kPolyP = 4;    // particles per thread per chunk (2 FFMA2 pairs)
-constexpr int kPolyMinBlocks = 4;  // 64 registers: 32 warps per SM to hide the Horner chains
+constexpr int kPolyMinBlocks = 2;  // pair-packed accumulators need ~118 registers at P = 4
 constexpr int kLinregCapSmall = 1024;
 constexpr int kLinregCapLarge = 3968;
 constexpr int kPolyCap = 64;
@@ -54,6 +54,8 @@ cudaError_t launch_linreg(const LinregParams<CAP>& prm, bool injected, int sm_co
 constexpr int kLinregVariant = 0;
 template <int CAP>
 cudaError_t launch_poly(const PolyParams<CAP>& prm, bool injected, int sm_count, int max_blocks,
-                        cudaStream_t stream);
+                        cudaStream_t stream, int variant);
+// Poly benchmark-kernel tuning (CUPPL_POLY_VARIANT): 0 = P4/2 blocks, 1 = P4/3, 2 = P2/4, 3 = P2/3.
+constexpr int kPolyVariant = 1;
 
 }  // namespace cuppl

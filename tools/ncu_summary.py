@@ -30,7 +30,7 @@ KEYS = {
 
 def unit_scale(unit: str) -> float:
     return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "msecond": 1, "usecond": 1e-3,
-            "nsecond": 1e-6}.get(unit, 1.0)
+            "nsecond": 1e-6, "us": 1e-3, "ns": 1e-6, "ms": 1, "s": 1e3, "second": 1e3}.get(unit, 1.0)
 
 
 def summarise(rep: Path) -> list:
