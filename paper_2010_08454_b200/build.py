@@ -50,11 +50,25 @@ def _deps() -> list[Path]:
     return sources() + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "cuppl_gpu.h"]
 
 
+STAMP = OUT_DIR / "libcuppl_gpu.sha256"
+
+
+def source_hash() -> str:
+    """Content hash of every input of the library (and the flags): file copies that do not
+    preserve modification times (e.g. a snapshot shipped to a GPU box) cannot fool it."""
+    import hashlib
+
+    h = hashlib.sha256(" ".join(ARCH + NVCC_FLAGS).encode())
+    for p in _deps():
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()
+
+
 def up_to_date() -> bool:
-    if not LIB.exists():
+    if not LIB.exists() or not STAMP.exists():
         return False
-    t = LIB.stat().st_mtime
-    return all(p.stat().st_mtime <= t for p in _deps())
+    return STAMP.read_text().strip() == source_hash()
 
 
 def _compile(src: Path, verbose: bool) -> Path:
@@ -83,6 +97,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    STAMP.write_text(source_hash())
     return LIB
 
 

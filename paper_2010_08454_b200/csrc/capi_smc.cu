@@ -10,7 +10,6 @@ using namespace cuppl;
 
 namespace {
 struct SmcWs {
-  unsigned long long* segoff;
   unsigned long long* tile_prefix;
   unsigned long long* flags;
   unsigned int* counters;
@@ -21,7 +20,6 @@ struct SmcWs {
 size_t align256(size_t v) { return (v + 255) & ~static_cast<size_t>(255); }
 
 size_t ws_layout(uint64_t n, SmcWs* w, void* base) {
-  const uint64_t n_segs = (n + kSegment - 1) / kSegment;
   const uint64_t n_tiles = (n + kTile - 1) / kTile;
   char* p = static_cast<char*>(base);
   size_t off = 0;
@@ -30,8 +28,6 @@ size_t ws_layout(uint64_t n, SmcWs* w, void* base) {
   const size_t counters_off = off;
   off = align256(off + 16);
   const size_t zero_end = off;
-  const size_t segoff_off = off;
-  off = align256(off + n_segs * 8);
   const size_t tiles_off = off;
   off = align256(off + n_tiles * 16);
   const size_t prefix_off = off;
@@ -39,7 +35,6 @@ size_t ws_layout(uint64_t n, SmcWs* w, void* base) {
   if (w) {
     w->flags = reinterpret_cast<unsigned long long*>(p + flags_off);
     w->counters = reinterpret_cast<unsigned int*>(p + counters_off);
-    w->segoff = reinterpret_cast<unsigned long long*>(p + segoff_off);
     w->tile_s = reinterpret_cast<double*>(p + tiles_off);
     w->tile_prefix = reinterpret_cast<unsigned long long*>(p + prefix_off);
     w->zero_bytes = zero_end;
@@ -120,7 +115,6 @@ int cuppl_smc_scan(const cuppl_smc_model* m, uint64_t n_local, float y, const ui
   a.y = y;
   a.S = sm.S;
   a.m_key = m_key;
-  a.segoff = w.segoff;
   a.tile_prefix = w.tile_prefix;
   a.flags = w.flags;
   a.counters = w.counters;
@@ -158,7 +152,6 @@ int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_to
   a.y_next = y_next;
   a.x = x;
   a.m_key = m_key;
-  a.segoff = w.segoff;
   a.tile_prefix = w.tile_prefix;
   a.tile_s = w.tile_s;
   a.stats_out = reinterpret_cast<double*>(stats_out);

@@ -191,87 +191,74 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(const __grid_cons
   }
   __syncthreads();
   const unsigned long long tile = s_tile;
-  // thread tid owns segment tid of the tile: particles [tile * 8192 + 32 tid, +32)
+  // thread tid owns particles [tile * 4096 + 16 tid, +16): one 16-byte load of states
   const unsigned long long p0 = tile * kTile + static_cast<unsigned long long>(tid) * kSegment;
-  uint4 v0 = make_uint4(0, 0, 0, 0), v1 = make_uint4(0, 0, 0, 0);
+  uint4 v = make_uint4(0, 0, 0, 0);
   int valid = 0;
   if (p0 + kSegment <= n) {
-    v0 = __ldcs(reinterpret_cast<const uint4*>(a.x + p0));
-    v1 = __ldcs(reinterpret_cast<const uint4*>(a.x + p0) + 1);
+    v = __ldcs(reinterpret_cast<const uint4*>(a.x + p0));
     valid = kSegment;
   } else if (p0 < n) {
     valid = static_cast<int>(n - p0);
     uint8_t tmp[kSegment];
     for (int k = 0; k < kSegment; ++k) tmp[k] = k < valid ? a.x[p0 + k] : 0;
-    v0 = *reinterpret_cast<const uint4*>(tmp);
-    v1 = *reinterpret_cast<const uint4*>(tmp + 16);
+    v = *reinterpret_cast<const uint4*>(tmp);
   }
-  const uint32_t words[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+  const uint32_t words[4] = {v.x, v.y, v.z, v.w};
   unsigned long long ws = 0;
   float s1 = 0.f, s2 = 0.f;
-  if (!HIST && valid == kSegment) {  // fast path: a full segment, no per-particle checks
-    uint32_t wsum_lo = 0, wsum_hi = 0;  // two u32 halves of 16 weights each never overflow 2^36
+  if (!HIST && valid == kSegment) {  // fast path: a full thread slice, no per-particle checks
+    uint32_t whi = 0, wlo = 0;  // 16 * (2^31 >> 4) = 2^31: the high parts fit one u32
 #pragma unroll
     for (int k = 0; k < kSegment; ++k) {
       const uint2 te = wes[(words[k >> 2] >> (8 * (k & 3))) & 0xFFu];
       const float e = __uint_as_float(te.y);
-      if (k < 16) wsum_lo += te.x >> 4; else wsum_hi += te.x >> 4;
-      ws += te.x & 15u;
+      whi += te.x >> 4;
+      wlo += te.x & 15u;
       s1 += e;
       s2 = fmaf(e, e, s2);
     }
-    ws += (static_cast<unsigned long long>(wsum_lo) + wsum_hi) << 4;
+    ws = (static_cast<unsigned long long>(whi) << 4) + wlo;
   } else {
 #pragma unroll
-  for (int k = 0; k < kSegment; ++k) {
-    const uint32_t st = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-    const bool ok = k < valid;
-    const uint2 te = wes[st];
-    const uint32_t w = ok ? te.x : 0u;
-    const float e = ok ? __uint_as_float(te.y) : 0.f;
-    ws += w;
-    s1 += e;
-    s2 = fmaf(e, e, s2);
-    if (HIST) {
-      // warp-aggregated state counts: one shared atomic per distinct state in the warp
-      const unsigned int key = ok ? st : 0xFFFFFFFFu;
-      const unsigned int grp = __match_any_sync(0xffffffffu, key);
-      if (ok && lane == __ffs(grp) - 1) atomicAdd(&cnt[st], static_cast<unsigned int>(__popc(grp)));
+    for (int k = 0; k < kSegment; ++k) {
+      const uint32_t st = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+      const bool ok = k < valid;
+      const uint2 te = wes[st];
+      const uint32_t w = ok ? te.x : 0u;
+      const float e = ok ? __uint_as_float(te.y) : 0.f;
+      ws += w;
+      s1 += e;
+      s2 = fmaf(e, e, s2);
+      if (HIST) {
+        // warp-aggregated state counts: one shared atomic per distinct state in the warp
+        const unsigned int key = ok ? st : 0xFFFFFFFFu;
+        const unsigned int grp = __match_any_sync(0xffffffffu, key);
+        if (ok && lane == __ffs(grp) - 1) atomicAdd(&cnt[st], static_cast<unsigned int>(__popc(grp)));
+      }
     }
-  }
   }
   double d1 = s1, d2 = s2;  // per-warp fp64 partials, fixed tree
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     d1 += __shfl_down_sync(0xffffffffu, d1, o);
     d2 += __shfl_down_sync(0xffffffffu, d2, o);
+    ws += __shfl_down_sync(0xffffffffu, ws, o);
   }
   if (lane == 0) {
     wpart[warp][0] = d1;
     wpart[warp][1] = d2;
+    wtot[warp] = ws;
   }
-  // inclusive scan of the tile's 256 segment sums (thread tid <-> segment tid)
-  unsigned long long incl = ws;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long u = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += u;
-  }
-  if (lane == 31) wtot[warp] = incl;
   __syncthreads();
-  unsigned long long wpre = 0, agg = 0;
-#pragma unroll
-  for (int w = 0; w < kSmcThreads / 32; ++w) {
-    if (w < warp) wpre += wtot[w];
-    agg += wtot[w];
-  }
-  const unsigned long long gs = tile * kTileSegs + tid;
-  if (gs * kSegment < n) a.segoff[gs] = incl + wpre;  // tile-local; K6 adds tile_prefix
   if (HIST) {
     for (int s = tid; s < a.S; s += kSmcThreads)
       if (cnt[s]) atomicAdd(&a.hist[s], static_cast<unsigned long long>(cnt[s]) * wS[s]);
   }
   if (warp != 0) return;  // only warp 0 waits on the predecessors
+  unsigned long long agg = 0;
+#pragma unroll
+  for (int w = 0; w < kSmcThreads / 32; ++w) agg += wtot[w];
   if (lane == 0) st_relaxed_u64(a.flags + tile, (tile == 0 ? kFlagIncl : kFlagAgg) | agg);
   const unsigned long long prefix = tile == 0 ? 0ull : warp_lookback(a.flags, tile);
   if (lane == 0) {
@@ -290,11 +277,14 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(const __grid_cons
 
 // ------------------------------------------------------------------ K6: resample --------
 // Comb in integers (D6): with T = Q N + R0 and A = floor(u T / 2^32) = Qa N + Ra,
-// target_j = floor((j 2^32 + u) T / (N 2^32)) = j Q + Qa + floor((j R0 + Ra) / N),
+// target_j = floor((j 2^32 + u) T / (N 2^32)) = floor((j T + A) / N)
+//          = j Q + Qa + floor((j R0 + Ra) / N),
 // where j R0 + Ra < N^2 < 2^62 (N < 2^31); every per-index quantity fits 32 bits.
 struct Comb {
   unsigned int N, Q, R0, Qa, Ra;
-  double invN, step_inv, a_over_t;  // 1/N, N/T, A/T
+  unsigned long long T, A;
+  double invN;              // 1 / N
+  double n_over_t, a_over_t;  // N / T, A / T: fp64 rank estimates (exact fix-up below)
   unsigned int u;
 };
 
@@ -315,125 +305,89 @@ __device__ __forceinline__ unsigned long long div_n(unsigned long long num, cons
   return static_cast<unsigned long long>(q);
 }
 
-// Cursor over consecutive targets: (j, target_j, (j R0 + Ra) mod N).
-struct CombCursor {
-  unsigned int j, mod;
-  unsigned long long tgt;
-  __device__ __forceinline__ void seek(unsigned int jj, const Comb& cb) {
-    j = jj;
-    const unsigned long long q =
-        div_n(static_cast<unsigned long long>(jj) * cb.R0 + cb.Ra, cb, &mod);
-    tgt = static_cast<unsigned long long>(jj) * cb.Q + cb.Qa + q;
-  }
-  __device__ __forceinline__ void next(const Comb& cb) {
-    ++j;
-    tgt += cb.Q;
-    mod += cb.R0;
-    if (mod >= cb.N) {
-      mod -= cb.N;
-      ++tgt;
-    }
-  }
-  // smallest j' >= j with target_j' >= c (N if none); long gaps re-seek from an estimate
-  __device__ __forceinline__ void advance_to(unsigned long long c, const Comb& cb) {
-    if (j >= cb.N || tgt >= c) return;
-    if (c - tgt > 4ull * cb.Q + 4ull) {
-      // target_j ~ (j + u/2^32) T / N  =>  j ~ c N / T - u / 2^32 (error << 1)
-      const double e = __dmul_rn(__ull2double_rn(c), cb.step_inv) - 2.0;
-      const unsigned int jj = e <= static_cast<double>(j) ? j
-                             : e >= static_cast<double>(cb.N) ? cb.N - 1
-                                                              : static_cast<unsigned int>(e);
-      if (jj > j) {
-        seek(jj, cb);
-        while (j > 0 && tgt >= c) seek(j - 1, cb);  // never taken unless the estimate was high
-      }
-    }
-    while (j < cb.N && tgt < c) next(cb);
-  }
-};
-
 __device__ __forceinline__ unsigned long long comb_target(unsigned int j, const Comb& cb) {
-  CombCursor c;
-  c.seek(j, cb);
-  return c.tgt;
+  unsigned int mod;
+  const unsigned long long q = div_n(static_cast<unsigned long long>(j) * cb.R0 + cb.Ra, cb, &mod);
+  return static_cast<unsigned long long>(j) * cb.Q + cb.Qa + q;
 }
 
-// smallest j in [0, N] with target_j >= c (N if none). target_j >= c <=> j T + A >= c N, so
-// F(c) = ceil((c N - A) / T): fp64 estimate, then exact fix-up on the integer targets.
-__device__ __forceinline__ unsigned int first_j_at_least(unsigned long long c, const Comb& cb) {
-  if (c == 0) return 0u;
-  const double est = __dmul_rn(__ull2double_rn(c), cb.step_inv) - cb.a_over_t;
-  unsigned int j = est <= 0.0 ? 0u : est >= static_cast<double>(cb.N) ? cb.N : static_cast<unsigned int>(ceil(est));
-  while (j > 0 && comb_target(j - 1, cb) >= c) --j;
-  while (j < cb.N && comb_target(j, cb) < c) ++j;
+// target_j >= c  <=>  j T + A >= c N   (exact, 128-bit)
+__device__ __forceinline__ bool comb_ge(unsigned int j, unsigned long long c, const Comb& cb) {
+  const unsigned long long lo = static_cast<unsigned long long>(j) * cb.T;
+  unsigned long long hi = __umul64hi(static_cast<unsigned long long>(j), cb.T);
+  const unsigned long long lo2 = lo + cb.A;
+  hi += lo2 < lo ? 1ull : 0ull;
+  const unsigned long long rlo = c * cb.N;
+  const unsigned long long rhi = __umul64hi(c, static_cast<unsigned long long>(cb.N));
+  return hi > rhi || (hi == rhi && lo2 >= rlo);
+}
+
+// Rank of a weight coordinate in the comb: F(c) = min{j in [0, N] : target_j >= c}
+// = clamp(ceil((c N - A) / T), 0, N). `est` is an fp64 estimate of (c N - A) / T with error
+// < 2^-18; ceil(est) is exact unless est lies within 2^-14 of an integer, when the integer
+// comparison decides (probability ~2^-13 per call: no divergence in practice).
+__device__ __noinline__ unsigned int comb_rank_exact(double est, unsigned long long c, const Comb& cb) {
+  unsigned int j = est <= 0.0 ? 0u : est >= static_cast<double>(cb.N) ? cb.N
+                                                                       : static_cast<unsigned int>(ceil(est));
+  while (j > 0 && comb_ge(j - 1, c, cb)) --j;
+  while (j < cb.N && !comb_ge(j, c, cb)) ++j;
   return j;
 }
-
-// Rank-local inclusive weight prefix at the end of segment s (K5 writes tile-local values).
-__device__ __forceinline__ unsigned long long seg_incl(const SmcResampleArgs& a, unsigned long long s) {
-  return __ldg(a.tile_prefix + s / kTileSegs) + __ldg(a.segoff + s);
+__device__ __forceinline__ unsigned int comb_rank(double est, unsigned long long c, const Comb& cb) {
+  // 1.5 * 2^52: doubles in [2^52, 2^53) are the integers, so for |est| < 2^51 rounding the sum
+  // up gives 1.5 * 2^52 + ceil(est) exactly and its low word is ceil(est) (est > -1: >= 0)
+  constexpr double kMagic = 6755399441055744.0;
+  const double t = __dadd_ru(est, kMagic);
+  const double frac = __dsub_rn(__dsub_rn(t, kMagic), est);  // ceil(est) - est, in [0, 1)
+  unsigned int j = static_cast<unsigned int>(__double2loint(t));
+  if (!(frac > 0x1p-14 && frac < 1.0 - 0x1p-14)) j = comb_rank_exact(est, c, cb);
+  return j;
+}
+__device__ __forceinline__ unsigned int comb_rank(unsigned long long c, const Comb& cb) {
+  if (c == 0) return 0u;
+  return comb_rank(__fma_rn(__ull2double_rn(c), cb.n_over_t, -cb.a_over_t), c, cb);
 }
 
-// Warp-cooperative rank-local upper bound: smallest local i with C_i > t (C = inclusive scan
-// of the rank's weights, represented by the segment prefixes + the lw of one segment). Returns
-// n_local if none. The segment is found with a 33-ary search (5 rounds for 3e6 segments), then
-// resolved inside the segment with a warp scan of its 32 weights.
-__device__ unsigned long long warp_upper_bound(unsigned long long t, const SmcResampleArgs& a,
-                                               const uint32_t* wS) {
-  const int lane = threadIdx.x & 31;
-  const unsigned long long n_segs = (a.n_local + kSegment - 1) / kSegment;
-  unsigned long long lo = 0, hi = n_segs;  // invariant: answer in [lo, hi]
-  while (hi - lo > 32) {
-    const unsigned long long span = hi - lo;
-    const unsigned long long p = lo + span * (lane + 1) / 33;  // strictly increasing, < hi
-    const unsigned int bal = __ballot_sync(0xffffffffu, seg_incl(a, p) > t);
-    if (!bal) {
-      lo = lo + span * 32 / 33 + 1;
-    } else {
-      const int fl = __ffs(bal) - 1;
-      const unsigned long long new_hi = lo + span * (fl + 1) / 33;
-      if (fl > 0) lo = lo + span * fl / 33 + 1;
-      hi = new_hi;
-    }
-  }
-  {
-    const unsigned long long p = lo + lane;
-    const unsigned int bal = __ballot_sync(0xffffffffu, p < hi && seg_incl(a, p) > t);
-    hi = bal ? lo + (__ffs(bal) - 1) : hi;
-  }
-  const unsigned long long s = hi;
-  if (s >= n_segs) return a.n_local;
-  const unsigned long long base = s > 0 ? seg_incl(a, s - 1) : 0ull;
-  const unsigned long long i = s * kSegment + lane;
-  const uint32_t w = i < a.n_local ? wS[a.x[i]] : 0u;
-  unsigned long long incl = w;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long u2 = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += u2;
-  }
-  const unsigned int bal = __ballot_sync(0xffffffffu, i < a.n_local && base + incl > t);
-  if (!bal) return a.n_local;
-  return s * kSegment + (__ffs(bal) - 1);
+// Alias draw from a shared-memory copy of the transition tables (entry layout as alias_draw).
+__device__ __forceinline__ int alias_draw_s(const unsigned long long* row, unsigned int K, uint32_t w) {
+  const unsigned long long p = static_cast<unsigned long long>(w) * K;
+  const unsigned int col = static_cast<unsigned int>(p >> 32);
+  const unsigned long long e = row[col];
+  return static_cast<uint32_t>(p) < (e & 0x1FFFFFFFFull) ? static_cast<int>(col) : static_cast<int>(e >> 40);
 }
 
-template <bool MULTI, bool DEBUG>
-__global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __grid_constant__ SmcModel m,
+// K6: CTA b owns an even share [jb_lo, jb_hi) of this rank's outputs. It stages its sources
+// tile by tile (the 4096-particle K5 tiles: states in shared memory, batch-relative integer
+// weight prefix in registers) and RANKS EVERY SOURCE INTO THE COMB: the comb targets are an
+// arithmetic progression, so the first child of source k is F(C_{k-1}) and its children are
+// [F(C_{k-1}), F(C_k)) -- O(1) arithmetic per source instead of a search per output. Each
+// source with children marks its first child's position in a 4096-output window; an output's
+// ancestor is the last mark at or before it (a block max-scan, since marks increase with the
+// position). Thread t then draws the new states of outputs [wb + 16 t, +16) (4 Philox blocks,
+// alias tables in shared memory) and stores them as one 16-byte write. No per-output search,
+// no data-dependent loop: the work per output and per source is uniform whatever the
+// offspring counts.
+template <bool MULTI, bool DEBUG, bool SMEM_ALIAS>
+__global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __grid_constant__ SmcModel m,
                                                                       SmcResampleArgs a) {
-  __shared__ unsigned long long cb_incl[kBatch];  // batch-relative inclusive weight prefix per source
-  __shared__ uint8_t xs[kBatch];                  // staged source states
-  __shared__ __align__(16) uint8_t obuf[kOutBuf + 16];  // new states, indexed from o0 & ~15
+  extern __shared__ __align__(16) unsigned long long alias_s[];  // [S][S] (SMEM_ALIAS)
+  __shared__ __align__(16) uint8_t xs[kBatch];         // staged source states
+  __shared__ __align__(16) uint16_t marks[kWindow];    // batch index + 1 of a first child
   __shared__ unsigned long long wsum[kSmcThreads / 32];
+  __shared__ unsigned int wmax[2 * (kSmcThreads / 32)];  // warp totals of both window halves
   __shared__ unsigned long long s_u64[4];
+  __shared__ unsigned int s_carry, s_jn;
   __shared__ unsigned long long s_rank_begin[MULTI ? kMaxRanks + 1 : 1];
   __shared__ uint32_t wS[kMaxStates];   // quantised weights of population t per state
+  __shared__ double wdS[kMaxStates];    // the same as doubles (exact)
   __shared__ float lwS1[kMaxStates];    // log-weights of population t + 1 per state
+  __shared__ uint8_t pres[kMaxStates];  // states present among this CTA's outputs
   __shared__ BlockScratch sc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (MULTI)
     for (int q = tid; q <= a.world; q += kSmcThreads) s_rank_begin[q] = a.rank_begin[q];
-  constexpr bool debug_anc = DEBUG;
   const unsigned long long n_tiles = a.n_tiles;
+  const unsigned int S = static_cast<unsigned int>(m.S);
 
   // CTA 0: fixed-order fp64 fold of K5's per-tile sums -> rank (sum e, sum e^2); reset K5's
   // tile counter. Every CTA clears a slice of the look-back words for the next scan.
@@ -469,24 +423,33 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
     build_tables(m, a.y_cur, key2f(*a.m_key), nullptr, eS, wS);
     build_tables(m, a.y_next, neg_inf_f(), lwS1, nullptr, nullptr);
   }
+  for (int s = tid; s < kMaxStates; s += kSmcThreads) pres[s] = 0;
+  for (int i = tid; i < kWindow / 8; i += kSmcThreads) reinterpret_cast<uint4*>(marks)[i] = make_uint4(0, 0, 0, 0);
+  if (SMEM_ALIAS) {
+    const unsigned int nA = S * S;
+    for (unsigned int i = tid; i < nA; i += kSmcThreads) alias_s[i] = __ldg(m.alias_trans + i);
+  }
   __syncthreads();
+  for (int s = tid; s < m.S; s += kSmcThreads) wdS[s] = static_cast<double>(wS[s]);
   const PhiloxKey key = make_key(a.key);
   Comb cb;
   cb.u = draw_block(key, a.t, 0u, CUPPL_TAG_SMC_COMB).x;
   cb.N = static_cast<unsigned int>(a.n_total);
+  cb.T = T;
   cb.Q = static_cast<unsigned int>(T / cb.N);
   cb.R0 = static_cast<unsigned int>(T % cb.N);
-  const unsigned long long A = __umul64hi(static_cast<unsigned long long>(cb.u) << 32, T);  // floor(u T / 2^32)
-  cb.Qa = static_cast<unsigned int>(A / cb.N);
-  cb.Ra = static_cast<unsigned int>(A % cb.N);
+  cb.A = __umul64hi(static_cast<unsigned long long>(cb.u) << 32, T);  // floor(u T / 2^32)
+  cb.Qa = static_cast<unsigned int>(cb.A / cb.N);
+  cb.Ra = static_cast<unsigned int>(cb.A % cb.N);
   cb.invN = 1.0 / static_cast<double>(cb.N);
-  cb.step_inv = static_cast<double>(cb.N) / static_cast<double>(T);
-  cb.a_over_t = static_cast<double>(A) / static_cast<double>(T);
+  cb.n_over_t = static_cast<double>(cb.N) / static_cast<double>(T);
+  cb.a_over_t = static_cast<double>(cb.A) / static_cast<double>(T);
 
   // this rank's outputs: J_r = {j : O <= target_j < O + Tr}; this CTA's even share of it
   if (tid == 0) {
-    s_u64[0] = a.rank == 0 ? 0ull : first_j_at_least(O, cb);
-    s_u64[1] = a.rank == a.world - 1 ? cb.N : first_j_at_least(O + Tr, cb);
+    s_carry = 0u;
+    s_u64[0] = a.rank == 0 ? 0ull : comb_rank(O, cb);
+    s_u64[1] = a.rank == a.world - 1 ? cb.N : comb_rank(O + Tr, cb);
   }
   __syncthreads();
   const unsigned long long jr_lo = s_u64[0], jr_hi = s_u64[1];
@@ -495,44 +458,56 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
   const unsigned long long jb_hi = jr_lo + span * (blockIdx.x + 1) / gridDim.x;
   if (jb_lo >= jb_hi) return;
 
-  // ancestor of the first output -> first batch starts at its segment boundary
+  // the tile holding the ancestor of the first output: the last tile whose exclusive prefix
+  // is <= its (rank-local) target (warp-cooperative 33-ary search over the tile prefixes)
   if (warp == 0) {
     const unsigned long long tl = comb_target(static_cast<unsigned int>(jb_lo), cb) - O;
-    const unsigned long long i0 = warp_upper_bound(tl, a, wS);
-    if (lane == 0) s_u64[2] = i0;
-  }
-  __syncthreads();
-  unsigned long long batch_base = (s_u64[2] / kSegment) * kSegment;
-  unsigned long long c_base = batch_base > 0 ? seg_incl(a, batch_base / kSegment - 1) : 0ull;
-  unsigned long long j_cur = jb_lo;
-  float bmax = neg_inf_f();
-  const unsigned int S = static_cast<unsigned int>(m.S);
-
-  while (j_cur < jb_hi && batch_base < a.n_local) {
-    // ---- stage 2048 sources: thread tid owns [batch_base + 8 tid, +8)
-    const unsigned long long i0 = batch_base + kBatchPerThread * tid;
-    uint32_t w[kBatchPerThread];
-    unsigned long long tw = 0;
-    if (i0 + kBatchPerThread <= a.n_local) {
-      const uint4 xx = __ldcs(reinterpret_cast<const uint4*>(a.x + i0));
-      *reinterpret_cast<uint4*>(xs + kBatchPerThread * tid) = xx;
-      const uint32_t xw[4] = {xx.x, xx.y, xx.z, xx.w};
-#pragma unroll
-      for (int k = 0; k < kBatchPerThread; ++k) {
-        w[k] = wS[(xw[k >> 2] >> (8 * (k & 3))) & 0xFFu];
-        tw += w[k];
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < kBatchPerThread; ++k) {
-        const bool ok = i0 + k < a.n_local;
-        const uint8_t st = ok ? a.x[i0 + k] : 0;
-        w[k] = ok ? wS[st] : 0u;
-        xs[kBatchPerThread * tid + k] = st;
-        tw += w[k];
+    unsigned long long lo = 0, hi = n_tiles;  // answer in [lo, hi): prefix[lo] <= tl
+    while (hi - lo > 32) {
+      const unsigned long long sp = hi - lo;
+      const unsigned long long p = lo + sp * (lane + 1) / 33;  // increasing, in (lo, hi)
+      const unsigned int bal = __ballot_sync(0xffffffffu, __ldg(a.tile_prefix + p) > tl);
+      if (!bal) {
+        lo = lo + sp * 32 / 33;
+      } else {
+        const int fl = __ffs(bal) - 1;  // first probe above tl
+        hi = lo + sp * (fl + 1) / 33;
+        if (fl > 0) lo = lo + sp * fl / 33;
       }
     }
-    // block exclusive scan of the thread sums -> batch-relative inclusive prefix per source
+    const unsigned long long p = lo + lane;
+    const unsigned int bal = __ballot_sync(0xffffffffu, p < hi && __ldg(a.tile_prefix + p) <= tl);
+    if (lane == 0) s_u64[2] = lo + (31 - __clz(bal));  // prefix[lo] <= tl: bal has bit 0
+  }
+  __syncthreads();
+  unsigned long long batch_base = s_u64[2] * kBatch;
+  unsigned long long c_base = __ldg(a.tile_prefix + s_u64[2]);
+  unsigned long long j_cur = jb_lo;
+  unsigned int carry = 0;
+  bool first = true;
+  const unsigned long long my_begin = MULTI ? s_rank_begin[a.rank] : 0ull;
+  int last_st = -1;
+
+  while (j_cur < jb_hi && batch_base < a.n_local) {
+    // ---- stage the tile: thread tid owns sources [batch_base + 16 tid, +16)
+    const unsigned long long i0 = batch_base + kSegment * tid;
+    const int nv = i0 >= a.n_local ? 0 : i0 + kSegment <= a.n_local ? kSegment : static_cast<int>(a.n_local - i0);
+    uint4 xx;
+    if (nv == kSegment) {
+      xx = __ldcs(reinterpret_cast<const uint4*>(a.x + i0));
+    } else {
+      uint8_t tmp[kSegment];
+#pragma unroll
+      for (int k = 0; k < kSegment; ++k) tmp[k] = k < nv ? a.x[i0 + k] : 0;
+      xx = *reinterpret_cast<const uint4*>(tmp);
+    }
+    reinterpret_cast<uint4*>(xs)[tid] = xx;
+    const uint32_t xw[4] = {xx.x, xx.y, xx.z, xx.w};
+    unsigned long long tw = 0;
+#pragma unroll
+    for (int k = 0; k < kSegment; ++k)
+      tw += k < nv ? wS[(xw[k >> 2] >> (8 * (k & 3))) & 0xFFu] : 0u;
+    // block exclusive scan of the thread sums -> this thread's batch-relative prefix
     unsigned long long incl = tw;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -541,114 +516,184 @@ __global__ void __launch_bounds__(kSmcThreads, 3) smc_resample_kernel(const __gr
     }
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    unsigned long long run = 0, btot = 0;
+    unsigned long long ex = incl - tw, btot = 0;
 #pragma unroll
     for (int q = 0; q < kSmcThreads / 32; ++q) {
-      if (q < warp) run += wsum[q];
+      if (q < warp) ex += wsum[q];
       btot += wsum[q];
     }
-    run += incl - tw;
-#pragma unroll
-    for (int k = 0; k < kBatchPerThread; ++k) {
-      run += w[k];
-      cb_incl[kBatchPerThread * tid + k] = run;
-    }
-    // outputs whose ancestors lie in this batch: [j_cur, j_next), j_next = F(C at batch end)
-    if (tid == kSmcThreads - 1) {
-      const unsigned long long c_end = c_base + btot;
-      const unsigned long long jn = c_end >= Tr ? jb_hi : first_j_at_least(O + c_end, cb);
-      s_u64[3] = jn < jb_hi ? jn : jb_hi;
-    }
-    __syncthreads();
-    const unsigned long long j_next = s_u64[3];
-    const unsigned long long off = O + c_base;  // global target of batch-relative weight 0
+    const unsigned long long c0 = O + c_base + ex;  // global weight coordinate of my source 0
+    const double est0 = __fma_rn(__ull2double_rn(c0), cb.n_over_t, -cb.a_over_t);
+    const unsigned int f0 = c0 == 0 ? 0u : comb_rank(est0, c0, cb);
 
-    // propagate [j_cur, j_next) in sub-rounds of at most kOutBuf outputs; thread tid takes an
-    // equal slice of consecutive outputs, finds the ancestor of its first by a branchless binary
-    // search over the staged prefix and the rest with a monotone merge pointer (targets increase
-    // with j); the new states are staged in shared memory and written out coalesced.
-    for (unsigned long long o0 = j_cur; o0 < j_next; o0 += kOutBuf) {
-      const unsigned long long o1 = o0 + kOutBuf < j_next ? o0 + kOutBuf : j_next;
-      const unsigned int n_out = static_cast<unsigned int>(o1 - o0);
-      const unsigned long long ob = o0 & ~15ull;  // obuf[j - ob]: same 16-byte phase as the owners' x
-      // slices of consecutive outputs, 4-aligned in j so a thread's Philox blocks (4 outputs
-      // each) are drawn at the same iteration by every lane
-      const unsigned long long a4 = o0 & ~3ull;
-      const unsigned int span4 = static_cast<unsigned int>(o1 - a4);
-      const unsigned int per = ((span4 + kSmcThreads - 1) / kSmcThreads + 3) & ~3u;
-      const unsigned long long q0 = a4 + static_cast<unsigned long long>(tid) * per;
-      const unsigned long long q1 = q0 + per < o1 ? q0 + per : o1;
-      const unsigned long long qs = q0 > o0 ? q0 : o0;
-      if (qs < q1) {
-        CombCursor cc;
-        cc.seek(static_cast<unsigned int>(qs), cb);
-        int k;
-        {  // smallest k with cb_incl[k] > t (exists: t < batch total): branchless, 12 steps
-          const unsigned long long t = cc.tgt - off;
-          int kk = 0;
+    // ---- outputs [j_cur, j_next) in 16-aligned windows of 8192 positions (one per batch
+    // unless the batch has > 8177 outputs)
+    unsigned long long o0 = j_cur;
+    while (true) {
+      const unsigned long long wb = o0 & ~15ull;
+      const unsigned long long we = wb + kWindow;
+      {  // rank my 16 sources into the comb; sources with children mark their first child
+        unsigned int fp = f0;
+        double cd = 0.0;
+        unsigned long long cr = 0;
 #pragma unroll
-          for (int step = kBatch / 2; step >= 1; step >>= 1)
-            kk += (cb_incl[kk + step - 1] <= t) ? step : 0;
-          k = kk;
+        for (int k = 0; k < kSegment; ++k) {
+          const uint32_t st = (xw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+          const uint32_t wk = k < nv ? wS[st] : 0u;
+          if (wk) {
+            cr += wk;
+            cd += wdS[st];  // exact: integer sums < 2^53
+            const unsigned int fn = comb_rank(__fma_rn(cd, cb.n_over_t, est0), c0 + cr, cb);
+            if (fp < fn) {
+              if (fp >= wb && fp < we) marks[fp - wb] = static_cast<uint16_t>(kSegment * tid + k + 1);
+              if (first && fp <= jb_lo && jb_lo < fn) s_carry = kSegment * tid + k + 1;
+            }
+            fp = fn;
+          }
         }
-        for (unsigned long long jg = q0; jg < q1; jg += 4) {
-          const uint4 wd = draw_block(key, jg >> 2, a.t + 1, CUPPL_TAG_SMC_STEP);
+        if (tid == kSmcThreads - 1) s_jn = fp;  // F(end of batch): first output of the next batch
+      }
+      __syncthreads();
+      const unsigned long long j_next = s_jn < jb_hi ? s_jn : jb_hi;
+      if (first) carry = s_carry;
+      first = false;
+      if (o0 >= j_next) break;  // no outputs (no marks were written either)
+      const unsigned long long o1 = we < j_next ? we : j_next;
+      // chunk c of this thread covers positions wb + 16 (tid + 256 c) + [0, 16)
+      unsigned int cm[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const uint4* mp = reinterpret_cast<const uint4*>(marks) + 2 * (tid + kSmcThreads * c);
+        const uint4 a0 = mp[0], a1 = mp[1];
+        const unsigned int m8 = __vmaxu2(__vmaxu2(__vmaxu2(a0.x, a0.y), __vmaxu2(a0.z, a0.w)),
+                                         __vmaxu2(__vmaxu2(a1.x, a1.y), __vmaxu2(a1.z, a1.w)));
+        cm[c] = max(m8 & 0xFFFFu, m8 >> 16);  // per-u16 max of the chunk's 16 marks
+      }
+      // inclusive max-scans over the threads (position order), both halves of the window
+      unsigned int pm0 = cm[0], pm1 = cm[1];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int t0 = __shfl_up_sync(0xffffffffu, pm0, o);
+        const unsigned int t1 = __shfl_up_sync(0xffffffffu, pm1, o);
+        if (lane >= o) {
+          pm0 = max(pm0, t0);
+          pm1 = max(pm1, t1);
+        }
+      }
+      if (lane == 31) {
+        wmax[warp] = pm0;
+        wmax[kSmcThreads / 32 + warp] = pm1;
+      }
+      __syncthreads();
+      unsigned int run0 = carry, run1 = carry, tot0 = carry, wall = carry;
+      {
+        const unsigned int e0 = __shfl_up_sync(0xffffffffu, pm0, 1);
+        const unsigned int e1 = __shfl_up_sync(0xffffffffu, pm1, 1);
+        if (lane > 0) {
+          run0 = max(run0, e0);
+          run1 = max(run1, e1);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < kSmcThreads / 32; ++q) {
+        if (q < warp) {
+          run0 = max(run0, wmax[q]);
+          run1 = max(run1, wmax[kSmcThreads / 32 + q]);
+        }
+        tot0 = max(tot0, wmax[q]);
+        wall = max(wall, wmax[kSmcThreads / 32 + q]);
+      }
+      run1 = max(run1, tot0);
+      wall = max(wall, tot0);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const unsigned long long jc = wb + kSegment * (tid + kSmcThreads * c);  // my first position
+        if (jc + kSegment <= o0 || jc >= o1) {  // chunk without outputs of this batch
+          uint4* mp = reinterpret_cast<uint4*>(marks) + 2 * (tid + kSmcThreads * c);
+          mp[0] = make_uint4(0, 0, 0, 0);
+          mp[1] = make_uint4(0, 0, 0, 0);
+          continue;
+        }
+        unsigned int run = c ? run1 : run0;
+        uint32_t mw[8];
+        {
+          uint4* mp = reinterpret_cast<uint4*>(marks) + 2 * (tid + kSmcThreads * c);
+          const uint4 a0 = mp[0], a1 = mp[1];
+          mp[0] = make_uint4(0, 0, 0, 0);
+          mp[1] = make_uint4(0, 0, 0, 0);
+          mw[0] = a0.x; mw[1] = a0.y; mw[2] = a0.z; mw[3] = a0.w;
+          mw[4] = a1.x; mw[5] = a1.y; mw[6] = a1.z; mw[7] = a1.w;
+        }
+        uint32_t outw[4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const uint4 wd = draw_block(key, (jc >> 2) + g, a.t + 1, CUPPL_TAG_SMC_STEP);
           const uint32_t wv[4] = {wd.x, wd.y, wd.z, wd.w};
+          uint32_t packed = 0;
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
-            const unsigned long long j = jg + h;
-            if (j < qs || j >= q1) continue;
-            const unsigned long long t = cc.tgt - off;  // batch-relative target, < btot
-            while (cb_incl[k] <= t) ++k;
-            const int xa = xs[k];
-            const int st = alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[h]);
-            obuf[j - ob] = static_cast<uint8_t>(st);
-            bmax = fmaxf(bmax, lwS1[st]);
-            if (debug_anc) {
-              int r = 0;
-              if (MULTI)
-                while (r + 1 < a.world && s_rank_begin[r + 1] <= j) ++r;
-              const unsigned long long rb = MULTI ? s_rank_begin[r] : 0ull;
-              const unsigned long long my = MULTI ? s_rank_begin[a.rank] : 0ull;
-              a.anc_out[r][j - rb] = my + batch_base + k;
+            const int i = 4 * g + h;
+            run = max(run, (mw[i >> 1] >> (16 * (i & 1))) & 0xFFFFu);
+            const unsigned int anc = (run - 1u) & (kBatch - 1);  // run >= 1 at every output
+            const int xa = xs[anc];
+            const int st = SMEM_ALIAS ? alias_draw_s(alias_s + xa * S, S, wv[h])
+                                      : alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[h]);
+            packed |= static_cast<uint32_t>(st) << (8 * h);
+            if (DEBUG) {
+              const unsigned long long j = jc + i;
+              if (j >= o0 && j < o1) {
+                int r = 0;
+                if (MULTI)
+                  while (r + 1 < a.world && s_rank_begin[r + 1] <= j) ++r;
+                const unsigned long long rb = MULTI ? s_rank_begin[r] : 0ull;
+                a.anc_out[r][j - rb] = my_begin + batch_base + anc;
+              }
             }
-            cc.next(cb);
+          }
+          outw[g] = packed;
+        }
+        // presence of the new states (max log-weight of population t + 1)
+#pragma unroll
+        for (int i = 0; i < kSegment; ++i) {
+          const int st = static_cast<int>((outw[i >> 2] >> (8 * (i & 3))) & 0xFFu);
+          if (st != last_st && jc + i >= o0 && jc + i < o1) {
+            pres[st] = 1;
+            last_st = st;
+          }
+        }
+        // store: one 16-byte write when the whole chunk is in [o0, o1) (rank boundaries are
+        // multiples of 16: a chunk never straddles two owners); bytes at the window edges
+        int r = 0;
+        if (MULTI)
+          while (r + 1 < a.world && s_rank_begin[r + 1] <= jc) ++r;
+        const unsigned long long rb = MULTI ? s_rank_begin[r] : 0ull;
+        if (jc >= o0 && jc + kSegment <= o1) {
+          __stcs(reinterpret_cast<uint4*>(a.x_out[r] + (jc - rb)),
+                 make_uint4(outw[0], outw[1], outw[2], outw[3]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < kSegment; ++i) {
+            const unsigned long long j = jc + i;
+            if (j >= o0 && j < o1) a.x_out[r][j - rb] = static_cast<uint8_t>(outw[i >> 2] >> (8 * (i & 3)));
           }
         }
       }
-      (void)n_out;
-      __syncthreads();
-      // coalesced copy-out of obuf[0, n_out) -> owners' x at global index o0 + i
-      int r = 0;
-      if (MULTI)
-        while (r + 1 < a.world && s_rank_begin[r + 1] <= o0) ++r;
-      unsigned long long g = o0;
-      while (g < o1) {
-        const unsigned long long rb = MULTI ? s_rank_begin[r] : 0ull;
-        const unsigned long long re = MULTI ? (r + 1 < a.world ? s_rank_begin[r + 1] : cb.N) : o1;
-        const unsigned long long e = re < o1 ? re : o1;
-        uint8_t* dst = a.x_out[r] + (g - rb);
-        const uint8_t* src = obuf + (g - ob);  // 16-byte phase of src == phase of dst
-        const unsigned int len = static_cast<unsigned int>(e - g);
-        // head bytes up to 16-byte alignment of dst, then uint4 chunks, then tail bytes
-        const unsigned int head = static_cast<unsigned int>((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15);
-        const unsigned int hb = head < len ? head : len;
-        if (tid < hb) dst[tid] = src[tid];
-        const unsigned int nv = (len - hb) / 16;
-        for (unsigned int v = tid; v < nv; v += kSmcThreads)
-          __stcs(reinterpret_cast<uint4*>(dst + hb) + v, reinterpret_cast<const uint4*>(src + hb)[v]);
-        for (unsigned int i = hb + 16 * nv + tid; i < len; i += kSmcThreads) dst[i] = src[i];
-        g = e;
-        ++r;
-      }
-      __syncthreads();  // obuf reuse
+      carry = wall;
+      o0 = we;
+      __syncthreads();  // wmax / marks / s_jn reuse
+      if (o0 >= j_next) break;
     }
-    __syncthreads();  // cb_incl / xs / wsum / s_u64 reuse
-    j_cur = j_next;
+    j_cur = s_jn < jb_hi ? s_jn : jb_hi;
     c_base += btot;
     batch_base += kBatch;
+    carry = 0;
+    __syncthreads();  // xs / wsum / s_jn reuse
   }
   if (MULTI) __threadfence_system();  // peer stores performed before the next collective
+  __syncthreads();
+  float bmax = neg_inf_f();
+  for (int s = tid; s < m.S; s += kSmcThreads)
+    if (pres[s]) bmax = fmaxf(bmax, lwS1[s]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
   if (lane == 0 && bmax > neg_inf_f()) atomicMax(a.m_key_next, f2key(bmax));
@@ -723,28 +768,38 @@ cudaError_t launch_smc_log_weights(const SmcModel& m, float y, const uint8_t* x,
   return cudaGetLastError();
 }
 
-template <bool MULTI, bool DEBUG>
+template <bool MULTI, bool DEBUG, bool SA>
 static cudaError_t launch_resample_t(const SmcModel& m, const SmcResampleArgs& a, int sm_count,
                                      cudaStream_t st) {
+  const size_t smem = SA ? static_cast<size_t>(m.S) * m.S * sizeof(unsigned long long) : 0;
+  auto kern = smc_resample_kernel<MULTI, DEBUG, SA>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
   int per_sm = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, smc_resample_kernel<MULTI, DEBUG>,
-                                                                kSmcThreads, 0);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSmcThreads, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   unsigned long long g = static_cast<unsigned long long>(sm_count) * per_sm;
   const unsigned long long want = (a.n_local + kBatch - 1) / kBatch;  // >= one batch per CTA
   if (g > want) g = want > 0 ? want : 1;
-  smc_resample_kernel<MULTI, DEBUG><<<static_cast<unsigned>(g), kSmcThreads, 0, st>>>(m, a);
+  kern<<<static_cast<unsigned>(g), kSmcThreads, smem, st>>>(m, a);
   return cudaGetLastError();
+}
+
+template <bool MULTI, bool DEBUG>
+static cudaError_t launch_resample_s(const SmcModel& m, const SmcResampleArgs& a, int sm_count,
+                                     cudaStream_t st) {
+  return m.S <= kSmemAliasMaxStates ? launch_resample_t<MULTI, DEBUG, true>(m, a, sm_count, st)
+                                    : launch_resample_t<MULTI, DEBUG, false>(m, a, sm_count, st);
 }
 
 cudaError_t launch_smc_resample(const SmcModel& m, const SmcResampleArgs& a, int sm_count,
                                 cudaStream_t st) {
   if (a.anc_out)
-    return a.world > 1 ? launch_resample_t<true, true>(m, a, sm_count, st)
-                       : launch_resample_t<false, true>(m, a, sm_count, st);
-  return a.world > 1 ? launch_resample_t<true, false>(m, a, sm_count, st)
-                     : launch_resample_t<false, false>(m, a, sm_count, st);
+    return a.world > 1 ? launch_resample_s<true, true>(m, a, sm_count, st)
+                       : launch_resample_s<false, true>(m, a, sm_count, st);
+  return a.world > 1 ? launch_resample_s<true, false>(m, a, sm_count, st)
+                     : launch_resample_s<false, false>(m, a, sm_count, st);
 }
 
 }  // namespace cuppl

@@ -7,12 +7,11 @@
 namespace cuppl {
 
 constexpr int kSmcThreads = 256;
-constexpr int kSegment = 32;                  // particles per segment offset
-constexpr int kTileSegs = 256;                // segments per K5 tile (one per thread)
-constexpr int kTile = kTileSegs * kSegment;   // 8192 particles per scan tile
-constexpr int kBatchPerThread = 16;           // sources per thread per K6 batch
-constexpr int kBatch = kSmcThreads * kBatchPerThread;  // 4096 sources per K6 batch
-constexpr int kOutBuf = 8192;                 // K6 output staging buffer (bytes = outputs)
+constexpr int kSegment = 16;                  // particles per thread in K5 / K6 (one uint4 of states)
+constexpr int kTile = kSmcThreads * kSegment;  // 4096 particles per K5 tile == K6 source batch
+constexpr int kBatch = kTile;
+constexpr int kWindow = 2 * kSmcThreads * kSegment;  // K6 output window: two 16-output chunks per thread
+constexpr int kSmemAliasMaxStates = 64;       // K6 stages the S x S alias tables in shared memory
 constexpr int kMaxStates = 256;               // particle state stored as u8
 constexpr int kMaxRanks = 64;
 
@@ -46,7 +45,6 @@ struct SmcScanArgs {
   float y;                       // observation of population t
   int S;
   const int* m_key;              // max of lw_t as an ordered int (global over ranks)
-  unsigned long long* segoff;    // [ceil(n/32)] TILE-local inclusive offsets per segment
   unsigned long long* tile_prefix;  // [n_tiles] exclusive prefix of the tile sums (look-back)
   unsigned long long* flags;     // [n_tiles] look-back words (status << 62 | value), zero on entry
   unsigned int* counters;        // [2]: dynamic tile id (zero on entry; K6 resets it)
@@ -66,7 +64,6 @@ struct SmcResampleArgs {
   int pad_;
   const uint8_t* x;
   const int* m_key;                        // max of lw_t (ordered int)
-  const unsigned long long* segoff;        // tile-local inclusive segment offsets
   const unsigned long long* tile_prefix;   // exclusive prefix of the tile sums
   const double* tile_s;                    // [n_tiles][2] per-tile sum e, sum e^2 (folded by CTA 0)
   double* stats_out;                       // [2]: rank sum e, sum e^2 of population t
