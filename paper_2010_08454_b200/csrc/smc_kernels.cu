@@ -368,7 +368,10 @@ __device__ __forceinline__ int alias_draw_s(const unsigned long long* row, unsig
 // no data-dependent loop: the work per output and per source is uniform whatever the
 // offspring counts.
 template <bool MULTI, bool DEBUG, bool SMEM_ALIAS>
-__global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __grid_constant__ SmcModel m,
+#ifndef CUPPL_SMC_MINBLOCKS
+#define CUPPL_SMC_MINBLOCKS 3
+#endif
+__global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample_kernel(const __grid_constant__ SmcModel m,
                                                                       SmcResampleArgs a) {
   extern __shared__ __align__(16) unsigned long long alias_s[];  // [S][S] (SMEM_ALIAS)
   __shared__ __align__(16) uint8_t xs[kBatch];         // staged source states
@@ -376,12 +379,11 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
   __shared__ unsigned long long wsum[kSmcThreads / 32];
   __shared__ unsigned int wmax[2 * (kSmcThreads / 32)];  // warp totals of both window halves
   __shared__ unsigned long long s_u64[4];
-  __shared__ unsigned int s_carry, s_jn;
+  __shared__ unsigned int s_jn;
   __shared__ unsigned long long s_rank_begin[MULTI ? kMaxRanks + 1 : 1];
   __shared__ uint32_t wS[kMaxStates];   // quantised weights of population t per state
   __shared__ double wdS[kMaxStates];    // the same as doubles (exact)
   __shared__ float lwS1[kMaxStates];    // log-weights of population t + 1 per state
-  __shared__ uint8_t pres[kMaxStates];  // states present among this CTA's outputs
   __shared__ BlockScratch sc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (MULTI)
@@ -423,7 +425,6 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
     build_tables(m, a.y_cur, key2f(*a.m_key), nullptr, eS, wS);
     build_tables(m, a.y_next, neg_inf_f(), lwS1, nullptr, nullptr);
   }
-  for (int s = tid; s < kMaxStates; s += kSmcThreads) pres[s] = 0;
   for (int i = tid; i < kWindow / 8; i += kSmcThreads) reinterpret_cast<uint4*>(marks)[i] = make_uint4(0, 0, 0, 0);
   if (SMEM_ALIAS) {
     const unsigned int nA = S * S;
@@ -432,22 +433,28 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
   __syncthreads();
   for (int s = tid; s < m.S; s += kSmcThreads) wdS[s] = static_cast<double>(wS[s]);
   const PhiloxKey key = make_key(a.key);
-  Comb cb;
-  cb.u = draw_block(key, a.t, 0u, CUPPL_TAG_SMC_COMB).x;
-  cb.N = static_cast<unsigned int>(a.n_total);
-  cb.T = T;
-  cb.Q = static_cast<unsigned int>(T / cb.N);
-  cb.R0 = static_cast<unsigned int>(T % cb.N);
-  cb.A = __umul64hi(static_cast<unsigned long long>(cb.u) << 32, T);  // floor(u T / 2^32)
-  cb.Qa = static_cast<unsigned int>(cb.A / cb.N);
-  cb.Ra = static_cast<unsigned int>(cb.A % cb.N);
-  cb.invN = 1.0 / static_cast<double>(cb.N);
-  cb.n_over_t = static_cast<double>(cb.N) / static_cast<double>(T);
-  cb.a_over_t = static_cast<double>(cb.A) / static_cast<double>(T);
+  __shared__ Comb s_cb;  // step constants (the rare exact rank path reads them here)
+  if (tid == 0) {
+    Comb c;
+    c.u = draw_block(key, a.t, 0u, CUPPL_TAG_SMC_COMB).x;
+    c.N = static_cast<unsigned int>(a.n_total);
+    c.T = T;
+    c.Q = static_cast<unsigned int>(T / c.N);
+    c.R0 = static_cast<unsigned int>(T % c.N);
+    c.A = __umul64hi(static_cast<unsigned long long>(c.u) << 32, T);  // floor(u T / 2^32)
+    c.Qa = static_cast<unsigned int>(c.A / c.N);
+    c.Ra = static_cast<unsigned int>(c.A % c.N);
+    c.invN = 1.0 / static_cast<double>(c.N);
+    c.n_over_t = static_cast<double>(c.N) / static_cast<double>(T);
+    c.a_over_t = static_cast<double>(c.A) / static_cast<double>(T);
+    s_cb = c;
+  }
+  __syncthreads();
+  const Comb& cb = s_cb;
+  const double n_over_t = cb.n_over_t;
 
   // this rank's outputs: J_r = {j : O <= target_j < O + Tr}; this CTA's even share of it
   if (tid == 0) {
-    s_carry = 0u;
     s_u64[0] = a.rank == 0 ? 0ull : comb_rank(O, cb);
     s_u64[1] = a.rank == a.world - 1 ? cb.N : comb_rank(O + Tr, cb);
   }
@@ -483,10 +490,8 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
   unsigned long long batch_base = s_u64[2] * kBatch;
   unsigned long long c_base = __ldg(a.tile_prefix + s_u64[2]);
   unsigned long long j_cur = jb_lo;
-  unsigned int carry = 0;
-  bool first = true;
+  float bmax = neg_inf_f();  // max log-weight of population t + 1 over this CTA's outputs
   const unsigned long long my_begin = MULTI ? s_rank_begin[a.rank] : 0ull;
-  int last_st = -1;
 
   while (j_cur < jb_hi && batch_base < a.n_local) {
     // ---- stage the tile: thread tid owns sources [batch_base + 16 tid, +16)
@@ -503,10 +508,14 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
     }
     reinterpret_cast<uint4*>(xs)[tid] = xx;
     const uint32_t xw[4] = {xx.x, xx.y, xx.z, xx.w};
-    unsigned long long tw = 0;
+    uint32_t twh = 0, twl = 0;  // 16 * (2^31 >> 4) = 2^31: the high parts fit one u32
 #pragma unroll
-    for (int k = 0; k < kSegment; ++k)
-      tw += k < nv ? wS[(xw[k >> 2] >> (8 * (k & 3))) & 0xFFu] : 0u;
+    for (int k = 0; k < kSegment; ++k) {
+      const uint32_t wk = k < nv ? wS[(xw[k >> 2] >> (8 * (k & 3))) & 0xFFu] : 0u;
+      twh += wk >> 4;
+      twl += wk & 15u;
+    }
+    const unsigned long long tw = (static_cast<unsigned long long>(twh) << 4) + twl;
     // block exclusive scan of the thread sums -> this thread's batch-relative prefix
     unsigned long long incl = tw;
 #pragma unroll
@@ -523,7 +532,7 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
       btot += wsum[q];
     }
     const unsigned long long c0 = O + c_base + ex;  // global weight coordinate of my source 0
-    const double est0 = __fma_rn(__ull2double_rn(c0), cb.n_over_t, -cb.a_over_t);
+    const double est0 = __fma_rn(__ull2double_rn(c0), n_over_t, -cb.a_over_t);
     const unsigned int f0 = c0 == 0 ? 0u : comb_rank(est0, c0, cb);
 
     // ---- outputs [j_cur, j_next) in 16-aligned windows of 8192 positions (one per batch
@@ -532,7 +541,11 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
     while (true) {
       const unsigned long long wb = o0 & ~15ull;
       const unsigned long long we = wb + kWindow;
-      {  // rank my 16 sources into the comb; sources with children mark their first child
+      {  // rank my 16 sources into the comb. A source with children in the window marks the
+         // position of its first child there (position 0 when its children straddle the
+         // window start): every window is self-contained, an output's ancestor is the last
+         // mark at or before it
+        const unsigned int wb32 = static_cast<unsigned int>(wb);  // N < 2^31: positions fit u32
         unsigned int fp = f0;
         double cd = 0.0;
         unsigned long long cr = 0;
@@ -543,11 +556,10 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
           if (wk) {
             cr += wk;
             cd += wdS[st];  // exact: integer sums < 2^53
-            const unsigned int fn = comb_rank(__fma_rn(cd, cb.n_over_t, est0), c0 + cr, cb);
-            if (fp < fn) {
-              if (fp >= wb && fp < we) marks[fp - wb] = static_cast<uint16_t>(kSegment * tid + k + 1);
-              if (first && fp <= jb_lo && jb_lo < fn) s_carry = kSegment * tid + k + 1;
-            }
+            const unsigned int fn = comb_rank(__fma_rn(cd, n_over_t, est0), c0 + cr, cb);
+            const unsigned int pos = fp > wb32 ? fp - wb32 : 0u;
+            if (fp < fn && fn > wb32 && pos < static_cast<unsigned int>(kWindow))
+              marks[pos] = static_cast<uint16_t>(kSegment * tid + k + 1);
             fp = fn;
           }
         }
@@ -555,8 +567,6 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
       }
       __syncthreads();
       const unsigned long long j_next = s_jn < jb_hi ? s_jn : jb_hi;
-      if (first) carry = s_carry;
-      first = false;
       if (o0 >= j_next) break;  // no outputs (no marks were written either)
       const unsigned long long o1 = we < j_next ? we : j_next;
       // chunk c of this thread covers positions wb + 16 (tid + 256 c) + [0, 16)
@@ -585,7 +595,7 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
         wmax[kSmcThreads / 32 + warp] = pm1;
       }
       __syncthreads();
-      unsigned int run0 = carry, run1 = carry, tot0 = carry, wall = carry;
+      unsigned int run0 = 0, run1 = 0, tot0 = 0;
       {
         const unsigned int e0 = __shfl_up_sync(0xffffffffu, pm0, 1);
         const unsigned int e1 = __shfl_up_sync(0xffffffffu, pm1, 1);
@@ -601,10 +611,8 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
           run1 = max(run1, wmax[kSmcThreads / 32 + q]);
         }
         tot0 = max(tot0, wmax[q]);
-        wall = max(wall, wmax[kSmcThreads / 32 + q]);
       }
       run1 = max(run1, tot0);
-      wall = max(wall, tot0);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const unsigned long long jc = wb + kSegment * (tid + kSmcThreads * c);  // my first position
@@ -615,6 +623,7 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
           continue;
         }
         unsigned int run = c ? run1 : run0;
+        const bool full = jc >= o0 && jc + kSegment <= o1;
         uint32_t mw[8];
         {
           uint4* mp = reinterpret_cast<uint4*>(marks) + 2 * (tid + kSmcThreads * c);
@@ -639,6 +648,7 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
             const int st = SMEM_ALIAS ? alias_draw_s(alias_s + xa * S, S, wv[h])
                                       : alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[h]);
             packed |= static_cast<uint32_t>(st) << (8 * h);
+            if (full) bmax = fmaxf(bmax, lwS1[st]);
             if (DEBUG) {
               const unsigned long long j = jc + i;
               if (j >= o0 && j < o1) {
@@ -652,33 +662,27 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
           }
           outw[g] = packed;
         }
-        // presence of the new states (max log-weight of population t + 1)
-#pragma unroll
-        for (int i = 0; i < kSegment; ++i) {
-          const int st = static_cast<int>((outw[i >> 2] >> (8 * (i & 3))) & 0xFFu);
-          if (st != last_st && jc + i >= o0 && jc + i < o1) {
-            pres[st] = 1;
-            last_st = st;
-          }
-        }
         // store: one 16-byte write when the whole chunk is in [o0, o1) (rank boundaries are
         // multiples of 16: a chunk never straddles two owners); bytes at the window edges
         int r = 0;
         if (MULTI)
           while (r + 1 < a.world && s_rank_begin[r + 1] <= jc) ++r;
         const unsigned long long rb = MULTI ? s_rank_begin[r] : 0ull;
-        if (jc >= o0 && jc + kSegment <= o1) {
+        if (full) {
           __stcs(reinterpret_cast<uint4*>(a.x_out[r] + (jc - rb)),
                  make_uint4(outw[0], outw[1], outw[2], outw[3]));
         } else {
 #pragma unroll
           for (int i = 0; i < kSegment; ++i) {
             const unsigned long long j = jc + i;
-            if (j >= o0 && j < o1) a.x_out[r][j - rb] = static_cast<uint8_t>(outw[i >> 2] >> (8 * (i & 3)));
+            if (j >= o0 && j < o1) {
+              const uint8_t st = static_cast<uint8_t>(outw[i >> 2] >> (8 * (i & 3)));
+              a.x_out[r][j - rb] = st;
+              bmax = fmaxf(bmax, lwS1[st]);
+            }
           }
         }
       }
-      carry = wall;
       o0 = we;
       __syncthreads();  // wmax / marks / s_jn reuse
       if (o0 >= j_next) break;
@@ -686,14 +690,9 @@ __global__ void __launch_bounds__(kSmcThreads, 2) smc_resample_kernel(const __gr
     j_cur = s_jn < jb_hi ? s_jn : jb_hi;
     c_base += btot;
     batch_base += kBatch;
-    carry = 0;
     __syncthreads();  // xs / wsum / s_jn reuse
   }
   if (MULTI) __threadfence_system();  // peer stores performed before the next collective
-  __syncthreads();
-  float bmax = neg_inf_f();
-  for (int s = tid; s < m.S; s += kSmcThreads)
-    if (pres[s]) bmax = fmaxf(bmax, lwS1[s]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
   if (lane == 0 && bmax > neg_inf_f()) atomicMax(a.m_key_next, f2key(bmax));
