@@ -163,6 +163,7 @@ int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_to
   a.m_key_next = m_key_next;
   a.flags_to_clear = w.flags;
   a.n_tiles = (n_local + kTile - 1) / kTile;
+  a.n_scan_blocks = (a.n_tiles + kScanTiles - 1) / kScanTiles;
   return cuda_status(launch_smc_resample(sm, a, sms, static_cast<cudaStream_t>(stream)),
                      "smc_resample");
 }
@@ -183,7 +184,8 @@ int cuppl_smc_fold(uint64_t n_local, double* stats_out, void* workspace, size_t 
   SmcWs w;
   if (int s = check_ws(n_local, workspace, workspace_bytes, &w)) return s;
   if (!stats_out) return set_error(CUPPL_E_ARGUMENT, "NULL buffer");
-  return cuda_status(launch_smc_fold(w.tile_s, (n_local + kTile - 1) / kTile, stats_out, w.counters,
+  const uint64_t n_tiles = (n_local + kTile - 1) / kTile;
+  return cuda_status(launch_smc_fold(w.tile_s, (n_tiles + kScanTiles - 1) / kScanTiles, stats_out, w.counters,
                                      static_cast<cudaStream_t>(stream)),
                      "smc_fold");
 }

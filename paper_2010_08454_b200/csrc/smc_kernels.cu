@@ -176,79 +176,94 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(const __grid_cons
   __shared__ uint32_t wS[kMaxStates];
   __shared__ float eS[kMaxStates];
   __shared__ uint2 wes[kMaxStates];  // (w, bits(e)) in one 64-bit entry: one LDS per particle
-  __shared__ unsigned long long wtot[kSmcThreads / 32];
+  __shared__ unsigned long long wtot[kScanTiles][kSmcThreads / 32];
   __shared__ double wpart[kSmcThreads / 32][2];
-  __shared__ unsigned int s_tile;
+  __shared__ unsigned int s_blk;
   __shared__ unsigned int cnt[HIST ? kMaxStates : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long n = a.n_local;
   const unsigned long long n_tiles = (n + kTile - 1) / kTile;
-  if (tid == 0) s_tile = atomicAdd(&a.counters[0], 1u);  // launch-order tile ids: look-back is deadlock free
+  const unsigned long long n_blocks = (n_tiles + kScanTiles - 1) / kScanTiles;
+  if (tid == 0) s_blk = atomicAdd(&a.counters[0], 1u);  // launch-order ids: look-back is deadlock free
   build_tables(m, a.y, key2f(*a.m_key), nullptr, eS, wS);
   for (int s = tid; s < a.S; s += kSmcThreads) {
     wes[s] = make_uint2(wS[s], __float_as_uint(eS[s]));
     if (HIST) cnt[s] = 0u;
   }
   __syncthreads();
-  const unsigned long long tile = s_tile;
-  // thread tid owns particles [tile * 4096 + 16 tid, +16): one 16-byte load of states
-  const unsigned long long p0 = tile * kTile + static_cast<unsigned long long>(tid) * kSegment;
-  uint4 v = make_uint4(0, 0, 0, 0);
-  int valid = 0;
-  if (p0 + kSegment <= n) {
-    v = __ldcs(reinterpret_cast<const uint4*>(a.x + p0));
-    valid = kSegment;
-  } else if (p0 < n) {
-    valid = static_cast<int>(n - p0);
-    uint8_t tmp[kSegment];
-    for (int k = 0; k < kSegment; ++k) tmp[k] = k < valid ? a.x[p0 + k] : 0;
-    v = *reinterpret_cast<const uint4*>(tmp);
-  }
-  const uint32_t words[4] = {v.x, v.y, v.z, v.w};
-  unsigned long long ws = 0;
-  float s1 = 0.f, s2 = 0.f;
-  if (!HIST && valid == kSegment) {  // fast path: a full thread slice, no per-particle checks
-    uint32_t whi = 0, wlo = 0;  // 16 * (2^31 >> 4) = 2^31: the high parts fit one u32
+  const unsigned long long blk = s_blk;
+  const unsigned long long tile0 = blk * kScanTiles;
+  // thread tid owns particles [tile * 4096 + 16 tid, +16) of each of the CTA's 8 tiles: all
+  // eight 16-byte loads are issued before any is used
+  uint4 v[kScanTiles];
+  int valid[kScanTiles];
 #pragma unroll
-    for (int k = 0; k < kSegment; ++k) {
-      const uint2 te = wes[(words[k >> 2] >> (8 * (k & 3))) & 0xFFu];
-      const float e = __uint_as_float(te.y);
-      whi += te.x >> 4;
-      wlo += te.x & 15u;
-      s1 += e;
-      s2 = fmaf(e, e, s2);
+  for (int u = 0; u < kScanTiles; ++u) {
+    const unsigned long long p0 = (tile0 + u) * kTile + static_cast<unsigned long long>(tid) * kSegment;
+    v[u] = make_uint4(0, 0, 0, 0);
+    valid[u] = 0;
+    if (p0 + kSegment <= n) {
+      v[u] = __ldcs(reinterpret_cast<const uint4*>(a.x + p0));
+      valid[u] = kSegment;
+    } else if (p0 < n) {
+      valid[u] = static_cast<int>(n - p0);
+      uint8_t tmp[kSegment];
+      for (int k = 0; k < kSegment; ++k) tmp[k] = k < valid[u] ? a.x[p0 + k] : 0;
+      v[u] = *reinterpret_cast<const uint4*>(tmp);
     }
-    ws = (static_cast<unsigned long long>(whi) << 4) + wlo;
-  } else {
+  }
+  double d1 = 0.0, d2 = 0.0;  // fp32 over each 16-particle slice, fp64 across slices (D10)
 #pragma unroll
-    for (int k = 0; k < kSegment; ++k) {
-      const uint32_t st = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-      const bool ok = k < valid;
-      const uint2 te = wes[st];
-      const uint32_t w = ok ? te.x : 0u;
-      const float e = ok ? __uint_as_float(te.y) : 0.f;
-      ws += w;
-      s1 += e;
-      s2 = fmaf(e, e, s2);
-      if (HIST) {
-        // warp-aggregated state counts: one shared atomic per distinct state in the warp
-        const unsigned int key = ok ? st : 0xFFFFFFFFu;
-        const unsigned int grp = __match_any_sync(0xffffffffu, key);
-        if (ok && lane == __ffs(grp) - 1) atomicAdd(&cnt[st], static_cast<unsigned int>(__popc(grp)));
+  for (int u = 0; u < kScanTiles; ++u) {
+    const uint32_t words[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+    unsigned long long ws = 0;
+    float s1 = 0.f, s2 = 0.f;
+    if (!HIST && valid[u] == kSegment) {  // fast path: a full thread slice, no per-particle checks
+      uint32_t whi = 0, wlo = 0;  // 16 * (2^31 >> 4) = 2^31: the high parts fit one u32
+#pragma unroll
+      for (int k = 0; k < kSegment; ++k) {
+        const uint2 te = wes[(words[k >> 2] >> (8 * (k & 3))) & 0xFFu];
+        const float e = __uint_as_float(te.y);
+        whi += te.x >> 4;
+        wlo += te.x & 15u;
+        s1 += e;
+        s2 = fmaf(e, e, s2);
+      }
+      ws = (static_cast<unsigned long long>(whi) << 4) + wlo;
+    } else {
+#pragma unroll
+      for (int k = 0; k < kSegment; ++k) {
+        const uint32_t st = (words[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+        const bool ok = k < valid[u];
+        const uint2 te = wes[st];
+        const uint32_t w = ok ? te.x : 0u;
+        const float e = ok ? __uint_as_float(te.y) : 0.f;
+        ws += w;
+        s1 += e;
+        s2 = fmaf(e, e, s2);
+        if (HIST) {
+          // warp-aggregated state counts: one shared atomic per distinct state in the warp
+          const unsigned int key = ok ? st : 0xFFFFFFFFu;
+          const unsigned int grp = __match_any_sync(0xffffffffu, key);
+          if (ok && lane == __ffs(grp) - 1) atomicAdd(&cnt[st], static_cast<unsigned int>(__popc(grp)));
+        }
       }
     }
+    d1 += s1;
+    d2 += s2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ws += __shfl_down_sync(0xffffffffu, ws, o);
+    if (lane == 0) wtot[u][warp] = ws;
   }
-  double d1 = s1, d2 = s2;  // per-warp fp64 partials, fixed tree
+  // per-warp fp64 partials, fixed tree
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     d1 += __shfl_down_sync(0xffffffffu, d1, o);
     d2 += __shfl_down_sync(0xffffffffu, d2, o);
-    ws += __shfl_down_sync(0xffffffffu, ws, o);
   }
   if (lane == 0) {
     wpart[warp][0] = d1;
     wpart[warp][1] = d2;
-    wtot[warp] = ws;
   }
   __syncthreads();
   if (HIST) {
@@ -256,22 +271,32 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(const __grid_cons
       if (cnt[s]) atomicAdd(&a.hist[s], static_cast<unsigned long long>(cnt[s]) * wS[s]);
   }
   if (warp != 0) return;  // only warp 0 waits on the predecessors
-  unsigned long long agg = 0;
+  // lane u < 8: aggregate of tile u, then the exclusive offsets of the tiles inside the block
+  unsigned long long tagg = 0;
+  if (lane < kScanTiles) {
 #pragma unroll
-  for (int w = 0; w < kSmcThreads / 32; ++w) agg += wtot[w];
-  if (lane == 0) st_relaxed_u64(a.flags + tile, (tile == 0 ? kFlagIncl : kFlagAgg) | agg);
-  const unsigned long long prefix = tile == 0 ? 0ull : warp_lookback(a.flags, tile);
+    for (int w = 0; w < kSmcThreads / 32; ++w) tagg += wtot[lane][w];
+  }
+  unsigned long long tincl = tagg;
+#pragma unroll
+  for (int o = 1; o < kScanTiles; o <<= 1) {
+    const unsigned long long t2 = __shfl_up_sync(0xffffffffu, tincl, o);
+    if (lane >= o) tincl += t2;
+  }
+  const unsigned long long agg = __shfl_sync(0xffffffffu, tincl, kScanTiles - 1);
+  if (lane == 0) st_relaxed_u64(a.flags + blk, (blk == 0 ? kFlagIncl : kFlagAgg) | agg);
+  const unsigned long long prefix = blk == 0 ? 0ull : warp_lookback(a.flags, blk);
+  if (lane == 0 && blk != 0) st_relaxed_u64(a.flags + blk, kFlagIncl | (prefix + agg));
+  if (lane < kScanTiles && tile0 + lane < n_tiles) a.tile_prefix[tile0 + lane] = prefix + tincl - tagg;
   if (lane == 0) {
-    if (tile != 0) st_relaxed_u64(a.flags + tile, kFlagIncl | (prefix + agg));
-    a.tile_prefix[tile] = prefix;
     double t1 = 0.0, t2 = 0.0;
     for (int w = 0; w < kSmcThreads / 32; ++w) {
       t1 += wpart[w][0];
       t2 += wpart[w][1];
     }
-    a.tile_s[2 * tile] = t1;
-    a.tile_s[2 * tile + 1] = t2;
-    if (tile == n_tiles - 1) a.rank_rec[0] = prefix + agg;  // T_r
+    a.tile_s[2 * blk] = t1;
+    a.tile_s[2 * blk + 1] = t2;
+    if (blk == n_blocks - 1) a.rank_rec[0] = prefix + agg;  // T_r
   }
 }
 
@@ -331,6 +356,21 @@ __device__ __noinline__ unsigned int comb_rank_exact(double est, unsigned long l
                                                                        : static_cast<unsigned int>(ceil(est));
   while (j > 0 && comb_ge(j - 1, c, cb)) --j;
   while (j < cb.N && !comb_ge(j, c, cb)) ++j;
+  return j;
+}
+__device__ __noinline__ unsigned int comb_rank_exact2(double est, unsigned long long c0, double cd,
+                                                     const Comb& cb) {
+  return comb_rank_exact(est, c0 + static_cast<unsigned long long>(cd), cb);
+}
+// Same, for the coordinate c0 + cd (cd an exact integer-valued double): the u64 coordinate is
+// only formed on the rare exact path.
+__device__ __forceinline__ unsigned int comb_rank(double est, unsigned long long c0, double cd,
+                                                  const Comb& cb) {
+  constexpr double kMagic = 6755399441055744.0;
+  const double t = __dadd_ru(est, kMagic);
+  const double frac = __dsub_rn(__dsub_rn(t, kMagic), est);
+  unsigned int j = static_cast<unsigned int>(__double2loint(t));
+  if (!(frac > 0x1p-14 && frac < 1.0 - 0x1p-14)) j = comb_rank_exact2(est, c0, cd, cb);
   return j;
 }
 __device__ __forceinline__ unsigned int comb_rank(double est, unsigned long long c, const Comb& cb) {
@@ -395,7 +435,7 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
   // tile counter. Every CTA clears a slice of the look-back words for the next scan.
   if (blockIdx.x == 0) {
     double f1 = 0.0, f2 = 0.0;
-    for (unsigned long long tt = tid; tt < n_tiles; tt += kSmcThreads) {
+    for (unsigned long long tt = tid; tt < a.n_scan_blocks; tt += kSmcThreads) {
       f1 += a.tile_s[2 * tt];
       f2 += a.tile_s[2 * tt + 1];
     }
@@ -508,14 +548,11 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
     }
     reinterpret_cast<uint4*>(xs)[tid] = xx;
     const uint32_t xw[4] = {xx.x, xx.y, xx.z, xx.w};
-    uint32_t twh = 0, twl = 0;  // 16 * (2^31 >> 4) = 2^31: the high parts fit one u32
+    double twd = 0.0;  // exact: 16 weights < 2^35
 #pragma unroll
-    for (int k = 0; k < kSegment; ++k) {
-      const uint32_t wk = k < nv ? wS[(xw[k >> 2] >> (8 * (k & 3))) & 0xFFu] : 0u;
-      twh += wk >> 4;
-      twl += wk & 15u;
-    }
-    const unsigned long long tw = (static_cast<unsigned long long>(twh) << 4) + twl;
+    for (int k = 0; k < kSegment; ++k)
+      twd += k < nv ? wdS[(xw[k >> 2] >> (8 * (k & 3))) & 0xFFu] : 0.0;
+    const unsigned long long tw = static_cast<unsigned long long>(twd);
     // block exclusive scan of the thread sums -> this thread's batch-relative prefix
     unsigned long long incl = tw;
 #pragma unroll
@@ -547,21 +584,16 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
          // mark at or before it
         const unsigned int wb32 = static_cast<unsigned int>(wb);  // N < 2^31: positions fit u32
         unsigned int fp = f0;
-        double cd = 0.0;
-        unsigned long long cr = 0;
+        double cd = 0.0;  // exact prefix of my sources (integer sums < 2^53)
+        const uint16_t mark0 = static_cast<uint16_t>(kSegment * tid + 1);
 #pragma unroll
         for (int k = 0; k < kSegment; ++k) {
           const uint32_t st = (xw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-          const uint32_t wk = k < nv ? wS[st] : 0u;
-          if (wk) {
-            cr += wk;
-            cd += wdS[st];  // exact: integer sums < 2^53
-            const unsigned int fn = comb_rank(__fma_rn(cd, n_over_t, est0), c0 + cr, cb);
-            const unsigned int pos = fp > wb32 ? fp - wb32 : 0u;
-            if (fp < fn && fn > wb32 && pos < static_cast<unsigned int>(kWindow))
-              marks[pos] = static_cast<uint16_t>(kSegment * tid + k + 1);
-            fp = fn;
-          }
+          cd += k < nv ? wdS[st] : 0.0;
+          const unsigned int fn = comb_rank(__fma_rn(cd, n_over_t, est0), c0, cd, cb);
+          if (fp < fn && fn > wb32 && fp < wb32 + static_cast<unsigned int>(kWindow))
+            marks[(fp > wb32 ? fp : wb32) - wb32] = static_cast<uint16_t>(mark0 + k);
+          fp = fn;
         }
         if (tid == kSmcThreads - 1) s_jn = fp;  // F(end of batch): first output of the next batch
       }
@@ -739,10 +771,11 @@ cudaError_t launch_smc_init(const SmcModel& m, const SmcInitArgs& a, int sm_coun
 cudaError_t launch_smc_scan(const SmcModel& m, const SmcScanArgs& a, int sm_count, cudaStream_t st) {
   (void)sm_count;
   const unsigned long long n_tiles = (a.n_local + kTile - 1) / kTile;
+  const unsigned long long n_blocks = (n_tiles + kScanTiles - 1) / kScanTiles;
   if (a.hist)
-    smc_scan_kernel<true><<<static_cast<unsigned>(n_tiles), kSmcThreads, 0, st>>>(m, a);
+    smc_scan_kernel<true><<<static_cast<unsigned>(n_blocks), kSmcThreads, 0, st>>>(m, a);
   else
-    smc_scan_kernel<false><<<static_cast<unsigned>(n_tiles), kSmcThreads, 0, st>>>(m, a);
+    smc_scan_kernel<false><<<static_cast<unsigned>(n_blocks), kSmcThreads, 0, st>>>(m, a);
   return cudaGetLastError();
 }
 

@@ -10,6 +10,7 @@ constexpr int kSmcThreads = 256;
 constexpr int kSegment = 16;                  // particles per thread in K5 / K6 (one uint4 of states)
 constexpr int kTile = kSmcThreads * kSegment;  // 4096 particles per K5 tile == K6 source batch
 constexpr int kBatch = kTile;
+constexpr int kScanTiles = 8;                 // K5 tiles per CTA (one table build + look-back per 32K particles)
 constexpr int kWindow = 2 * kSmcThreads * kSegment;  // K6 output window: two 16-output chunks per thread
 constexpr int kSmemAliasMaxStates = 64;       // K6 stages the S x S alias tables in shared memory
 constexpr int kMaxStates = 256;               // particle state stored as u8
@@ -48,7 +49,7 @@ struct SmcScanArgs {
   unsigned long long* tile_prefix;  // [n_tiles] exclusive prefix of the tile sums (look-back)
   unsigned long long* flags;     // [n_tiles] look-back words (status << 62 | value), zero on entry
   unsigned int* counters;        // [2]: dynamic tile id (zero on entry; K6 resets it)
-  double* tile_s;                // [n_tiles][2] per-tile sum e, sum e^2
+  double* tile_s;                // [n_scan_blocks][2] per-CTA sum e, sum e^2 (fixed 8-tile blocks)
   unsigned long long* hist;      // [S] integer filtering weights of x_t (NULL: skip), zero on entry
   unsigned long long* rank_rec;  // [4]: T_r written by the last tile (other words untouched)
 };
@@ -65,7 +66,7 @@ struct SmcResampleArgs {
   const uint8_t* x;
   const int* m_key;                        // max of lw_t (ordered int)
   const unsigned long long* tile_prefix;   // exclusive prefix of the tile sums
-  const double* tile_s;                    // [n_tiles][2] per-tile sum e, sum e^2 (folded by CTA 0)
+  const double* tile_s;                    // [n_scan_blocks][2] per-K5-CTA sum e, sum e^2 (folded by CTA 0)
   double* stats_out;                       // [2]: rank sum e, sum e^2 of population t
   unsigned int* counters;                  // K5 counters, reset here
   const unsigned long long* rank_recs;     // [world][4] gathered rank records of step t
@@ -75,6 +76,7 @@ struct SmcResampleArgs {
   int* m_key_next;                         // atomicMax of lw_{t+1} over the outputs written here
   unsigned long long* flags_to_clear;      // K5 look-back words, zeroed for the next scan
   unsigned long long n_tiles;
+  unsigned long long n_scan_blocks;        // K5 CTAs = ceil(n_tiles / kScanTiles)
 };
 
 cudaError_t launch_smc_init(const SmcModel& m, const SmcInitArgs& a, int sm_count, cudaStream_t st);
