@@ -214,6 +214,7 @@ def calibrate_fp32(device) -> float:
 
 
 def load_traffic(workload: str):
+    """ncu-measured DRAM bytes (dram__bytes_read + write) per launch of the dominant kernel."""
     p = ROOT / "profiles" / "traffic.json"
     if p.exists():
         try:
@@ -315,7 +316,7 @@ def run_ours(args) -> dict | None:
             "peak": peak / 1e12,
             "unit": "TFLOP/s",
             "frac": achieved / peak,
-            "traffic": load_traffic(args.workload),
+            "traffic": (load_traffic(args.workload) or {}).get("bytes_per_launch"),
             "peak_source": "measured FFMA2 ceiling on this GPU (csrc/calib_kernels.cu kind 0); "
                            "MEASURED_PEAKS.json has no fp32 CUDA-core figure",
             "nominal_peak": nominal / 1e12,
@@ -331,7 +332,7 @@ def run_ours(args) -> dict | None:
             rate = per_gpu / kernel_s
             roof = {"bound": "issue (fma pipe: Philox IMAD.WIDE + fp32 FFMA2)", "achieved": rate,
                     "peak": roof_rate, "unit": "particles/s", "frac": rate / roof_rate,
-                    "traffic": load_traffic(args.workload),
+                    "traffic": (load_traffic(args.workload) or {}).get("bytes_per_launch"),
                     "peak_source": f"measured: Philox {ph:.3g} blocks/s (calib kind 2) + FFMA2 {peak / 1e12:.1f} "
                                    "TFLOP/s (kind 0), 1 block + {fpp:.0f} flops per particle".replace("{fpp:.0f}", f"{fpp:.0f}"),
                     "flops_per_particle": fpp}
@@ -403,13 +404,14 @@ def run_ours_engine(args) -> dict | None:
     if args.workload == "smc":
         n = args.particles or wl["particles_per_gpu"]
         T = model.T
+        runner = smc.SmcRunner(model, n, Rng(1), steps=T, device=device)  # buffers built once
 
         def step(k):
-            r = smc.SmcRunner(model, n, Rng(1).split(k), steps=T, device=device)
-            r.init()
+            runner.reseed(Rng(1).split(k))
+            runner.init()
             for t in range(T):
-                r.step(t)
-            return r
+                runner.step(t)
+            return runner
         units_per_step = T  # time steps of the whole (strong-scaled) population
     else:
         chains = args.particles or wl["particles_per_gpu"]
@@ -428,6 +430,8 @@ def run_ours_engine(args) -> dict | None:
     clocks = ClockSampler(local)
     clocks.start()
     last = None
+    if args.workload == "smc":
+        runner.k6_events = []  # dominant kernel (K6) timed live on its stream
     for k in range(args.steps):
         flush.zero_()
         starts[k].record()
@@ -459,14 +463,26 @@ def run_ours_engine(args) -> dict | None:
            "clocks": clk}
     if args.workload == "smc":
         peak, src = _hbm_peak()
-        bytes_step = 14.0 * n / world  # per GPU: K5 reads lw; K6 reads lw + x, writes x' + lw' (u8 state)
-        achieved = bytes_step * units_per_step / (t_ms / args.steps / 1e3) / 1e9
+        k6 = [a.elapsed_time(b) for a, b in runner.k6_events]
+        runner.k6_events = None
+        k6_ms = sum(k6) / len(k6)
+        # SURVEY.md §8(d) C4 per-unit figure, K6 share, s = 1 B state: reads lw_t (4) + ancestor
+        # x_t (s), writes x_{t+1} (s) + lw_{t+1} (4). This build never stores a log-weight (a
+        # state's weight is tabulated per step), so K6 moves ~1.6 B/particle (ncu traffic below)
+        # and is bound by instruction issue, not HBM.
+        k6_bytes = 10.0 * n / world
+        achieved = k6_bytes / (k6_ms / 1e3) / 1e9
+        tr = load_traffic("smc")
         res["config"].update({"particles": n, "time_steps": T, "state": "u8", "resampling": "systematic every step",
                               "parallelism": f"particle-partitioned dp{world} (NCCL max all-reduce + 32-B "
                                              "record all-gather per step, CUDA-IPC peer stores)"})
-        res["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                           "frac": achieved / peak, "traffic": load_traffic("smc"), "peak_source": src,
-                           "bytes_per_particle_step": 14}
+        res["roofline"] = {"bound": "hbm", "kernel": "smc_resample_kernel (K6)", "achieved": achieved, "peak": peak,
+                           "unit": "GB/s", "frac": achieved / peak,
+                           "traffic": None if tr is None else tr["bytes_per_launch"] * (n / tr["n"]),
+                           "peak_source": src, "algorithmic_bytes_per_particle": 10,
+                           "k6_ms_avg": k6_ms, "k6_share_of_step": k6_ms * T / (t_ms / args.steps),
+                           "note": "state-only populations: measured DRAM traffic ~1.6 B/particle vs the "
+                                   "survey's 10 B; K6 is issue-bound"}
         res["particle_steps_per_s"] = n * units_per_step * args.steps / (t_ms / 1e3)
         res["gpu_launches"] = args.steps * (1 + 2 * T)
         # e2e: public API from host data (model arrays host -> device tables), result to host
@@ -486,7 +502,7 @@ def run_ours_engine(args) -> dict | None:
         res["config"].update({"chains": units_per_step // args.mh_steps, "steps_per_chain": args.mh_steps,
                               "semantics": "full re-execution per step (reference LMH)"})
         res["roofline"] = {"bound": "fp32", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
-                           "frac": achieved / peak, "traffic": load_traffic("mh"),
+                           "frac": achieved / peak, "traffic": (load_traffic("mh") or {}).get("bytes_per_launch"),
                            "peak_source": "measured FFMA2 ceiling (csrc/calib_kernels.cu kind 0)",
                            "flops_per_chain_step": fl}
         res["gpu_launches"] = args.steps
@@ -513,13 +529,15 @@ def cpu_baseline_engine(args, model) -> dict:
     core.build()
     threads = os.cpu_count() or 1
     if args.workload == "smc":
-        n, T = 100_000, 200
+        n_full = args.particles or WORKLOADS["smc"]["particles_per_gpu"]
+        n, T = 1_000_000, 50
         t0 = time.perf_counter()
         core.smc_run(model, n, 0x9E0160293A33AAF7, steps=T)
         dt = time.perf_counter() - t0
-        return {"value": T / dt, "unit": "time-steps/s", "cores": 1, "kind": "port",
-                "sample": f"{n} particles x {T} steps, oracle/cuppl_oracle.c or_smc_step (scalar, 1 thread); "
-                          f"{n * T / dt:.3g} particle-steps/s"}
+        return {"value": n * T / dt / n_full, "unit": "time-steps/s", "cores": threads, "kind": "port",
+                "sample": f"{n} particles x {T} steps, oracle/cuppl_oracle.c or_smc_step (OpenMP {threads} "
+                          f"threads): {n * T / dt:.3g} particle-steps/s, quoted per step of the "
+                          f"{n_full}-particle filter (linear in particles)"}
     chains, steps = 64, 2000
     t0 = time.perf_counter()
     core.mh_gmm(model.ys, model.K, model.prior_sd, model.sigma, chains, steps, 0x9E0160293A33AAF7, threads=threads)
@@ -541,12 +559,14 @@ def run_reference(args) -> dict | None:
     threads = os.cpu_count() or 1
     key = 0x9E0160293A33AAF7
     if args.workload == "smc":
-        per_step, cores = 20_000, 1
-        sample = f"{per_step} particles x 50 time steps per step (or_smc_step, scalar)"
+        per_step, cores = 1_000_000, threads
+        n_full = args.particles or wl["particles_per_gpu"]
+        sample = (f"{per_step} particles x 20 time steps per step (or_smc_step, OpenMP {threads}), rate quoted "
+                  f"per time step of the {n_full}-particle filter (linear in particles)")
 
         def step(k):
-            core.smc_run(model, per_step, key + k, steps=50)
-        units = 50
+            core.smc_run(model, per_step, key + k, steps=20)
+        units = 20 * per_step / n_full
     elif args.workload == "mh":
         per_step, cores = 64, threads
         sample = f"{per_step} chains x 200 steps per step (or_mh_gmm, fp64, OpenMP {threads})"
@@ -575,7 +595,8 @@ def run_reference(args) -> dict | None:
     return {
         "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if args.workload == "smc" else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
         "impl": "reference",
         "config": {"workload": wl["name"], "units_per_step": units, "n_points": wl["n_points"]},
         "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port", "sample": sample},

@@ -36,12 +36,25 @@ class OrRecord(C.Structure):
         return d
 
 
+def _source_hash() -> str:
+    import hashlib
+
+    h = hashlib.sha256()
+    for p in sorted(HERE.glob("*.c")) + [HERE / "Makefile"]:
+        h.update(p.name.encode())
+        h.update(p.read_bytes())
+    return h.hexdigest()
+
+
 def build() -> Path:
-    """Compile the C restatement (make, in-tree)."""
-    srcs = list(HERE.glob("*.c")) + [HERE / "Makefile"]
-    if LIB_PATH.exists() and all(s.stat().st_mtime <= LIB_PATH.stat().st_mtime for s in srcs):
+    """Compile the C restatement (make, in-tree). Content-hash stamped, so a copied tree whose
+    modification times are not preserved still rebuilds exactly when the sources changed."""
+    stamp = LIB_PATH.with_suffix(".sha256")
+    h = _source_hash()
+    if LIB_PATH.exists() and stamp.exists() and stamp.read_text().strip() == h:
         return LIB_PATH
-    subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+    subprocess.run(["make", "-s", "-B", "-C", str(HERE)], check=True)
+    stamp.write_text(h)
     return LIB_PATH
 
 

@@ -586,19 +586,27 @@ int or_smc_step(uint64_t N, uint64_t key, uint32_t t, const uint64_t* aliasA, in
   for (uint64_t i = 0; i < N; ++i)
     if (lw[i] > M) M = lw[i];
   uint64_t* C = (uint64_t*)malloc(sizeof(uint64_t) * (N ? N : 1));
-  if (!C) return 1;
+  float* E = (float*)malloc(sizeof(float) * (N ? N : 1));
+  if (!C || !E) { free(C); free(E); return 1; }
+  /* per-particle weights in parallel; the prefix and the fp64 sums sequentially (fixed order) */
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < (int64_t)N; ++i) {
+    E[i] = M > -INFINITY ? or_smc_e(lw[i], M) : 0.0f;
+    C[i] = or_smc_w(E[i]);
+  }
   uint64_t T = 0;
   double s1 = 0.0, s2 = 0.0;
   if (hist) memset(hist, 0, sizeof(uint64_t) * (size_t)S);
   for (uint64_t i = 0; i < N; ++i) {
-    const float e = M > -INFINITY ? or_smc_e(lw[i], M) : 0.0f;
-    const uint32_t w = or_smc_w(e);
+    const uint64_t w = C[i];
+    const double e = (double)E[i];
     T += w;
     C[i] = T;
-    s1 += (double)e;
-    s2 += (double)e * (double)e;
+    s1 += e;
+    s2 += e * e;
     if (hist) hist[x[i]] += w;
   }
+  free(E);
   st->M = M;
   st->T = T;
   st->s1 = s1;
@@ -606,7 +614,9 @@ int or_smc_step(uint64_t N, uint64_t key, uint32_t t, const uint64_t* aliasA, in
   st->status = T == 0 ? 2 : 0;
   if (T == 0 || !x_out) { free(C); return T == 0 ? 2 : 0; }
   const uint32_t u = or_comb_word(key, t);
-  for (uint64_t j = 0; j < N; ++j) {
+#pragma omp parallel for schedule(static)
+  for (int64_t jj = 0; jj < (int64_t)N; ++jj) {
+    const uint64_t j = (uint64_t)jj;
     const uint64_t tj = or_comb_target(j, u, T, N);
     uint64_t lo = 0, hi = N - 1; /* smallest i with C[i] > tj (exists: C[N-1] = T > tj) */
     while (lo < hi) {

@@ -210,6 +210,7 @@ class SmcRunner:
         self.ancestors = []
         self._pending_anc = None
         self.cur = 0
+        self.k6_events = None  # list of (start, end) CUDA events per K6 launch when profiling
 
     # ------------------------------------------------------------------ collectives -------
     def _exchange_arenas(self):
@@ -297,6 +298,13 @@ class SmcRunner:
         return out.cpu().numpy()
 
     # ------------------------------------------------------------------ steps -------------
+    def reseed(self, rng):
+        """Reuse the runner's buffers for a new run with another generator."""
+        self.key = key_of(rng)
+        self.seed = seed_of(rng)
+        self.ancestors = []
+        self._pending_anc = None
+
     def init(self):
         L = N.lib()
         st = N.stream_ptr(self.device)
@@ -326,6 +334,12 @@ class SmcRunner:
             return
         nxt = 1 - self.cur
         xt, at = self._tables[nxt]
+        ev = None
+        if self.k6_events is not None:
+            import torch
+
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
         for rk in self.ranks:
             N.check(L.cuppl_smc_resample(
                 C.byref(self.cm), rk.n, self.N, self.key, t, rk.r, self.world, float(self.ys[t]),
@@ -333,6 +347,9 @@ class SmcRunner:
                 N.ptr(self.gathered[t]), N.ptr(self.rank_begin), N.ptr(xt),
                 None if at is None else N.ptr(at), N.ptr(rk.m_key[t + 1:t + 2]), N.ptr(rk.stats[t]),
                 N.ptr(rk.ws), rk.ws.numel(), st), "smc_resample", seed=self.seed, step=t)
+        if ev is not None:
+            ev[1].record()
+            self.k6_events.append(ev)
         if self.record_ancestors:
             self._pending_anc = nxt  # complete only after the next collective (peer stores)
         self.cur = nxt
