@@ -9,12 +9,16 @@
 using namespace cuppl;
 
 namespace {
-int padded(int D) { return ((D + kMhPadPoints - 1) / kMhPadPoints) * kMhPadPoints; }
+int padded(int D) {
+  int M = 0, NT = 0;
+  mh_shape(D, &M, &NT);
+  return 8 * NT * M;
+}
 }  // namespace
 
 extern "C" {
 
-int cuppl_mh_padded_points(int D) { return D < 1 ? kMhPadPoints : padded(D); }
+int cuppl_mh_padded_points(int D) { return padded(D < 1 ? 1 : D); }
 
 int cuppl_mh_gmm(const float* y, int D, int K, float prior_sd, float sigma, uint32_t n_chains,
                  uint32_t chain_begin, uint32_t n_steps, uint32_t burn_in, uint32_t thin,
@@ -27,15 +31,24 @@ int cuppl_mh_gmm(const float* y, int D, int K, float prior_sd, float sigma, uint
   if (thin < 1) return set_error(CUPPL_E_ARGUMENT, "thin must be >= 1");
   if (!y || !mu_out || !ll_out || !stats_out) return set_error(CUPPL_E_ARGUMENT, "NULL buffer");
   if (n_chains == 0) return CUPPL_OK;
-  int dev = 0, max_smem = 0;
+  int M = 0, NT = 0;
+  mh_shape(D, &M, &NT);
+  if (M > kMhMaxGroupsPerThread)
+    return set_error(CUPPL_E_CAPACITY, "D=%d exceeds %d points", D, 8 * kMhMaxThreads * kMhMaxGroupsPerThread);
+  const int G = NT * M, D_pad = 8 * G;
+  int dev = 0, max_smem = 0, sms = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
   e = cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
-  const int D_pad = padded(D);
-  int cpc = kMhMaxChainsPerCta;
-  while (cpc > 1 && mh_smem_bytes(D_pad, cpc) > static_cast<size_t>(max_smem)) --cpc;
-  if (mh_smem_bytes(D_pad, cpc) > static_cast<size_t>(max_smem))
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaDeviceGetAttribute");
+  // chains per CTA: one wave over the SMs, at most one per lane of warp 0, within shared memory
+  int cpc = static_cast<int>((n_chains + sms - 1) / sms);
+  if (cpc > kMhMaxChainsPerCta) cpc = kMhMaxChainsPerCta;
+  if (cpc < 1) cpc = 1;
+  while (cpc > 1 && mh_smem_bytes(G, K, cpc, NT) > static_cast<size_t>(max_smem)) --cpc;
+  if (mh_smem_bytes(G, K, cpc, NT) > static_cast<size_t>(max_smem))
     return set_error(CUPPL_E_CAPACITY, "D=%d does not fit in shared memory", D);
   MhArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -47,6 +60,9 @@ int cuppl_mh_gmm(const float* y, int D, int K, float prior_sd, float sigma, uint
   a.thin = thin;
   a.D = D;
   a.D_pad = D_pad;
+  a.G = G;
+  a.threads = NT;
+  a.groups_per_thread = M;
   a.K = K;
   a.prior_sd = prior_sd;
   a.neg_half_inv_var = static_cast<float>(-0.5 / (static_cast<double>(sigma) * sigma));

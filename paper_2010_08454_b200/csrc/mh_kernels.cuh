@@ -6,9 +6,22 @@
 
 namespace cuppl {
 
-constexpr int kMhMaxK = 7;            // mixture components (3-bit labels; code 7 is padding)
-constexpr int kMhPadPoints = 256;     // data padded to 32 lanes x 8 points
-constexpr int kMhMaxChainsPerCta = 28;
+constexpr int kMhMaxK = 7;            // mixture components (label K is padding)
+constexpr int kMhMaxThreads = 640;    // threads per CTA (each holds 8-point groups of y)
+constexpr int kMhMaxGroupsPerThread = 8;  // D <= 640 * 8 * 8 = 40960 points
+constexpr int kMhMaxChainsPerCta = 32;    // one chain per lane of warp 0
+constexpr int kMhTab = 64;                // pair-code table entries (W^2 <= 64: K <= 7)
+
+// Point groups per thread (M) and threads per CTA (NT) for D points: D is padded to 8 NT M.
+inline void mh_shape(int D, int* M, int* NT) {
+  const int g = (D + 7) / 8;
+  int m = (g + kMhMaxThreads - 1) / kMhMaxThreads;
+  if (m < 1) m = 1;
+  int nt = ((g + m - 1) / m + 31) / 32 * 32;
+  if (nt < 32) nt = 32;
+  *M = m;
+  *NT = nt;
+}
 
 struct MhArgs {
   unsigned long long key;
@@ -18,7 +31,10 @@ struct MhArgs {
   unsigned int burn_in;       // steps not recorded
   unsigned int thin;          // record every thin-th step after burn-in
   int D;                      // data points
-  int D_pad;                  // padded to a multiple of kMhPadPoints
+  int D_pad;                  // 8 G
+  int G;                      // 8-point groups = threads * groups_per_thread
+  int threads;                // threads per CTA
+  int groups_per_thread;      // M: y values per thread = 8 M (registers)
   int K;                      // components
   float prior_sd;             // mu_k ~ normal(0, prior_sd)
   float neg_half_inv_var;     // -0.5 / sigma^2
@@ -33,7 +49,7 @@ struct MhArgs {
   unsigned int pad_;
 };
 
-size_t mh_smem_bytes(int D_pad, int chains_per_cta);
+size_t mh_smem_bytes(int G, int K, int chains_per_cta, int threads);
 cudaError_t launch_mh_gmm(const MhArgs& a, cudaStream_t st);
 
 }  // namespace cuppl
