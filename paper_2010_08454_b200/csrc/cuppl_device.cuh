@@ -22,10 +22,12 @@ constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint64_t p0 = static_cast<uint64_t>(kPhiloxM0) * c.x;
-    const uint64_t p1 = static_cast<uint64_t>(kPhiloxM1) * c.z;
-    const uint32_t hi0 = static_cast<uint32_t>(p0 >> 32), lo0 = static_cast<uint32_t>(p0);
-    const uint32_t hi1 = static_cast<uint32_t>(p1 >> 32), lo1 = static_cast<uint32_t>(p1);
+    // explicit 32x32 -> 64 multiplies (one IMAD.WIDE.U32 each) split into (lo, hi)
+    uint32_t lo0, hi0, lo1, hi1;
+    asm("{\n\t.reg .b64 p;\n\tmul.wide.u32 p, %2, %3;\n\tmov.b64 {%0, %1}, p;\n\t}"
+        : "=r"(lo0), "=r"(hi0) : "r"(c.x), "n"(kPhiloxM0));
+    asm("{\n\t.reg .b64 p;\n\tmul.wide.u32 p, %2, %3;\n\tmov.b64 {%0, %1}, p;\n\t}"
+        : "=r"(lo1), "=r"(hi1) : "r"(c.z), "n"(kPhiloxM1));
     c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
     k0 += kPhiloxW0;
     k1 += kPhiloxW1;
