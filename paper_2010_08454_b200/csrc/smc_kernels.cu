@@ -409,7 +409,7 @@ __device__ __forceinline__ int alias_draw_s(const unsigned long long* row, unsig
 // offspring counts.
 template <bool MULTI, bool DEBUG, bool SMEM_ALIAS>
 #ifndef CUPPL_SMC_MINBLOCKS
-#define CUPPL_SMC_MINBLOCKS 3
+#define CUPPL_SMC_MINBLOCKS 4
 #endif
 __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample_kernel(const __grid_constant__ SmcModel m,
                                                                       SmcResampleArgs a) {
@@ -549,9 +549,14 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
     reinterpret_cast<uint4*>(xs)[tid] = xx;
     const uint32_t xw[4] = {xx.x, xx.y, xx.z, xx.w};
     double twd = 0.0;  // exact: 16 weights < 2^35
+    if (nv == kSegment) {
 #pragma unroll
-    for (int k = 0; k < kSegment; ++k)
-      twd += k < nv ? wdS[(xw[k >> 2] >> (8 * (k & 3))) & 0xFFu] : 0.0;
+      for (int k = 0; k < kSegment; ++k) twd += wdS[(xw[k >> 2] >> (8 * (k & 3))) & 0xFFu];
+    } else {
+#pragma unroll
+      for (int k = 0; k < kSegment; ++k)
+        twd += k < nv ? wdS[(xw[k >> 2] >> (8 * (k & 3))) & 0xFFu] : 0.0;
+    }
     const unsigned long long tw = static_cast<unsigned long long>(twd);
     // block exclusive scan of the thread sums -> this thread's batch-relative prefix
     unsigned long long incl = tw;
@@ -589,7 +594,7 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
 #pragma unroll
         for (int k = 0; k < kSegment; ++k) {
           const uint32_t st = (xw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-          cd += k < nv ? wdS[st] : 0.0;
+          cd += (nv == kSegment || k < nv) ? wdS[st] : 0.0;
           const unsigned int fn = comb_rank(__fma_rn(cd, n_over_t, est0), c0, cd, cb);
           if (fp < fn && fn > wb32 && fp < wb32 + static_cast<unsigned int>(kWindow))
             marks[(fp > wb32 ? fp : wb32) - wb32] = static_cast<uint16_t>(mark0 + k);
