@@ -88,3 +88,31 @@ def test_mh_statistics_match_oracle_chains(cuda, oracle_lib):
     assert np.all(np.abs(post.chain_means.mean(axis=0) - ref_chain.mean(axis=0)) < 5 * se + 0.05)
     acc_ref = sref[:, 7].sum() / (128 * 3000)
     assert abs(post.acceptance - acc_ref) < 0.02
+
+
+@pytest.mark.parametrize("D", [7, 20_000])
+def test_mh_data_shapes_match_oracle_initial_trace(cuda, oracle_lib, D):
+    """Tiny and large data sets (1 to 4 register groups of points per thread): the initial
+    traces and log-likelihoods equal the oracle's."""
+    import torch
+
+    from oracle import core
+    from paper_2010_08454_b200 import _native as N
+    from paper_2010_08454_b200 import models
+
+    m = models.GaussianMixture.synthetic(n_points=D)
+    L = N.lib()
+    K = m.K
+    y = torch.zeros(L.cuppl_mh_padded_points(D), device=cuda)
+    y[:D] = torch.tensor(m.ys, device=cuda)
+    nc = 40
+    mu = torch.empty((nc, K), device=cuda)
+    ll = torch.empty(nc, device=cuda)
+    st = torch.zeros((nc, 2 * K + 2), dtype=torch.float64, device=cuda)
+    N.check(L.cuppl_mh_gmm(N.ptr(y), D, K, 10.0, 1.0, nc, 0, 0, 0, 1, KEY, N.ptr(mu), N.ptr(ll), N.ptr(st),
+                           None, 0, N.stream_ptr()))
+    mu0, ll0 = mu.cpu().numpy(), ll.cpu().numpy()
+    for c in range(nc):
+        z, mref, lref = core.mh_gmm_init(m.ys, K, 10.0, 1.0, c, KEY)
+        assert np.allclose(mu0[c], mref, rtol=1e-5, atol=1e-4)
+        assert abs(ll0[c] - lref) <= 1e-4 * abs(lref) + 1e-2

@@ -24,7 +24,8 @@ def _gpu_run(model, n, steps, local_world=None, record_ancestors=True, hist_step
     return res, x, lw, anc
 
 
-@pytest.mark.parametrize("n,S,steps", [(100_000, 50, 12), (8 * 1031, 7, 20), (64, 3, 10), (262_144, 50, 5)])
+@pytest.mark.parametrize("n,S,steps", [(100_000, 50, 12), (8 * 1031, 7, 20), (64, 3, 10), (262_144, 50, 5),
+                                       (70_001, 100, 6), (20_000, 256, 4)])
 def test_smc_bit_exact_single_rank(cuda, oracle_lib, n, S, steps):
     from paper_2010_08454_b200 import models
 
