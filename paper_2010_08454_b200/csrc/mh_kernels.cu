@@ -215,8 +215,12 @@ __global__ void __launch_bounds__(kMhMaxThreads, 1) mh_gmm_kernel(const MhArgs a
   };
   // lane c of warp 0: the log-likelihood of chain c from the warp partials (fixed order)
   auto fold = [&]() -> float {
+    float p[kMhMaxThreads / 32];  // independent loads first, then a fixed-order sum
+#pragma unroll
+    for (int w = 0; w < kMhMaxThreads / 32; ++w) p[w] = w < NT / 32 ? parts[w * 32 + lane] : 0.f;
     float s = 0.f;
-    for (int w = 0; w < NT / 32; ++w) s += parts[w * 32 + lane];
+#pragma unroll
+    for (int w = 0; w < kMhMaxThreads / 32; ++w) s += p[w];
     return fmaf(a.neg_half_inv_var, s, a.ll_const);
   };
 
