@@ -219,17 +219,14 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(const __grid_cons
     unsigned long long ws = 0;
     float s1 = 0.f, s2 = 0.f;
     if (!HIST && valid[u] == kSegment) {  // fast path: a full thread slice, no per-particle checks
-      uint32_t whi = 0, wlo = 0;  // 16 * (2^31 >> 4) = 2^31: the high parts fit one u32
 #pragma unroll
       for (int k = 0; k < kSegment; ++k) {
         const uint2 te = wes[(words[k >> 2] >> (8 * (k & 3))) & 0xFFu];
         const float e = __uint_as_float(te.y);
-        whi += te.x >> 4;
-        wlo += te.x & 15u;
+        ws += te.x;
         s1 += e;
         s2 = fmaf(e, e, s2);
       }
-      ws = (static_cast<unsigned long long>(whi) << 4) + wlo;
     } else {
 #pragma unroll
       for (int k = 0; k < kSegment; ++k) {
