@@ -718,8 +718,8 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
         }
       }
       o0 = we;
-      __syncthreads();  // wmax / marks / s_jn reuse
-      if (o0 >= j_next) break;
+      if (o0 >= j_next) break;  // the end-of-batch barrier below orders the reuse
+      __syncthreads();          // wmax / marks / s_jn reuse by the next window
     }
     j_cur = s_jn < jb_hi ? s_jn : jb_hi;
     c_base += btot;
