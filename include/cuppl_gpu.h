@@ -25,8 +25,15 @@
 #ifndef CUPPL_GPU_H
 #define CUPPL_GPU_H
 
+#ifdef __CUDACC_RTC__  /* runtime-compiled model kernels (NVRTC): no libc headers */
+typedef unsigned long long uint64_t;
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef unsigned char uint8_t;
+#else
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -62,6 +69,7 @@ typedef enum cuppl_status {
 #define CUPPL_TAG_MH 5u        /* MH chains (block = step)                    */
 #define CUPPL_TAG_MH_INIT 6u   /* MH initial trace                            */
 #define CUPPL_TAG_DIST 7u      /* batch dist_sample                           */
+#define CUPPL_TAG_DSL 8u       /* runtime-compiled CuPPL models (frontend.py)  */
 
 /* Distribution tags: order of the constructors in pkg/src/cuppl/builtins.py:86-94, plus
  * categorical (absent from the reference catalog). */

@@ -5,8 +5,10 @@
 // SPEC.md:303-329) with the generator replaced by Philox. The CPU
 // oracle (oracle/cuppl_oracle.c) restates every transform here from the same u32 words.
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 #include "../../include/cuppl_gpu.h"
 
 namespace cuppl {

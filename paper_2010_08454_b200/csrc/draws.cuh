@@ -1,0 +1,132 @@
+// draws.cuh — per-particle word streams and the distribution scores, shared by the batch
+// dist kernels (dist_kernels.cu) and the runtime-compiled model kernels (frontend.py, NVRTC).
+//
+// A WordStream replays the reference draw algorithms (pkg/src/cuppl/rng.py:43-117) on the
+// Philox words of blocks (id, 0..), tag: one stream per particle plays the role of
+// Rng.split(i) (rng.py:31-37), and successive sample sites consume it in program order.
+#pragma once
+#include "cuppl_device.cuh"
+
+namespace cuppl {
+
+struct WordStream {
+  PhiloxKey key;
+  uint64_t id;
+  uint32_t tag, blk;
+  uint32_t buf[4];
+  int pos;
+  float spare;
+  bool has_spare;
+
+  __device__ __forceinline__ void init(PhiloxKey k, uint64_t i, uint32_t t) {
+    key = k;
+    id = i;
+    tag = t;
+    blk = 0;
+    pos = 4;
+    has_spare = false;
+    spare = 0.f;
+  }
+  __device__ __forceinline__ uint32_t next() {
+    if (pos == 4) {
+      const uint4 b = draw_block(key, id, blk++, tag);
+      buf[0] = b.x;
+      buf[1] = b.y;
+      buf[2] = b.z;
+      buf[3] = b.w;
+      pos = 0;
+    }
+    return buf[pos++];
+  }
+  __device__ __forceinline__ float uniform() { return u01_closed0(next()); }
+  __device__ __forceinline__ float uniform_pos() { return u01_open0(next()); }
+  __device__ __forceinline__ float normal() {
+    if (has_spare) {
+      has_spare = false;
+      return spare;
+    }
+    const uint32_t wa = next();
+    const uint32_t wb = next();
+    const float2 z = box_muller(wa, wb);
+    spare = z.y;
+    has_spare = true;
+    return z.x;
+  }
+  __device__ __forceinline__ uint32_t randint(uint32_t range) {
+    uint32_t k;
+    while (!lemire(next(), range, &k)) {
+    }
+    return k;
+  }
+  // Marsaglia-Tsang (cuppl/rng.py:79-98); accurate logf for the acceptance test.
+  __device__ float gamma(float shape) {
+    float boost = 1.0f;
+    if (shape < 1.0f) {
+      const float u = uniform_pos();
+      boost = powf(u, 1.0f / shape);
+      shape += 1.0f;
+    }
+    const float d = shape - 1.0f / 3.0f;
+    const float c = 1.0f / sqrtf(9.0f * d);
+    for (;;) {
+      const float x = normal();
+      float v = 1.0f + c * x;
+      if (v <= 0.0f) continue;
+      v = v * v * v;
+      const float u = uniform();
+      if (u < 1.0f - 0.0331f * (x * x) * (x * x)) return d * v * boost;
+      if (u > 0.0f && logf(u) < 0.5f * x * x + d * (1.0f - v + logf(v))) return d * v * boost;
+    }
+  }
+  __device__ int poisson(float lam) {
+    // explicit DFS over the halving tree: same leaf order as the reference recursion
+    float stack[64];
+    int sp = 0;
+    stack[sp++] = lam;
+    int total = 0;
+    while (sp > 0) {
+      const float l = stack[--sp];
+      if (l < 30.0f) {
+        const float limit = expf(-l);
+        int k = 0;
+        float p = uniform();
+        while (p > limit) {
+          ++k;
+          p *= uniform();
+        }
+        total += k;
+      } else {
+        const float half = floorf(l / 2.0f);
+        stack[sp++] = l - half;  // processed second
+        stack[sp++] = half;      // processed first
+      }
+    }
+    return total;
+  }
+};
+
+// Natural-log density / mass; -inf outside the support.
+__device__ __forceinline__ float score_normal(float x, float m, float sd) {
+  const float z = (x - m) / sd;
+  return -0.5f * z * z - logf(sd) - kHalfLog2Pi;
+}
+__device__ __forceinline__ float score_bernoulli(bool v, float p) { return v ? logf(p) : log1pf(-p); }
+__device__ __forceinline__ float score_poisson(int k, float lam) {
+  return k < 0 ? neg_inf_f() : (k == 0 ? 0.f : k * logf(lam)) - lam - lgammaf(k + 1.0f);
+}
+__device__ __forceinline__ float score_uniform_discrete(int k, int a, int b) {
+  return (k >= a && k < b) ? -logf(static_cast<float>(b - a)) : neg_inf_f();
+}
+__device__ __forceinline__ float score_uniform_continuous(float x, float a, float b) {
+  return (x >= a && x <= b) ? -logf(b - a) : neg_inf_f();
+}
+__device__ __forceinline__ float score_beta(float x, float a, float b) {
+  return (x >= 0.f && x <= 1.f)
+             ? (a - 1.f) * logf(x) + (b - 1.f) * log1pf(-x) - (lgammaf(a) + lgammaf(b) - lgammaf(a + b))
+             : neg_inf_f();
+}
+__device__ __forceinline__ float score_exponential(float x, float r) {
+  return x >= 0.f ? logf(r) - r * x : neg_inf_f();
+}
+
+}  // namespace cuppl

@@ -1,0 +1,878 @@
+"""GPU model compiler: CuPPL source -> CUDA C++ -> NVRTC (sm_100a) -> importance sampling.
+
+SURVEY.md §8(f) row 1 (the paper's NVVM code-generation story): a model
+written in CuPPL reaches the GPU without a hand-registered descriptor.
+
+    src = '''
+      xs <- [-1.0, 0.0, 1.0];  ys <- [2.1, 0.9, 0.2];
+      model <- function() {
+        a <- sample(normal(0, 10));
+        b <- sample(normal(0, 10));
+        factor(reduce(function(acc, i) { acc + dist-score(normal(a * xs[i] + b, 1), ys[i]) },
+                      0, repeat(function(i) { i }, length(xs))));
+        [a, b]
+      };
+      importance(model, 100000)
+    '''
+    m = frontend.compile_program(src)
+    post = infer.run_importance(m, 10**8, Rng(1))
+
+Semantics (the reference's importance engine): each particle runs the model
+once; `sample(d)` draws from the prior, `factor(x)` adds x to the log-weight, `observe(d, v)`
+is factor(dist-score(d, v)) (cuppl/desugar.py:37-39). Every particle owns one word stream
+(Philox blocks (pid, 0..), tag CUPPL_TAG_DSL) consumed in program order by the reference draw
+algorithms (rng.py:43-117; csrc/draws.cuh) — the GPU form of rng.split(i).
+
+The compiler is a staged evaluator: the program is evaluated at compile time over symbolic
+values (scalars are C++ expressions, data vectors live in one device buffer, user functions
+and closures are inlined at their call sites), and side effects (draws, factors) are emitted
+as CUDA statements in program order. `repeat` / `map` are fused into the `reduce` that
+consumes them unless they draw, in which case they are materialised in program order into a
+bounded local array. The supported subset is first-order: scalars (real, int, bool), vectors
+of bounded length, no recursion, no unit-returning user functions as values.
+
+The kernel fuses the model with the importance-sampling record (log-sum-exp, ESS, mode,
+moments of the returned components, histogram of a discrete return or of a returned vector's
+length) exactly like the hand-written kernels (csrc/is_accum.cuh).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import math
+from dataclasses import dataclass, field
+from pathlib import Path
+
+import numpy as np
+
+from . import lang
+from .errors import CupError, InferRuntimeError, InvalidDistParamError
+
+CSRC = Path(__file__).resolve().parent / "csrc"
+INCLUDE = Path(__file__).resolve().parent.parent / "include"
+TAG_DSL = 8  # CUPPL_TAG_DSL
+MAX_STATS = 16  # cuppl_is_record.stat_w
+MAX_BINS = 8   # cuppl_is_record.bin_w
+MAX_TRACE_DRAWS = 256
+
+
+class CompileError(CupError):
+    kind = "compile"
+
+
+# ----------------------------------------------------------------------------- values ----
+@dataclass
+class S:
+    """A scalar: C++ expression `code` of type real | int | bool."""
+
+    code: str
+    ty: str
+    pure: bool = True  # no side effects (draws / factors) were needed to produce it
+
+
+@dataclass
+class DataVec:
+    off: int
+    n: int
+
+    def length(self):
+        return S(str(self.n), "int")
+
+    def bound(self):
+        return self.n
+
+    def elem(self, g, i: S):
+        return S(f"__ldg(D + {self.off} + ({i.code}))", "real")
+
+
+@dataclass
+class LocVec:
+    var: str
+    bound_: int
+    length_: S
+    ty: str
+
+    def length(self):
+        return self.length_
+
+    def bound(self):
+        return self.bound_
+
+    def elem(self, g, i: S):
+        return S(f"{self.var}[{i.code}]", self.ty)
+
+
+@dataclass
+class LazyVec:
+    """repeat(f, n) / map(f, v) with a pure element function: elements built on demand."""
+
+    length_: S
+    bound_: int | None
+    gen: object  # callable(compiler, index S) -> value
+
+    def length(self):
+        return self.length_
+
+    def bound(self):
+        return self.bound_
+
+    def elem(self, comp, i: S):
+        return self.gen(comp, i)
+
+
+@dataclass
+class ConstVec:
+    """A vector literal of model values (a returned tuple such as [a, b])."""
+
+    items: list
+
+    def length(self):
+        return S(str(len(self.items)), "int")
+
+    def bound(self):
+        return len(self.items)
+
+
+@dataclass
+class Fn:
+    params: list
+    body: object
+    env: dict
+    name: str = "<lambda>"
+
+
+@dataclass
+class Dist:
+    kind: str
+    args: list
+
+
+_DISTS = {  # name: (arity, sample type)
+    "normal": (2, "real"), "uniform-continuous": (2, "real"), "uniform-discrete": (2, "int"),
+    "bernoulli": (1, "bool"), "beta": (2, "real"), "exponential": (1, "real"), "poisson": (1, "int"),
+}
+_MATH1 = {"exp": "expf", "log": "logf", "sqrt": "sqrtf", "abs": "fabsf", "floor": "floorf"}
+_CMP = {"==", "!=", "<", "<=", ">", ">="}
+
+
+# ----------------------------------------------------------------------------- codegen ---
+class _Gen:
+    def __init__(self, data: list):
+        self.lines: list[str] = []
+        self.ind = 2
+        self.n = 0
+        self.data = data  # flat float list of all data vectors
+        self.draw_bound = 0  # upper bound of sample calls per particle
+        self.loop_mult = [1]
+        self.depth = 0
+        self.bounds: dict = {}  # C variable of a uniform-discrete draw -> largest value
+
+    def fresh(self, p="t"):
+        self.n += 1
+        return f"{p}{self.n}"
+
+    def emit(self, line: str):
+        self.lines.append(" " * self.ind + line)
+
+    def open(self, head: str):
+        self.emit(head + " {")
+        self.ind += 2
+
+    def close(self):
+        self.ind -= 2
+        self.emit("}")
+
+    def let(self, v: S, hint="t") -> S:
+        if v.code.isidentifier() or _is_literal(v.code):
+            return v
+        name = self.fresh(hint)
+        self.emit(f"const {_cty(v.ty)} {name} = {v.code};")
+        return S(name, v.ty, v.pure)
+
+
+def _cty(ty):
+    return {"real": "float", "int": "int", "bool": "bool"}[ty]
+
+
+def _is_literal(code: str) -> bool:
+    try:
+        float(code.rstrip("f"))
+        return True
+    except ValueError:
+        return code in ("true", "false")
+
+
+def _lit(v) -> S:
+    if isinstance(v, bool):
+        return S("true" if v else "false", "bool")
+    if isinstance(v, int):
+        return S(str(v), "int")
+    return S(repr(float(np.float32(v))) + "f", "real")
+
+
+def _real(v: S) -> str:
+    return f"static_cast<float>({v.code})" if v.ty != "real" else v.code
+
+
+def _scalar(v, what) -> S:
+    if not isinstance(v, S):
+        raise CompileError(f"{what}: expected a scalar, got {type(v).__name__}")
+    return v
+
+
+class _Compiler:
+    def __init__(self, prog: lang.Program, data: dict | None):
+        self.prog = prog
+        self.g = _Gen([])
+        self.globals: dict = {}
+        self.external = dict(data or {})
+        self.model = None
+        self.default_n = None
+
+    # -------------------------------------------------------------- top level ----
+    def _data_vec(self, values) -> DataVec:
+        arr = np.asarray(values, dtype=np.float64).reshape(-1)
+        off = len(self.g.data)
+        self.g.data.extend(np.float32(arr).tolist())
+        return DataVec(off, len(arr))
+
+    def top(self):
+        for name, e in self.prog.bindings:
+            self.globals[name] = self._global_value(name, e)
+        res = self.prog.result
+        if not (isinstance(res, lang.Call) and isinstance(res.fn, lang.Var) and res.fn.name == "importance"):
+            raise CompileError("the program result must be importance(model, n) (mcmc / enumerate run on "
+                               "the registered engines)")
+        if len(res.args) != 2:
+            raise CompileError("importance takes (model, n)")
+        m = self._global_value("<model>", res.args[0])
+        if not isinstance(m, Fn) or m.params:
+            raise CompileError("importance's first argument must be a zero-argument model function")
+        n = self._global_value("<n>", res.args[1])
+        if not (isinstance(n, S) and n.ty == "int" and _is_literal(n.code)):
+            raise CompileError("importance's sample count must be an integer constant")
+        self.model, self.default_n = m, int(n.code)
+
+    def _global_value(self, name, e):
+        if isinstance(e, lang.VecLit):
+            vals = []
+            for x in e.elems:
+                v = self._global_value(name, x)
+                if not (isinstance(v, S) and _is_literal(v.code)):
+                    raise CompileError(f"top-level vector {name} must hold numeric constants")
+                vals.append(float(v.code.rstrip("f")) if v.code not in ("true", "false") else float(v.code == "true"))
+            return self._data_vec(vals)
+        if isinstance(e, lang.Num):
+            return _lit(e.value)
+        if isinstance(e, lang.Bool):
+            return _lit(e.value)
+        if isinstance(e, lang.Unary) and e.op == "-" and isinstance(e.arg, lang.Num):
+            return _lit(-e.arg.value)
+        if isinstance(e, lang.Lambda):
+            return Fn(e.params, e.body, self.globals, name)
+        if isinstance(e, lang.Var):
+            return self._lookup(e.name, self.globals)
+        raise CompileError(f"top-level binding {name}: only constants, numeric vectors and functions "
+                           "are supported outside the model")
+
+    def _lookup(self, name, env):
+        if name in env:
+            return env[name]
+        if name in self.globals:
+            return self.globals[name]
+        if name in self.external:
+            v = self._data_vec(self.external.pop(name))
+            self.globals[name] = v
+            return v
+        raise CompileError(f"unbound variable {name}")
+
+    # -------------------------------------------------------------- expressions --
+    def ev(self, e, env):
+        g = self.g
+        if isinstance(e, lang.Num):
+            return _lit(e.value)
+        if isinstance(e, lang.Bool):
+            return _lit(e.value)
+        if isinstance(e, lang.Var):
+            if e.name in _DISTS or e.name in _MATH1:
+                raise CompileError(f"builtin {e.name} must be applied")
+            return self._lookup(e.name, env)
+        if isinstance(e, lang.Lambda):
+            return Fn(e.params, e.body, dict(env))
+        if isinstance(e, lang.Block):
+            env = dict(env)
+            for name, rhs in e.stmts:
+                v = self.ev(rhs, env)
+                if isinstance(v, S) and not v.pure:
+                    v = g.let(v)
+                if name is not None:
+                    env[name] = g.let(v, "v") if isinstance(v, S) else v
+            return self.ev(e.result, env)
+        if isinstance(e, lang.Unary):
+            a = _scalar(self.ev(e.arg, env), e.op)
+            if e.op == "-":
+                return S(f"(-{a.code})", a.ty if a.ty != "bool" else "int", a.pure)
+            return S(f"(!{a.code})", "bool", a.pure)
+        if isinstance(e, lang.BinOp):
+            return self._binop(e, env)
+        if isinstance(e, lang.If):
+            return self._if(e, env)
+        if isinstance(e, lang.Index):
+            v = self.ev(e.vec, env)
+            i = _scalar(self.ev(e.idx, env), "index")
+            if i.ty != "int":
+                raise CompileError("vector index must be an int")
+            if isinstance(v, ConstVec):
+                if not _is_literal(i.code):
+                    raise CompileError("a vector literal of model values is indexed by constants only")
+                return v.items[int(i.code)]
+            if not hasattr(v, "elem"):
+                raise CompileError("indexing a non-vector")
+            return v.elem(self, i)
+        if isinstance(e, lang.VecLit):
+            items = [self.ev(x, env) for x in e.elems]
+            if all(isinstance(x, S) and _is_literal(x.code) for x in items):
+                return self._data_vec([float(x.code.rstrip("f")) if x.ty != "bool" else float(x.code == "true")
+                                       for x in items])
+            return ConstVec([_scalar(x, "vector element") for x in items])
+        if isinstance(e, lang.Call):
+            return self._call(e, env)
+        raise CompileError(f"unsupported expression {type(e).__name__}")
+
+    def _binop(self, e, env):
+        a = _scalar(self.ev(e.lhs, env), e.op)
+        b = _scalar(self.ev(e.rhs, env), e.op)
+        pure = a.pure and b.pure
+        if e.op in ("&&", "||"):
+            return S(f"({a.code} {e.op} {b.code})", "bool", pure)
+        if e.op in _CMP:
+            if "real" in (a.ty, b.ty):
+                return S(f"({_real(a)} {e.op} {_real(b)})", "bool", pure)
+            return S(f"({a.code} {e.op} {b.code})", "bool", pure)
+        if a.ty == "int" and b.ty == "int":
+            return S(f"({a.code} {e.op} {b.code})", "int", pure)
+        if e.op == "%":
+            return S(f"fmodf({_real(a)}, {_real(b)})", "real", pure)
+        return S(f"({_real(a)} {e.op} {_real(b)})", "real", pure)
+
+    def _if(self, e, env):
+        g = self.g
+        c = _scalar(self.ev(e.cond, env), "if condition")
+        mark = len(g.lines)
+        t = self.ev(e.then, dict(env))
+        f = self.ev(e.orelse, dict(env))
+        if len(g.lines) == mark and isinstance(t, S) and isinstance(f, S) and t.pure and f.pure:
+            ty = "real" if "real" in (t.ty, f.ty) else t.ty
+            tc, fc = (_real(t), _real(f)) if ty == "real" else (t.code, f.code)
+            return S(f"({c.code} ? {tc} : {fc})", ty, c.pure)
+        # side effects in a branch: emit real control flow (draws happen on the taken path only)
+        del g.lines[mark:]
+        res = g.fresh("r")
+        g.emit(f"float {res} = 0.f;")
+        g.open(f"if ({c.code})")
+        t = self.ev(e.then, dict(env))
+        tt = t.ty if isinstance(t, S) else None
+        if isinstance(t, S):
+            g.emit(f"{res} = {_real(t)};")
+        g.close()
+        g.open("else")
+        f = self.ev(e.orelse, dict(env))
+        if isinstance(f, S):
+            g.emit(f"{res} = {_real(f)};")
+        g.close()
+        if tt is None:
+            return None
+        ty = "real" if "real" in (tt, f.ty) else tt
+        return S(res if ty == "real" else f"static_cast<{_cty(ty)}>({res})", ty, False)
+
+    # -------------------------------------------------------------- calls --------
+    def _call(self, e, env):
+        g = self.g
+        if isinstance(e.fn, lang.Var) and e.fn.name not in env and e.fn.name not in self.globals:
+            name = e.fn.name
+            if name in _DISTS:
+                arity, _ = _DISTS[name]
+                if len(e.args) != arity:
+                    raise CompileError(f"{name} takes {arity} argument(s)")
+                return Dist(name, [_scalar(self.ev(a, env), name) for a in e.args])
+            if name in ("sample", "sample*"):
+                d = self.ev(e.args[0], env)
+                if not isinstance(d, Dist):
+                    raise CompileError("sample expects a distribution")
+                return self._sample(d)
+            if name == "factor":
+                x = _scalar(self.ev(e.args[0], env), "factor")
+                g.emit(f"lw += {_real(x)};")
+                return None
+            if name == "observe":
+                d = self.ev(e.args[0], env)
+                v = _scalar(self.ev(e.args[1], env), "observe")
+                g.emit(f"lw += {self._score(d, v)};")
+                return None
+            if name == "dist-score":
+                d = self.ev(e.args[0], env)
+                v = _scalar(self.ev(e.args[1], env), "dist-score")
+                return S(self._score(d, v), "real")
+            if name in _MATH1:
+                x = _scalar(self.ev(e.args[0], env), name)
+                return S(f"{_MATH1[name]}({_real(x)})", "real", x.pure)
+            if name == "pow":
+                a, b = (_scalar(self.ev(x, env), "pow") for x in e.args)
+                return S(f"powf({_real(a)}, {_real(b)})", "real", a.pure and b.pure)
+            if name == "to-real":
+                x = _scalar(self.ev(e.args[0], env), name)
+                return S(_real(x), "real", x.pure)
+            if name == "to-int":
+                x = _scalar(self.ev(e.args[0], env), name)
+                return S(f"static_cast<int>({x.code})", "int", x.pure)
+            if name == "length":
+                v = self.ev(e.args[0], env)
+                return v.length()
+            if name == "repeat":
+                return self._repeat(e, env)
+            if name == "map":
+                return self._map(e, env)
+            if name == "reduce":
+                return self._reduce(e, env)
+            raise CompileError(f"{name} is not supported in GPU models")
+        f = self.ev(e.fn, env)
+        if not isinstance(f, Fn):
+            raise CompileError("calling a non-function")
+        return self._apply(f, [self.ev(a, env) for a in e.args])
+
+    def _apply(self, f: Fn, args):
+        if len(args) != len(f.params):
+            raise CompileError(f"{f.name} takes {len(f.params)} argument(s)")
+        self.g.depth += 1
+        if self.g.depth > 64:
+            raise CompileError("recursion is not supported in GPU models")
+        env = dict(f.env)
+        for p, a in zip(f.params, args):
+            env[p] = self.g.let(a, "a") if isinstance(a, S) else a
+        try:
+            return self.ev(f.body, env)
+        finally:
+            self.g.depth -= 1
+
+    def _sample(self, d: Dist) -> S:
+        g = self.g
+        g.draw_bound += g.loop_mult[-1]
+        a = [g.let(x) for x in d.args]
+        v = g.fresh("x")
+        k = d.kind
+        if k == "normal":
+            g.emit(f"const float {v} = {_real(a[0])} + {_real(a[1])} * ws.normal();")
+        elif k == "uniform-continuous":
+            g.emit(f"const float {v} = {_real(a[0])} + ({_real(a[1])} - {_real(a[0])}) * ws.uniform();")
+        elif k == "uniform-discrete":
+            g.emit(f"if (!({a[1].code} > {a[0].code})) err |= 1u;")
+            g.emit(f"const int {v} = {a[0].code} + static_cast<int>(ws.randint(static_cast<unsigned>("
+                   f"{a[1].code} > {a[0].code} ? {a[1].code} - {a[0].code} : 1)));")
+        elif k == "bernoulli":
+            g.emit(f"const bool {v} = ws.uniform() < {_real(a[0])};")
+        elif k == "beta":
+            gx, gy = g.fresh("gx"), g.fresh("gy")
+            g.emit(f"const float {gx} = ws.gamma({_real(a[0])});")
+            g.emit(f"const float {gy} = ws.gamma({_real(a[1])});")
+            g.emit(f"const float {v} = {gx} / ({gx} + {gy});")
+        elif k == "exponential":
+            g.emit(f"const float {v} = -logf(ws.uniform_pos()) / {_real(a[0])};")
+        elif k == "poisson":
+            g.emit(f"const int {v} = ws.poisson({_real(a[0])});")
+        if k == "uniform-discrete" and _is_literal(a[1].code):
+            g.bounds[v] = max(int(a[1].code) - 1, 0)
+        ty = _DISTS[k][1]
+        g.emit(f"if (draws_out && nd < MAXD) draws_out[idx * MAXD + nd] = static_cast<float>({v});")
+        g.emit("++nd;")
+        return S(v, ty, False)
+
+    def _score(self, d, v: S) -> str:
+        if not isinstance(d, Dist):
+            raise CompileError("dist-score / observe expect a distribution")
+        a = d.args
+        k = d.kind
+        if k == "normal":
+            return f"score_normal({_real(v)}, {_real(a[0])}, {_real(a[1])})"
+        if k == "uniform-continuous":
+            return f"score_uniform_continuous({_real(v)}, {_real(a[0])}, {_real(a[1])})"
+        if k == "uniform-discrete":
+            return f"score_uniform_discrete({v.code}, {a[0].code}, {a[1].code})"
+        if k == "bernoulli":
+            return f"score_bernoulli({v.code}, {_real(a[0])})"
+        if k == "beta":
+            return f"score_beta({_real(v)}, {_real(a[0])}, {_real(a[1])})"
+        if k == "exponential":
+            return f"score_exponential({_real(v)}, {_real(a[0])})"
+        return f"score_poisson({v.code}, {_real(a[0])})"
+
+    def _repeat(self, e, env):
+        g = self.g
+        f = self.ev(e.args[0], env)
+        n = _scalar(self.ev(e.args[1], env), "repeat length")
+        if not isinstance(f, Fn) or len(f.params) != 1:
+            raise CompileError("repeat expects a one-argument function")
+        n = g.let(n, "n")
+        bound = self._bound_of(n)
+        # a pure element function is fused into its consumer; one that draws is evaluated now,
+        # in order, into a bounded local array (the reference evaluates repeat eagerly)
+        if not self._effects(f.body, f.env):
+            return LazyVec(n, bound, lambda comp, i: comp._apply(f, [i]))
+        probe_v = self._sandbox()._apply(f, [S("i_probe", "int")])
+        if bound is None:
+            raise CompileError("a repeat that draws needs a bounded length (constant, data length or a "
+                               "uniform-discrete draw)")
+        arr, i = g.fresh("vec"), g.fresh("i")
+        ty = probe_v.ty if isinstance(probe_v, S) else "real"
+        g.emit(f"{_cty(ty)} {arr}[{bound}];")
+        g.open(f"for (int {i} = 0; {i} < {n.code}; ++{i})")
+        g.loop_mult.append(g.loop_mult[-1] * bound)
+        v = self._apply(f, [S(i, "int")])
+        g.loop_mult.pop()
+        g.emit(f"{arr}[{i}] = {v.code};")
+        g.close()
+        return LocVec(arr, bound, n, ty)
+
+    def _bound_of(self, n: S):
+        if _is_literal(n.code) and n.ty == "int":
+            return int(n.code)
+        return self.g.bounds.get(n.code)
+
+    def _map(self, e, env):
+        g = self.g
+        f = self.ev(e.args[0], env)
+        v = self.ev(e.args[1], env)
+        if not isinstance(f, Fn) or len(f.params) != 1 or not hasattr(v, "elem"):
+            raise CompileError("map expects (function, vector)")
+        if not self._effects(f.body, f.env):
+            return LazyVec(v.length(), v.bound(), lambda comp, i: comp._apply(f, [v.elem(comp, i)]))
+        # effects: evaluated now, element by element in order (the reference's eager map)
+        bound = v.bound()
+        probe = self._sandbox()._apply(f, [v.elem(self._sandbox(), S("i_probe", "int"))])
+        keep = isinstance(probe, S) and bound is not None
+        arr, i = g.fresh("vec"), g.fresh("i")
+        if keep:
+            g.emit(f"{_cty(probe.ty)} {arr}[{bound}];")
+        g.open(f"for (int {i} = 0; {i} < {v.length().code}; ++{i})")
+        g.loop_mult.append(g.loop_mult[-1] * (bound or 1))
+        r = self._apply(f, [v.elem(self, S(i, "int"))])
+        g.loop_mult.pop()
+        if keep:
+            g.emit(f"{arr}[{i}] = {r.code};")
+        g.close()
+        return LocVec(arr, bound, v.length(), probe.ty) if keep else None
+
+    def _reduce(self, e, env):
+        g = self.g
+        f = self.ev(e.args[0], env)
+        init = _scalar(self.ev(e.args[1], env), "reduce init")
+        v = self.ev(e.args[2], env)
+        if not isinstance(f, Fn) or len(f.params) != 2 or not hasattr(v, "elem"):
+            raise CompileError("reduce expects (function(acc, x), init, vector)")
+        acc, i = g.fresh("acc"), g.fresh("i")
+        # the accumulator type is the body's type given a real (or int) accumulator
+        ty = "real" if init.ty == "real" else init.ty
+        sb = self._sandbox()
+        r = sb._apply(f, [S("acc_probe", ty), v.elem(sb, S("i_probe", "int"))])
+        if isinstance(r, S) and r.ty == "real":
+            ty = "real"
+        g.emit(f"{_cty(ty)} {acc} = {init.code if ty != 'real' else _real(init)};")
+        n = v.length()
+        bound = v.bound() or 1
+        g.open(f"for (int {i} = 0; {i} < {n.code}; ++{i})")
+        g.loop_mult.append(g.loop_mult[-1] * bound)
+        x = v.elem(self, S(i, "int"))
+        r = self._apply(f, [S(acc, ty), x])
+        g.loop_mult.pop()
+        g.emit(f"{acc} = {r.code if ty != 'real' else _real(r)};")
+        g.close()
+        return S(acc, ty, False)
+
+    # -------------------------------------------------------------- helpers ----
+    def _sandbox(self):
+        """A throwaway copy for type probes: nothing it emits or binds reaches this compiler."""
+        c = _Compiler.__new__(_Compiler)
+        c.prog, c.model, c.default_n = self.prog, self.model, self.default_n
+        c.globals, c.external = dict(self.globals), dict(self.external)
+        c.g = _Gen(list(self.g.data))
+        c.g.n, c.g.bounds = self.g.n, dict(self.g.bounds)
+        return c
+
+    def _effects(self, node, env, seen=None) -> bool:
+        """Conservative: does evaluating `node` draw or add to the log-weight?"""
+        seen = seen if seen is not None else set()
+        if isinstance(node, lang.Call):
+            if isinstance(node.fn, lang.Var):
+                name = node.fn.name
+                if name in ("sample", "sample*", "factor", "observe"):
+                    return True
+                f = env.get(name, self.globals.get(name))
+                if isinstance(f, Fn) and id(f) not in seen:
+                    seen.add(id(f))
+                    if self._effects(f.body, f.env, seen):
+                        return True
+            return any(self._effects(x, env, seen) for x in [node.fn] + node.args)
+        if isinstance(node, lang.Var):
+            f = env.get(node.name, self.globals.get(node.name))
+            if isinstance(f, Fn) and id(f) not in seen:
+                seen.add(id(f))
+                return self._effects(f.body, f.env, seen)
+            return False
+        if isinstance(node, (list, tuple)):
+            return any(self._effects(x, env, seen) for x in node)
+        if hasattr(node, "__dataclass_fields__"):
+            return any(self._effects(getattr(node, k), env, seen) for k in node.__dataclass_fields__)
+        return False
+
+    # -------------------------------------------------------------- the model ----
+    def compile(self):
+        self.top()
+        self.g.bounds = {}
+        return self._apply(self.model, [])
+
+
+@dataclass
+class CompiledModel:
+    """A CuPPL model compiled for the GPU (importance sampling)."""
+
+    source: str
+    cuda: str
+    data: np.ndarray
+    n_stats: int
+    n_bins: int
+    stat_names: list
+    return_kind: str  # "real" | "int" | "bool" | "vector" | "none"
+    return_width: int
+    max_draws: int
+    default_n: int
+    kind: str = "dsl"
+    _fn: object = field(default=None, repr=False)
+
+
+_KERNEL = r'''
+#include "draws.cuh"
+#include "is_accum.cuh"
+using namespace cuppl;
+#define MAXD {maxd}
+extern "C" __global__ void __launch_bounds__(256)
+cuppl_dsl_model(const float* __restrict__ D, unsigned long long pid_begin, unsigned long long n,
+                unsigned int k0, unsigned int k1, cuppl_is_record* block_recs, unsigned int* counter,
+                cuppl_is_record* rec_out, float* lw_out, float* draws_out, float* ret_out,
+                unsigned int* err_out) {{
+  ThreadAcc<{ns}, {nb}> acc;
+  acc.init();
+  const PhiloxKey key{{k0, k1}};
+  unsigned int err = 0u;
+  for (unsigned long long idx = blockIdx.x * 256ull + threadIdx.x; idx < n;
+       idx += static_cast<unsigned long long>(gridDim.x) * 256ull) {{
+    const unsigned long long pid = pid_begin + idx;
+    WordStream ws;
+    ws.init(key, pid, {tag}u);
+    float lw = 0.f;
+    int nd = 0;
+{body}
+    float f[{ns_arr}] = {{{stats}}};
+    acc.add(lw, pid, f, {bin});
+    if (lw_out) lw_out[idx] = lw;
+    if (ret_out) {{
+{ret_store}
+    }}
+    (void)nd;
+  }}
+  if (err) atomicOr(err_out, err);
+  is_epilogue(acc, block_recs, counter, rec_out);
+}}
+'''
+
+
+def _return_parts(ret, g: _Gen):
+    """(stat expressions, stat names, bin expression, n_bins, kind, width, store lines)."""
+    if ret is None:
+        return [], [], "0", 0, "none", 0, []
+    if isinstance(ret, S):
+        v = g.let(ret, "ret")
+        st = [_real(v), f"{_real(v)} * {_real(v)}"]
+        if ret.ty in ("int", "bool"):
+            b = f"(({v.code}) >= 0 && ({v.code}) < {MAX_BINS} ? static_cast<int>({v.code}) : -1)"
+            return st, ["value", "value^2"], b, MAX_BINS, ret.ty, 1, [f"ret_out[idx] = {_real(v)};"]
+        return st, ["value", "value^2"], "0", 0, "real", 1, [f"ret_out[idx] = {_real(v)};"]
+    if isinstance(ret, ConstVec):
+        items = [g.let(x, "ret") for x in ret.items]
+        if 2 * len(items) > MAX_STATS:
+            raise CompileError(f"at most {MAX_STATS // 2} returned components")
+        st = [_real(x) for x in items] + [f"{_real(x)} * {_real(x)}" for x in items]
+        names = [f"v{k}" for k in range(len(items))] + [f"v{k}^2" for k in range(len(items))]
+        store = [f"ret_out[idx * {len(items)} + {k}] = {_real(x)};" for k, x in enumerate(items)]
+        return st, names, "0", 0, "vector", len(items), store
+    if isinstance(ret, LocVec):
+        if ret.bound_ > MAX_STATS // 2:
+            raise CompileError(f"returned vectors are bounded by {MAX_STATS // 2} elements")
+        comps = [f"({k} < {ret.length_.code} ? static_cast<float>({ret.var}[{k}]) : 0.f)" for k in range(ret.bound_)]
+        names = [f"v{k}" for k in range(ret.bound_)]
+        b = f"(({ret.length_.code}) >= 0 && ({ret.length_.code}) < {MAX_BINS} ? ({ret.length_.code}) : -1)"
+        store = [f"ret_out[idx * {ret.bound_ + 1} + {k}] = {c};" for k, c in enumerate(comps)]
+        store.append(f"ret_out[idx * {ret.bound_ + 1} + {ret.bound_}] = static_cast<float>({ret.length_.code});")
+        return comps, names, b, MAX_BINS, "vector", ret.bound_ + 1, store
+    raise CompileError(f"unsupported return value {type(ret).__name__}")
+
+
+def compile_program(source: str, data: dict | None = None) -> CompiledModel:
+    """Parse and compile a CuPPL program whose result is importance(model, n)."""
+    prog = lang.parse(source)
+    comp = _Compiler(prog, data)
+    ret = comp.compile()
+    g = comp.g
+    stats, names, bin_expr, nb, kind, width, store = _return_parts(ret, g)
+    maxd = g.draw_bound if 0 < g.draw_bound <= MAX_TRACE_DRAWS else 1
+    body = "\n".join("  " + line for line in g.lines)
+    cuda = _KERNEL.format(maxd=maxd, ns=len(stats), nb=nb, ns_arr=max(len(stats), 1),
+                          stats=", ".join(stats) if stats else "0.f", bin=bin_expr, tag=TAG_DSL,
+                          body=body, ret_store="\n".join("      " + s for s in store))
+    data_arr = np.asarray(g.data if g.data else [0.0], dtype=np.float32)
+    return CompiledModel(source=source, cuda=cuda, data=data_arr, n_stats=len(stats), n_bins=nb,
+                         stat_names=names, return_kind=kind, return_width=width,
+                         max_draws=g.draw_bound, default_n=comp.default_n)
+
+
+# ----------------------------------------------------------------------------- JIT -------
+_MODULES: dict = {}
+
+
+def _nvrtc_cubin(src: str) -> bytes:
+    from cuda.bindings import nvrtc
+
+    def ok(r, what):
+        err = r[0]
+        if err != nvrtc.nvrtcResult.NVRTC_SUCCESS:
+            raise InferRuntimeError(f"NVRTC {what} failed: {err}")
+        return r[1:] if len(r) > 2 else (r[1] if len(r) == 2 else None)
+
+    prog = ok(nvrtc.nvrtcCreateProgram(src.encode(), b"cuppl_model.cu", 0, [], []), "create")
+    opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-lineinfo", b"-default-device",
+            f"-I{CSRC}".encode(), f"-I{INCLUDE}".encode()]
+    r = nvrtc.nvrtcCompileProgram(prog, len(opts), opts)
+    if r[0] != nvrtc.nvrtcResult.NVRTC_SUCCESS:
+        size = ok(nvrtc.nvrtcGetProgramLogSize(prog), "log size")
+        log = b" " * size
+        nvrtc.nvrtcGetProgramLog(prog, log)
+        raise CompileError("NVRTC compilation failed:\n" + log.decode(errors="replace"))
+    size = ok(nvrtc.nvrtcGetCUBINSize(prog), "cubin size")
+    cubin = b" " * size
+    ok(nvrtc.nvrtcGetCUBIN(prog, cubin), "cubin")
+    nvrtc.nvrtcDestroyProgram(prog)
+    return cubin
+
+
+def _function(model: CompiledModel):
+    """Load (once per process and source) the compiled kernel; returns a CUfunction."""
+    from cuda.bindings import driver as cu
+
+    h = hashlib.sha256(model.cuda.encode()).hexdigest()
+    if h not in _MODULES:
+        import torch
+
+        torch.cuda.init()  # the primary context torch uses is current for the driver calls
+        cubin = _nvrtc_cubin(model.cuda)
+        err, mod = cu.cuModuleLoadData(cubin)
+        if err != cu.CUresult.CUDA_SUCCESS:
+            raise InferRuntimeError(f"cuModuleLoadData failed: {err}")
+        err, fn = cu.cuModuleGetFunction(mod, b"cuppl_dsl_model")
+        if err != cu.CUresult.CUDA_SUCCESS:
+            raise InferRuntimeError(f"cuModuleGetFunction failed: {err}")
+        _MODULES[h] = (mod, fn)
+    return _MODULES[h][1]
+
+
+class DslLauncher:
+    """Launcher of a compiled model with the IsLauncher interface (launch(lo, hi, key, ...),
+    .rec): infer.run_importance shards and merges it like the hand-written kernels."""
+
+    def __init__(self, model: CompiledModel, device=None):
+        import torch
+
+        from . import _native as N
+
+        self.model = model
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        props = torch.cuda.get_device_properties(self.device)
+        self.sms = props.multi_processor_count
+        self.max_grid = self.sms * 8
+        self.data = torch.from_numpy(model.data).to(self.device)
+        self.ws = torch.zeros(256 + self.max_grid * N.REC_BYTES, dtype=torch.uint8, device=self.device)
+        self.rec = torch.empty(N.REC_BYTES, dtype=torch.uint8, device=self.device)
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.fn = _function(model)
+
+    def launch(self, pid_begin: int, pid_end: int, key: int, lw_out=None, draws_out=None, ret_out=None,
+               rec_out=None, stream=None, **_):
+        import torch
+        from cuda.bindings import driver as cu
+
+        from . import _native as N
+
+        n = pid_end - pid_begin
+        if n <= 0:
+            raise ValueError("empty particle range")
+        grid = int(min(self.max_grid, (n + 255) // 256))
+        rec = self.rec if rec_out is None else rec_out
+        counter = self.ws[:4]
+        blocks = self.ws[256:]
+        st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        vals = [C.c_uint64(self.data.data_ptr()), C.c_uint64(pid_begin), C.c_uint64(n),
+                C.c_uint32(key & 0xFFFFFFFF), C.c_uint32(key >> 32), C.c_uint64(blocks.data_ptr()),
+                C.c_uint64(counter.data_ptr()), C.c_uint64(rec.data_ptr()), C.c_uint64(N.ptr(lw_out) or 0),
+                C.c_uint64(N.ptr(draws_out) or 0), C.c_uint64(N.ptr(ret_out) or 0),
+                C.c_uint64(self.err.data_ptr())]
+        ptrs = (C.c_void_p * len(vals))(*[C.addressof(v) for v in vals])
+        err, = cu.cuLaunchKernel(self.fn, grid, 1, 1, 256, 1, 1, 0, st, C.addressof(ptrs), 0)
+        if err != cu.CUresult.CUDA_SUCCESS:
+            raise InferRuntimeError(f"cuLaunchKernel failed: {err}")
+
+    def check_errors(self):
+        if int(self.err.item()):
+            self.err.zero_()
+            raise InvalidDistParamError("uniform-discrete(a, b) needs b > a (SPEC.md:347)")
+
+    def trace_of(self, pid: int, key: int):
+        """Return value of one particle (re-executed: the streams are counter-based)."""
+        import torch
+
+        w = max(self.model.return_width, 1)
+        out = torch.empty(w, dtype=torch.float32, device=self.device)
+        rec = torch.empty_like(self.rec)
+        self.launch(pid, pid + 1, key, ret_out=out, rec_out=rec)
+        v = out.cpu().numpy().astype(float).tolist()
+        k = self.model.return_kind
+        if k in ("int", "bool"):
+            return int(v[0]) if k == "int" else bool(v[0])
+        if k == "real":
+            return v[0]
+        if k == "vector" and self.model.n_bins:  # bounded vector: components then length
+            return v[:int(v[-1])]
+        return v
+
+
+def distribution_from_record(model: CompiledModel, rec, n: int, launcher: DslLauncher, key: int):
+    """EmpiricalDistribution of a compiled model from its merged record."""
+    from .errors import AllZeroWeightError
+    from .infer import EmpiricalDistribution, record_to_dict
+
+    if rec.n_finite == 0:
+        raise AllZeroWeightError("every particle has log-weight -inf (SPEC.md:421)")
+    S_, S2, M = rec.sum_w, rec.sum_w2, rec.max_lw
+    out = EmpiricalDistribution(n=n, record=record_to_dict(rec))
+    out.log_z = M + math.log(S_) - math.log(n)
+    out.ess = S_ * S_ / S2
+    out.mode_log_weight = rec.argmax_lw
+    out.mode_index = int(rec.argmax_pid)
+    out.mode = launcher.trace_of(out.mode_index, key)
+    st = np.array(rec.stat_w[:model.n_stats]) / S_
+    out.mean = {name: float(v) for name, v in zip(model.stat_names, st) if not name.endswith("^2")}
+    half = model.n_stats // 2
+    if model.stat_names and model.stat_names[-1].endswith("^2"):
+        out.stats = {f"var_{model.stat_names[k]}": float(st[half + k] - st[k] ** 2) for k in range(half)}
+    if model.n_bins:
+        bins = np.array(rec.bin_w[:model.n_bins]) / S_
+        conv = bool if model.return_kind == "bool" else int
+        out.support = [(conv(k), float(p)) for k, p in enumerate(bins) if p > 0]
+    return out

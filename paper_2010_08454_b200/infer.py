@@ -301,6 +301,10 @@ def run_importance(model, n_samples: int, rng, *, return_traces: bool = False, g
 
     if n_samples < 1:
         raise ValueError("n_samples must be >= 1")
+    from .frontend import CompiledModel
+
+    if isinstance(model, CompiledModel):
+        return _run_compiled(model, n_samples, rng, return_traces=return_traces, group=group, device=device)
     if not isinstance(model, (PolyRegression, LinearRegression)):
         raise InferRuntimeError(f"no importance-sampling kernel for {type(model).__name__}")
     rank, world = _world(group)
@@ -327,3 +331,33 @@ def run_importance(model, n_samples: int, rng, *, return_traces: bool = False, g
         raise
     rec = merge_records(recs)
     return _distribution_from_record(model, rec, n_samples, launcher, key, traces)
+
+
+def _run_compiled(model, n_samples: int, rng, *, return_traces: bool, group, device) -> EmpiricalDistribution:
+    """run_importance for a model compiled from CuPPL source (frontend.py, NVRTC)."""
+    import torch
+
+    from .frontend import MAX_TRACE_DRAWS, DslLauncher, distribution_from_record
+
+    rank, world = _world(group)
+    lo, hi = shard_range(n_samples, rank, world)
+    key = key_of(rng)
+    launcher = DslLauncher(model, device)
+    traces, lw, draws = {}, None, None
+    if return_traces:
+        n_local = hi - lo
+        lw = torch.empty(n_local, dtype=torch.float32, device=launcher.device)
+        traces = {"log_weight": lw, "pid_begin": lo}
+        if 0 < model.max_draws <= MAX_TRACE_DRAWS:
+            draws = torch.zeros((n_local, model.max_draws), dtype=torch.float32, device=launcher.device)
+            traces["draws"] = draws
+    try:
+        launcher.launch(lo, hi, key, lw_out=lw, draws_out=draws)
+        recs = _gather_records(launcher.rec, group)
+        launcher.check_errors()
+    except InferRuntimeError as e:
+        e.seed = seed_of(rng)
+        raise
+    out = distribution_from_record(model, merge_records(recs), n_samples, launcher, key)
+    out.traces = traces
+    return out
