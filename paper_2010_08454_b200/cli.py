@@ -4,11 +4,11 @@ pkg/pyproject.toml:16), over this package's GPU engines.
     python -m paper_2010_08454_b200 run --model poly --samples 100000 --seed 1 --format tsv
     python -m paper_2010_08454_b200 bench --filter smc --repeats 3
 
-The reference's `run <file.cup>` compiles a CuPPL program; that front end (lexer .. lowering)
-is out of this build's scope, so `run` takes one of the registered
-model descriptors instead (`--model poly | linreg | gmm | hmm`, the BASELINE.json configs) and
-keeps the reference's flags, defaults and exit codes: 0 success, 1 usage / configuration
-error, 2 runtime (inference) error. `--seed` falls back to the CUPPL_SEED environment
+`run <file.cup>` compiles the program (its result must be importance(model, n)) to CUDA with
+frontend.py / NVRTC; `run --model poly | linreg | gmm | hmm` runs one of the registered
+hand-written engines (the BASELINE.json configs). The reference's flags, defaults and exit
+codes are kept: 0 success, 1 usage / compile / configuration error, 2 runtime (inference)
+error. `--seed` falls back to the CUPPL_SEED environment
 variable. Posteriors are printed with posterior.serialize_posterior.
 
 `bench` runs every selected workload `--repeats` times with fixed seeds after checking its
@@ -86,10 +86,49 @@ def _seed(args) -> int:
     return int(env) if env else 0
 
 
+def _run_file(args) -> int:
+    """`run <file.cup>`: compile the program's importance(model, n) for the GPU and run it."""
+    from . import frontend, infer
+    from .errors import CupError
+    from .posterior import serialize_posterior
+    from .rng import Rng
+
+    try:
+        src = open(args.file).read()
+    except OSError:
+        print(f"error: file not found: {args.file}", file=sys.stderr)  # SPEC.md:481
+        return 1
+    try:
+        model = frontend.compile_program(src)
+    except CupError as e:
+        print(e.render() if hasattr(e, "render") else f"error: {e}", file=sys.stderr)
+        return 1
+    if args.inference not in (None, "importance"):
+        print("error: compiled programs run with --inference importance", file=sys.stderr)
+        return 1
+    try:
+        post = infer.run_importance(model, args.samples or model.default_n, Rng(_seed(args)))
+        text = serialize_posterior(post, args.format)
+    except ValueError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 1
+    except CupError as e:
+        print(e.render() if hasattr(e, "render") else f"error: {e}", file=sys.stderr)
+        return 2
+    sys.stdout.write(text)
+    sys.stdout.flush()
+    return 0
+
+
 def cmd_run(args) -> int:
     from .errors import CupError
     from .posterior import serialize_posterior
 
+    if args.file:
+        return _run_file(args)
+    if not args.model:
+        print("error: run needs a program file or --model", file=sys.stderr)
+        return 1
     inference = args.inference or DEFAULT_INFERENCE[args.model]
     samples = args.samples or DEFAULT_SAMPLES.get(inference, 100_000)
     if samples < 1 or args.thin < 1:
@@ -197,7 +236,9 @@ def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="cuppl-gpu", description=__doc__.split("\n\n")[0])
     sub = ap.add_subparsers(dest="cmd", required=True)
     r = sub.add_parser("run", help="run one inference and print the posterior")
-    r.add_argument("--model", choices=tuple(DEFAULT_INFERENCE), required=True)
+    r.add_argument("file", nargs="?", help="CuPPL program whose result is importance(model, n) (compiled for "
+                   "the GPU by frontend.py)")
+    r.add_argument("--model", choices=tuple(DEFAULT_INFERENCE))
     r.add_argument("--inference", choices=("importance", "mcmc", "smc"))
     r.add_argument("--samples", type=int, default=0, help="particles (importance, smc) or steps per chain (mcmc)")
     r.add_argument("--seed", type=int, default=None)

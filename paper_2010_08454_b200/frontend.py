@@ -55,6 +55,8 @@ TAG_DSL = 8  # CUPPL_TAG_DSL
 MAX_STATS = 16  # cuppl_is_record.stat_w
 MAX_BINS = 8   # cuppl_is_record.bin_w
 MAX_TRACE_DRAWS = 256
+MAX_CONST_DATA = 16_000  # floats kept in the module's __constant__ bank (64 KB); larger: __ldg
+DATA_SYM = "DATA"        # resolved by the kernel prelude to the constant bank or the buffer
 
 
 class CompileError(CupError):
@@ -82,8 +84,8 @@ class DataVec:
     def bound(self):
         return self.n
 
-    def elem(self, g, i: S):
-        return S(f"__ldg(D + {self.off} + ({i.code}))", "real")
+    def elem(self, comp, i: S):
+        return S(f"{DATA_SYM}({self.off} + ({i.code}))", "real")
 
 
 @dataclass
@@ -99,8 +101,16 @@ class LocVec:
     def bound(self):
         return self.bound_
 
-    def elem(self, g, i: S):
-        return S(f"{self.var}[{i.code}]", self.ty)
+    def elem(self, comp, i: S):
+        if _is_literal(i.code) or self.bound_ > 8:
+            return S(f"{self.var}[{i.code}]", self.ty)
+        # small vector, computed index: a select chain over static elements keeps the array
+        # in registers (a dynamic index would spill it to local memory)
+        k = comp.g.let(i, "k")
+        code = f"{self.var}[{self.bound_ - 1}]"
+        for j in range(self.bound_ - 2, -1, -1):
+            code = f"({k.code} == {j} ? {self.var}[{j}] : {code})"
+        return S(code, self.ty)
 
 
 @dataclass
@@ -419,6 +429,9 @@ class _Compiler:
                 return S(f"{_MATH1[name]}({_real(x)})", "real", x.pure)
             if name == "pow":
                 a, b = (_scalar(self.ev(x, env), "pow") for x in e.args)
+                if _is_literal(b.code) and float(b.code.rstrip("f")) == 2.0:
+                    a = g.let(a, "p")
+                    return S(f"({_real(a)} * {_real(a)})", "real", a.pure)
                 return S(f"powf({_real(a)}, {_real(b)})", "real", a.pure and b.pure)
             if name == "to-real":
                 x = _scalar(self.ev(e.args[0], env), name)
@@ -466,7 +479,7 @@ class _Compiler:
         elif k == "uniform-continuous":
             g.emit(f"const float {v} = {_real(a[0])} + ({_real(a[1])} - {_real(a[0])}) * ws.uniform();")
         elif k == "uniform-discrete":
-            g.emit(f"if (!({a[1].code} > {a[0].code})) err |= 1u;")
+            g.emit(f"if (valid && !({a[1].code} > {a[0].code})) err |= 1u;")
             g.emit(f"const int {v} = {a[0].code} + static_cast<int>(ws.randint(static_cast<unsigned>("
                    f"{a[1].code} > {a[0].code} ? {a[1].code} - {a[0].code} : 1)));")
         elif k == "bernoulli":
@@ -483,7 +496,7 @@ class _Compiler:
         if k == "uniform-discrete" and _is_literal(a[1].code):
             g.bounds[v] = max(int(a[1].code) - 1, 0)
         ty = _DISTS[k][1]
-        g.emit(f"if (draws_out && nd < MAXD) draws_out[idx * MAXD + nd] = static_cast<float>({v});")
+        g.emit(f"if (draws_out && valid && nd < MAXD) draws_out[idx * MAXD + nd] = static_cast<float>({v});")
         g.emit("++nd;")
         return S(v, ty, False)
 
@@ -493,7 +506,17 @@ class _Compiler:
         a = d.args
         k = d.kind
         if k == "normal":
-            return f"score_normal({_real(v)}, {_real(a[0])}, {_real(a[1])})"
+            sd = a[1]
+            if _is_literal(sd.code):  # fold 1/sd and -ln sd - ln(2 pi)/2: one FFMA chain per point
+                sdv = float(sd.code.rstrip("f"))
+                if not sdv > 0:
+                    raise CompileError("normal(mean, sd): sd must be > 0")
+                inv = repr(float(np.float32(1.0 / sdv))) + "f"
+                c = repr(float(np.float32(-math.log(sdv) - 0.5 * math.log(2 * math.pi)))) + "f"
+                z = self.g.fresh("z")
+                self.g.emit(f"const float {z} = ({_real(v)} - {_real(a[0])}) * {inv};")
+                return f"fmaf(-0.5f * {z}, {z}, {c})"
+            return f"score_normal({_real(v)}, {_real(a[0])}, {_real(sd)})"
         if k == "uniform-continuous":
             return f"score_uniform_continuous({_real(v)}, {_real(a[0])}, {_real(a[1])})"
         if k == "uniform-discrete":
@@ -525,13 +548,69 @@ class _Compiler:
         arr, i = g.fresh("vec"), g.fresh("i")
         ty = probe_v.ty if isinstance(probe_v, S) else "real"
         g.emit(f"{_cty(ty)} {arr}[{bound}];")
-        g.open(f"for (int {i} = 0; {i} < {n.code}; ++{i})")
+        depth = self._loop(i, n, bound)
         g.loop_mult.append(g.loop_mult[-1] * bound)
         v = self._apply(f, [S(i, "int")])
         g.loop_mult.pop()
         g.emit(f"{arr}[{i}] = {v.code};")
-        g.close()
+        for _ in range(depth):
+            g.close()
         return LocVec(arr, bound, n, ty)
+
+    def _gaussian_reduce(self, f: Fn, init: S, v):
+        """reduce(function(acc, x) { acc + dist-score(normal(m, sd), y) }, init, v) with a
+        constant sd: sum (y - m)^2 with one FFMA per element, constants applied once
+        (-0.5/sd^2 * sum + n (-ln sd - ln(2 pi)/2)), as the hand-written kernels do."""
+        body = f.body
+        while isinstance(body, lang.Block) and not body.stmts:
+            body = body.result
+        if not (isinstance(body, lang.BinOp) and body.op == "+" and isinstance(body.lhs, lang.Var)
+                and body.lhs.name == f.params[0] and isinstance(body.rhs, lang.Call)
+                and isinstance(body.rhs.fn, lang.Var) and body.rhs.fn.name == "dist-score"
+                and len(body.rhs.args) == 2 and isinstance(body.rhs.args[0], lang.Call)
+                and isinstance(body.rhs.args[0].fn, lang.Var) and body.rhs.args[0].fn.name == "normal"
+                and len(body.rhs.args[0].args) == 2):
+            return None
+        g = self.g
+        env0 = dict(f.env, **{f.params[0]: S("0.f", "real"), f.params[1]: S("0", "int")})
+        if self._effects(body.rhs, env0):
+            return None
+        sd = self._sandbox().ev(body.rhs.args[0].args[1], dict(env0))
+        if not (isinstance(sd, S) and _is_literal(sd.code) and float(sd.code.rstrip("f")) > 0):
+            return None
+        sdv = float(sd.code.rstrip("f"))
+        acc, i = g.fresh("ss"), g.fresh("i")
+        g.emit(f"float {acc} = 0.f;")
+        n = v.length()
+        depth = self._loop(i, n, v.bound())
+        env = dict(f.env)
+        env[f.params[0]] = S("0.f", "real")
+        env[f.params[1]] = g.let(v.elem(self, S(i, "int")), "e")
+        m = _scalar(self.ev(body.rhs.args[0].args[0], env), "normal mean")
+        y = _scalar(self.ev(body.rhs.args[1], env), "observed value")
+        z = g.fresh("z")
+        g.emit(f"const float {z} = {_real(y)} - {_real(m)};")
+        g.emit(f"{acc} = fmaf({z}, {z}, {acc});")
+        for _ in range(depth):
+            g.close()
+        k = repr(float(np.float32(-0.5 / (sdv * sdv)))) + "f"
+        c = repr(float(np.float32(-math.log(sdv) - 0.5 * math.log(2 * math.pi)))) + "f"
+        return S(f"({_real(init)} + fmaf({k}, {acc}, static_cast<float>({n.code}) * {c}))", "real", False)
+
+    def _loop(self, i: str, n: S, bound):
+        """Open `for i < n`: small known bounds are unrolled with a guard (static indices keep
+        bounded vectors in registers); long data loops are partially unrolled."""
+        g = self.g
+        if bound is not None and bound <= 16:
+            g.emit("#pragma unroll")
+            g.open(f"for (int {i} = 0; {i} < {bound}; ++{i})")
+            if not (_is_literal(n.code) and int(n.code) == bound):
+                g.open(f"if ({i} < {n.code})")
+                return 2
+            return 1
+        g.emit("#pragma unroll 4")
+        g.open(f"for (int {i} = 0; {i} < {n.code}; ++{i})")
+        return 1
 
     def _bound_of(self, n: S):
         if _is_literal(n.code) and n.ty == "int":
@@ -553,13 +632,14 @@ class _Compiler:
         arr, i = g.fresh("vec"), g.fresh("i")
         if keep:
             g.emit(f"{_cty(probe.ty)} {arr}[{bound}];")
-        g.open(f"for (int {i} = 0; {i} < {v.length().code}; ++{i})")
+        depth = self._loop(i, v.length(), bound)
         g.loop_mult.append(g.loop_mult[-1] * (bound or 1))
         r = self._apply(f, [v.elem(self, S(i, "int"))])
         g.loop_mult.pop()
         if keep:
             g.emit(f"{arr}[{i}] = {r.code};")
-        g.close()
+        for _ in range(depth):
+            g.close()
         return LocVec(arr, bound, v.length(), probe.ty) if keep else None
 
     def _reduce(self, e, env):
@@ -569,6 +649,9 @@ class _Compiler:
         v = self.ev(e.args[2], env)
         if not isinstance(f, Fn) or len(f.params) != 2 or not hasattr(v, "elem"):
             raise CompileError("reduce expects (function(acc, x), init, vector)")
+        fused = self._gaussian_reduce(f, init, v)
+        if fused is not None:
+            return fused
         acc, i = g.fresh("acc"), g.fresh("i")
         # the accumulator type is the body's type given a real (or int) accumulator
         ty = "real" if init.ty == "real" else init.ty
@@ -578,14 +661,15 @@ class _Compiler:
             ty = "real"
         g.emit(f"{_cty(ty)} {acc} = {init.code if ty != 'real' else _real(init)};")
         n = v.length()
-        bound = v.bound() or 1
-        g.open(f"for (int {i} = 0; {i} < {n.code}; ++{i})")
-        g.loop_mult.append(g.loop_mult[-1] * bound)
+        bound = v.bound()
+        depth = self._loop(i, n, bound)
+        g.loop_mult.append(g.loop_mult[-1] * (bound or 1))
         x = v.elem(self, S(i, "int"))
         r = self._apply(f, [S(acc, ty), x])
         g.loop_mult.pop()
         g.emit(f"{acc} = {r.code if ty != 'real' else _real(r)};")
-        g.close()
+        for _ in range(depth):
+            g.close()
         return S(acc, ty, False)
 
     # -------------------------------------------------------------- helpers ----
@@ -654,6 +738,7 @@ _KERNEL = r'''
 #include "is_accum.cuh"
 using namespace cuppl;
 #define MAXD {maxd}
+{data_decl}
 extern "C" __global__ void __launch_bounds__(256)
 cuppl_dsl_model(const float* __restrict__ D, unsigned long long pid_begin, unsigned long long n,
                 unsigned int k0, unsigned int k1, cuppl_is_record* block_recs, unsigned int* counter,
@@ -663,19 +748,25 @@ cuppl_dsl_model(const float* __restrict__ D, unsigned long long pid_begin, unsig
   acc.init();
   const PhiloxKey key{{k0, k1}};
   unsigned int err = 0u;
-  for (unsigned long long idx = blockIdx.x * 256ull + threadIdx.x; idx < n;
-       idx += static_cast<unsigned long long>(gridDim.x) * 256ull) {{
+  // block-uniform chunk loop (lanes past the end run masked): the model body stays in
+  // uniform control flow, so warp-uniform data indices use the uniform datapath
+  for (unsigned long long base = blockIdx.x * 256ull; base < n;
+       base += static_cast<unsigned long long>(gridDim.x) * 256ull) {{
+    const unsigned long long idx = base + threadIdx.x;
+    const bool valid = idx < n;
     const unsigned long long pid = pid_begin + idx;
     WordStream ws;
     ws.init(key, pid, {tag}u);
     float lw = 0.f;
     int nd = 0;
 {body}
-    float f[{ns_arr}] = {{{stats}}};
-    acc.add(lw, pid, f, {bin});
-    if (lw_out) lw_out[idx] = lw;
-    if (ret_out) {{
+    if (valid) {{
+      float f[{ns_arr}] = {{{stats}}};
+      acc.add(lw, pid, f, {bin});
+      if (lw_out) lw_out[idx] = lw;
+      if (ret_out) {{
 {ret_store}
+      }}
     }}
     (void)nd;
   }}
@@ -725,10 +816,14 @@ def compile_program(source: str, data: dict | None = None) -> CompiledModel:
     stats, names, bin_expr, nb, kind, width, store = _return_parts(ret, g)
     maxd = g.draw_bound if 0 < g.draw_bound <= MAX_TRACE_DRAWS else 1
     body = "\n".join("  " + line for line in g.lines)
-    cuda = _KERNEL.format(maxd=maxd, ns=len(stats), nb=nb, ns_arr=max(len(stats), 1),
-                          stats=", ".join(stats) if stats else "0.f", bin=bin_expr, tag=TAG_DSL,
-                          body=body, ret_store="\n".join("      " + s for s in store))
     data_arr = np.asarray(g.data if g.data else [0.0], dtype=np.float32)
+    if len(data_arr) <= MAX_CONST_DATA:  # warp-uniform indices: constant-cache broadcasts
+        data_decl = f"__constant__ float DC[{len(data_arr)}];\n#define {DATA_SYM}(i) DC[i]"
+    else:
+        data_decl = f"#define {DATA_SYM}(i) __ldg(D + (i))"
+    cuda = _KERNEL.format(maxd=maxd, data_decl=data_decl, ns=len(stats), nb=nb, ns_arr=max(len(stats), 1),
+                          stats=", ".join(stats) if stats else "0.f", bin=bin_expr, tag=TAG_DSL,
+                          body=body, ret_store="\n".join("        " + s for s in store))
     return CompiledModel(source=source, cuda=cuda, data=data_arr, n_stats=len(stats), n_bins=nb,
                          stat_names=names, return_kind=kind, return_width=width,
                          max_draws=g.draw_bound, default_n=comp.default_n)
@@ -767,7 +862,7 @@ def _function(model: CompiledModel):
     """Load (once per process and source) the compiled kernel; returns a CUfunction."""
     from cuda.bindings import driver as cu
 
-    h = hashlib.sha256(model.cuda.encode()).hexdigest()
+    h = hashlib.sha256(model.cuda.encode() + model.data.tobytes()).hexdigest()
     if h not in _MODULES:
         import torch
 
@@ -779,6 +874,13 @@ def _function(model: CompiledModel):
         err, fn = cu.cuModuleGetFunction(mod, b"cuppl_dsl_model")
         if err != cu.CUresult.CUDA_SUCCESS:
             raise InferRuntimeError(f"cuModuleGetFunction failed: {err}")
+        if "__constant__ float DC[" in model.cuda:  # the data live in this module's constant bank
+            err, dptr, size = cu.cuModuleGetGlobal(mod, b"DC")
+            if err != cu.CUresult.CUDA_SUCCESS or size != model.data.nbytes:
+                raise InferRuntimeError(f"cuModuleGetGlobal(DC) failed: {err}")
+            err, = cu.cuMemcpyHtoD(dptr, model.data.ctypes.data, model.data.nbytes)
+            if err != cu.CUresult.CUDA_SUCCESS:
+                raise InferRuntimeError(f"cuMemcpyHtoD(DC) failed: {err}")
         _MODULES[h] = (mod, fn)
     return _MODULES[h][1]
 

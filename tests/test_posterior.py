@@ -48,10 +48,14 @@ def test_empty_support_refused_in_tsv():
     assert json.loads(serialize_posterior(_D([]), "json"))["support"] == []
 
 
-def test_cli_usage_errors_exit_1():
+def test_cli_usage_errors_exit_1(tmp_path):
     assert main(["run", "--model", "nope"]) == 1
     assert main(["run", "--model", "poly", "--thin", "0"]) == 1
     assert main([]) == 1
+    assert main(["run", str(tmp_path / "missing.cup")]) == 1
+    bad = tmp_path / "bad.cup"
+    bad.write_text("model <- function() { shift(k, 1) }; importance(model, 10)")
+    assert main(["run", str(bad)]) == 1  # compile error
 
 
 @pytest.mark.gpu
@@ -73,3 +77,22 @@ def test_cli_bench_checks_then_times(cuda, capsys):
     assert main(["bench", "--filter", "poly", "--repeats", "2"]) == 0
     out = capsys.readouterr().out
     assert "poly" in out and " ok" in out
+
+
+@pytest.mark.gpu
+def test_cli_run_program_file(cuda, capsys, tmp_path):
+    prog = tmp_path / "coin.cup"
+    prog.write_text("""
+      flips <- [1, 1, 1, 1, 1, 1, 1, 1, 0, 0];
+      model <- function() {
+        p <- sample(beta(1, 1));
+        factor(reduce(function(acc, f) { acc + dist-score(bernoulli(p), f > 0.5) }, 0.0, flips));
+        p > 0.5
+      };
+      importance(model, 400000)
+    """)
+    assert main(["run", str(prog), "--seed", "2", "--format", "json"]) == 0
+    obj = json.loads(capsys.readouterr().out)
+    probs = {e["value"]: e["prob"] for e in obj["support"]}
+    # posterior Beta(9, 3): P(p > 0.5) = 1 - I_0.5(9, 3) = 0.96728515625
+    assert abs(probs[True] - 0.96728515625) < 0.01
