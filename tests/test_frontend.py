@@ -177,3 +177,30 @@ def test_gpu_compiled_linreg_matches_handwritten_kernel(cuda):
     assert abs(d.log_z - log_z) < 0.1 and abs(h.log_z - log_z) < 0.1
     sd = np.sqrt(np.diag(cov))
     assert abs(d.mean["v0"] - mean[0]) < 0.2 * sd[0] + 0.01 and abs(d.mean["v1"] - mean[1]) < 0.2 * sd[1] + 0.01
+
+
+@pytest.mark.gpu
+def test_gpu_monte_carlo_rate_and_point_mass(cuda):
+    """SPEC.md:439-442 / acceptance 5: the importance estimate's error shrinks ~2x from n to
+    4n (RMS over 30 seeds, ratio in [1.5, 2.7]); n = 1 is a point mass."""
+    from paper_2010_08454_b200 import Rng, infer
+
+    src = """
+      flips <- [1, 1, 1, 1, 1, 1, 1, 1, 0, 0];
+      model <- function() {
+        p <- sample(beta(1, 1));
+        factor(reduce(function(acc, f) { acc + dist-score(bernoulli(p), f > 0.5) }, 0.0, flips));
+        p
+      };
+      importance(model, 1000)
+    """
+    m = frontend.compile_program(src)
+    exact = 9.0 / 12.0  # Beta(9, 3)
+    err = {}
+    for n in (2000, 8000):
+        e = [infer.run_importance(m, n, Rng(100 + s)).mean["value"] - exact for s in range(30)]
+        err[n] = math.sqrt(sum(x * x for x in e) / len(e))
+    assert 1.5 <= err[2000] / err[8000] <= 2.7, err
+    one = infer.run_importance(frontend.compile_program(
+        "model <- function() { sample(uniform-discrete(0, 7)) }; importance(model, 1)"), 1, Rng(4))
+    assert len(one.support) == 1 and one.support[0][1] == 1.0
