@@ -13,7 +13,7 @@ struct WordStream {
   PhiloxKey key;
   uint64_t id;
   uint32_t tag, blk;
-  uint32_t buf[4];
+  uint32_t b0, b1, b2, b3;  // the current block, in registers (no dynamically indexed array)
   int pos;
   float spare;
   bool has_spare;
@@ -30,13 +30,15 @@ struct WordStream {
   __device__ __forceinline__ uint32_t next() {
     if (pos == 4) {
       const uint4 b = draw_block(key, id, blk++, tag);
-      buf[0] = b.x;
-      buf[1] = b.y;
-      buf[2] = b.z;
-      buf[3] = b.w;
+      b0 = b.x;
+      b1 = b.y;
+      b2 = b.z;
+      b3 = b.w;
       pos = 0;
     }
-    return buf[pos++];
+    const uint32_t w = pos == 0 ? b0 : pos == 1 ? b1 : pos == 2 ? b2 : b3;
+    ++pos;
+    return w;
   }
   __device__ __forceinline__ float uniform() { return u01_closed0(next()); }
   __device__ __forceinline__ float uniform_pos() { return u01_open0(next()); }
