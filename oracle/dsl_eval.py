@@ -164,3 +164,54 @@ class Interpreter:
             raise ValueError(n)
         f = self.ev(e.fn, env)
         return self.apply(f, [self.ev(a, env) for a in e.args])
+
+
+class _NeedChoice(Exception):
+    def __init__(self, support):
+        super().__init__()
+        self.support = support
+
+
+class Enumerator(Interpreter):
+    """Exact enumeration by re-execution (SPEC.md:438's brute-force forced-choice oracle):
+    a run with a choice prefix either completes or asks for the next choice point's support;
+    every completed path contributes exp(sum of choice log-masses + factors)."""
+
+    def run_forced(self, prefix):
+        self._prefix = prefix
+        self._k = 0
+        self._lw = 0.0
+        ret = self.apply(self.model, [])
+        return self._lw, ret
+
+    def call(self, e, env):
+        if isinstance(e.fn, lang.Var) and e.fn.name in ("sample", "sample*") and e.fn.name not in env:
+            d = self.ev(e.args[0], env)
+            if d.kind == "bernoulli":
+                support = [True, False]
+            elif d.kind == "uniform-discrete":
+                support = list(range(int(d.args[0]), int(d.args[1])))
+            else:
+                raise ValueError(f"{d.kind} has no finite support")
+            if self._k >= len(self._prefix):
+                raise _NeedChoice(support)
+            v = self._prefix[self._k]
+            self._k += 1
+            self._lw += sem.dist_score(_TAGS[d.kind], d.args, v)
+            return v
+        return super().call(e, env)
+
+    def posterior(self):
+        """{return value: probability}, log evidence (fp64)."""
+        mass, stack = {}, [[]]
+        while stack:
+            prefix = stack.pop()
+            try:
+                lw, ret = self.run_forced(prefix)
+            except _NeedChoice as need:
+                stack.extend(prefix + [v] for v in need.support)
+                continue
+            key = tuple(ret) if isinstance(ret, list) else ret
+            mass[key] = mass.get(key, 0.0) + math.exp(lw)
+        z = sum(mass.values())
+        return {k: v / z for k, v in mass.items()}, math.log(z)

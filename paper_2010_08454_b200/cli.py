@@ -103,11 +103,14 @@ def _run_file(args) -> int:
     except CupError as e:
         print(e.render() if hasattr(e, "render") else f"error: {e}", file=sys.stderr)
         return 1
-    if args.inference not in (None, "importance"):
-        print("error: compiled programs run with --inference importance", file=sys.stderr)
+    if args.inference not in (None, model.engine):
+        print(f"error: this program's engine is {model.engine} (its result expression)", file=sys.stderr)
         return 1
     try:
-        post = infer.run_importance(model, args.samples or model.default_n, Rng(_seed(args)))
+        if model.engine == "enumerate":
+            post = infer.run_enumeration(model, args.max_executions or None)
+        else:
+            post = infer.run_importance(model, args.samples or model.default_n, Rng(_seed(args)))
         text = serialize_posterior(post, args.format)
     except ValueError as e:
         print(f"error: {e}", file=sys.stderr)
@@ -239,7 +242,8 @@ def main(argv=None) -> int:
     r.add_argument("file", nargs="?", help="CuPPL program whose result is importance(model, n) (compiled for "
                    "the GPU by frontend.py)")
     r.add_argument("--model", choices=tuple(DEFAULT_INFERENCE))
-    r.add_argument("--inference", choices=("importance", "mcmc", "smc"))
+    r.add_argument("--inference", choices=("importance", "mcmc", "smc", "enumerate"))
+    r.add_argument("--max-executions", type=int, default=0, help="enumeration: bound on the path space")
     r.add_argument("--samples", type=int, default=0, help="particles (importance, smc) or steps per chain (mcmc)")
     r.add_argument("--seed", type=int, default=None)
     r.add_argument("--burn-in", type=int, default=0)

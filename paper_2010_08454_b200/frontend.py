@@ -239,6 +239,8 @@ class _Compiler:
         self.external = dict(data or {})
         self.model = None
         self.default_n = None
+        self.engine = "importance"
+        self.radix = 1  # enumeration: largest support size of a choice point
 
     # -------------------------------------------------------------- top level ----
     def _data_vec(self, values) -> DataVec:
@@ -251,11 +253,13 @@ class _Compiler:
         for name, e in self.prog.bindings:
             self.globals[name] = self._global_value(name, e)
         res = self.prog.result
-        if not (isinstance(res, lang.Call) and isinstance(res.fn, lang.Var) and res.fn.name == "importance"):
-            raise CompileError("the program result must be importance(model, n) (mcmc / enumerate run on "
-                               "the registered engines)")
+        if not (isinstance(res, lang.Call) and isinstance(res.fn, lang.Var)
+                and res.fn.name in ("importance", "enumerate")):
+            raise CompileError("the program result must be importance(model, n) or enumerate(model, "
+                               "max_executions) (mcmc runs on the registered engines)")
+        self.engine = res.fn.name
         if len(res.args) != 2:
-            raise CompileError("importance takes (model, n)")
+            raise CompileError(f"{self.engine} takes (model, n)")
         m = self._global_value("<model>", res.args[0])
         if not isinstance(m, Fn) or m.params:
             raise CompileError("importance's first argument must be a zero-argument model function")
@@ -369,9 +373,10 @@ class _Compiler:
     def _if(self, e, env):
         g = self.g
         c = _scalar(self.ev(e.cond, env), "if condition")
-        mark = len(g.lines)
+        mark, b0 = len(g.lines), g.draw_bound
         t = self.ev(e.then, dict(env))
         f = self.ev(e.orelse, dict(env))
+        g.draw_bound = b0
         if len(g.lines) == mark and isinstance(t, S) and isinstance(f, S) and t.pure and f.pure:
             ty = "real" if "real" in (t.ty, f.ty) else t.ty
             tc, fc = (_real(t), _real(f)) if ty == "real" else (t.code, f.code)
@@ -386,11 +391,13 @@ class _Compiler:
         if isinstance(t, S):
             g.emit(f"{res} = {_real(t)};")
         g.close()
+        bt, g.draw_bound = g.draw_bound - b0, b0
         g.open("else")
         f = self.ev(e.orelse, dict(env))
         if isinstance(f, S):
             g.emit(f"{res} = {_real(f)};")
         g.close()
+        g.draw_bound = b0 + max(bt, g.draw_bound - b0)  # draws per path: the longer branch
         if tt is None:
             return None
         ty = "real" if "real" in (tt, f.ty) else tt
@@ -474,6 +481,8 @@ class _Compiler:
         a = [g.let(x) for x in d.args]
         v = g.fresh("x")
         k = d.kind
+        if self.engine == "enumerate":
+            return self._choose(d, a, v)
         if k == "normal":
             g.emit(f"const float {v} = {_real(a[0])} + {_real(a[1])} * ws.normal();")
         elif k == "uniform-continuous":
@@ -499,6 +508,39 @@ class _Compiler:
         g.emit(f"if (draws_out && valid && nd < MAXD) draws_out[idx * MAXD + nd] = static_cast<float>({v});")
         g.emit("++nd;")
         return S(v, ty, False)
+
+    def _choose(self, d: Dist, a, v) -> S:
+        """Enumeration: the next choice is the next base-R digit of the path index (forced
+        choices); its log-mass is added to the path weight; a digit outside the
+        site's support kills the path."""
+        g = self.g
+        k = d.kind
+        if k == "bernoulli":
+            self.radix = max(self.radix, 2)
+            g.emit("{ const unsigned dg = static_cast<unsigned>(rem % ENUM_R); rem /= ENUM_R; ++nd;")
+            g.emit(f"  if (dg > 1u) dead = true;")
+            g.emit(f"  lw += dg == 0u ? logf({_real(a[0])}) : log1pf(-{_real(a[0])});")
+            g.emit(f"  chosen = dg == 0u; }}")
+            g.emit(f"const bool {v} = chosen;")
+            return S(v, "bool", False)
+        if k == "uniform-discrete":
+            if not (_is_literal(a[0].code) and _is_literal(a[1].code)):
+                raise CompileError("enumeration needs uniform-discrete bounds known at compile time")
+            lo, hi = int(a[0].code), int(a[1].code)
+            if hi <= lo:
+                raise CompileError("uniform-discrete(a, b) needs b > a (SPEC.md:347)")
+            self.radix = max(self.radix, hi - lo)
+            g.bounds[v] = hi - 1
+            g.emit("{ const unsigned dg = static_cast<unsigned>(rem % ENUM_R); rem /= ENUM_R; ++nd;")
+            g.emit(f"  if (dg >= {hi - lo}u) dead = true;")
+            g.emit(f"  lw += {repr(float(np.float32(-math.log(hi - lo))))}f;")
+            g.emit(f"  chosen_i = {lo} + static_cast<int>(dg); }}")
+            g.emit(f"const int {v} = chosen_i;")
+            return S(v, "int", False)
+        from .errors import ContinuousDistError
+
+        raise ContinuousDistError(f"enumeration needs finite-support distributions; {k} is not "
+                                  "(SPEC.md:394)")
 
     def _score(self, d, v: S) -> str:
         if not isinstance(d, Dist):
@@ -677,6 +719,7 @@ class _Compiler:
         """A throwaway copy for type probes: nothing it emits or binds reaches this compiler."""
         c = _Compiler.__new__(_Compiler)
         c.prog, c.model, c.default_n = self.prog, self.model, self.default_n
+        c.engine, c.radix = self.engine, self.radix
         c.globals, c.external = dict(self.globals), dict(self.external)
         c.g = _Gen(list(self.g.data))
         c.g.n, c.g.bounds = self.g.n, dict(self.g.bounds)
@@ -729,6 +772,8 @@ class CompiledModel:
     return_width: int
     max_draws: int
     default_n: int
+    engine: str = "importance"
+    radix: int = 1
     kind: str = "dsl"
     _fn: object = field(default=None, repr=False)
 
@@ -759,7 +804,9 @@ cuppl_dsl_model(const float* __restrict__ D, unsigned long long pid_begin, unsig
     ws.init(key, pid, {tag}u);
     float lw = 0.f;
     int nd = 0;
+{enum_init}
 {body}
+{enum_final}
     if (valid) {{
       float f[{ns_arr}] = {{{stats}}};
       acc.add(lw, pid, f, {bin});
@@ -821,12 +868,24 @@ def compile_program(source: str, data: dict | None = None) -> CompiledModel:
         data_decl = f"__constant__ float DC[{len(data_arr)}];\n#define {DATA_SYM}(i) DC[i]"
     else:
         data_decl = f"#define {DATA_SYM}(i) __ldg(D + (i))"
-    cuda = _KERNEL.format(maxd=maxd, data_decl=data_decl, ns=len(stats), nb=nb, ns_arr=max(len(stats), 1),
+    enum_init = enum_final = ""
+    if comp.engine == "enumerate":
+        radix = max(comp.radix, 2)
+        maxd = max(g.draw_bound, 1)
+        data_decl += f"\n#define ENUM_R {radix}ull"
+        enum_init = ("    unsigned long long rem = pid;  // base-R digits: the forced choices of this path\n"
+                     "    bool dead = false, chosen = false;\n    int chosen_i = 0;\n    (void)chosen; (void)chosen_i;")
+        # a path that made nd < MAXD choices stands for R^(MAXD - nd) indices: divide them out
+        enum_final = (f"    if (dead) lw = neg_inf_f();\n"
+                      f"    lw -= static_cast<float>(MAXD - nd) * {repr(float(np.float32(math.log(radix))))}f;")
+    cuda = _KERNEL.format(maxd=maxd, data_decl=data_decl, enum_init=enum_init, enum_final=enum_final,
+                          ns=len(stats), nb=nb, ns_arr=max(len(stats), 1),
                           stats=", ".join(stats) if stats else "0.f", bin=bin_expr, tag=TAG_DSL,
                           body=body, ret_store="\n".join("        " + s for s in store))
     return CompiledModel(source=source, cuda=cuda, data=data_arr, n_stats=len(stats), n_bins=nb,
                          stat_names=names, return_kind=kind, return_width=width,
-                         max_draws=g.draw_bound, default_n=comp.default_n)
+                         max_draws=g.draw_bound, default_n=comp.default_n, engine=comp.engine,
+                         radix=max(comp.radix, 2) if comp.engine == "enumerate" else 1)
 
 
 # ----------------------------------------------------------------------------- JIT -------

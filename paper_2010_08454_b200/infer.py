@@ -361,3 +361,36 @@ def _run_compiled(model, n_samples: int, rng, *, return_traces: bool, group, dev
     out = distribution_from_record(model, merge_records(recs), n_samples, launcher, key)
     out.traces = traces
     return out
+
+
+def run_enumeration(model, max_executions: int | None = None, max_depth: int | None = None, *, group=None,
+                    device=None) -> EmpiricalDistribution:
+    """run_enumeration of a compiled program `enumerate(model, n)` on the GPU.
+
+    Exact: every path through the model's choice points is executed as a forced-choice run (one
+    GPU thread per index of the base-R choice space, frontend.py), weighted by the log-masses of
+    its choices plus its factors; the posterior is normalised over all paths. Paths shard over
+    ranks like particles. `max_executions` bounds the index space (the whole space is
+    enumerated — there is no breadth-first truncation); `max_depth` bounds the choice points.
+    """
+    from .frontend import CompiledModel, DslLauncher, distribution_from_record
+
+    if not isinstance(model, CompiledModel) or model.engine != "enumerate":
+        raise InferRuntimeError("run_enumeration needs a program compiled from enumerate(model, n)")
+    depth = model.max_draws
+    if max_depth is not None and depth > max_depth:
+        raise InferRuntimeError(f"the model has up to {depth} choice points > max_depth={max_depth}")
+    n_paths = model.radix ** max(depth, 1)
+    limit = max_executions if max_executions is not None else 2**36
+    if n_paths > limit:
+        raise InferRuntimeError(f"{n_paths} paths (radix {model.radix}, depth {depth}) exceed {limit}")
+    rank, world = _world(group)
+    lo, hi = shard_range(n_paths, rank, world)
+    launcher = DslLauncher(model, device)
+    launcher.launch(lo, hi, 0)
+    recs = _gather_records(launcher.rec, group)
+    launcher.check_errors()
+    rec = merge_records(recs)
+    out = distribution_from_record(model, rec, n_paths, launcher, 0)
+    out.log_z = rec.max_lw + math.log(rec.sum_w)  # exact evidence: the sum over paths
+    return out
