@@ -70,6 +70,7 @@ typedef enum cuppl_status {
 #define CUPPL_TAG_MH_INIT 6u   /* MH initial trace                            */
 #define CUPPL_TAG_DIST 7u      /* batch dist_sample                           */
 #define CUPPL_TAG_DSL 8u       /* runtime-compiled CuPPL models (frontend.py)  */
+#define CUPPL_TAG_DSL_MH 9u    /* compiled LMH chains: id = step << 32 | chain  */
 
 /* Distribution tags: order of the constructors in pkg/src/cuppl/builtins.py:86-94, plus
  * categorical (absent from the reference catalog). */

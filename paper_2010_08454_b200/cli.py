@@ -109,6 +109,9 @@ def _run_file(args) -> int:
     try:
         if model.engine == "enumerate":
             post = infer.run_enumeration(model, args.max_executions or None)
+        elif model.engine == "mcmc":
+            post = infer.run_lmh(model, args.samples or model.default_n, Rng(_seed(args)), chains=args.chains,
+                                 burn_in=args.burn_in, thin=args.thin)
         else:
             post = infer.run_importance(model, args.samples or model.default_n, Rng(_seed(args)))
         text = serialize_posterior(post, args.format)

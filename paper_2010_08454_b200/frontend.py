@@ -52,6 +52,7 @@ from .errors import CupError, InferRuntimeError, InvalidDistParamError
 CSRC = Path(__file__).resolve().parent / "csrc"
 INCLUDE = Path(__file__).resolve().parent.parent / "include"
 TAG_DSL = 8  # CUPPL_TAG_DSL
+TAG_DSL_MH = 9  # CUPPL_TAG_DSL_MH: LMH step streams, id = step << 32 | chain
 MAX_STATS = 16  # cuppl_is_record.stat_w
 MAX_BINS = 8   # cuppl_is_record.bin_w
 MAX_TRACE_DRAWS = 256
@@ -162,6 +163,8 @@ _DISTS = {  # name: (arity, sample type)
     "normal": (2, "real"), "uniform-continuous": (2, "real"), "uniform-discrete": (2, "int"),
     "bernoulli": (1, "bool"), "beta": (2, "real"), "exponential": (1, "real"), "poisson": (1, "int"),
 }
+_KIND_CODE = {"normal": 0, "uniform-continuous": 1, "uniform-discrete": 2, "bernoulli": 3, "beta": 4,
+              "exponential": 5, "poisson": 6}
 _MATH1 = {"exp": "expf", "log": "logf", "sqrt": "sqrtf", "abs": "fabsf", "floor": "floorf"}
 _CMP = {"==", "!=", "<", "<=", ">", ">="}
 
@@ -254,9 +257,9 @@ class _Compiler:
             self.globals[name] = self._global_value(name, e)
         res = self.prog.result
         if not (isinstance(res, lang.Call) and isinstance(res.fn, lang.Var)
-                and res.fn.name in ("importance", "enumerate")):
-            raise CompileError("the program result must be importance(model, n) or enumerate(model, "
-                               "max_executions) (mcmc runs on the registered engines)")
+                and res.fn.name in ("importance", "enumerate", "mcmc")):
+            raise CompileError("the program result must be importance(model, n), mcmc(model, n) or "
+                               "enumerate(model, max_executions)")
         self.engine = res.fn.name
         if len(res.args) != 2:
             raise CompileError(f"{self.engine} takes (model, n)")
@@ -475,6 +478,32 @@ class _Compiler:
         finally:
             self.g.depth -= 1
 
+    def _emit_draw(self, k: str, a, v: str, decl: bool = True):
+        """Draw from the particle's / step's word stream into `v` (the reference algorithms,
+        csrc/draws.cuh; the same consumption as the batch dist_sample kernel)."""
+        g = self.g
+        ty = _DISTS[k][1]
+        lhs = f"const {_cty(ty)} {v}" if decl else v
+        if k == "normal":
+            g.emit(f"{lhs} = {_real(a[0])} + {_real(a[1])} * ws.normal();")
+        elif k == "uniform-continuous":
+            g.emit(f"{lhs} = {_real(a[0])} + ({_real(a[1])} - {_real(a[0])}) * ws.uniform();")
+        elif k == "uniform-discrete":
+            g.emit(f"if (valid && !({a[1].code} > {a[0].code})) err |= 1u;")
+            g.emit(f"{lhs} = {a[0].code} + static_cast<int>(ws.randint(static_cast<unsigned>("
+                   f"{a[1].code} > {a[0].code} ? {a[1].code} - {a[0].code} : 1)));")
+        elif k == "bernoulli":
+            g.emit(f"{lhs} = ws.uniform() < {_real(a[0])};")
+        elif k == "beta":
+            gx, gy = g.fresh("gx"), g.fresh("gy")
+            g.emit(f"const float {gx} = ws.gamma({_real(a[0])});")
+            g.emit(f"const float {gy} = ws.gamma({_real(a[1])});")
+            g.emit(f"{lhs} = {gx} / ({gx} + {gy});")
+        elif k == "exponential":
+            g.emit(f"{lhs} = -logf(ws.uniform_pos()) / {_real(a[0])};")
+        elif k == "poisson":
+            g.emit(f"{lhs} = ws.poisson({_real(a[0])});")
+
     def _sample(self, d: Dist) -> S:
         g = self.g
         g.draw_bound += g.loop_mult[-1]
@@ -483,30 +512,41 @@ class _Compiler:
         k = d.kind
         if self.engine == "enumerate":
             return self._choose(d, a, v)
-        if k == "normal":
-            g.emit(f"const float {v} = {_real(a[0])} + {_real(a[1])} * ws.normal();")
-        elif k == "uniform-continuous":
-            g.emit(f"const float {v} = {_real(a[0])} + ({_real(a[1])} - {_real(a[0])}) * ws.uniform();")
-        elif k == "uniform-discrete":
-            g.emit(f"if (valid && !({a[1].code} > {a[0].code})) err |= 1u;")
-            g.emit(f"const int {v} = {a[0].code} + static_cast<int>(ws.randint(static_cast<unsigned>("
-                   f"{a[1].code} > {a[0].code} ? {a[1].code} - {a[0].code} : 1)));")
-        elif k == "bernoulli":
-            g.emit(f"const bool {v} = ws.uniform() < {_real(a[0])};")
-        elif k == "beta":
-            gx, gy = g.fresh("gx"), g.fresh("gy")
-            g.emit(f"const float {gx} = ws.gamma({_real(a[0])});")
-            g.emit(f"const float {gy} = ws.gamma({_real(a[1])});")
-            g.emit(f"const float {v} = {gx} / ({gx} + {gy});")
-        elif k == "exponential":
-            g.emit(f"const float {v} = -logf(ws.uniform_pos()) / {_real(a[0])};")
-        elif k == "poisson":
-            g.emit(f"const int {v} = ws.poisson({_real(a[0])});")
         if k == "uniform-discrete" and _is_literal(a[1].code):
             g.bounds[v] = max(int(a[1].code) - 1, 0)
         ty = _DISTS[k][1]
+        if self.engine == "mcmc":
+            return self._lmh_site(d, a, v, ty)
+        self._emit_draw(k, a, v)
         g.emit(f"if (draws_out && valid && nd < MAXD) draws_out[idx * MAXD + nd] = static_cast<float>({v});")
         g.emit("++nd;")
+        return S(v, ty, False)
+
+    def _lmh_site(self, d: Dist, a, v: str, ty: str) -> S:
+        """LMH: the nd-th sample call of this execution reuses the trace database entry nd when
+        its kind matches and it is not the proposed site; otherwise it
+        draws fresh from the step's stream. The site's score under the current parameters enters
+        the log-joint; fresh sites also enter l_fresh and reused ones are marked for l_stale."""
+        g = self.g
+        kc = _KIND_CODE[d.kind]
+        fv, re, sc = g.fresh("fv"), g.fresh("re"), g.fresh("sc")
+        g.emit(f"const bool {re} = nd < oldLen && oldKind[nd] == {kc} && nd != kstar;")
+        g.emit(f"float {fv};")
+        g.open(f"if ({re})")
+        g.emit(f"{fv} = oldVal[nd];")
+        g.emit("reused |= 1ull << nd;")
+        g.close()
+        g.open("else")
+        tmp = g.fresh("x")
+        self._emit_draw(d.kind, a, tmp)
+        g.emit(f"{fv} = static_cast<float>({tmp});")
+        g.close()
+        val = {"real": fv, "int": f"static_cast<int>({fv})", "bool": f"({fv} != 0.f)"}[ty]
+        g.emit(f"const {_cty(ty)} {v} = {val};")
+        g.emit(f"const float {sc} = {self._score(d, S(v, ty))};")
+        g.emit(f"if (!{re}) lfresh += {sc};")
+        g.emit(f"lw += {sc};")
+        g.emit(f"newVal[nd] = {fv}; newKind[nd] = {kc}; newScore[nd] = {sc}; ++nd;")
         return S(v, ty, False)
 
     def _choose(self, d: Dist, a, v) -> S:
@@ -823,6 +863,81 @@ cuppl_dsl_model(const float* __restrict__ D, unsigned long long pid_begin, unsig
 '''
 
 
+_MCMC_KERNEL = r"""
+#include "draws.cuh"
+using namespace cuppl;
+#define MAXD {maxd}
+{data_decl}
+// many independent LMH chains, one thread each (SPEC.md:408-416); the trace database of the
+// current state (old*) and of the proposal (new*) live in per-thread arrays
+extern "C" __global__ void __launch_bounds__(128)
+cuppl_dsl_mcmc(const float* __restrict__ D, unsigned int n_chains, unsigned int chain_begin,
+               unsigned int n_steps, unsigned int burn_in, unsigned int thin, unsigned int k0,
+               unsigned int k1, double* stats_out, unsigned int* err_out) {{
+  const PhiloxKey key{{k0, k1}};
+  unsigned int err = 0u;
+  const bool valid = true;
+  for (unsigned int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_chains; c += gridDim.x * blockDim.x) {{
+    const unsigned int chain = chain_begin + c;
+    float oldVal[MAXD], newVal[MAXD], oldScore[MAXD], newScore[MAXD];
+    unsigned char oldKind[MAXD], newKind[MAXD];
+    int oldLen = 0;
+    float ll = 0.f;
+    float curf[{ns_arr}];
+    int curbin = -1;
+    double sums[{ns_arr}], binc[{nb_arr}], nrec = 0.0, nacc = 0.0;
+    for (int k = 0; k < {ns_arr}; ++k) {{ curf[k] = 0.f; sums[k] = 0.0; }}
+    for (int k = 0; k < {nb_arr}; ++k) binc[k] = 0.0;
+    for (unsigned int s = 0; s < n_steps; ++s) {{  // sample s: the initial trace, then s MH steps
+      WordStream ws;
+      ws.init(key, (static_cast<unsigned long long>(s) << 32) | chain, {tag}u);
+      int kstar = -1;  // proposed site: uniform over the current trace database
+      if (s > 0 && oldLen > 0) kstar = static_cast<int>(ws.randint(static_cast<unsigned>(oldLen)));
+      float lw = 0.f, lfresh = 0.f;
+      int nd = 0;
+      unsigned long long reused = 0ull;
+{body}
+      float f[{ns_arr}] = {{{stats}}};
+      const int bin = {bin};
+      float lstale = 0.f;  // old sites the proposal did not reuse (incl. the proposed one)
+      for (int i = 0; i < oldLen; ++i)
+        if (!((reused >> i) & 1ull)) lstale += oldScore[i];
+      bool accept = true;
+      if (s > 0) {{  // SURVEY.md D8: single-site prior-proposal ratio with the |DB| terms
+        const float la = (lw - ll) + logf(static_cast<float>(oldLen > 0 ? oldLen : 1)) -
+                         logf(static_cast<float>(nd > 0 ? nd : 1)) + lstale - lfresh;
+        accept = logf(ws.uniform_pos()) < la;
+        nacc += accept ? 1.0 : 0.0;
+      }}
+      if (accept) {{
+        for (int i = 0; i < nd; ++i) {{
+          oldVal[i] = newVal[i];
+          oldScore[i] = newScore[i];
+          oldKind[i] = newKind[i];
+        }}
+        oldLen = nd;
+        ll = lw;
+        for (int k = 0; k < {ns_arr}; ++k) curf[k] = f[k];
+        curbin = bin;
+      }}
+      if (s >= burn_in && (s - burn_in) % thin == 0) {{
+        for (int k = 0; k < {ns_arr}; ++k) sums[k] += curf[k];
+        if (curbin >= 0 && curbin < {nb_arr}) binc[curbin] += 1.0;
+        nrec += 1.0;
+      }}
+      (void)lfresh;
+    }}
+    double* out = stats_out + static_cast<unsigned long long>(c) * ({ns_arr} + {nb_arr} + 2);
+    for (int k = 0; k < {ns_arr}; ++k) out[k] = sums[k];
+    for (int k = 0; k < {nb_arr}; ++k) out[{ns_arr} + k] = binc[k];
+    out[{ns_arr} + {nb_arr}] = nrec;
+    out[{ns_arr} + {nb_arr} + 1] = nacc;
+  }}
+  if (err) atomicOr(err_out, err);
+}}
+"""
+
+
 def _return_parts(ret, g: _Gen):
     """(stat expressions, stat names, bin expression, n_bins, kind, width, store lines)."""
     if ret is None:
@@ -878,6 +993,16 @@ def compile_program(source: str, data: dict | None = None) -> CompiledModel:
         # a path that made nd < MAXD choices stands for R^(MAXD - nd) indices: divide them out
         enum_final = (f"    if (dead) lw = neg_inf_f();\n"
                       f"    lw -= static_cast<float>(MAXD - nd) * {repr(float(np.float32(math.log(radix))))}f;")
+    if comp.engine == "mcmc":
+        if g.draw_bound > 64:
+            raise CompileError("mcmc supports up to 64 sample calls per execution")
+        cuda = _MCMC_KERNEL.format(maxd=max(g.draw_bound, 1), data_decl=data_decl, ns_arr=max(len(stats), 1),
+                                   nb_arr=max(nb, 1), stats=", ".join(stats) if stats else "0.f",
+                                   bin=bin_expr if nb else "-1", tag=TAG_DSL_MH,
+                                   body="\n".join("    " + line for line in g.lines))
+        return CompiledModel(source=source, cuda=cuda, data=data_arr, n_stats=len(stats), n_bins=nb,
+                             stat_names=names, return_kind=kind, return_width=width,
+                             max_draws=g.draw_bound, default_n=comp.default_n, engine="mcmc")
     cuda = _KERNEL.format(maxd=maxd, data_decl=data_decl, enum_init=enum_init, enum_final=enum_final,
                           ns=len(stats), nb=nb, ns_arr=max(len(stats), 1),
                           stats=", ".join(stats) if stats else "0.f", bin=bin_expr, tag=TAG_DSL,
@@ -930,7 +1055,8 @@ def _function(model: CompiledModel):
         err, mod = cu.cuModuleLoadData(cubin)
         if err != cu.CUresult.CUDA_SUCCESS:
             raise InferRuntimeError(f"cuModuleLoadData failed: {err}")
-        err, fn = cu.cuModuleGetFunction(mod, b"cuppl_dsl_model")
+        name = b"cuppl_dsl_mcmc" if model.engine == "mcmc" else b"cuppl_dsl_model"
+        err, fn = cu.cuModuleGetFunction(mod, name)
         if err != cu.CUresult.CUDA_SUCCESS:
             raise InferRuntimeError(f"cuModuleGetFunction failed: {err}")
         if "__constant__ float DC[" in model.cuda:  # the data live in this module's constant bank
@@ -1037,3 +1163,35 @@ def distribution_from_record(model: CompiledModel, rec, n: int, launcher: DslLau
         conv = bool if model.return_kind == "bool" else int
         out.support = [(conv(k), float(p)) for k, p in enumerate(bins) if p > 0]
     return out
+
+
+def run_mcmc(model: CompiledModel, n_steps: int, rng, *, chains: int = 4096, burn_in: int = 0, thin: int = 1,
+             chain_begin: int = 0, device=None) -> dict:
+    """Launch the compiled LMH kernel: `chains` chains of `n_steps` steps. Returns per-chain
+    statistics [chains, n_stats + n_bins + 2] (sums of the returned components, bin counts,
+    records, acceptances) as a numpy array."""
+    import torch
+    from cuda.bindings import driver as cu
+
+    from .rng import key_of
+
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    data = torch.from_numpy(model.data).to(dev)
+    fn = _function(model)
+    width = max(model.n_stats, 1) + max(model.n_bins, 1) + 2
+    stats = torch.zeros((chains, width), dtype=torch.float64, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    key = key_of(rng)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    grid = int(min((chains + 127) // 128, sms * 16))
+    vals = [C.c_uint64(data.data_ptr()), C.c_uint32(chains), C.c_uint32(chain_begin), C.c_uint32(n_steps),
+            C.c_uint32(burn_in), C.c_uint32(thin), C.c_uint32(key & 0xFFFFFFFF), C.c_uint32(key >> 32),
+            C.c_uint64(stats.data_ptr()), C.c_uint64(err.data_ptr())]
+    ptrs = (C.c_void_p * len(vals))(*[C.addressof(v) for v in vals])
+    st = torch.cuda.current_stream(dev).cuda_stream
+    e, = cu.cuLaunchKernel(fn, grid, 1, 1, 128, 1, 1, 0, st, C.addressof(ptrs), 0)
+    if e != cu.CUresult.CUDA_SUCCESS:
+        raise InferRuntimeError(f"cuLaunchKernel failed: {e}")
+    if int(err.item()):
+        raise InvalidDistParamError("uniform-discrete(a, b) needs b > a (SPEC.md:347)")
+    return stats.cpu().numpy()

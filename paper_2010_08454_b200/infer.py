@@ -273,7 +273,12 @@ def normalize(samples, *, device=None) -> EmpiricalDistribution:
 def run_lmh(model, n_samples: int, rng, *, chains: int = 4096, burn_in: int = 0, thin: int = 1,
             return_trace: bool = False, group=None, device=None):
     """Lightweight Metropolis-Hastings as `chains` independent GPU chains of
-    `n_samples` steps (mh.py, kernel K7)."""
+    `n_samples` steps (mh.py, kernel K7; compiled programs: frontend.py)."""
+    from .frontend import CompiledModel
+
+    if isinstance(model, CompiledModel):
+        return _run_compiled_lmh(model, n_samples, rng, chains=chains, burn_in=burn_in, thin=thin, group=group,
+                                 device=device)
     from .mh import run_lmh as _run
 
     return _run(model, n_samples, rng, chains=chains, burn_in=burn_in, thin=thin,
@@ -393,4 +398,48 @@ def run_enumeration(model, max_executions: int | None = None, max_depth: int | N
     rec = merge_records(recs)
     out = distribution_from_record(model, rec, n_paths, launcher, 0)
     out.log_z = rec.max_lw + math.log(rec.sum_w)  # exact evidence: the sum over paths
+    return out
+
+
+def _run_compiled_lmh(model, n_samples: int, rng, *, chains: int, burn_in: int, thin: int, group,
+                      device) -> EmpiricalDistribution:
+    """run_lmh of a program compiled from mcmc(model, n): `chains` chains, each recording the
+    initial trace and the states after each of the following n_samples - 1 single-site steps;
+    the chains are sharded over ranks and their statistics gathered (replicas)."""
+    import torch
+
+    from .frontend import run_mcmc
+
+    if model.engine != "mcmc":
+        raise InferRuntimeError("run_lmh needs a program compiled from mcmc(model, n)")
+    if n_samples < 1 or chains < 1 or thin < 1:
+        raise ValueError("n_samples, chains and thin must be >= 1")
+    rank, world = _world(group)
+    c0, c1 = shard_range(chains, rank, world)
+    st = run_mcmc(model, n_samples, rng, chains=c1 - c0, burn_in=burn_in, thin=thin, chain_begin=c0,
+                  device=device) if c1 > c0 else np.zeros((0, 1))
+    if world > 1:  # pragma: no cover - multi-GPU
+        import torch.distributed as dist
+
+        parts = [None] * world
+        dist.all_gather_object(parts, st, group=group)
+        st = np.concatenate([p for p in parts if len(p)])
+    ns, nb = max(model.n_stats, 1), max(model.n_bins, 1)
+    nrec = st[:, ns + nb].sum()
+    if nrec <= 0:
+        raise InferRuntimeError("no recorded samples (n_samples <= burn_in)")
+    out = EmpiricalDistribution(n=int(nrec))
+    means = st[:, :ns].sum(axis=0) / nrec
+    out.mean = {name: float(v) for name, v in zip(model.stat_names, means) if not name.endswith("^2")}
+    if model.stat_names and model.stat_names[-1].endswith("^2"):
+        half = model.n_stats // 2
+        out.stats = {f"var_{model.stat_names[k]}": float(means[half + k] - means[k] ** 2) for k in range(half)}
+    if model.n_bins:
+        probs = st[:, ns:ns + nb].sum(axis=0) / nrec
+        conv = bool if model.return_kind == "bool" else int
+        out.support = [(conv(k), float(p)) for k, p in enumerate(probs) if p > 0]
+    steps = max(n_samples - 1, 1)
+    out.stats["acceptance"] = float(st[:, ns + nb + 1].sum() / (len(st) * steps))
+    out.stats["chains"] = chains
+    out.record = {"chain_stats": st}
     return out

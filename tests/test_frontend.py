@@ -262,3 +262,33 @@ def test_gpu_enumeration_spec_example(cuda):
         "model <- function() { sample(bernoulli(0.3)) }; enumerate(model, 100)"))
     got = dict(post.support)
     assert abs(got[True] - 0.3) < 1e-7 and abs(got[False] - 0.7) < 1e-7
+
+
+@pytest.mark.gpu
+def test_gpu_compiled_lmh_spec_rows(cuda):
+    """run_lmh on compiled programs: prior recovery, TV < 0.02 against the
+    exact enumeration posterior on a two-choice-point model, a conjugate posterior, n = 1."""
+    from paper_2010_08454_b200 import Rng, infer
+
+    prior = frontend.compile_program("model <- function() { sample(bernoulli(0.3)) }; mcmc(model, 100)")
+    post = infer.run_lmh(prior, 2000, Rng(1), chains=256)
+    assert abs(dict(post.support)[True] - 0.3) < 0.02
+    mc = infer.run_lmh(frontend.compile_program(ENUM_TWO.replace("enumerate(model, 10000)", "mcmc(model, 10)")),
+                       5000, Rng(2), chains=1024, burn_in=500)
+    ex = infer.run_enumeration(frontend.compile_program(ENUM_TWO))
+    pm, pe = dict(mc.support), dict(ex.support)
+    tv = 0.5 * sum(abs(pm.get(k, 0.0) - pe.get(k, 0.0)) for k in set(pm) | set(pe))
+    assert tv < 0.02, (pm, pe)
+    coin = frontend.compile_program("""
+      flips <- [1, 1, 1, 1, 1, 1, 1, 1, 0, 0];
+      model <- function() {
+        p <- sample(beta(1, 1));
+        map(function(f) { observe(bernoulli(p), f > 0.5) }, flips);
+        p
+      };
+      mcmc(model, 10000)""")
+    post = infer.run_lmh(coin, 4000, Rng(3), chains=1024, burn_in=500)
+    assert abs(post.mean["value"] - 0.75) < 0.02  # Beta(9, 3)
+    assert 0.0 < post.stats["acceptance"] < 1.0
+    one = infer.run_lmh(prior, 1, Rng(4), chains=1)
+    assert len(one.support) == 1 and one.support[0][1] == 1.0
