@@ -35,6 +35,18 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "weighted particles/sec (importance sampling)"
+
+# C2 in CuPPL surface syntax (the dsl-linreg workload): xs / ys are bound from the host data
+DSL_LINREG = """
+model <- function() {
+  a <- sample(normal(0, 10));
+  b <- sample(normal(0, 10));
+  factor(reduce(function(acc, i) { acc + dist-score(normal(a * xs[i] + b, 1), ys[i]) }, 0.0,
+                repeat(function(i) { i }, length(xs))));
+  [a, b]
+};
+importance(model, 1000000000)
+"""
 UNIT = "particles/s"
 
 WORKLOADS = {
@@ -55,6 +67,12 @@ WORKLOADS = {
         "particles_per_gpu": 100_000_000,
         "n_points": 1000,
     },
+    "dsl-linreg": {
+        "name": "C2 written in CuPPL and compiled (frontend.py -> NVRTC sm_100a): Bayesian linear regression IS, "
+                "1e9 particles/GPU, 1k points",
+        "particles_per_gpu": 10**9,
+        "n_points": 1000,
+    },
     "mh": {
         "name": "C3: GMM K=5, 10k points, 4096 LMH chains x 10k steps (BASELINE configs[2])",
         "particles_per_gpu": 4096,
@@ -64,6 +82,7 @@ WORKLOADS = {
 METRICS = {
     "linreg": (METRIC, UNIT),
     "poly": (METRIC, UNIT),
+    "dsl-linreg": (METRIC, UNIT),
     "smc": ("SMC steps/sec", "time-steps/s"),
     "mh": ("MH chain-steps/sec", "chain-steps/s"),
 }
@@ -73,7 +92,7 @@ def make_model(workload: str):
     from paper_2010_08454_b200 import models
 
     w = WORKLOADS[workload]
-    if workload == "linreg":
+    if workload in ("linreg", "dsl-linreg"):
         return models.LinearRegression.synthetic(n_points=w["n_points"])
     if workload == "smc":
         return models.HiddenMarkovModel.synthetic(S=50, T=w["n_points"])
@@ -84,7 +103,7 @@ def make_model(workload: str):
 
 def flops_per_particle(workload: str, n_points: int) -> float:
     """Algorithmic fp32 flops of one particle's model evaluation."""
-    if workload == "linreg":
+    if workload in ("linreg", "dsl-linreg"):
         return 5.0 * n_points  # per point: (y - b) add, fma(-a, x, .), fma(r, r, acc)
     # poly, E[n] = 3: Horner (n-1) fma + (y - p) add + fma(r, r, acc) per point
     return n_points * (2 * 2 + 1 + 2)
@@ -157,8 +176,8 @@ def cpu_baseline(workload: str, model, target_s: float = 12.0, threads: int | No
     threads = threads or os.cpu_count() or 1
     key = 0x9E0160293A33AAF7
     run = (lambda lo, hi: core.is_linreg(model.xs, model.ys, model.sigma, lo, hi, key, threads=threads)) \
-        if workload == "linreg" else (lambda lo, hi: core.is_poly(model.xs, model.ys, lo, hi, key, threads=threads))
-    n = 20_000 if workload == "linreg" else 500_000
+        if workload in ("linreg", "dsl-linreg") else (lambda lo, hi: core.is_poly(model.xs, model.ys, lo, hi, key, threads=threads))
+    n = 20_000 if workload in ("linreg", "dsl-linreg") else 500_000
     t0 = time.perf_counter()
     run(0, n)
     dt = time.perf_counter() - t0
@@ -242,7 +261,14 @@ def run_ours(args) -> dict | None:
     wl = WORKLOADS[args.workload]
     per_gpu = args.particles or wl["particles_per_gpu"]
     model = make_model(args.workload)
-    launcher = infer.IsLauncher(model, device)
+    if args.workload == "dsl-linreg":  # the same model and data, from CuPPL source
+        from paper_2010_08454_b200 import frontend
+
+        src_model, model = model, frontend.compile_program(DSL_LINREG, data={"xs": model.xs, "ys": model.ys})
+        launcher = frontend.DslLauncher(model, device)
+    else:
+        src_model = model
+        launcher = infer.IsLauncher(model, device)
     base = Rng(1)
     lo = rank * per_gpu
     hi = lo + per_gpu
@@ -299,7 +325,7 @@ def run_ours(args) -> dict | None:
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_value = world * per_gpu * e2e_steps / (e2e_ms.item() / 1e3)
-    h2d = model.xs.nbytes + model.ys.nbytes
+    h2d = src_model.xs.nbytes + src_model.ys.nbytes
     d2h = 256 * world + (16 if args.workload == "poly" else 8) + (4 if args.workload == "poly" else 0)
 
     result = None
@@ -364,7 +390,8 @@ def run_ours(args) -> dict | None:
             "clocks": clk,
         }
         if world == 1 and not args.no_cpu_baseline:
-            result["cpu_baseline"] = cpu_baseline(args.workload, model)
+            result["cpu_baseline"] = cpu_baseline("linreg" if args.workload == "dsl-linreg" else args.workload,
+                                                  src_model)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -575,12 +602,12 @@ def run_reference(args) -> dict | None:
             core.mh_gmm(model.ys, model.K, model.prior_sd, model.sigma, per_step, 200, key + k, threads=threads)
         units = per_step * 200
     else:
-        per_step, cores = (1_000_000 if args.workload == "linreg" else 20_000_000), threads
+        per_step, cores = (1_000_000 if args.workload in ("linreg", "dsl-linreg") else 20_000_000), threads
         sample = (f"{per_step} particles per step of the same workload (oracle/cuppl_oracle.c: C restatement of "
                   "the reference semantics; the reference ships no executable inference engine)")
 
         def step(k):
-            if args.workload == "linreg":
+            if args.workload in ("linreg", "dsl-linreg"):
                 core.is_linreg(model.xs, model.ys, model.sigma, k * per_step, (k + 1) * per_step, key, threads=threads)
             else:
                 core.is_poly(model.xs, model.ys, k * per_step, (k + 1) * per_step, key, threads=threads)
