@@ -72,6 +72,7 @@ class S:
     code: str
     ty: str
     pure: bool = True  # no side effects (draws / factors) were needed to produce it
+    mul: tuple | None = None  # packed product (x, y): a following add fuses into one fma2
 
 
 @dataclass
@@ -86,6 +87,8 @@ class DataVec:
         return self.n
 
     def elem(self, comp, i: S):
+        if i.ty == "int2":  # elements i, i + 1 as one 8-byte load (offsets are even, i is even)
+            return S(f"{DATA_SYM}2({self.off} + ({i.code}))", "real2")
         return S(f"{DATA_SYM}({self.off} + ({i.code}))", "real")
 
 
@@ -205,7 +208,22 @@ class _Gen:
 
 
 def _cty(ty):
-    return {"real": "float", "int": "int", "bool": "bool"}[ty]
+    return {"real": "float", "int": "int", "bool": "bool", "real2": "f32x2", "int2": "int"}[ty]
+
+
+class _PairUnsupported(Exception):
+    """An operation without a packed (two data points per instruction) form: the peephole
+    falls back to the scalar loop."""
+
+
+def _pair(v: S) -> str:
+    """f32x2 code of a scalar (broadcast) or packed value."""
+    if v.ty == "real2":
+        return v.code
+    if v.ty in ("int2", "bool"):
+        raise _PairUnsupported(v.ty)
+    r = _real(v)
+    return f"pack2({r}, {r})"
 
 
 def _is_literal(code: str) -> bool:
@@ -225,6 +243,8 @@ def _lit(v) -> S:
 
 
 def _real(v: S) -> str:
+    if v.ty in ("real2", "int2"):
+        raise _PairUnsupported(v.ty)
     return f"static_cast<float>({v.code})" if v.ty != "real" else v.code
 
 
@@ -248,6 +268,8 @@ class _Compiler:
     # -------------------------------------------------------------- top level ----
     def _data_vec(self, values) -> DataVec:
         arr = np.asarray(values, dtype=np.float64).reshape(-1)
+        if len(self.g.data) % 2:  # even offsets: pairs of elements load as one f32x2
+            self.g.data.append(0.0)
         off = len(self.g.data)
         self.g.data.extend(np.float32(arr).tolist())
         return DataVec(off, len(arr))
@@ -328,6 +350,10 @@ class _Compiler:
             return self.ev(e.result, env)
         if isinstance(e, lang.Unary):
             a = _scalar(self.ev(e.arg, env), e.op)
+            if a.ty in ("real2", "int2"):
+                if e.op != "-" or a.ty == "int2":
+                    raise _PairUnsupported(e.op)
+                return S(f"mul2({a.code}, pack2(-1.f, -1.f))", "real2", a.pure)
             if e.op == "-":
                 return S(f"(-{a.code})", a.ty if a.ty != "bool" else "int", a.pure)
             return S(f"(!{a.code})", "bool", a.pure)
@@ -338,7 +364,9 @@ class _Compiler:
         if isinstance(e, lang.Index):
             v = self.ev(e.vec, env)
             i = _scalar(self.ev(e.idx, env), "index")
-            if i.ty != "int":
+            if i.ty == "int2" and not isinstance(v, DataVec):
+                raise _PairUnsupported("pair index into a non-data vector")
+            if i.ty not in ("int", "int2"):
                 raise CompileError("vector index must be an int")
             if isinstance(v, ConstVec):
                 if not _is_literal(i.code):
@@ -361,6 +389,19 @@ class _Compiler:
         a = _scalar(self.ev(e.lhs, env), e.op)
         b = _scalar(self.ev(e.rhs, env), e.op)
         pure = a.pure and b.pure
+        if "real2" in (a.ty, b.ty) or "int2" in (a.ty, b.ty):
+            if e.op == "+":
+                if a.mul is not None:
+                    return S(f"fma2({a.mul[0]}, {a.mul[1]}, {_pair(b)})", "real2", pure)
+                if b.mul is not None:
+                    return S(f"fma2({b.mul[0]}, {b.mul[1]}, {_pair(a)})", "real2", pure)
+                return S(f"add2({_pair(a)}, {_pair(b)})", "real2", pure)
+            if e.op == "-":
+                return S(f"fma2({_pair(b)}, pack2(-1.f, -1.f), {_pair(a)})", "real2", pure)
+            if e.op == "*":
+                pa, pb = _pair(a), _pair(b)
+                return S(f"mul2({pa}, {pb})", "real2", pure, mul=(pa, pb))
+            raise _PairUnsupported(e.op)
         if e.op in ("&&", "||"):
             return S(f"({a.code} {e.op} {b.code})", "bool", pure)
         if e.op in _CMP:
@@ -661,6 +702,11 @@ class _Compiler:
         if not (isinstance(sd, S) and _is_literal(sd.code) and float(sd.code.rstrip("f")) > 0):
             return None
         sdv = float(sd.code.rstrip("f"))
+        n = v.length()
+        if _is_literal(n.code) and int(n.code) >= 2 and isinstance(v, (DataVec, LazyVec)):
+            packed = self._gaussian_reduce_packed(f, body, v, int(n.code), init, sdv)
+            if packed is not None:
+                return packed
         acc, i = g.fresh("ss"), g.fresh("i")
         g.emit(f"float {acc} = 0.f;")
         n = v.length()
@@ -678,6 +724,50 @@ class _Compiler:
         k = repr(float(np.float32(-0.5 / (sdv * sdv)))) + "f"
         c = repr(float(np.float32(-math.log(sdv) - 0.5 * math.log(2 * math.pi)))) + "f"
         return S(f"({_real(init)} + fmaf({k}, {acc}, static_cast<float>({n.code}) * {c}))", "real", False)
+
+    def _gaussian_reduce_packed(self, f: Fn, body, v, n: int, init: S, sdv: float):
+        """The Gaussian-likelihood reduce over pairs of elements: elements (i, i + 1) of the
+        data as one f32x2, the particle's scalars broadcast, so each FFMA2 / FADD2 covers two
+        data points (the hand-written kernels pack two particles instead). None if some
+        operation has no packed form."""
+        sb = self._sandbox()
+        try:  # dry run: every operation of m and y must have a packed form
+            envp = dict(f.env)
+            envp[f.params[0]] = S("0.f", "real")
+            envp[f.params[1]] = v.elem(sb, S("ip", "int2"))
+            m2 = sb.ev(body.rhs.args[0].args[0], envp)
+            y2 = sb.ev(body.rhs.args[1], envp)
+            _pair(m2), _pair(y2)
+        except (_PairUnsupported, CompileError):
+            return None
+        g = self.g
+        acc, i = g.fresh("ss"), g.fresh("i")
+        g.emit(f"f32x2 {acc} = pack2(0.f, 0.f);")
+        g.emit("#pragma unroll 4")
+        g.open(f"for (int {i} = 0; {i} + 1 < {n}; {i} += 2)")
+        env = dict(f.env)
+        env[f.params[0]] = S("0.f", "real")
+        env[f.params[1]] = g.let(v.elem(self, S(i, "int2")), "e")
+        m = self.ev(body.rhs.args[0].args[0], env)
+        y = self.ev(body.rhs.args[1], env)
+        z = g.fresh("z")
+        g.emit(f"const f32x2 {z} = fma2({_pair(m)}, pack2(-1.f, -1.f), {_pair(y)});")
+        g.emit(f"{acc} = fma2({z}, {z}, {acc});")
+        g.close()
+        tot = g.fresh("ss")
+        g.emit(f"float {tot} = unpack2({acc}).x + unpack2({acc}).y;")
+        if n % 2:  # odd length: the last element, scalar
+            env = dict(f.env)
+            env[f.params[0]] = S("0.f", "real")
+            env[f.params[1]] = g.let(v.elem(self, S(str(n - 1), "int")), "e")
+            m = _scalar(self.ev(body.rhs.args[0].args[0], env), "normal mean")
+            y = _scalar(self.ev(body.rhs.args[1], env), "observed value")
+            z = g.fresh("z")
+            g.emit(f"const float {z} = {_real(y)} - {_real(m)};")
+            g.emit(f"{tot} = fmaf({z}, {z}, {tot});")
+        k = repr(float(np.float32(-0.5 / (sdv * sdv)))) + "f"
+        c = repr(float(np.float32(-math.log(sdv) - 0.5 * math.log(2 * math.pi)))) + "f"
+        return S(f"({_real(init)} + fmaf({k}, {tot}, {float(n)}f * {c}))", "real", False)
 
     def _loop(self, i: str, n: S, bound):
         """Open `for i < n`: small known bounds are unrolled with a guard (static indices keep
@@ -980,9 +1070,11 @@ def compile_program(source: str, data: dict | None = None) -> CompiledModel:
     body = "\n".join("  " + line for line in g.lines)
     data_arr = np.asarray(g.data if g.data else [0.0], dtype=np.float32)
     if len(data_arr) <= MAX_CONST_DATA:  # warp-uniform indices: constant-cache broadcasts
-        data_decl = f"__constant__ float DC[{len(data_arr)}];\n#define {DATA_SYM}(i) DC[i]"
+        data_decl = (f"__constant__ __align__(8) float DC[{len(data_arr)}];\n#define {DATA_SYM}(i) DC[i]\n"
+                     f"#define {DATA_SYM}2(i) (*reinterpret_cast<const f32x2*>(&DC[i]))")
     else:
-        data_decl = f"#define {DATA_SYM}(i) __ldg(D + (i))"
+        data_decl = (f"#define {DATA_SYM}(i) __ldg(D + (i))\n"
+                     f"#define {DATA_SYM}2(i) __ldg(reinterpret_cast<const unsigned long long*>(D + (i)))")
     enum_init = enum_final = ""
     if comp.engine == "enumerate":
         radix = max(comp.radix, 2)
@@ -1059,7 +1151,7 @@ def _function(model: CompiledModel):
         err, fn = cu.cuModuleGetFunction(mod, name)
         if err != cu.CUresult.CUDA_SUCCESS:
             raise InferRuntimeError(f"cuModuleGetFunction failed: {err}")
-        if "__constant__ float DC[" in model.cuda:  # the data live in this module's constant bank
+        if " float DC[" in model.cuda:  # the data live in this module's constant bank
             err, dptr, size = cu.cuModuleGetGlobal(mod, b"DC")
             if err != cu.CUresult.CUDA_SUCCESS or size != model.data.nbytes:
                 raise InferRuntimeError(f"cuModuleGetGlobal(DC) failed: {err}")
