@@ -1,0 +1,277 @@
+// dsl_lanes.cuh — lane-polymorphic value types for runtime-compiled model kernels (frontend.py).
+//
+// The model compiler emits one body text in terms of VF / VI / VB (real, int, bool), VF2 (a
+// packed pair of reals) and helpers (sel, to_f, to_i, to_b, ud_draw, ...). With LANES == 1
+// these are the plain scalar types and functions: one particle per thread. With LANES == P > 1
+// every particle-dependent value is a Lane<T> holding P particles of the same thread and every
+// operation is applied lane by lane, fully unrolled, so the P particles' instruction streams
+// interleave (ILP) and each uniform operand — a data element read from the constant bank, a
+// loop index — is loaded once for all P particles, as the hand-written kernels do with their P
+// particles per thread (is_kernels.cu). Control flow on a lane value (`if (Lane<bool>)`, a loop
+// bound that differs per particle) has no conversion and fails to compile: the host then
+// compiles the same text with LANES == 1.
+#pragma once
+#include "draws.cuh"
+
+#ifndef LANES
+#define LANES 1
+#endif
+#ifndef MAXD
+#error "define MAXD (the per-particle draw-record width) before including dsl_lanes.cuh"
+#endif
+
+namespace cuppl {
+
+template <bool B, class T = void>
+struct enable_if_ {};
+template <class T>
+struct enable_if_<true, T> {
+  typedef T type;
+};
+
+template <class T>
+struct Lane {
+  T v[LANES];
+  Lane() = default;
+  __device__ __forceinline__ Lane(const T& x) {
+#pragma unroll
+    for (int p = 0; p < LANES; ++p) v[p] = x;
+  }
+  template <class U>
+  __device__ __forceinline__ Lane(const Lane<U>& o) {
+#pragma unroll
+    for (int p = 0; p < LANES; ++p) v[p] = static_cast<T>(o.v[p]);
+  }
+  template <class U>
+  __device__ __forceinline__ Lane& operator+=(const U& o);
+};
+
+template <class T>
+struct is_lane {
+  static constexpr bool v = false;
+};
+template <class T>
+struct is_lane<Lane<T>> {
+  static constexpr bool v = true;
+};
+template <class... A>
+struct any_lane {
+  static constexpr bool v = (is_lane<A>::v || ...);
+};
+
+template <class T>
+__device__ __forceinline__ const T& lane_at(const T& x, int) {
+  return x;
+}
+template <class T>
+__device__ __forceinline__ const T& lane_at(const Lane<T>& x, int p) {
+  return x.v[p];
+}
+template <class T>
+__device__ __forceinline__ T& lane_ref(T& x, int) {
+  return x;
+}
+template <class T>
+__device__ __forceinline__ T& lane_ref(Lane<T>& x, int p) {
+  return x.v[p];
+}
+
+template <class T>
+template <class U>
+__device__ __forceinline__ Lane<T>& Lane<T>::operator+=(const U& o) {
+#pragma unroll
+  for (int p = 0; p < LANES; ++p) v[p] += lane_at(o, p);
+  return *this;
+}
+
+// f(lanes...) = Lane{ f(lane 0 of each argument), ..., f(lane P-1 ...) }; scalars broadcast
+#define CUPPL_LIFT(fn)                                                                      \
+  template <class... A, class = typename enable_if_<any_lane<A...>::v>::type>               \
+  __device__ __forceinline__ auto fn(const A&... a) {                                       \
+    Lane<decltype(fn(lane_at(a, 0)...))> r;                                                 \
+    _Pragma("unroll") for (int p = 0; p < LANES; ++p) r.v[p] = fn(lane_at(a, p)...);       \
+    return r;                                                                               \
+  }
+
+#define CUPPL_LANE_BINOP(op)                                                                \
+  template <class A, class B, class = typename enable_if_<any_lane<A, B>::v>::type>         \
+  __device__ __forceinline__ auto operator op(const A& a, const B& b) {                     \
+    Lane<decltype(lane_at(a, 0) op lane_at(b, 0))> r;                                       \
+    _Pragma("unroll") for (int p = 0; p < LANES; ++p) r.v[p] = lane_at(a, p) op lane_at(b, p); \
+    return r;                                                                               \
+  }
+
+CUPPL_LANE_BINOP(+)
+CUPPL_LANE_BINOP(-)
+CUPPL_LANE_BINOP(*)
+CUPPL_LANE_BINOP(/)
+CUPPL_LANE_BINOP(%)
+CUPPL_LANE_BINOP(<)
+CUPPL_LANE_BINOP(<=)
+CUPPL_LANE_BINOP(>)
+CUPPL_LANE_BINOP(>=)
+CUPPL_LANE_BINOP(==)
+CUPPL_LANE_BINOP(!=)
+CUPPL_LANE_BINOP(&&)
+CUPPL_LANE_BINOP(||)
+
+template <class T>
+__device__ __forceinline__ Lane<T> operator-(const Lane<T>& a) {
+  Lane<T> r;
+#pragma unroll
+  for (int p = 0; p < LANES; ++p) r.v[p] = -a.v[p];
+  return r;
+}
+__device__ __forceinline__ Lane<bool> operator!(const Lane<bool>& a) {
+  Lane<bool> r;
+#pragma unroll
+  for (int p = 0; p < LANES; ++p) r.v[p] = !a.v[p];
+  return r;
+}
+
+// ------------------------------------------------------------------ scalar helpers ------
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(int x) { return static_cast<float>(x); }
+__device__ __forceinline__ float to_f(bool x) { return x ? 1.f : 0.f; }
+__device__ __forceinline__ int to_i(float x) { return static_cast<int>(x); }
+__device__ __forceinline__ int to_i(int x) { return x; }
+__device__ __forceinline__ int to_i(bool x) { return x ? 1 : 0; }
+__device__ __forceinline__ bool to_b(float x) { return x != 0.f; }
+__device__ __forceinline__ bool to_b(int x) { return x != 0; }
+__device__ __forceinline__ bool to_b(bool x) { return x; }
+__device__ __forceinline__ float hsum2(f32x2 v) {
+  const float2 t = unpack2(v);
+  return t.x + t.y;
+}
+template <class A, class B>
+__device__ __forceinline__ A sel_(bool c, const A& a, const B& b) {
+  return c ? a : static_cast<A>(b);
+}
+
+// pure select: both operands are already evaluated (they are side-effect free)
+template <class C, class A, class B>
+__device__ __forceinline__ auto sel(const C& c, const A& a, const B& b) {
+  if constexpr (any_lane<C, A, B>::v) {
+    Lane<decltype(sel_(lane_at(c, 0), lane_at(a, 0), lane_at(b, 0)))> r;
+#pragma unroll
+    for (int p = 0; p < LANES; ++p) r.v[p] = sel_(lane_at(c, p), lane_at(a, p), lane_at(b, p));
+    return r;
+  } else {
+    return sel_(c, a, b);
+  }
+}
+
+// the CUDA math builtins live in the global namespace: make them visible next to their lifts
+using ::expf;
+using ::logf;
+using ::log1pf;
+using ::sqrtf;
+using ::fabsf;
+using ::floorf;
+using ::fmodf;
+using ::powf;
+using ::fmaf;
+
+CUPPL_LIFT(to_f)
+CUPPL_LIFT(to_i)
+CUPPL_LIFT(to_b)
+CUPPL_LIFT(hsum2)
+CUPPL_LIFT(pack2)
+CUPPL_LIFT(fma2)
+CUPPL_LIFT(add2)
+CUPPL_LIFT(mul2)
+CUPPL_LIFT(expf)
+CUPPL_LIFT(logf)
+CUPPL_LIFT(log1pf)
+CUPPL_LIFT(sqrtf)
+CUPPL_LIFT(fabsf)
+CUPPL_LIFT(floorf)
+CUPPL_LIFT(fmodf)
+CUPPL_LIFT(powf)
+CUPPL_LIFT(fmaf)
+CUPPL_LIFT(score_normal)
+CUPPL_LIFT(score_bernoulli)
+CUPPL_LIFT(score_poisson)
+CUPPL_LIFT(score_uniform_discrete)
+CUPPL_LIFT(score_uniform_continuous)
+CUPPL_LIFT(score_beta)
+CUPPL_LIFT(score_exponential)
+
+// ------------------------------------------------------------------ draws --------------
+// uniform-discrete(lo, hi): support [lo, hi); an empty range raises
+// InvalidDistParamError on the host (err word) and draws from [lo, lo + 1)
+__device__ __forceinline__ unsigned ud_check(bool valid, int lo, int hi) {
+  return valid && !(hi > lo) ? 1u : 0u;
+}
+__device__ __forceinline__ int ud_draw(WordStream& ws, int lo, int hi) {
+  return lo + static_cast<int>(ws.randint(static_cast<unsigned>(hi > lo ? hi - lo : 1)));
+}
+__device__ __forceinline__ void store_draw(float* out, unsigned long long idx, bool valid, int nd, float x) {
+  if (out && valid && nd < MAXD) out[idx * MAXD + nd] = x;
+}
+
+#if LANES > 1
+// P particles' word streams of one thread: draw k of lane p is draw k of particle p's stream
+struct LaneStream {
+  WordStream s[LANES];
+  __device__ __forceinline__ void init(PhiloxKey k, const Lane<unsigned long long>& id, uint32_t t) {
+#pragma unroll
+    for (int p = 0; p < LANES; ++p) s[p].init(k, id.v[p], t);
+  }
+#define CUPPL_STREAM0(T, fn)                                                                \
+  __device__ __forceinline__ Lane<T> fn() {                                                 \
+    Lane<T> r;                                                                              \
+    _Pragma("unroll") for (int p = 0; p < LANES; ++p) r.v[p] = s[p].fn();                   \
+    return r;                                                                               \
+  }
+#define CUPPL_STREAM1(T, fn)                                                                \
+  template <class A>                                                                        \
+  __device__ __forceinline__ Lane<T> fn(const A& a) {                                       \
+    Lane<T> r;                                                                              \
+    _Pragma("unroll") for (int p = 0; p < LANES; ++p) r.v[p] = s[p].fn(lane_at(a, p));      \
+    return r;                                                                               \
+  }
+  CUPPL_STREAM0(float, uniform)
+  CUPPL_STREAM0(float, uniform_pos)
+  CUPPL_STREAM0(float, normal)
+  CUPPL_STREAM1(float, gamma)
+  CUPPL_STREAM1(int, poisson)
+#undef CUPPL_STREAM0
+#undef CUPPL_STREAM1
+};
+template <class A, class B>
+__device__ __forceinline__ unsigned ud_check(const Lane<bool>& valid, const A& lo, const B& hi) {
+  unsigned e = 0u;
+#pragma unroll
+  for (int p = 0; p < LANES; ++p) e |= ud_check(valid.v[p], lane_at(lo, p), lane_at(hi, p));
+  return e;
+}
+template <class A, class B>
+__device__ __forceinline__ Lane<int> ud_draw(LaneStream& ws, const A& lo, const B& hi) {
+  Lane<int> r;
+#pragma unroll
+  for (int p = 0; p < LANES; ++p) r.v[p] = ud_draw(ws.s[p], lane_at(lo, p), lane_at(hi, p));
+  return r;
+}
+template <class X>
+__device__ __forceinline__ void store_draw(float* out, const Lane<unsigned long long>& idx,
+                                           const Lane<bool>& valid, int nd, const X& x) {
+#pragma unroll
+  for (int p = 0; p < LANES; ++p) store_draw(out, idx.v[p], valid.v[p], nd, to_f(lane_at(x, p)));
+}
+typedef Lane<float> VF;
+typedef Lane<int> VI;
+typedef Lane<bool> VB;
+typedef Lane<f32x2> VF2;
+typedef Lane<unsigned long long> VU64;
+typedef LaneStream VStream;
+#else
+typedef float VF;
+typedef int VI;
+typedef bool VB;
+typedef f32x2 VF2;
+typedef unsigned long long VU64;
+typedef WordStream VStream;
+#endif
+
+}  // namespace cuppl

@@ -41,6 +41,7 @@ from __future__ import annotations
 import ctypes as C
 import hashlib
 import math
+import os
 from dataclasses import dataclass, field
 from pathlib import Path
 
@@ -58,6 +59,7 @@ MAX_BINS = 8   # cuppl_is_record.bin_w
 MAX_TRACE_DRAWS = 256
 MAX_CONST_DATA = 16_000  # floats kept in the module's __constant__ bank (64 KB); larger: __ldg
 DATA_SYM = "DATA"        # resolved by the kernel prelude to the constant bank or the buffer
+DSL_LANES = 8            # particles per thread of an importance kernel (CUPPL_DSL_LANES overrides)
 
 
 class CompileError(CupError):
@@ -113,7 +115,7 @@ class LocVec:
         k = comp.g.let(i, "k")
         code = f"{self.var}[{self.bound_ - 1}]"
         for j in range(self.bound_ - 2, -1, -1):
-            code = f"({k.code} == {j} ? {self.var}[{j}] : {code})"
+            code = f"sel({k.code} == {j}, {self.var}[{j}], {code})"
         return S(code, self.ty)
 
 
@@ -203,12 +205,12 @@ class _Gen:
         if v.code.isidentifier() or _is_literal(v.code):
             return v
         name = self.fresh(hint)
-        self.emit(f"const {_cty(v.ty)} {name} = {v.code};")
+        self.emit(f"const auto {name} = {v.code};")
         return S(name, v.ty, v.pure)
 
 
 def _cty(ty):
-    return {"real": "float", "int": "int", "bool": "bool", "real2": "f32x2", "int2": "int"}[ty]
+    return {"real": "VF", "int": "VI", "bool": "VB", "real2": "VF2", "int2": "int"}[ty]
 
 
 class _PairUnsupported(Exception):
@@ -245,7 +247,7 @@ def _lit(v) -> S:
 def _real(v: S) -> str:
     if v.ty in ("real2", "int2"):
         raise _PairUnsupported(v.ty)
-    return f"static_cast<float>({v.code})" if v.ty != "real" else v.code
+    return f"to_f({v.code})" if v.ty != "real" else v.code
 
 
 def _scalar(v, what) -> S:
@@ -424,11 +426,11 @@ class _Compiler:
         if len(g.lines) == mark and isinstance(t, S) and isinstance(f, S) and t.pure and f.pure:
             ty = "real" if "real" in (t.ty, f.ty) else t.ty
             tc, fc = (_real(t), _real(f)) if ty == "real" else (t.code, f.code)
-            return S(f"({c.code} ? {tc} : {fc})", ty, c.pure)
+            return S(f"sel({c.code}, {tc}, {fc})", ty, c.pure)
         # side effects in a branch: emit real control flow (draws happen on the taken path only)
         del g.lines[mark:]
         res = g.fresh("r")
-        g.emit(f"float {res} = 0.f;")
+        g.emit(f"VF {res} = 0.f;")
         g.open(f"if ({c.code})")
         t = self.ev(e.then, dict(env))
         tt = t.ty if isinstance(t, S) else None
@@ -445,7 +447,7 @@ class _Compiler:
         if tt is None:
             return None
         ty = "real" if "real" in (tt, f.ty) else tt
-        return S(res if ty == "real" else f"static_cast<{_cty(ty)}>({res})", ty, False)
+        return S(res if ty == "real" else f"to_{ty[0]}({res})", ty, False)
 
     # -------------------------------------------------------------- calls --------
     def _call(self, e, env):
@@ -489,7 +491,7 @@ class _Compiler:
                 return S(_real(x), "real", x.pure)
             if name == "to-int":
                 x = _scalar(self.ev(e.args[0], env), name)
-                return S(f"static_cast<int>({x.code})", "int", x.pure)
+                return S(f"to_i({x.code})", "int", x.pure)
             if name == "length":
                 v = self.ev(e.args[0], env)
                 return v.length()
@@ -530,15 +532,14 @@ class _Compiler:
         elif k == "uniform-continuous":
             g.emit(f"{lhs} = {_real(a[0])} + ({_real(a[1])} - {_real(a[0])}) * ws.uniform();")
         elif k == "uniform-discrete":
-            g.emit(f"if (valid && !({a[1].code} > {a[0].code})) err |= 1u;")
-            g.emit(f"{lhs} = {a[0].code} + static_cast<int>(ws.randint(static_cast<unsigned>("
-                   f"{a[1].code} > {a[0].code} ? {a[1].code} - {a[0].code} : 1)));")
+            g.emit(f"err |= ud_check(valid, {a[0].code}, {a[1].code});")
+            g.emit(f"{lhs} = ud_draw(ws, {a[0].code}, {a[1].code});")
         elif k == "bernoulli":
             g.emit(f"{lhs} = ws.uniform() < {_real(a[0])};")
         elif k == "beta":
             gx, gy = g.fresh("gx"), g.fresh("gy")
-            g.emit(f"const float {gx} = ws.gamma({_real(a[0])});")
-            g.emit(f"const float {gy} = ws.gamma({_real(a[1])});")
+            g.emit(f"const auto {gx} = ws.gamma({_real(a[0])});")
+            g.emit(f"const auto {gy} = ws.gamma({_real(a[1])});")
             g.emit(f"{lhs} = {gx} / ({gx} + {gy});")
         elif k == "exponential":
             g.emit(f"{lhs} = -logf(ws.uniform_pos()) / {_real(a[0])};")
@@ -559,7 +560,7 @@ class _Compiler:
         if self.engine == "mcmc":
             return self._lmh_site(d, a, v, ty)
         self._emit_draw(k, a, v)
-        g.emit(f"if (draws_out && valid && nd < MAXD) draws_out[idx * MAXD + nd] = static_cast<float>({v});")
+        g.emit(f"store_draw(draws_out, idx, valid, nd, {v});")
         g.emit("++nd;")
         return S(v, ty, False)
 
@@ -637,7 +638,7 @@ class _Compiler:
                 inv = repr(float(np.float32(1.0 / sdv))) + "f"
                 c = repr(float(np.float32(-math.log(sdv) - 0.5 * math.log(2 * math.pi)))) + "f"
                 z = self.g.fresh("z")
-                self.g.emit(f"const float {z} = ({_real(v)} - {_real(a[0])}) * {inv};")
+                self.g.emit(f"const auto {z} = ({_real(v)} - {_real(a[0])}) * {inv};")
                 return f"fmaf(-0.5f * {z}, {z}, {c})"
             return f"score_normal({_real(v)}, {_real(a[0])}, {_real(sd)})"
         if k == "uniform-continuous":
@@ -708,7 +709,7 @@ class _Compiler:
             if packed is not None:
                 return packed
         acc, i = g.fresh("ss"), g.fresh("i")
-        g.emit(f"float {acc} = 0.f;")
+        g.emit(f"VF {acc} = 0.f;")
         n = v.length()
         depth = self._loop(i, n, v.bound())
         env = dict(f.env)
@@ -717,13 +718,13 @@ class _Compiler:
         m = _scalar(self.ev(body.rhs.args[0].args[0], env), "normal mean")
         y = _scalar(self.ev(body.rhs.args[1], env), "observed value")
         z = g.fresh("z")
-        g.emit(f"const float {z} = {_real(y)} - {_real(m)};")
+        g.emit(f"const auto {z} = {_real(y)} - {_real(m)};")
         g.emit(f"{acc} = fmaf({z}, {z}, {acc});")
         for _ in range(depth):
             g.close()
         k = repr(float(np.float32(-0.5 / (sdv * sdv)))) + "f"
         c = repr(float(np.float32(-math.log(sdv) - 0.5 * math.log(2 * math.pi)))) + "f"
-        return S(f"({_real(init)} + fmaf({k}, {acc}, static_cast<float>({n.code}) * {c}))", "real", False)
+        return S(f"({_real(init)} + fmaf({k}, {acc}, to_f({n.code}) * {c}))", "real", False)
 
     def _gaussian_reduce_packed(self, f: Fn, body, v, n: int, init: S, sdv: float):
         """The Gaussian-likelihood reduce over pairs of elements: elements (i, i + 1) of the
@@ -742,7 +743,7 @@ class _Compiler:
             return None
         g = self.g
         acc, i = g.fresh("ss"), g.fresh("i")
-        g.emit(f"f32x2 {acc} = pack2(0.f, 0.f);")
+        g.emit(f"VF2 {acc} = pack2(0.f, 0.f);")
         g.emit("#pragma unroll 4")
         g.open(f"for (int {i} = 0; {i} + 1 < {n}; {i} += 2)")
         env = dict(f.env)
@@ -751,11 +752,11 @@ class _Compiler:
         m = self.ev(body.rhs.args[0].args[0], env)
         y = self.ev(body.rhs.args[1], env)
         z = g.fresh("z")
-        g.emit(f"const f32x2 {z} = fma2({_pair(m)}, pack2(-1.f, -1.f), {_pair(y)});")
+        g.emit(f"const auto {z} = fma2({_pair(m)}, pack2(-1.f, -1.f), {_pair(y)});")
         g.emit(f"{acc} = fma2({z}, {z}, {acc});")
         g.close()
         tot = g.fresh("ss")
-        g.emit(f"float {tot} = unpack2({acc}).x + unpack2({acc}).y;")
+        g.emit(f"VF {tot} = hsum2({acc});")
         if n % 2:  # odd length: the last element, scalar
             env = dict(f.env)
             env[f.params[0]] = S("0.f", "real")
@@ -763,7 +764,7 @@ class _Compiler:
             m = _scalar(self.ev(body.rhs.args[0].args[0], env), "normal mean")
             y = _scalar(self.ev(body.rhs.args[1], env), "observed value")
             z = g.fresh("z")
-            g.emit(f"const float {z} = {_real(y)} - {_real(m)};")
+            g.emit(f"const auto {z} = {_real(y)} - {_real(m)};")
             g.emit(f"{tot} = fmaf({z}, {z}, {tot});")
         k = repr(float(np.float32(-0.5 / (sdv * sdv)))) + "f"
         c = repr(float(np.float32(-math.log(sdv) - 0.5 * math.log(2 * math.pi)))) + "f"
@@ -909,11 +910,12 @@ class CompiledModel:
 
 
 _KERNEL = r'''
-#include "draws.cuh"
+#define MAXD {maxd}
+#include "dsl_lanes.cuh"
 #include "is_accum.cuh"
 using namespace cuppl;
-#define MAXD {maxd}
 {data_decl}
+// LANES particles per thread (dsl_lanes.cuh): particle (base + p * 256 + threadIdx.x) is lane p
 extern "C" __global__ void __launch_bounds__(256)
 cuppl_dsl_model(const float* __restrict__ D, unsigned long long pid_begin, unsigned long long n,
                 unsigned int k0, unsigned int k1, cuppl_is_record* block_recs, unsigned int* counter,
@@ -925,24 +927,34 @@ cuppl_dsl_model(const float* __restrict__ D, unsigned long long pid_begin, unsig
   unsigned int err = 0u;
   // block-uniform chunk loop (lanes past the end run masked): the model body stays in
   // uniform control flow, so warp-uniform data indices use the uniform datapath
-  for (unsigned long long base = blockIdx.x * 256ull; base < n;
-       base += static_cast<unsigned long long>(gridDim.x) * 256ull) {{
-    const unsigned long long idx = base + threadIdx.x;
-    const bool valid = idx < n;
-    const unsigned long long pid = pid_begin + idx;
-    WordStream ws;
+  for (unsigned long long base = blockIdx.x * (256ull * LANES); base < n;
+       base += static_cast<unsigned long long>(gridDim.x) * (256ull * LANES)) {{
+    VU64 idx;
+    VB valid;
+#pragma unroll
+    for (int p_ = 0; p_ < LANES; ++p_) {{
+      lane_ref(idx, p_) = base + p_ * 256ull + threadIdx.x;
+      lane_ref(valid, p_) = lane_ref(idx, p_) < n;
+    }}
+    const VU64 pid = idx + pid_begin;
+    VStream ws;
     ws.init(key, pid, {tag}u);
-    float lw = 0.f;
+    VF lw = 0.f;
     int nd = 0;
 {enum_init}
 {body}
 {enum_final}
-    if (valid) {{
-      float f[{ns_arr}] = {{{stats}}};
-      acc.add(lw, pid, f, {bin});
-      if (lw_out) lw_out[idx] = lw;
-      if (ret_out) {{
+#pragma unroll
+    for (int p_ = 0; p_ < LANES; ++p_) {{
+      const unsigned long long idx_ = lane_at(idx, p_);
+      if (lane_at(valid, p_)) {{
+        const float lw_ = lane_at(lw, p_);
+        float f[{ns_arr}] = {{{stats}}};
+        acc.add(lw_, pid_begin + idx_, f, lane_at({bin}, p_));
+        if (lw_out) lw_out[idx_] = lw_;
+        if (ret_out) {{
 {ret_store}
+        }}
       }}
     }}
     (void)nd;
@@ -954,9 +966,9 @@ cuppl_dsl_model(const float* __restrict__ D, unsigned long long pid_begin, unsig
 
 
 _MCMC_KERNEL = r"""
-#include "draws.cuh"
-using namespace cuppl;
 #define MAXD {maxd}
+#include "dsl_lanes.cuh"
+using namespace cuppl;
 {data_decl}
 // many independent LMH chains, one thread each (SPEC.md:408-416); the trace database of the
 // current state (old*) and of the proposal (new*) live in per-thread arrays
@@ -1029,32 +1041,31 @@ cuppl_dsl_mcmc(const float* __restrict__ D, unsigned int n_chains, unsigned int 
 
 
 def _return_parts(ret, g: _Gen):
-    """(stat expressions, stat names, bin expression, n_bins, kind, width, store lines)."""
+    """(stat expressions, stat names, bin expression, n_bins, kind, width, stores); a store is
+    (component index, value expression) of ret_out[idx * width + k]."""
     if ret is None:
         return [], [], "0", 0, "none", 0, []
     if isinstance(ret, S):
         v = g.let(ret, "ret")
         st = [_real(v), f"{_real(v)} * {_real(v)}"]
         if ret.ty in ("int", "bool"):
-            b = f"(({v.code}) >= 0 && ({v.code}) < {MAX_BINS} ? static_cast<int>({v.code}) : -1)"
-            return st, ["value", "value^2"], b, MAX_BINS, ret.ty, 1, [f"ret_out[idx] = {_real(v)};"]
-        return st, ["value", "value^2"], "0", 0, "real", 1, [f"ret_out[idx] = {_real(v)};"]
+            b = f"sel(({v.code}) >= 0 && ({v.code}) < {MAX_BINS}, to_i({v.code}), -1)"
+            return st, ["value", "value^2"], b, MAX_BINS, ret.ty, 1, [(0, _real(v))]
+        return st, ["value", "value^2"], "0", 0, "real", 1, [(0, _real(v))]
     if isinstance(ret, ConstVec):
         items = [g.let(x, "ret") for x in ret.items]
         if 2 * len(items) > MAX_STATS:
             raise CompileError(f"at most {MAX_STATS // 2} returned components")
         st = [_real(x) for x in items] + [f"{_real(x)} * {_real(x)}" for x in items]
         names = [f"v{k}" for k in range(len(items))] + [f"v{k}^2" for k in range(len(items))]
-        store = [f"ret_out[idx * {len(items)} + {k}] = {_real(x)};" for k, x in enumerate(items)]
-        return st, names, "0", 0, "vector", len(items), store
+        return st, names, "0", 0, "vector", len(items), [(k, _real(x)) for k, x in enumerate(items)]
     if isinstance(ret, LocVec):
         if ret.bound_ > MAX_STATS // 2:
             raise CompileError(f"returned vectors are bounded by {MAX_STATS // 2} elements")
-        comps = [f"({k} < {ret.length_.code} ? static_cast<float>({ret.var}[{k}]) : 0.f)" for k in range(ret.bound_)]
+        comps = [f"sel({k} < {ret.length_.code}, to_f({ret.var}[{k}]), 0.f)" for k in range(ret.bound_)]
         names = [f"v{k}" for k in range(ret.bound_)]
-        b = f"(({ret.length_.code}) >= 0 && ({ret.length_.code}) < {MAX_BINS} ? ({ret.length_.code}) : -1)"
-        store = [f"ret_out[idx * {ret.bound_ + 1} + {k}] = {c};" for k, c in enumerate(comps)]
-        store.append(f"ret_out[idx * {ret.bound_ + 1} + {ret.bound_}] = static_cast<float>({ret.length_.code});")
+        b = f"sel(({ret.length_.code}) >= 0 && ({ret.length_.code}) < {MAX_BINS}, to_i({ret.length_.code}), -1)"
+        store = list(enumerate(comps)) + [(ret.bound_, f"to_f({ret.length_.code})")]
         return comps, names, b, MAX_BINS, "vector", ret.bound_ + 1, store
     raise CompileError(f"unsupported return value {type(ret).__name__}")
 
@@ -1066,11 +1077,15 @@ def compile_program(source: str, data: dict | None = None) -> CompiledModel:
     ret = comp.compile()
     g = comp.g
     stats, names, bin_expr, nb, kind, width, store = _return_parts(ret, g)
+    lane_stats = [f"lane_at({x}, p_)" for x in stats]
     maxd = g.draw_bound if 0 < g.draw_bound <= MAX_TRACE_DRAWS else 1
     body = "\n".join("  " + line for line in g.lines)
     data_arr = np.asarray(g.data if g.data else [0.0], dtype=np.float32)
     if len(data_arr) <= MAX_CONST_DATA:  # warp-uniform indices: constant-cache broadcasts
-        data_decl = (f"__constant__ __align__(8) float DC[{len(data_arr)}];\n#define {DATA_SYM}(i) DC[i]\n"
+        data_decl = (f"__constant__ __align__(8) float DC[{len(data_arr)}];\n"
+                     "__device__ __forceinline__ float dat(int i) { return DC[i]; }\n"
+                     "CUPPL_LIFT(dat)  // a per-particle index: one constant-bank read per lane\n"
+                     f"#define {DATA_SYM}(i) dat(i)\n"
                      f"#define {DATA_SYM}2(i) (*reinterpret_cast<const f32x2*>(&DC[i]))")
     else:
         data_decl = (f"#define {DATA_SYM}(i) __ldg(D + (i))\n"
@@ -1097,8 +1112,9 @@ def compile_program(source: str, data: dict | None = None) -> CompiledModel:
                              max_draws=g.draw_bound, default_n=comp.default_n, engine="mcmc")
     cuda = _KERNEL.format(maxd=maxd, data_decl=data_decl, enum_init=enum_init, enum_final=enum_final,
                           ns=len(stats), nb=nb, ns_arr=max(len(stats), 1),
-                          stats=", ".join(stats) if stats else "0.f", bin=bin_expr, tag=TAG_DSL,
-                          body=body, ret_store="\n".join("        " + s for s in store))
+                          stats=", ".join(lane_stats) if stats else "0.f", bin=bin_expr, tag=TAG_DSL,
+                          body=body, ret_store="\n".join(f"          ret_out[idx_ * {width} + {k}] = lane_at({x}, p_);"
+                                                         for k, x in store))
     return CompiledModel(source=source, cuda=cuda, data=data_arr, n_stats=len(stats), n_bins=nb,
                          stat_names=names, return_kind=kind, return_width=width,
                          max_draws=g.draw_bound, default_n=comp.default_n, engine=comp.engine,
@@ -1109,7 +1125,7 @@ def compile_program(source: str, data: dict | None = None) -> CompiledModel:
 _MODULES: dict = {}
 
 
-def _nvrtc_cubin(src: str) -> bytes:
+def _nvrtc_cubin(src: str, lanes: int = 1) -> bytes:
     from cuda.bindings import nvrtc
 
     def ok(r, what):
@@ -1120,7 +1136,7 @@ def _nvrtc_cubin(src: str) -> bytes:
 
     prog = ok(nvrtc.nvrtcCreateProgram(src.encode(), b"cuppl_model.cu", 0, [], []), "create")
     opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-lineinfo", b"-default-device",
-            f"-I{CSRC}".encode(), f"-I{INCLUDE}".encode()]
+            f"-DLANES={lanes}".encode(), f"-I{CSRC}".encode(), f"-I{INCLUDE}".encode()]
     r = nvrtc.nvrtcCompileProgram(prog, len(opts), opts)
     if r[0] != nvrtc.nvrtcResult.NVRTC_SUCCESS:
         size = ok(nvrtc.nvrtcGetProgramLogSize(prog), "log size")
@@ -1134,23 +1150,48 @@ def _nvrtc_cubin(src: str) -> bytes:
     return cubin
 
 
+def _lanes_to_try(model: CompiledModel) -> list:
+    if model.engine != "importance":
+        return [1]
+    want = int(os.environ.get("CUPPL_DSL_LANES", DSL_LANES))
+    return [k for k in (8, 4, 2) if k <= want] + [1]
+
+
 def _function(model: CompiledModel):
-    """Load (once per process and source) the compiled kernel; returns a CUfunction."""
+    """Load (once per process and source) the compiled kernel; returns (CUfunction, lanes).
+    Importance kernels are first built with DSL_LANES particles per thread; a program whose
+    control flow depends on particle values does not compile that way (dsl_lanes.cuh), and a
+    build that spills registers is not kept: both fall back to one particle per thread."""
     from cuda.bindings import driver as cu
 
-    h = hashlib.sha256(model.cuda.encode() + model.data.tobytes()).hexdigest()
+    h = hashlib.sha256(model.cuda.encode() + model.data.tobytes() + repr(_lanes_to_try(model)).encode()).hexdigest()
     if h not in _MODULES:
         import torch
 
         torch.cuda.init()  # the primary context torch uses is current for the driver calls
-        cubin = _nvrtc_cubin(model.cuda)
-        err, mod = cu.cuModuleLoadData(cubin)
-        if err != cu.CUresult.CUDA_SUCCESS:
-            raise InferRuntimeError(f"cuModuleLoadData failed: {err}")
         name = b"cuppl_dsl_mcmc" if model.engine == "mcmc" else b"cuppl_dsl_model"
-        err, fn = cu.cuModuleGetFunction(mod, name)
-        if err != cu.CUresult.CUDA_SUCCESS:
-            raise InferRuntimeError(f"cuModuleGetFunction failed: {err}")
+        lane_divergent = False
+        for lanes in _lanes_to_try(model):
+            if lanes > 1 and lane_divergent:
+                continue
+            try:
+                cubin = _nvrtc_cubin(model.cuda, lanes)
+            except CompileError:
+                if lanes == 1:
+                    raise
+                lane_divergent = True  # a type error in lane form: no lane count will build
+                continue
+            err, mod = cu.cuModuleLoadData(cubin)
+            if err != cu.CUresult.CUDA_SUCCESS:
+                raise InferRuntimeError(f"cuModuleLoadData failed: {err}")
+            err, fn = cu.cuModuleGetFunction(mod, name)
+            if err != cu.CUresult.CUDA_SUCCESS:
+                raise InferRuntimeError(f"cuModuleGetFunction failed: {err}")
+            err, local = cu.cuFuncGetAttribute(cu.CUfunction_attribute.CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, fn)
+            if lanes > 1 and err == cu.CUresult.CUDA_SUCCESS and local > 0:
+                cu.cuModuleUnload(mod)
+                continue
+            break
         if " float DC[" in model.cuda:  # the data live in this module's constant bank
             err, dptr, size = cu.cuModuleGetGlobal(mod, b"DC")
             if err != cu.CUresult.CUDA_SUCCESS or size != model.data.nbytes:
@@ -1158,8 +1199,8 @@ def _function(model: CompiledModel):
             err, = cu.cuMemcpyHtoD(dptr, model.data.ctypes.data, model.data.nbytes)
             if err != cu.CUresult.CUDA_SUCCESS:
                 raise InferRuntimeError(f"cuMemcpyHtoD(DC) failed: {err}")
-        _MODULES[h] = (mod, fn)
-    return _MODULES[h][1]
+        _MODULES[h] = (mod, fn, lanes)
+    return _MODULES[h][1], _MODULES[h][2]
 
 
 class DslLauncher:
@@ -1180,7 +1221,7 @@ class DslLauncher:
         self.ws = torch.zeros(256 + self.max_grid * N.REC_BYTES, dtype=torch.uint8, device=self.device)
         self.rec = torch.empty(N.REC_BYTES, dtype=torch.uint8, device=self.device)
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
-        self.fn = _function(model)
+        self.fn, self.lanes = _function(model)
 
     def launch(self, pid_begin: int, pid_end: int, key: int, lw_out=None, draws_out=None, ret_out=None,
                rec_out=None, stream=None, **_):
@@ -1192,7 +1233,7 @@ class DslLauncher:
         n = pid_end - pid_begin
         if n <= 0:
             raise ValueError("empty particle range")
-        grid = int(min(self.max_grid, (n + 255) // 256))
+        grid = int(min(self.max_grid, (n + 256 * self.lanes - 1) // (256 * self.lanes)))
         rec = self.rec if rec_out is None else rec_out
         counter = self.ws[:4]
         blocks = self.ws[256:]
@@ -1269,7 +1310,7 @@ def run_mcmc(model: CompiledModel, n_steps: int, rng, *, chains: int = 4096, bur
 
     dev = device or torch.device("cuda", torch.cuda.current_device())
     data = torch.from_numpy(model.data).to(dev)
-    fn = _function(model)
+    fn, _ = _function(model)
     width = max(model.n_stats, 1) + max(model.n_bins, 1) + 2
     stats = torch.zeros((chains, width), dtype=torch.float64, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)

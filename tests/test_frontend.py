@@ -55,6 +55,21 @@ model <- function() {
 importance(model, 100000)
 """
 
+# lane-uniform control flow with per-particle discrete values: a component drawn per particle,
+# a data read at that index, a pure if (select), a discrete return (histogram)
+MIXTURE = """
+mus <- [-2.0, 3.0, 0.5];
+model <- function() {
+  z <- sample(uniform-discrete(0, 3));
+  s <- if (z == 1) { 0.5 } else { 1.0 };
+  x <- sample(normal(mus[z], s));
+  observe(normal(x, 0.7), 2.5);
+  observe(poisson(exp(x / 4.0)), 2);
+  z
+};
+importance(model, 100000)
+"""
+
 BRANCHY = """
 model <- function() {
   k <- sample(uniform-discrete(0, 3));
@@ -82,7 +97,7 @@ def test_parse_and_reject():
 def test_codegen_shapes():
     m = frontend.compile_program(FIG1)
     assert m.max_draws == 5 and m.n_bins == 8 and m.return_kind == "vector"
-    assert "ws.randint" in m.cuda and "ws.normal()" in m.cuda and "is_epilogue" in m.cuda
+    assert "ud_draw" in m.cuda and "ws.normal()" in m.cuda and "is_epilogue" in m.cuda
     m2 = frontend.compile_program(LINREG)
     assert m2.stat_names == ["v0", "v1", "v0^2", "v1^2"] and m2.max_draws == 2
     m3 = frontend.compile_program(BRANCHY)
@@ -108,7 +123,7 @@ def test_interpreter_known_value():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("src", [LINREG, FIG1, COIN, BRANCHY], ids=["linreg", "fig1", "coin", "branchy"])
+@pytest.mark.parametrize("src", [LINREG, FIG1, COIN, BRANCHY, MIXTURE], ids=["linreg", "fig1", "coin", "branchy", "mixture"])
 def test_gpu_log_weights_match_interpreter(cuda, src):
     """Injected-draw parity: the GPU records every draw; the fp64 interpreter
     replays them; log-weights agree to 1e-5 relative (fp32 evaluation)."""
@@ -127,6 +142,40 @@ def test_gpu_log_weights_match_interpreter(cuda, src):
             assert math.isinf(lw[i]) and lw[i] < 0
             continue
         assert abs(lw[i] - ref) <= 1e-5 * abs(ref) + 2e-5, (i, lw[i], ref, draws[i])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("src", [LINREG, COIN, MIXTURE], ids=["linreg", "coin", "mixture"])
+def test_gpu_lanes_match_one_particle_per_thread(cuda, src, monkeypatch):
+    """A lane-uniform program builds with several particles per thread (dsl_lanes.cuh); it
+    draws the same streams and weights as the one-particle-per-thread build of the same text."""
+    from paper_2010_08454_b200 import Rng, infer
+
+    m = frontend.compile_program(src)
+    assert frontend.DslLauncher(m).lanes > 1
+    n = 5000  # not a multiple of 256 * lanes: masked lanes in the last chunk
+    a = infer.run_importance(m, n, Rng(11), return_traces=True)
+    monkeypatch.setenv("CUPPL_DSL_LANES", "1")
+    assert frontend.DslLauncher(m).lanes == 1
+    b = infer.run_importance(m, n, Rng(11), return_traces=True)
+    np.testing.assert_array_equal(a.traces["draws"].cpu().numpy(), b.traces["draws"].cpu().numpy())
+    np.testing.assert_allclose(a.traces["log_weight"].cpu().numpy(), b.traces["log_weight"].cpu().numpy(),
+                               rtol=1e-6, atol=1e-6)
+    assert abs(a.log_z - b.log_z) < 1e-5 * abs(b.log_z) + 1e-6
+    assert a.mode_index == b.mode_index
+
+
+def test_lane_divergent_programs_fall_back():
+    """Control flow on particle values has no lane form: NVRTC rejects the lane build (the
+    loader then builds LANES=1); lane-uniform programs build at LANES=8."""
+    for src, lane_ok in ((LINREG, True), (MIXTURE, True), (FIG1, False), (BRANCHY, False)):
+        m = frontend.compile_program(src)
+        frontend._nvrtc_cubin(m.cuda, 1)
+        if lane_ok:
+            frontend._nvrtc_cubin(m.cuda, 8)
+        else:
+            with pytest.raises(frontend.CompileError):
+                frontend._nvrtc_cubin(m.cuda, 8)
 
 
 @pytest.mark.gpu

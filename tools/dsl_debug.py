@@ -19,7 +19,7 @@ for name in sys.argv[1:] or ["FIG1", "LINREG"]:
     src = getattr(t, name)
     m = frontend.compile_program(src)
     post = infer.run_importance(m, 64, Rng(3), return_traces=True)
-    h = __import__("hashlib").sha256(m.cuda.encode() + m.data.tobytes()).hexdigest()
+    h = __import__("hashlib").sha256(m.cuda.encode() + m.data.tobytes() + repr(frontend._lanes_to_try(m)).encode()).hexdigest()
     mod = frontend._MODULES[h][0]
     err, dptr, size = cu.cuModuleGetGlobal(mod, b"DC")
     buf = np.zeros(size // 4, dtype=np.float32)
