@@ -197,15 +197,38 @@ CUPPL_LIFT(score_uniform_continuous)
 CUPPL_LIFT(score_beta)
 CUPPL_LIFT(score_exponential)
 
+// ------------------------------------------------------------------ masks --------------
+// Particle-dependent control flow in lane form: a bounded loop `i < n` or an `if` with side
+// effects opens a mask m (bool, or Lane<bool> when the condition differs per particle) and an
+// `if (lanes_any(m))` block; inside it draws consume a lane's stream only where its mask bit
+// is set, factors add sel(m, x, 0) and outer accumulators are updated as sel(m, new, old).
+// With LANES == 1 (or a uniform condition) m is true inside its block and this is plain code.
+__device__ __forceinline__ bool lanes_any(bool m) { return m; }
+
 // ------------------------------------------------------------------ draws --------------
 // uniform-discrete(lo, hi): support [lo, hi); an empty range raises
 // InvalidDistParamError on the host (err word) and draws from [lo, lo + 1)
 __device__ __forceinline__ unsigned ud_check(bool valid, int lo, int hi) {
   return valid && !(hi > lo) ? 1u : 0u;
 }
-__device__ __forceinline__ int ud_draw(WordStream& ws, int lo, int hi) {
+__device__ __forceinline__ int ud_draw1(WordStream& ws, int lo, int hi) {
   return lo + static_cast<int>(ws.randint(static_cast<unsigned>(hi > lo ? hi - lo : 1)));
 }
+// one-stream draws: the enclosing block already holds the mask
+template <class M>
+__device__ __forceinline__ int ud_draw(WordStream& ws, int lo, int hi, const M&) {
+  return ud_draw1(ws, lo, hi);
+}
+template <class M>
+__device__ __forceinline__ float draw_normal(WordStream& ws, const M&) { return ws.normal(); }
+template <class M>
+__device__ __forceinline__ float draw_uniform(WordStream& ws, const M&) { return ws.uniform(); }
+template <class M>
+__device__ __forceinline__ float draw_uniform_pos(WordStream& ws, const M&) { return ws.uniform_pos(); }
+template <class M>
+__device__ __forceinline__ float draw_gamma(WordStream& ws, float a, const M&) { return ws.gamma(a); }
+template <class M>
+__device__ __forceinline__ int draw_poisson(WordStream& ws, float lam, const M&) { return ws.poisson(lam); }
 __device__ __forceinline__ void store_draw(float* out, unsigned long long idx, bool valid, int nd, float x) {
   if (out && valid && nd < MAXD) out[idx * MAXD + nd] = x;
 }
@@ -218,27 +241,36 @@ struct LaneStream {
 #pragma unroll
     for (int p = 0; p < LANES; ++p) s[p].init(k, id.v[p], t);
   }
-#define CUPPL_STREAM0(T, fn)                                                                \
-  __device__ __forceinline__ Lane<T> fn() {                                                 \
-    Lane<T> r;                                                                              \
-    _Pragma("unroll") for (int p = 0; p < LANES; ++p) r.v[p] = s[p].fn();                   \
-    return r;                                                                               \
-  }
-#define CUPPL_STREAM1(T, fn)                                                                \
-  template <class A>                                                                        \
-  __device__ __forceinline__ Lane<T> fn(const A& a) {                                       \
-    Lane<T> r;                                                                              \
-    _Pragma("unroll") for (int p = 0; p < LANES; ++p) r.v[p] = s[p].fn(lane_at(a, p));      \
-    return r;                                                                               \
-  }
-  CUPPL_STREAM0(float, uniform)
-  CUPPL_STREAM0(float, uniform_pos)
-  CUPPL_STREAM0(float, normal)
-  CUPPL_STREAM1(float, gamma)
-  CUPPL_STREAM1(int, poisson)
-#undef CUPPL_STREAM0
-#undef CUPPL_STREAM1
 };
+__device__ __forceinline__ bool lanes_any(const Lane<bool>& m) {
+  bool r = false;
+#pragma unroll
+  for (int p = 0; p < LANES; ++p) r = r || m.v[p];
+  return r;
+}
+// lane p draws from its own stream only where its mask bit is set (0 elsewhere)
+#define CUPPL_LANE_DRAW0(T, name, fn)                                                       \
+  template <class M>                                                                        \
+  __device__ __forceinline__ Lane<T> name(LaneStream& ws, const M& m) {                     \
+    Lane<T> r;                                                                              \
+    _Pragma("unroll") for (int p = 0; p < LANES; ++p) r.v[p] = lane_at(m, p) ? ws.s[p].fn() : T(0); \
+    return r;                                                                               \
+  }
+#define CUPPL_LANE_DRAW1(T, name, fn)                                                       \
+  template <class A, class M>                                                               \
+  __device__ __forceinline__ Lane<T> name(LaneStream& ws, const A& a, const M& m) {         \
+    Lane<T> r;                                                                              \
+    _Pragma("unroll") for (int p = 0; p < LANES; ++p)                                       \
+      r.v[p] = lane_at(m, p) ? ws.s[p].fn(lane_at(a, p)) : T(0);                             \
+    return r;                                                                               \
+  }
+CUPPL_LANE_DRAW0(float, draw_normal, normal)
+CUPPL_LANE_DRAW0(float, draw_uniform, uniform)
+CUPPL_LANE_DRAW0(float, draw_uniform_pos, uniform_pos)
+CUPPL_LANE_DRAW1(float, draw_gamma, gamma)
+CUPPL_LANE_DRAW1(int, draw_poisson, poisson)
+#undef CUPPL_LANE_DRAW0
+#undef CUPPL_LANE_DRAW1
 template <class A, class B>
 __device__ __forceinline__ unsigned ud_check(const Lane<bool>& valid, const A& lo, const B& hi) {
   unsigned e = 0u;
@@ -246,18 +278,19 @@ __device__ __forceinline__ unsigned ud_check(const Lane<bool>& valid, const A& l
   for (int p = 0; p < LANES; ++p) e |= ud_check(valid.v[p], lane_at(lo, p), lane_at(hi, p));
   return e;
 }
-template <class A, class B>
-__device__ __forceinline__ Lane<int> ud_draw(LaneStream& ws, const A& lo, const B& hi) {
+template <class A, class B, class M>
+__device__ __forceinline__ Lane<int> ud_draw(LaneStream& ws, const A& lo, const B& hi, const M& m) {
   Lane<int> r;
 #pragma unroll
-  for (int p = 0; p < LANES; ++p) r.v[p] = ud_draw(ws.s[p], lane_at(lo, p), lane_at(hi, p));
+  for (int p = 0; p < LANES; ++p)
+    r.v[p] = lane_at(m, p) ? ud_draw1(ws.s[p], lane_at(lo, p), lane_at(hi, p)) : 0;
   return r;
 }
-template <class X>
+template <class N, class X>
 __device__ __forceinline__ void store_draw(float* out, const Lane<unsigned long long>& idx,
-                                           const Lane<bool>& valid, int nd, const X& x) {
+                                           const Lane<bool>& valid, const N& nd, const X& x) {
 #pragma unroll
-  for (int p = 0; p < LANES; ++p) store_draw(out, idx.v[p], valid.v[p], nd, to_f(lane_at(x, p)));
+  for (int p = 0; p < LANES; ++p) store_draw(out, idx.v[p], valid.v[p], lane_at(nd, p), to_f(lane_at(x, p)));
 }
 typedef Lane<float> VF;
 typedef Lane<int> VI;

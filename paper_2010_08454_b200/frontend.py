@@ -185,6 +185,8 @@ class _Gen:
         self.loop_mult = [1]
         self.depth = 0
         self.bounds: dict = {}  # C variable of a uniform-discrete draw -> largest value
+        self.masks: list = []  # (indent, C name) of the open particle masks, innermost last
+        self.masked = False  # some control flow depends on particle values
 
     def fresh(self, p="t"):
         self.n += 1
@@ -200,6 +202,38 @@ class _Gen:
     def close(self):
         self.ind -= 2
         self.emit("}")
+        while self.masks and self.masks[-1][0] > self.ind:
+            self.masks.pop()
+
+    def mask(self):
+        """The innermost open particle mask (None at the top level of the model)."""
+        return self.masks[-1][1] if self.masks else None
+
+    def open_masked(self, cond: str):
+        """`if (cond)` on particle values (dsl_lanes.cuh): the block runs when some lane needs
+        it, and its effects apply to the lanes of mask (outer masks && cond)."""
+        m = self.fresh("m")
+        self.masked = True
+        outer = self.mask()
+        self.emit(f"const auto {m} = {outer + ' && ' if outer else ''}({cond});")
+        self.open(f"if (lanes_any({m}))")
+        self.masks.append((self.ind, m))
+
+    def assign(self, var: str, expr: str):
+        """var = expr in the active lanes."""
+        m = self.mask()
+        self.emit(f"{var} = sel({m}, {expr}, {var});" if m else f"{var} = {expr};")
+
+    def add_lw(self, x: str):
+        m = self.mask()
+        self.emit(f"lw += sel({m}, {x}, 0.f);" if m else f"lw += {x};")
+
+    def valid_m(self) -> str:
+        m = self.mask()
+        return f"valid && {m}" if m else "valid"
+
+    def draw_m(self) -> str:
+        return self.mask() or "true"
 
     def let(self, v: S, hint="t") -> S:
         if v.code.isidentifier() or _is_literal(v.code):
@@ -431,17 +465,18 @@ class _Compiler:
         del g.lines[mark:]
         res = g.fresh("r")
         g.emit(f"VF {res} = 0.f;")
-        g.open(f"if ({c.code})")
+        cv = g.let(c, "c")
+        g.open_masked(cv.code)
         t = self.ev(e.then, dict(env))
         tt = t.ty if isinstance(t, S) else None
         if isinstance(t, S):
-            g.emit(f"{res} = {_real(t)};")
+            g.assign(res, _real(t))
         g.close()
         bt, g.draw_bound = g.draw_bound - b0, b0
-        g.open("else")
+        g.open_masked(f"!{cv.code}")
         f = self.ev(e.orelse, dict(env))
         if isinstance(f, S):
-            g.emit(f"{res} = {_real(f)};")
+            g.assign(res, _real(f))
         g.close()
         g.draw_bound = b0 + max(bt, g.draw_bound - b0)  # draws per path: the longer branch
         if tt is None:
@@ -466,12 +501,12 @@ class _Compiler:
                 return self._sample(d)
             if name == "factor":
                 x = _scalar(self.ev(e.args[0], env), "factor")
-                g.emit(f"lw += {_real(x)};")
+                g.add_lw(_real(x))
                 return None
             if name == "observe":
                 d = self.ev(e.args[0], env)
                 v = _scalar(self.ev(e.args[1], env), "observe")
-                g.emit(f"lw += {self._score(d, v)};")
+                g.add_lw(self._score(d, v))
                 return None
             if name == "dist-score":
                 d = self.ev(e.args[0], env)
@@ -527,24 +562,25 @@ class _Compiler:
         g = self.g
         ty = _DISTS[k][1]
         lhs = f"const {_cty(ty)} {v}" if decl else v
+        m = g.draw_m()
         if k == "normal":
-            g.emit(f"{lhs} = {_real(a[0])} + {_real(a[1])} * ws.normal();")
+            g.emit(f"{lhs} = fmaf({_real(a[1])}, draw_normal(ws, {m}), {_real(a[0])});")
         elif k == "uniform-continuous":
-            g.emit(f"{lhs} = {_real(a[0])} + ({_real(a[1])} - {_real(a[0])}) * ws.uniform();")
+            g.emit(f"{lhs} = fmaf({_real(a[1])} - {_real(a[0])}, draw_uniform(ws, {m}), {_real(a[0])});")
         elif k == "uniform-discrete":
-            g.emit(f"err |= ud_check(valid, {a[0].code}, {a[1].code});")
-            g.emit(f"{lhs} = ud_draw(ws, {a[0].code}, {a[1].code});")
+            g.emit(f"err |= ud_check({g.valid_m()}, {a[0].code}, {a[1].code});")
+            g.emit(f"{lhs} = ud_draw(ws, {a[0].code}, {a[1].code}, {m});")
         elif k == "bernoulli":
-            g.emit(f"{lhs} = ws.uniform() < {_real(a[0])};")
+            g.emit(f"{lhs} = draw_uniform(ws, {m}) < {_real(a[0])};")
         elif k == "beta":
             gx, gy = g.fresh("gx"), g.fresh("gy")
-            g.emit(f"const auto {gx} = ws.gamma({_real(a[0])});")
-            g.emit(f"const auto {gy} = ws.gamma({_real(a[1])});")
+            g.emit(f"const auto {gx} = draw_gamma(ws, {_real(a[0])}, {m});")
+            g.emit(f"const auto {gy} = draw_gamma(ws, {_real(a[1])}, {m});")
             g.emit(f"{lhs} = {gx} / ({gx} + {gy});")
         elif k == "exponential":
-            g.emit(f"{lhs} = -logf(ws.uniform_pos()) / {_real(a[0])};")
+            g.emit(f"{lhs} = -logf(draw_uniform_pos(ws, {m})) / {_real(a[0])};")
         elif k == "poisson":
-            g.emit(f"{lhs} = ws.poisson({_real(a[0])});")
+            g.emit(f"{lhs} = draw_poisson(ws, {_real(a[0])}, {m});")
 
     def _sample(self, d: Dist) -> S:
         g = self.g
@@ -560,8 +596,8 @@ class _Compiler:
         if self.engine == "mcmc":
             return self._lmh_site(d, a, v, ty)
         self._emit_draw(k, a, v)
-        g.emit(f"store_draw(draws_out, idx, valid, nd, {v});")
-        g.emit("++nd;")
+        g.emit(f"store_draw(draws_out, idx, {g.valid_m()}, nd, {v});")
+        g.emit(f"nd += to_i({g.mask()});" if g.mask() else "nd += 1;")
         return S(v, ty, False)
 
     def _lmh_site(self, d: Dist, a, v: str, ty: str) -> S:
@@ -719,7 +755,7 @@ class _Compiler:
         y = _scalar(self.ev(body.rhs.args[1], env), "observed value")
         z = g.fresh("z")
         g.emit(f"const auto {z} = {_real(y)} - {_real(m)};")
-        g.emit(f"{acc} = fmaf({z}, {z}, {acc});")
+        g.assign(acc, f"fmaf({z}, {z}, {acc})")
         for _ in range(depth):
             g.close()
         k = repr(float(np.float32(-0.5 / (sdv * sdv)))) + "f"
@@ -778,7 +814,7 @@ class _Compiler:
             g.emit("#pragma unroll")
             g.open(f"for (int {i} = 0; {i} < {bound}; ++{i})")
             if not (_is_literal(n.code) and int(n.code) == bound):
-                g.open(f"if ({i} < {n.code})")
+                g.open_masked(f"{i} < {n.code}")
                 return 2
             return 1
         g.emit("#pragma unroll 4")
@@ -840,7 +876,7 @@ class _Compiler:
         x = v.elem(self, S(i, "int"))
         r = self._apply(f, [S(acc, ty), x])
         g.loop_mult.pop()
-        g.emit(f"{acc} = {r.code if ty != 'real' else _real(r)};")
+        g.assign(acc, r.code if ty != 'real' else _real(r))
         for _ in range(depth):
             g.close()
         return S(acc, ty, False)
@@ -905,6 +941,7 @@ class CompiledModel:
     default_n: int
     engine: str = "importance"
     radix: int = 1
+    masked: bool = False  # particle-dependent control flow (lane builds are opt-in)
     kind: str = "dsl"
     _fn: object = field(default=None, repr=False)
 
@@ -940,7 +977,7 @@ cuppl_dsl_model(const float* __restrict__ D, unsigned long long pid_begin, unsig
     VStream ws;
     ws.init(key, pid, {tag}u);
     VF lw = 0.f;
-    int nd = 0;
+    VI nd = 0;
 {enum_init}
 {body}
 {enum_final}
@@ -1118,7 +1155,7 @@ def compile_program(source: str, data: dict | None = None) -> CompiledModel:
     return CompiledModel(source=source, cuda=cuda, data=data_arr, n_stats=len(stats), n_bins=nb,
                          stat_names=names, return_kind=kind, return_width=width,
                          max_draws=g.draw_bound, default_n=comp.default_n, engine=comp.engine,
-                         radix=max(comp.radix, 2) if comp.engine == "enumerate" else 1)
+                         radix=max(comp.radix, 2) if comp.engine == "enumerate" else 1, masked=g.masked)
 
 
 # ----------------------------------------------------------------------------- JIT -------
@@ -1151,9 +1188,14 @@ def _nvrtc_cubin(src: str, lanes: int = 1) -> bytes:
 
 
 def _lanes_to_try(model: CompiledModel) -> list:
+    """Lane counts to build, best first. Programs with particle-dependent control flow build
+    at one particle per thread unless CUPPL_DSL_LANES asks otherwise: their masked lane form
+    is correct but measured slower (Fig.1: 6.0e10 particles/s at 1 lane, 4.3e10 at 2, 2.9e10
+    at 8 — per-lane conditional draws and a select per masked update)."""
     if model.engine != "importance":
         return [1]
-    want = int(os.environ.get("CUPPL_DSL_LANES", DSL_LANES))
+    env = os.environ.get("CUPPL_DSL_LANES")
+    want = int(env) if env else (1 if model.masked else DSL_LANES)
     return [k for k in (8, 4, 2) if k <= want] + [1]
 
 
