@@ -104,16 +104,20 @@ __device__ __forceinline__ float fast_cos(float x) {
 constexpr float kLn2 = 0.69314718055994530942f;
 constexpr float kLog2e = 1.44269504088896340736f;
 constexpr float kTwoPi = 6.28318530717958647692f;
+constexpr float kPi = 3.14159265358979323846f;
 constexpr float kHalfLog2Pi = 0.91893853320467274178f;
 
 // Box-Muller pair (cuppl/rng.py:58-71 without the cached spare: both normals are used).
 // u1 in (0,1] from wa, u2 in [0,1) from wb; r = sqrt(-2 ln u1); (r cos 2pi u2, r sin 2pi u2).
+// The angle is taken as 2pi u2 - pi in [-pi, pi) — sin.approx / cos.approx meet their 2^-20.5
+// absolute-error bound only there (2pi u2 up to 2pi measured ~1.6e-5) — and the signs flipped:
+// cos(t + pi) = -cos t, sin(t + pi) = -sin t.
 __device__ __forceinline__ float2 box_muller(uint32_t wa, uint32_t wb) {
   const float u1 = u01_open0(wa);
   const float u2 = u01_closed0(wb);
   const float r = fast_sqrt(-2.0f * kLn2 * fast_lg2(u1));
-  const float th = kTwoPi * u2;
-  return make_float2(r * fast_cos(th), r * fast_sin(th));
+  const float th = fmaf(kTwoPi, u2, -kPi);
+  return make_float2(-r * fast_cos(th), -r * fast_sin(th));
 }
 
 // ---------------------------------------------------------------- packed fp32 ----------

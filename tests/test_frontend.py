@@ -198,6 +198,30 @@ def test_lane_divergent_programs_fall_back():
 
 
 @pytest.mark.gpu
+def test_gpu_streams_keyed_by_global_pid(cuda):
+    """A particle's draws depend only on (key, global pid): the same in a window crossing 2^32
+    as launched alone, and pid 2^32 + k differs from pid k (the counter's high word)."""
+    import torch
+
+    m = frontend.compile_program(LINREG)
+    la = frontend.DslLauncher(m)
+    key = 0x1234_5678_9ABC_DEF0
+    first, n = (1 << 32) - 700, 1400
+    draws = torch.empty((n, m.max_draws), dtype=torch.float32, device=la.device)
+    lw = torch.empty(n, dtype=torch.float32, device=la.device)
+    la.launch(first, first + n, key, lw_out=lw, draws_out=draws)
+    for k in (0, 699, 700, 1399):
+        d1 = torch.empty((1, m.max_draws), dtype=torch.float32, device=la.device)
+        l1 = torch.empty(1, dtype=torch.float32, device=la.device)
+        la.launch(first + k, first + k + 1, key, lw_out=l1, draws_out=d1)
+        assert torch.equal(d1[0], draws[k]) and torch.equal(l1[0], lw[k])
+    low = torch.empty((700, m.max_draws), dtype=torch.float32, device=la.device)
+    la.launch(0, 700, key, draws_out=low)  # pids k = 0..699 vs 2^32 + k (draws[700:])
+    assert not torch.equal(low, draws[700:])
+    assert (low != draws[700:]).all(dim=1).float().mean() > 0.99
+
+
+@pytest.mark.gpu
 def test_gpu_known_answers(cuda):
     from paper_2010_08454_b200 import Rng, infer
 

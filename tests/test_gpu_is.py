@@ -158,32 +158,44 @@ def test_linreg_injected_draws_parity(cuda, oracle_lib, D):
     assert S == pytest.approx(ref["sum_w"], rel=1e-3)
 
 
-def test_poly_philox_traces_match_oracle(cuda, oracle_lib):
+# particle-id windows: small ids, one crossing 2^32 (the counter's high word), and C5's range
+# (1e11 particles: ids above 2^36)
+PID_WINDOWS = [12345, (1 << 32) - 40_000, 10**11 - 7]
+
+
+@pytest.mark.parametrize("first", PID_WINDOWS)
+def test_poly_philox_traces_match_oracle(cuda, oracle_lib, first):
     """Philox mode: the degree draws are bit-exact; coefficients agree to fp32 SFU accuracy; the
     log-weight of the GPU's own trace agrees with the oracle fp64 evaluation (D11)."""
     from paper_2010_08454_b200 import models
 
     m = models.PolyRegression.synthetic()
-    n, first = 100_000, 12345
+    n = 100_000
     lw, deg, coef, rec = _run_traced(m, n, KEY, first=first)
     _, (lw_ref, deg_ref, coef_ref) = oracle_lib.is_poly(m.xs, m.ys, first, first + n, KEY, traces=True)
     assert np.array_equal(deg, deg_ref)
-    assert np.all(np.abs(coef - coef_ref) <= 1e-4 * (1 + np.abs(coef_ref)))
+    # fp32 SFU Box-Muller: lg2.approx's absolute error (~2^-22) is a large relative error of the
+    # radius when u1 -> 1, so normals near 0 carry |dz| up to ~4e-5 (x sd = 10 here)
+    assert np.all(np.abs(coef - coef_ref) <= 1e-4 * np.abs(coef_ref) + 5e-4)
     inj = np.concatenate([deg[:, None].astype(np.float32), coef], axis=1)
     _, (lw_inj, _, _) = oracle_lib.is_poly(m.xs, m.ys, first, first + n, KEY, injected=inj, traces=True)
     assert tol_ok(lw, lw_inj).all()
 
 
-def test_linreg_philox_traces_match_oracle(cuda, oracle_lib):
+@pytest.mark.parametrize("first", [0] + PID_WINDOWS[1:])
+def test_linreg_philox_traces_match_oracle(cuda, oracle_lib, first):
     from paper_2010_08454_b200 import models
 
     m = models.LinearRegression.synthetic()
     n = 50_000
-    lw, _, coef, rec = _run_traced(m, n, KEY)
-    _, (lw_ref, coef_ref) = oracle_lib.is_linreg(m.xs, m.ys, 1.0, 0, n, KEY, traces=True)
-    assert np.all(np.abs(coef - coef_ref) <= 1e-4 * (1 + np.abs(coef_ref)))
-    _, (lw_inj, _) = oracle_lib.is_linreg(m.xs, m.ys, 1.0, 0, n, KEY, injected=coef, traces=True)
+    lw, _, coef, rec = _run_traced(m, n, KEY, first=first)
+    _, (lw_ref, coef_ref) = oracle_lib.is_linreg(m.xs, m.ys, 1.0, first, first + n, KEY, traces=True)
+    assert np.all(np.abs(coef - coef_ref) <= 1e-4 * np.abs(coef_ref) + 5e-4)  # see the poly test
+    _, (lw_inj, _) = oracle_lib.is_linreg(m.xs, m.ys, 1.0, first, first + n, KEY, injected=coef, traces=True)
     assert tol_ok(lw, lw_inj).all()
+    # the record's mode is a global particle id (u64)
+    k = int(np.argmax(lw))
+    assert rec["argmax_pid"] == first + k or lw[int(rec["argmax_pid"]) - first] == lw[k]
 
 
 def test_is_deterministic_and_traces_do_not_change_record(cuda):
