@@ -25,7 +25,8 @@ def _gpu_run(model, n, steps, local_world=None, record_ancestors=True, hist_step
 
 
 @pytest.mark.parametrize("n,S,steps", [(100_000, 50, 12), (8 * 1031, 7, 20), (64, 3, 10), (262_144, 50, 5),
-                                       (70_001, 100, 6), (20_000, 256, 4)])
+                                       (70_001, 100, 6), (20_000, 256, 4),
+                                       (16, 4, 5), (17, 3, 6), (33, 2, 4), (4097, 2, 5)])
 def test_smc_bit_exact_single_rank(cuda, oracle_lib, n, S, steps):
     from paper_2010_08454_b200 import models
 
@@ -56,6 +57,33 @@ def test_smc_rank_partition_invariance(cuda, oracle_lib, R):
     assert np.array_equal(res.total_weight, ref["T"])
     for t in range(steps - 1):
         assert np.array_equal(anc[t], ref["ancestors"][t]), f"R={R}: ancestors differ at step {t}"
+    assert np.array_equal(x, ref["x"]) and np.array_equal(lw.view(np.uint32), ref["lw"].view(np.uint32))
+
+
+def test_smc_population_below_rank_granule_is_refused(cuda):
+    """Rank boundaries are multiples of 16 particles (16-byte state stores): fewer than 16 per
+    rank is refused up front rather than run on empty ranks."""
+    from paper_2010_08454_b200 import models, smc
+
+    m = models.HiddenMarkovModel.synthetic(S=4, T=3, seed=6)
+    for n, R in ((1, 1), (15, 1), (127, 8)):
+        with pytest.raises(ValueError):
+            smc.SmcRunner(m, n, KEY, local_world=R if R > 1 else None, steps=3)
+
+
+@pytest.mark.parametrize("n,R", [(128, 8), (131, 8), (4096 * 3 + 1, 3)])
+def test_smc_small_rank_shares(cuda, oracle_lib, n, R):
+    """The smallest rank shares (16 particles, ragged last rank) and tile-boundary splits stay
+    bit-exact."""
+    from paper_2010_08454_b200 import models
+
+    steps = 6
+    m = models.HiddenMarkovModel.synthetic(S=5, T=steps, seed=6)
+    res, x, lw, anc = _gpu_run(m, n, steps, local_world=R)
+    ref = oracle_lib.smc_run(m, n, KEY, record_ancestors=True)
+    assert np.array_equal(res.total_weight, ref["T"])
+    for t in range(steps - 1):
+        assert np.array_equal(anc[t], ref["ancestors"][t]), f"ancestors differ at step {t}"
     assert np.array_equal(x, ref["x"]) and np.array_equal(lw.view(np.uint32), ref["lw"].view(np.uint32))
 
 
