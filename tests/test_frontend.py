@@ -197,6 +197,42 @@ def test_lane_divergent_programs_fall_back():
                 frontend._nvrtc_cubin(m.cuda, 8)
 
 
+LINREG_EXT = """
+model <- function() {
+  a <- sample(normal(0, 10));
+  b <- sample(normal(0, 10));
+  factor(reduce(function(acc, i) { acc + dist-score(normal(a * xs[i] + b, 1), ys[i]) }, 0.0,
+                repeat(function(i) { i }, length(xs))));
+  [a, b]
+};
+importance(model, 1000)
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("D", [1, 2, 3, 999, 1000, 17_000])
+def test_gpu_data_lengths_match_interpreter(cuda, D):
+    """Host data of any length: odd lengths take the packed reduce's scalar tail; more than
+    MAX_CONST_DATA floats move the data from the constant bank to global loads."""
+    from oracle.dsl_eval import Interpreter
+    from paper_2010_08454_b200 import Rng, infer
+
+    rs = np.random.default_rng(D)
+    xs = rs.uniform(-1, 1, D)
+    ys = 2 * xs - 1 + rs.normal(size=D)
+    data = {"xs": xs, "ys": ys}
+    m = frontend.compile_program(LINREG_EXT, data=dict(data))
+    assert ("__ldg" in m.cuda) == (2 * D > frontend.MAX_CONST_DATA)
+    n = 3000
+    post = infer.run_importance(m, n, Rng(2), return_traces=True)
+    lw = post.traces["log_weight"].cpu().numpy().astype(float)
+    draws = post.traces["draws"].cpu().numpy().astype(float)
+    it = Interpreter(LINREG_EXT, data=data)
+    for i in range(0, n, 37):
+        ref, _ = it.run(draws[i])
+        assert abs(lw[i] - ref) <= 1e-5 * abs(ref) + 2e-5, (D, i, lw[i], ref)
+
+
 @pytest.mark.gpu
 def test_gpu_streams_keyed_by_global_pid(cuda):
     """A particle's draws depend only on (key, global pid): the same in a window crossing 2^32
