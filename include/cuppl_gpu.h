@@ -170,6 +170,10 @@ typedef struct cuppl_smc_model {
                                /*   entry = thr (bits 0..32, in [0, 2^32]) | alias << 40    */
   const uint64_t* alias_init;  /* device [S] alias table of the initial distribution       */
   const float* mu;            /* HOST [S] emission means (passed by value to the kernels)   */
+  const uint64_t* key_dev;    /* optional DEVICE Philox key: when non-NULL, cuppl_smc_init /  */
+                              /*   cuppl_smc_resample read the key here at run time and ignore */
+                              /*   their `key` argument (one captured CUDA graph of the whole  */
+                              /*   time-step loop then serves every seed)                      */
 } cuppl_smc_model;
 
 /* Scratch for one rank of n_local particles: segment offsets, look-back words, counters,

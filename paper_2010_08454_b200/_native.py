@@ -69,6 +69,7 @@ class SmcModel(C.Structure):
         ("alias_trans", C.c_void_p),
         ("alias_init", C.c_void_p),
         ("mu", C.c_void_p),
+        ("key_dev", C.c_void_p),
     ]
 
 

@@ -92,6 +92,7 @@ int cuppl_smc_init(const cuppl_smc_model* m, uint64_t n_local, uint64_t j_begin,
   a.n_local = n_local;
   a.j_begin = j_begin;
   a.key = key;
+  a.key_dev = reinterpret_cast<const unsigned long long*>(m->key_dev);
   a.y0 = y0;
   a.x = x;
   a.m_key = m_key;
@@ -145,6 +146,7 @@ int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_to
   a.n_local = n_local;
   a.n_total = n_total;
   a.key = key;
+  a.key_dev = reinterpret_cast<const unsigned long long*>(m->key_dev);
   a.t = t;
   a.rank = rank;
   a.world = world;

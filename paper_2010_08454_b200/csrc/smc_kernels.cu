@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kSmcThreads) smc_init_kernel(const __grid_cons
   __shared__ float lwS[kMaxStates];
   build_tables(m, a.y0, neg_inf_f(), lwS, nullptr, nullptr);
   __syncthreads();
-  const PhiloxKey key = make_key(a.key);
+  const PhiloxKey key = make_key(a.key_dev ? *a.key_dev : a.key);
   float bmax = neg_inf_f();
   const unsigned long long nq = (a.n_local + 3) / 4;
   for (unsigned long long q = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
@@ -469,7 +469,7 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
   }
   __syncthreads();
   for (int s = tid; s < m.S; s += kSmcThreads) wdS[s] = static_cast<double>(wS[s]);
-  const PhiloxKey key = make_key(a.key);
+  const PhiloxKey key = make_key(a.key_dev ? *a.key_dev : a.key);
   __shared__ Comb s_cb;  // step constants (the rare exact rank path reads them here)
   if (tid == 0) {
     Comb c;

@@ -34,6 +34,7 @@ struct SmcInitArgs {
   unsigned long long n_local;  // particles on this rank
   unsigned long long j_begin;  // global index of local particle 0 (multiple of 8)
   unsigned long long key;
+  const unsigned long long* key_dev;  // when non-NULL: the key, read at run time (graph replay)
   float y0;
   int pad_;
   uint8_t* x;
@@ -58,6 +59,7 @@ struct SmcResampleArgs {
   unsigned long long n_local;
   unsigned long long n_total;
   unsigned long long key;
+  const unsigned long long* key_dev;  // when non-NULL: the key, read at run time (graph replay)
   unsigned int t;  // population being resampled; the new one is t + 1
   int rank, world;
   float y_cur;     // observation of population t (source weights)

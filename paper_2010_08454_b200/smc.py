@@ -141,7 +141,7 @@ class _Rank:
 class SmcRunner:
     def __init__(self, model: HiddenMarkovModel, n_particles: int, rng, *, group=None, device=None,
                  record_ancestors: bool = False, hist_steps=None, local_world: int | None = None,
-                 steps: int | None = None):
+                 steps: int | None = None, graph: bool = False):
         import torch
 
         if not isinstance(model, HiddenMarkovModel):
@@ -211,6 +211,20 @@ class SmcRunner:
         self._pending_anc = None
         self.cur = 0
         self.k6_events = None  # list of (start, end) CUDA events per K6 launch when profiling
+        self.k6_every = 1      # time every k-th K6 launch only (fewer event nodes in a graph)
+        # CUDA graph of the whole run (init + T steps): one process, no ancestor snapshots (their
+        # host-side list cannot be replayed). The Philox key then lives in device memory
+        # (cuppl_smc_model.key_dev), so one capture serves every reseed.
+        self.use_graph = bool(graph) and not self.multiprocess and not record_ancestors
+        self.key_dev = None
+        if self.use_graph:
+            import torch
+
+            self.key_dev = torch.zeros(1, dtype=torch.int64, device=dev)
+            self.cm.key_dev = self.key_dev.data_ptr()
+        self._graph = None
+        self._graph_cur = 0
+        self._capturing = False
 
     # ------------------------------------------------------------------ collectives -------
     def _exchange_arenas(self):
@@ -308,6 +322,8 @@ class SmcRunner:
     def init(self):
         L = N.lib()
         st = N.stream_ptr(self.device)
+        for h in self.hist.values():
+            h.zero_()
         for rk in self.ranks:
             N.check(L.cuppl_smc_init(C.byref(self.cm), rk.n, rk.lo, self.key, float(self.ys[0]),
                                      N.ptr(rk.x[0]), N.ptr(rk.m_key[0:1]), N.ptr(rk.ws), rk.ws.numel(), st),
@@ -335,10 +351,12 @@ class SmcRunner:
         nxt = 1 - self.cur
         xt, at = self._tables[nxt]
         ev = None
-        if self.k6_events is not None:
+        if self.k6_events is not None and t % self.k6_every == 0:
             import torch
 
-            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ext = self._capturing  # inside a graph: event-record nodes that time every replay
+            ev = (torch.cuda.Event(enable_timing=True, external=ext),
+                  torch.cuda.Event(enable_timing=True, external=ext))
             ev[0].record()
         for rk in self.ranks:
             N.check(L.cuppl_smc_resample(
@@ -370,11 +388,45 @@ class SmcRunner:
             self._pending_anc = None
 
     def run(self) -> SmcResult:
-        self.init()
-        for t in range(self.T):
-            self.step(t)
-        self._snapshot_ancestors()
+        self.launch()
         return self.result()
+
+    def launch(self):
+        """Enqueue a whole run (init + T steps) on the current stream: replay of the captured
+        graph in graph mode, else step by step."""
+        if not self.use_graph:
+            self.init()
+            for t in range(self.T):
+                self.step(t)
+            self._snapshot_ancestors()
+            return
+        import torch
+
+        self.key_dev.fill_(int(np.uint64(self.key).view(np.int64)))
+        if self._graph is None:
+            self._capture()
+        self._graph.replay()
+        self.cur = self._graph_cur
+
+    def _capture(self):
+        import torch
+
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        self._capturing = True
+        try:
+            with torch.cuda.graph(g, capture_error_mode="relaxed"):
+                self.init()
+                for t in range(self.T):
+                    self.step(t)
+        finally:
+            self._capturing = False
+        self._graph = g
+        self._graph_cur = self.cur
+
+    def k6_ms(self) -> float:
+        """Sum of the recorded K6 launch durations (after a synchronize)."""
+        return sum(a.elapsed_time(b) for a, b in self.k6_events or [])
 
     def result(self) -> SmcResult:
         g = self.gathered.cpu().numpy().view(np.uint64)
@@ -405,8 +457,10 @@ class SmcRunner:
 
 def run_smc(model: HiddenMarkovModel, n_particles: int, rng, *, steps: int | None = None,
             record_ancestors: bool = False, hist_steps=None, group=None, device=None,
-            local_world: int | None = None) -> SmcResult:
-    """Bootstrap particle filter with systematic resampling at every step."""
+            local_world: int | None = None, graph: bool = False) -> SmcResult:
+    """Bootstrap particle filter with systematic resampling at every step.
+    graph=True captures the run as one CUDA graph (worth it when a runner is reused: see
+    SmcRunner.launch)."""
     r = SmcRunner(model, n_particles, rng, group=group, device=device, record_ancestors=record_ancestors,
-                  hist_steps=hist_steps, local_world=local_world, steps=steps)
+                  hist_steps=hist_steps, local_world=local_world, steps=steps, graph=graph)
     return r.run()
