@@ -55,6 +55,53 @@ def test_record_layout_matches_header():
     assert C.sizeof(_native.Dist) == 40
 
 
+def test_smc_model_layout_matches_header():
+    from paper_2010_08454_b200 import _native
+
+    text = (ROOT / "include" / "cuppl_gpu.h").read_text()
+    body = re.search(r"typedef struct cuppl_smc_model \{(.*?)\} cuppl_smc_model;", text, re.S).group(1)
+    fields = re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(\w+);", body, re.M)
+    assert fields == [f for f, _ in _native.SmcModel._fields_]
+    assert C.sizeof(_native.SmcModel) == 48
+
+
+def test_smc_arguments_rejected_before_cuda(native_lib):
+    """SMC entry points validate their arguments on the host and name the problem."""
+    from paper_2010_08454_b200 import _native
+
+    L = _native.lib()
+    m = _native.SmcModel()
+    m.n_states, m.inv_sd, m.c = 4, 1.0, -0.9189385
+    mu = np.zeros(4, dtype=np.float32)
+    alias = np.zeros(4 * 4, dtype=np.uint64)
+    m.alias_trans = alias.ctypes.data
+    m.alias_init = alias.ctypes.data
+    m.mu = mu.ctypes.data
+    n = 4096
+    wsb = L.cuppl_smc_workspace_bytes(n)
+    ws = np.zeros(wsb, dtype=np.uint8)
+    x = np.zeros(n, dtype=np.uint8)
+    mk = np.zeros(2, dtype=np.int32)
+    # NULL population buffer
+    rc = L.cuppl_smc_init(C.byref(m), n, 0, 1, 0.0, None, mk.ctypes.data, ws.ctypes.data, wsb, None)
+    assert rc == _native.E_ARGUMENT and b"NULL" in L.cuppl_last_error()
+    # rank boundaries are multiples of 16
+    rc = L.cuppl_smc_init(C.byref(m), n, 8, 1, 0.0, x.ctypes.data, mk.ctypes.data, ws.ctypes.data, wsb, None)
+    assert rc == _native.E_ARGUMENT and b"16" in L.cuppl_last_error()
+    # workspace too small
+    rc = L.cuppl_smc_init(C.byref(m), n, 0, 1, 0.0, x.ctypes.data, mk.ctypes.data, ws.ctypes.data, wsb - 1, None)
+    assert rc != _native.OK
+    # rank outside the world
+    rc = L.cuppl_smc_resample(C.byref(m), n, n, 1, 0, 3, 2, 0.0, 0.0, x.ctypes.data, mk.ctypes.data,
+                              ws.ctypes.data, ws.ctypes.data, ws.ctypes.data, None, mk.ctypes.data,
+                              ws.ctypes.data, ws.ctypes.data, wsb, None)
+    assert rc == _native.E_ARGUMENT and b"world" in L.cuppl_last_error()
+    # too many states for the one-byte population
+    m.n_states = 300
+    rc = L.cuppl_smc_init(C.byref(m), n, 0, 1, 0.0, x.ctypes.data, mk.ctypes.data, ws.ctypes.data, wsb, None)
+    assert rc != _native.OK
+
+
 def test_invalid_params_rejected_before_cuda(native_lib):
     """Parameter validation happens on the host, so it works (and maps errors) without a GPU."""
     from paper_2010_08454_b200 import _native, errors
