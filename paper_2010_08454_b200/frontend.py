@@ -701,21 +701,51 @@ class _Compiler:
         # in order, into a bounded local array (the reference evaluates repeat eagerly)
         if not self._effects(f.body, f.env):
             return LazyVec(n, bound, lambda comp, i: comp._apply(f, [i]))
+        if self._observe_loop(f, LazyVec(n, bound, lambda comp, i: i)):
+            return None
         probe_v = self._sandbox()._apply(f, [S("i_probe", "int")])
-        if bound is None:
+        keep = isinstance(probe_v, S)  # a unit-valued body (observe, factor) runs for its effects
+        if bound is None and keep:
             raise CompileError("a repeat that draws needs a bounded length (constant, data length or a "
                                "uniform-discrete draw)")
         arr, i = g.fresh("vec"), g.fresh("i")
-        ty = probe_v.ty if isinstance(probe_v, S) else "real"
-        g.emit(f"{_cty(ty)} {arr}[{bound}];")
+        if keep:
+            g.emit(f"{_cty(probe_v.ty)} {arr}[{bound}];")
         depth = self._loop(i, n, bound)
-        g.loop_mult.append(g.loop_mult[-1] * bound)
+        g.loop_mult.append(g.loop_mult[-1] * (bound or 1))
         v = self._apply(f, [S(i, "int")])
         g.loop_mult.pop()
-        g.emit(f"{arr}[{i}] = {v.code};")
+        if keep:
+            g.emit(f"{arr}[{i}] = {v.code};")
         for _ in range(depth):
             g.close()
-        return LocVec(arr, bound, n, ty)
+        return LocVec(arr, bound, n, probe_v.ty) if keep else None
+
+    def _observe_loop(self, f: Fn, v) -> bool:
+        """map / repeat of `observe(normal(m, sd), y)` with a constant sd: the observes of a
+        data loop are one Gaussian-likelihood reduce (the packed peephole below) whose sum is
+        added to the log-weight once — the same terms, summed in a different order."""
+        body = f.body
+        while isinstance(body, lang.Block) and not body.stmts:
+            body = body.result
+        if not (len(f.params) == 1 and isinstance(body, lang.Call) and isinstance(body.fn, lang.Var)
+                and body.fn.name == "observe" and len(body.args) == 2):
+            return False
+        d = body.args[0]
+        if not (isinstance(d, lang.Call) and isinstance(d.fn, lang.Var) and d.fn.name == "normal"
+                and len(d.args) == 2):
+            return False
+        if any(name in f.env or name in self.globals for name in ("observe", "normal", "dist-score")):
+            return False
+        acc = "__observe_acc"
+        red = Fn([acc, f.params[0]], lang.BinOp("+", lang.Var(acc), lang.Call(lang.Var("dist-score"),
+                                                                               [d, body.args[1]])),
+                 f.env, "<observe loop>")
+        r = self._gaussian_reduce(red, S("0.f", "real"), v)
+        if r is None:
+            return False
+        self.g.add_lw(_real(r))
+        return True
 
     def _gaussian_reduce(self, f: Fn, init: S, v):
         """reduce(function(acc, x) { acc + dist-score(normal(m, sd), y) }, init, v) with a
@@ -834,6 +864,8 @@ class _Compiler:
             raise CompileError("map expects (function, vector)")
         if not self._effects(f.body, f.env):
             return LazyVec(v.length(), v.bound(), lambda comp, i: comp._apply(f, [v.elem(comp, i)]))
+        if self._observe_loop(f, v):
+            return None
         # effects: evaluated now, element by element in order (the reference's eager map)
         bound = v.bound()
         probe = self._sandbox()._apply(f, [v.elem(self._sandbox(), S("i_probe", "int"))])

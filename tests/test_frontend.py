@@ -70,6 +70,35 @@ model <- function() {
 importance(model, 100000)
 """
 
+def _obs_prog(stmt):
+    return """
+xs <- [-1.0, -0.5, 0.0, 0.5, 1.0, 1.5, -2.0];
+ys <- [3.1, 1.9, 1.0, 0.1, -1.2, -2.1, 5.2];
+model <- function() {
+  a <- sample(normal(0, 10));
+  b <- sample(normal(0, 10));
+  %s
+  [a, b]
+};
+importance(model, 1000)
+""" % stmt
+
+
+# the observe-per-datum forms (map / repeat of observe), one with a particle-dependent sd,
+# and a repeat of a unit-valued factor
+OBS_REPEAT = _obs_prog("repeat(function(i) { observe(normal(a * xs[i] + b, 1), ys[i]) }, length(xs));")
+OBS_MAP = _obs_prog("map(function(i) { observe(normal(a * xs[i] + b, 0.5), ys[i]) }, "
+                    "repeat(function(i) { i }, length(xs)));")
+OBS_VARSD = _obs_prog("repeat(function(i) { observe(normal(a * xs[i] + b, a * a + 1.0), ys[i]) }, length(xs));")
+FACTOR_REPEAT = _obs_prog("repeat(function(i) { factor(-0.1 * a * xs[i]) }, length(xs));")
+
+
+def test_observe_loops_compile_to_the_packed_reduce():
+    for src, packed in ((OBS_REPEAT, True), (OBS_MAP, True), (OBS_VARSD, False), (FACTOR_REPEAT, False)):
+        m = frontend.compile_program(src)
+        assert ("fma2" in m.cuda) == packed and not m.masked
+
+
 # a loop whose length is a draw with no static bound: no lane form (one particle per thread)
 UNBOUNDED = """
 model <- function() {
@@ -134,8 +163,10 @@ def test_interpreter_known_value():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("src", [LINREG, FIG1, COIN, BRANCHY, MIXTURE, UNBOUNDED],
-                         ids=["linreg", "fig1", "coin", "branchy", "mixture", "unbounded"])
+@pytest.mark.parametrize("src", [LINREG, FIG1, COIN, BRANCHY, MIXTURE, UNBOUNDED, OBS_REPEAT, OBS_MAP,
+                                 OBS_VARSD, FACTOR_REPEAT],
+                         ids=["linreg", "fig1", "coin", "branchy", "mixture", "unbounded", "obs-repeat",
+                              "obs-map", "obs-varsd", "factor-repeat"])
 def test_gpu_log_weights_match_interpreter(cuda, src):
     """Injected-draw parity: the GPU records every draw; the fp64 interpreter
     replays them; log-weights agree to 1e-5 relative (fp32 evaluation)."""
