@@ -108,9 +108,11 @@ struct WordStream {
 };
 
 // Natural-log density / mass; -inf outside the support.
+// normal: z = (x - m) * (1 / sd) with a correctly rounded reciprocal (|dz| <= 1 ulp of a
+// division); 1/sd and ln sd depend on sd only, so they leave a data loop when sd does not vary
 __device__ __forceinline__ float score_normal(float x, float m, float sd) {
-  const float z = (x - m) / sd;
-  return -0.5f * z * z - logf(sd) - kHalfLog2Pi;
+  const float z = (x - m) * __frcp_rn(sd);
+  return fmaf(-0.5f * z, z, -logf(sd) - kHalfLog2Pi);
 }
 __device__ __forceinline__ float score_bernoulli(bool v, float p) { return v ? logf(p) : log1pf(-p); }
 __device__ __forceinline__ float score_poisson(int k, float lam) {
