@@ -21,9 +21,9 @@ from . import semantics as sem
 
 _TAGS = {"normal": sem.NORMAL, "bernoulli": sem.BERNOULLI, "poisson": sem.POISSON,
          "uniform-discrete": sem.UNIFORM_DISCRETE, "uniform-continuous": sem.UNIFORM_CONTINUOUS,
-         "beta": sem.BETA, "exponential": sem.EXPONENTIAL}
+         "beta": sem.BETA, "exponential": sem.EXPONENTIAL, "categorical": sem.CATEGORICAL}
 _KIND = {"normal": float, "uniform-continuous": float, "beta": float, "exponential": float,
-         "uniform-discrete": int, "poisson": int, "bernoulli": bool}
+         "uniform-discrete": int, "poisson": int, "bernoulli": bool, "categorical": int}
 
 
 class _Fn:
@@ -191,6 +191,8 @@ class Enumerator(Interpreter):
                 support = [True, False]
             elif d.kind == "uniform-discrete":
                 support = list(range(int(d.args[0]), int(d.args[1])))
+            elif d.kind == "categorical":
+                support = list(range(len(d.args[0])))
             else:
                 raise ValueError(f"{d.kind} has no finite support")
             if self._k >= len(self._prefix):

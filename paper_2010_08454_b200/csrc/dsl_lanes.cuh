@@ -171,6 +171,7 @@ using ::floorf;
 using ::fmodf;
 using ::powf;
 using ::fmaf;
+using ::fminf;
 
 CUPPL_LIFT(to_f)
 CUPPL_LIFT(to_i)
@@ -189,6 +190,7 @@ CUPPL_LIFT(floorf)
 CUPPL_LIFT(fmodf)
 CUPPL_LIFT(powf)
 CUPPL_LIFT(fmaf)
+CUPPL_LIFT(fminf)
 CUPPL_LIFT(score_normal)
 CUPPL_LIFT(score_bernoulli)
 CUPPL_LIFT(score_poisson)
@@ -229,6 +231,14 @@ template <class M>
 __device__ __forceinline__ float draw_gamma(WordStream& ws, float a, const M&) { return ws.gamma(a); }
 template <class M>
 __device__ __forceinline__ int draw_poisson(WordStream& ws, float lam, const M&) { return ws.poisson(lam); }
+// categorical(w): P(k) = w_k / sum w; weights must be >= 0 and not all 0
+__device__ __forceinline__ unsigned cat_check(bool valid, float tot, float wmin) {
+  return valid && !(tot > 0.f && wmin >= 0.f) ? 2u : 0u;
+}
+__device__ __forceinline__ float score_categorical(int k, int n, float wk, float tot) {
+  return (k >= 0 && k < n && wk > 0.f) ? logf(wk / tot) : neg_inf_f();
+}
+CUPPL_LIFT(score_categorical)
 __device__ __forceinline__ void store_draw(float* out, unsigned long long idx, bool valid, int nd, float x) {
   if (out && valid && nd < MAXD) out[idx * MAXD + nd] = x;
 }
@@ -276,6 +286,13 @@ __device__ __forceinline__ unsigned ud_check(const Lane<bool>& valid, const A& l
   unsigned e = 0u;
 #pragma unroll
   for (int p = 0; p < LANES; ++p) e |= ud_check(valid.v[p], lane_at(lo, p), lane_at(hi, p));
+  return e;
+}
+template <class T, class W>
+__device__ __forceinline__ unsigned cat_check(const Lane<bool>& valid, const T& tot, const W& wmin) {
+  unsigned e = 0u;
+#pragma unroll
+  for (int p = 0; p < LANES; ++p) e |= cat_check(valid.v[p], lane_at(tot, p), lane_at(wmin, p));
   return e;
 }
 template <class A, class B, class M>

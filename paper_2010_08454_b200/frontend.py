@@ -167,9 +167,11 @@ class Dist:
 _DISTS = {  # name: (arity, sample type)
     "normal": (2, "real"), "uniform-continuous": (2, "real"), "uniform-discrete": (2, "int"),
     "bernoulli": (1, "bool"), "beta": (2, "real"), "exponential": (1, "real"), "poisson": (1, "int"),
+    "categorical": (1, "int"),  # categorical(weights): a vector of static length
 }
+MAX_CATEGORIES = 32
 _KIND_CODE = {"normal": 0, "uniform-continuous": 1, "uniform-discrete": 2, "bernoulli": 3, "beta": 4,
-              "exponential": 5, "poisson": 6}
+              "exponential": 5, "poisson": 6, "categorical": 7}
 _MATH1 = {"exp": "expf", "log": "logf", "sqrt": "sqrtf", "abs": "fabsf", "floor": "floorf"}
 _CMP = {"==", "!=", "<", "<=", ">", ">="}
 
@@ -493,6 +495,8 @@ class _Compiler:
                 arity, _ = _DISTS[name]
                 if len(e.args) != arity:
                     raise CompileError(f"{name} takes {arity} argument(s)")
+                if name == "categorical":
+                    return Dist(name, [self._cat_weights(self.ev(e.args[0], env))])
                 return Dist(name, [_scalar(self.ev(a, env), name) for a in e.args])
             if name in ("sample", "sample*"):
                 d = self.ev(e.args[0], env)
@@ -581,17 +585,33 @@ class _Compiler:
             g.emit(f"{lhs} = -logf(draw_uniform_pos(ws, {m})) / {_real(a[0])};")
         elif k == "poisson":
             g.emit(f"{lhs} = draw_poisson(ws, {_real(a[0])}, {m});")
+        elif k == "categorical":  # k = #{j < n-1 : w_0 + .. + w_j <= u * sum w}
+            w = a[0]
+            tot, wmin = self._cat_total(w), g.fresh("cmin")
+            g.emit(f"const auto {wmin} = {self._fold('fminf', w)};")
+            g.emit(f"err |= cat_check({g.valid_m()}, {tot}, {wmin});")
+            u = g.fresh("cu")
+            g.emit(f"const auto {u} = draw_uniform(ws, {m}) * {tot};")
+            terms, cum = [], None
+            for j in range(len(w) - 1):
+                c = g.fresh("cc")
+                g.emit(f"const auto {c} = {w[j] if cum is None else f'{cum} + {w[j]}'};")
+                terms.append(f"to_i({c} <= {u})")
+                cum = c
+            g.emit(f"{lhs} = {' + '.join(terms) if terms else '0'};")
 
     def _sample(self, d: Dist) -> S:
         g = self.g
         g.draw_bound += g.loop_mult[-1]
-        a = [g.let(x) for x in d.args]
+        a = d.args if d.kind == "categorical" else [g.let(x) for x in d.args]
         v = g.fresh("x")
         k = d.kind
         if self.engine == "enumerate":
             return self._choose(d, a, v)
         if k == "uniform-discrete" and _is_literal(a[1].code):
             g.bounds[v] = max(int(a[1].code) - 1, 0)
+        if k == "categorical":
+            g.bounds[v] = len(a[0]) - 1
         ty = _DISTS[k][1]
         if self.engine == "mcmc":
             return self._lmh_site(d, a, v, ty)
@@ -655,6 +675,18 @@ class _Compiler:
             g.emit(f"  chosen_i = {lo} + static_cast<int>(dg); }}")
             g.emit(f"const int {v} = chosen_i;")
             return S(v, "int", False)
+        if k == "categorical":
+            w = a[0]
+            n = len(w)
+            self.radix = max(self.radix, n)
+            g.bounds[v] = n - 1
+            tot = self._cat_total(w)
+            g.emit("{ const unsigned dg = static_cast<unsigned>(rem % ENUM_R); rem /= ENUM_R; ++nd;")
+            g.emit(f"  if (dg >= {n}u) dead = true;")
+            g.emit(f"  chosen_i = static_cast<int>(dg);")
+            g.emit(f"  lw += dg < {n}u ? score_categorical(chosen_i, {n}, {self._cat_pick(w, 'chosen_i')}, {tot}) : 0.f; }}")
+            g.emit(f"const int {v} = chosen_i;")
+            return S(v, "int", False)
         from .errors import ContinuousDistError
 
         raise ContinuousDistError(f"enumeration needs finite-support distributions; {k} is not "
@@ -687,7 +719,45 @@ class _Compiler:
             return f"score_beta({_real(v)}, {_real(a[0])}, {_real(a[1])})"
         if k == "exponential":
             return f"score_exponential({_real(v)}, {_real(a[0])})"
+        if k == "categorical":
+            kk = self.g.let(S(f"to_i({v.code})", "int"), "k")
+            return (f"score_categorical({kk.code}, {len(a[0])}, {self._cat_pick(a[0], kk.code)}, "
+                    f"{self._cat_total(a[0])})")
         return f"score_poisson({v.code}, {_real(a[0])})"
+
+    # -------------------------------------------------------------- categorical --
+    def _cat_weights(self, vec) -> list:
+        """The weight vector of categorical(w) as C expressions (static length <= MAX_CATEGORIES)."""
+        if isinstance(vec, ConstVec):
+            items = [_real(_scalar(x, "categorical weight")) for x in vec.items]
+        elif hasattr(vec, "elem"):
+            n = vec.length()
+            if not (_is_literal(n.code) and n.ty == "int"):
+                raise CompileError("categorical needs a weight vector of static length")
+            items = [_real(self.g.let(vec.elem(self, S(str(j), "int")), "w")) for j in range(int(n.code))]
+        else:
+            raise CompileError("categorical expects a vector of weights")
+        if not 1 <= len(items) <= MAX_CATEGORIES:
+            raise CompileError(f"categorical supports 1..{MAX_CATEGORIES} categories")
+        return items
+
+    def _fold(self, fn: str, w: list) -> str:
+        code = w[-1]
+        for x in reversed(w[:-1]):
+            code = f"{fn}({x}, {code})"
+        return code
+
+    def _cat_total(self, w: list) -> str:
+        code = w[0]
+        for x in w[1:]:
+            code = f"({code} + {x})"
+        return self.g.let(S(code, "real"), "ctot").code
+
+    def _cat_pick(self, w: list, k: str) -> str:
+        code = w[-1]
+        for j in range(len(w) - 2, -1, -1):
+            code = f"sel({k} == {j}, {w[j]}, {code})"
+        return code
 
     def _repeat(self, e, env):
         g = self.g
@@ -1323,9 +1393,12 @@ class DslLauncher:
             raise InferRuntimeError(f"cuLaunchKernel failed: {err}")
 
     def check_errors(self):
-        if int(self.err.item()):
+        e = int(self.err.item())
+        if e:
             self.err.zero_()
-            raise InvalidDistParamError("uniform-discrete(a, b) needs b > a (SPEC.md:347)")
+            if e & 1:
+                raise InvalidDistParamError("uniform-discrete(a, b) needs b > a (SPEC.md:347)")
+            raise InvalidDistParamError("categorical(w): weights must be >= 0 and not all 0 (SURVEY.md D5)")
 
     def trace_of(self, pid: int, key: int):
         """Return value of one particle (re-executed: the streams are counter-based)."""

@@ -99,6 +99,28 @@ def test_observe_loops_compile_to_the_packed_reduce():
         assert ("fma2" in m.cuda) == packed and not m.masked
 
 
+# categorical: weights that depend on a draw, a data index by the drawn label
+CAT_MIX = """
+ys <- [-2.1, -1.9, 3.2, 2.8, 3.1, -2.2];
+mus <- [-2.0, 3.0];
+model <- function() {
+  w <- sample(beta(2, 2));
+  map(function(y) { z <- sample(categorical([w, 1.0 - w])); observe(normal(mus[z], 0.5), y) }, ys);
+  w
+};
+importance(model, 100000)
+"""
+CAT_ENUM = """
+model <- function() {
+  z <- sample(categorical([0.2, 0.5, 0.3]));
+  b <- sample(bernoulli(0.3));
+  observe(normal(to-real(z), 1), 1.7);
+  if (b) { z + 3 } else { z }
+};
+enumerate(model, 100)
+"""
+
+
 # a loop whose length is a draw with no static bound: no lane form (one particle per thread)
 UNBOUNDED = """
 model <- function() {
@@ -164,9 +186,9 @@ def test_interpreter_known_value():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("src", [LINREG, FIG1, COIN, BRANCHY, MIXTURE, UNBOUNDED, OBS_REPEAT, OBS_MAP,
-                                 OBS_VARSD, FACTOR_REPEAT],
+                                 OBS_VARSD, FACTOR_REPEAT, CAT_MIX],
                          ids=["linreg", "fig1", "coin", "branchy", "mixture", "unbounded", "obs-repeat",
-                              "obs-map", "obs-varsd", "factor-repeat"])
+                              "obs-map", "obs-varsd", "factor-repeat", "categorical"])
 def test_gpu_log_weights_match_interpreter(cuda, src):
     """Injected-draw parity: the GPU records every draw; the fp64 interpreter
     replays them; log-weights agree to 1e-5 relative (fp32 evaluation)."""
@@ -397,7 +419,7 @@ def test_enumeration_compile_and_reject():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("src", [ENUM_TWO, ENUM_BINOMIAL], ids=["two-choice", "binomial"])
+@pytest.mark.parametrize("src", [ENUM_TWO, ENUM_BINOMIAL, CAT_ENUM], ids=["two-choice", "binomial", "categorical"])
 def test_gpu_enumeration_matches_forced_choice_oracle(cuda, src):
     """enumeration equals the brute-force forced-choice evaluation (fp32 device
     arithmetic: 1e-6 per probability instead of the fp64 reference's 1e-12)."""
@@ -411,6 +433,34 @@ def test_gpu_enumeration_matches_forced_choice_oracle(cuda, src):
     for k, p in ref.items():
         assert abs(got[k] - p) < 1e-6, (k, got[k], p)
     assert abs(post.log_z - log_z) < 1e-5
+
+
+def test_categorical_compile_checks():
+    m = frontend.compile_program(CAT_MIX)
+    assert m.max_draws == 7 and "cat_check" in m.cuda
+    e = frontend.compile_program(CAT_ENUM)  # a categorical choice point scores its digit
+    assert e.radix == 3 and "score_categorical" in e.cuda
+    with pytest.raises(frontend.CompileError):  # weights of a length known only at run time
+        frontend.compile_program("model <- function() { n <- sample(uniform-discrete(1, 4)); "
+                                 "sample(categorical(repeat(function(i) { 1.0 }, n))) }; importance(model, 10)")
+
+
+@pytest.mark.gpu
+def test_gpu_categorical_lmh_and_invalid_weights(cuda):
+    """LMH over a categorical choice point agrees with its exact enumeration (TV); weights that
+    are all 0 raise InvalidDistParamError."""
+    from paper_2010_08454_b200 import Rng, infer
+    from paper_2010_08454_b200.errors import InvalidDistParamError
+
+    ex = dict(infer.run_enumeration(frontend.compile_program(CAT_ENUM)).support)
+    mc = infer.run_lmh(frontend.compile_program(CAT_ENUM.replace("enumerate(model, 100)", "mcmc(model, 10)")),
+                       3000, Rng(6), chains=512, burn_in=200)
+    got = dict(mc.support)
+    tv = 0.5 * sum(abs(got.get(k, 0.0) - p) for k, p in ex.items())
+    assert tv < 0.03, (got, ex)
+    bad = frontend.compile_program("model <- function() { sample(categorical([0.0, 0.0])) }; importance(model, 10)")
+    with pytest.raises(InvalidDistParamError):
+        infer.run_importance(bad, 1000, Rng(1))
 
 
 @pytest.mark.gpu
