@@ -207,6 +207,29 @@ CUPPL_LIFT(score_exponential)
 // With LANES == 1 (or a uniform condition) m is true inside its block and this is plain code.
 __device__ __forceinline__ bool lanes_any(bool m) { return m; }
 
+// var = x in the lanes of mask m (a per-lane predicated move, which ptxas folds into the
+// instruction producing x) — the masked-update form of the generated code
+template <class T, class M, class X>
+__device__ __forceinline__ void masked_set(T& var, const M& m, const X& x) {
+  if constexpr (is_lane<T>::v) {
+#pragma unroll
+    for (int p = 0; p < LANES; ++p)
+      if (lane_at(m, p)) var.v[p] = lane_at(x, p);
+  } else {
+    if (lane_at(m, 0)) var = x;
+  }
+}
+template <class T, class M, class X>
+__device__ __forceinline__ void masked_add(T& var, const M& m, const X& x) {
+  if constexpr (is_lane<T>::v) {
+#pragma unroll
+    for (int p = 0; p < LANES; ++p)
+      if (lane_at(m, p)) var.v[p] += lane_at(x, p);
+  } else {
+    if (lane_at(m, 0)) var += x;
+  }
+}
+
 // ------------------------------------------------------------------ draws --------------
 // uniform-discrete(lo, hi): support [lo, hi); an empty range raises
 // InvalidDistParamError on the host (err word) and draws from [lo, lo + 1)

@@ -224,11 +224,11 @@ class _Gen:
     def assign(self, var: str, expr: str):
         """var = expr in the active lanes."""
         m = self.mask()
-        self.emit(f"{var} = sel({m}, {expr}, {var});" if m else f"{var} = {expr};")
+        self.emit(f"masked_set({var}, {m}, {expr});" if m else f"{var} = {expr};")
 
     def add_lw(self, x: str):
         m = self.mask()
-        self.emit(f"lw += sel({m}, {x}, 0.f);" if m else f"lw += {x};")
+        self.emit(f"masked_add(lw, {m}, {x});" if m else f"lw += {x};")
 
     def valid_m(self) -> str:
         m = self.mask()
