@@ -162,3 +162,15 @@ def test_shard_range_partitions():
             rs = [shard_range(n, r, R) for r in range(R)]
             assert rs[0][0] == 0 and rs[-1][1] == n
             assert all(rs[i][1] == rs[i + 1][0] for i in range(R - 1))
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    """No CPU fallback: without the built library every entry point raises NativeLibraryError."""
+    from paper_2010_08454_b200 import _native, errors
+
+    monkeypatch.setattr(_native, "LIB_PATH", tmp_path / "libcuppl_gpu.so")
+    monkeypatch.setattr(_native, "_lib", None)
+    with pytest.raises(errors.NativeLibraryError, match="no CPU fallback"):
+        _native.lib()
+    with pytest.raises(errors.NativeLibraryError):
+        _native.check(_native.E_CUDA)  # status mapping needs the library's message too
