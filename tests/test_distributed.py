@@ -70,3 +70,22 @@ def test_gloo_world2_record_gather_and_merge(oracle_lib, native_lib):
         assert sw == pytest.approx(full["sum_w"], rel=1e-12)
         assert np.allclose(bins, full["bin_w"][:3], rtol=1e-12)
     assert res[0][1:] == res[1][1:]  # every rank merges to identical bytes
+
+
+def test_rank_partitions():
+    """IS / MH shard contiguous ranges of near-equal size; SMC rank boundaries are multiples of
+    16 (16-byte state stores) that cover the population in order."""
+    from paper_2010_08454_b200 import infer, smc
+
+    rs = np.random.default_rng(0)
+    for world in range(1, 9):
+        for n in [world, 16 * world, 1000, 10**9 + 7, int(rs.integers(1, 10**12))]:
+            parts = [infer.shard_range(n, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(parts[r][1] == parts[r + 1][0] for r in range(world - 1))
+            sizes = [hi - lo for lo, hi in parts]
+            assert max(sizes) - min(sizes) <= 1
+            if n >= 16 * world and n < 2**31:
+                b = smc.rank_boundaries(n, world)
+                assert b[0] == 0 and b[-1] == n and len(b) == world + 1
+                assert all(x % 16 == 0 for x in b[:-1]) and all(b[r] < b[r + 1] for r in range(world))
