@@ -75,12 +75,14 @@ class S:
     ty: str
     pure: bool = True  # no side effects (draws / factors) were needed to produce it
     mul: tuple | None = None  # packed product (x, y): a following add fuses into one fma2
+    finite: bool = False  # known finite (a literal, an element of finite data): 0 * x == 0
 
 
 @dataclass
 class DataVec:
     off: int
     n: int
+    finite: bool = True  # every element is a finite number (checked when the data are bound)
 
     def length(self):
         return S(str(self.n), "int")
@@ -91,7 +93,7 @@ class DataVec:
     def elem(self, comp, i: S):
         if i.ty == "int2":  # elements i, i + 1 as one 8-byte load (offsets are even, i is even)
             return S(f"{DATA_SYM}2({self.off} + ({i.code}))", "real2")
-        return S(f"{DATA_SYM}({self.off} + ({i.code}))", "real")
+        return S(f"{DATA_SYM}({self.off} + ({i.code}))", "real", finite=self.finite)
 
 
 @dataclass
@@ -242,7 +244,7 @@ class _Gen:
             return v
         name = self.fresh(hint)
         self.emit(f"const auto {name} = {v.code};")
-        return S(name, v.ty, v.pure)
+        return S(name, v.ty, v.pure, finite=v.finite)
 
 
 def _cty(ty):
@@ -276,8 +278,13 @@ def _lit(v) -> S:
     if isinstance(v, bool):
         return S("true" if v else "false", "bool")
     if isinstance(v, int):
-        return S(str(v), "int")
-    return S(repr(float(np.float32(v))) + "f", "real")
+        return S(str(v), "int", finite=True)
+    f = float(np.float32(v))
+    return S(repr(f) + "f", "real", finite=math.isfinite(f))
+
+
+def _real_lit(v: S, value: float) -> bool:
+    return v.ty == "real" and _is_literal(v.code) and float(v.code.rstrip("f")) == value
 
 
 def _real(v: S) -> str:
@@ -310,7 +317,7 @@ class _Compiler:
             self.g.data.append(0.0)
         off = len(self.g.data)
         self.g.data.extend(np.float32(arr).tolist())
-        return DataVec(off, len(arr))
+        return DataVec(off, len(arr), bool(np.isfinite(np.float32(arr)).all()))
 
     def top(self):
         for name, e in self.prog.bindings:
@@ -448,6 +455,15 @@ class _Compiler:
             return S(f"({a.code} {e.op} {b.code})", "bool", pure)
         if a.ty == "int" and b.ty == "int":
             return S(f"({a.code} {e.op} {b.code})", "int", pure)
+        if a.ty == "real" and b.ty == "real":  # exact folds (up to the sign of a zero)
+            if e.op == "*" and (_real_lit(a, 0.0) and b.finite or _real_lit(b, 0.0) and a.finite):
+                return S("0.0f", "real", pure, finite=True)
+            if e.op == "*" and _real_lit(a, 1.0):
+                return b
+            if e.op == "*" and _real_lit(b, 1.0) or e.op in ("+", "-") and _real_lit(b, 0.0):
+                return a
+            if e.op == "+" and _real_lit(a, 0.0):
+                return b
         if e.op == "%":
             return S(f"fmodf({_real(a)}, {_real(b)})", "real", pure)
         return S(f"({_real(a)} {e.op} {_real(b)})", "real", pure)
@@ -906,13 +922,13 @@ class _Compiler:
         c = repr(float(np.float32(-math.log(sdv) - 0.5 * math.log(2 * math.pi)))) + "f"
         return S(f"({_real(init)} + fmaf({k}, {tot}, {float(n)}f * {c}))", "real", False)
 
-    def _loop(self, i: str, n: S, bound):
+    def _loop(self, i: str, n: S, bound, start: int = 0):
         """Open `for i < n`: small known bounds are unrolled with a guard (static indices keep
         bounded vectors in registers); long data loops are partially unrolled."""
         g = self.g
         if bound is not None and bound <= 16:
             g.emit("#pragma unroll")
-            g.open(f"for (int {i} = 0; {i} < {bound}; ++{i})")
+            g.open(f"for (int {i} = {start}; {i} < {bound}; ++{i})")
             if not (_is_literal(n.code) and int(n.code) == bound):
                 g.open_masked(f"{i} < {n.code}")
                 return 2
@@ -973,8 +989,22 @@ class _Compiler:
         g.emit(f"{_cty(ty)} {acc} = {init.code if ty != 'real' else _real(init)};")
         n = v.length()
         bound = v.bound()
-        depth = self._loop(i, n, bound)
-        g.loop_mult.append(g.loop_mult[-1] * (bound or 1))
+        start = 0
+        if ty == "real" and init.ty == "real" and _is_literal(init.code) and bound is not None and 1 <= bound <= 16:
+            # peel element 0: the body sees the literal init, so e.g. Horner's first step
+            # 0 * x + c folds to c (frontend _binop) instead of a multiply-add by zero
+            if not _is_literal(n.code):
+                g.open_masked(f"0 < {n.code}")
+            if not _is_literal(n.code) or int(n.code) >= 1:
+                r0 = self._apply(f, [init, v.elem(self, S("0", "int"))])
+                g.assign(acc, _real(r0))
+            if not _is_literal(n.code):
+                g.close()
+            start = 1
+            if bound == 1:
+                return S(acc, ty, False)
+        depth = self._loop(i, n, bound, start)
+        g.loop_mult.append(g.loop_mult[-1] * (bound - start if bound else 1))
         x = v.elem(self, S(i, "int"))
         r = self._apply(f, [S(acc, ty), x])
         g.loop_mult.pop()
