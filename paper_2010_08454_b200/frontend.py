@@ -1294,7 +1294,7 @@ def compile_program(source: str, data: dict | None = None) -> CompiledModel:
 _MODULES: dict = {}
 
 
-def _nvrtc_cubin(src: str, lanes: int = 1) -> bytes:
+def _nvrtc_cubin(src: str, lanes: int = 1, extra: tuple = ()) -> bytes:
     from cuda.bindings import nvrtc
 
     def ok(r, what):
@@ -1306,6 +1306,7 @@ def _nvrtc_cubin(src: str, lanes: int = 1) -> bytes:
     prog = ok(nvrtc.nvrtcCreateProgram(src.encode(), b"cuppl_model.cu", 0, [], []), "create")
     opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-lineinfo", b"-default-device",
             f"-DLANES={lanes}".encode(), f"-I{CSRC}".encode(), f"-I{INCLUDE}".encode()]
+    opts += [o.encode() for o in extra]
     r = nvrtc.nvrtcCompileProgram(prog, len(opts), opts)
     if r[0] != nvrtc.nvrtcResult.NVRTC_SUCCESS:
         size = ok(nvrtc.nvrtcGetProgramLogSize(prog), "log size")

@@ -302,3 +302,56 @@ def test_normalize_tensors_matches_is_record(cuda):
         assert r["probs"][d - 2] == pytest.approx(p, rel=1e-4, abs=1e-7)
     assert r["log_z"] == pytest.approx(post.log_z, abs=1e-4)
     assert r["argmax"] == post.mode_index
+
+
+CURAND_CHECK = r"""
+#define MAXD 1
+#include <curand_philox4x32_x.h>
+#include "cuppl_device.cuh"
+extern "C" __global__ void philox_vs_curand(const uint4* ctr, const unsigned int* keys, uint4* ours,
+                                            uint4* theirs, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint2 k = make_uint2(keys[2 * i], keys[2 * i + 1]);
+  theirs[i] = curand_Philox4x32_10(ctr[i], k);
+  ours[i] = cuppl::philox4x32_10(ctr[i], k.x, k.y);
+}
+"""
+
+
+def test_philox_matches_curand(cuda):
+    """the Philox4x32-10 block function equals cuRAND's
+    curand_Philox4x32_10 (curand_philox4x32_x.h of this CUDA toolkit) on random counters and keys,
+    including counter words at 2^32 - 1."""
+    import ctypes as C
+
+    import torch
+    from cuda.bindings import driver as cu
+
+    from paper_2010_08454_b200 import frontend
+
+    cubin = frontend._nvrtc_cubin(CURAND_CHECK, 1, ("-I/usr/local/cuda/include",))
+    torch.cuda.init()
+    err, mod = cu.cuModuleLoadData(cubin)
+    assert err == cu.CUresult.CUDA_SUCCESS
+    err, fn = cu.cuModuleGetFunction(mod, b"philox_vs_curand")
+    assert err == cu.CUresult.CUDA_SUCCESS
+    n = 1 << 16
+    rs = np.random.default_rng(3)
+    ctr = rs.integers(0, 2**32, size=(n, 4), dtype=np.uint64).astype(np.uint32)
+    ctr[:64] = 0xFFFFFFFF  # all-ones words
+    ctr[64:128, 0] = 0xFFFFFFFF
+    keys = rs.integers(0, 2**32, size=(n, 2), dtype=np.uint64).astype(np.uint32)
+    d_ctr = torch.from_numpy(ctr.view(np.int32)).to(cuda)
+    d_keys = torch.from_numpy(keys.view(np.int32)).to(cuda)
+    ours = torch.zeros((n, 4), dtype=torch.int32, device=cuda)
+    theirs = torch.ones((n, 4), dtype=torch.int32, device=cuda)
+    vals = [C.c_uint64(d_ctr.data_ptr()), C.c_uint64(d_keys.data_ptr()), C.c_uint64(ours.data_ptr()),
+            C.c_uint64(theirs.data_ptr()), C.c_int32(n)]
+    ptrs = (C.c_void_p * len(vals))(*[C.addressof(v) for v in vals])
+    st = torch.cuda.current_stream().cuda_stream
+    err, = cu.cuLaunchKernel(fn, n // 256, 1, 1, 256, 1, 1, 0, st, C.addressof(ptrs), 0)
+    assert err == cu.CUresult.CUDA_SUCCESS
+    torch.cuda.synchronize()
+    assert torch.equal(ours, theirs)
+    cu.cuModuleUnload(mod)

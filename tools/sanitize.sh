@@ -1,0 +1,14 @@
+# compute-sanitizer over smoke() (every engine: IS poly/linreg, SMC K4-K6, MH K7, a compiled
+# CuPPL model) with each tool; summaries under gpurun_out/sanitize/ (SURVEY.md §4 item 5).
+OUT=gpurun_out/sanitize
+mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()"
+SM="python -c 'import __graft_entry__ as g; g.smoke()'"
+for tool in memcheck racecheck synccheck initcheck; do
+  extra=""
+  [ $tool = initcheck ] && extra="--track-unused-memory no"
+  [ $tool = memcheck ] && extra="--leak-check no"
+  timeout 1500 compute-sanitizer --tool $tool $extra --print-limit 30 bash -c "$SM" > $OUT/$tool.log 2>&1
+  echo "$tool exit=$?"
+  grep -E "ERROR SUMMARY|RACECHECK SUMMARY|smoke " $OUT/$tool.log | tail -8
+done
