@@ -225,6 +225,7 @@ class SmcRunner:
         self._graph = None
         self._graph_cur = 0
         self._capturing = False
+        self.t_next = 0  # next population to scan (eager runs; see advance / snapshot)
 
     # ------------------------------------------------------------------ collectives -------
     def _exchange_arenas(self):
@@ -320,10 +321,13 @@ class SmcRunner:
         self._pending_anc = None
 
     def init(self):
+        self.t_next = 0
         L = N.lib()
         st = N.stream_ptr(self.device)
         for h in self.hist.values():
             h.zero_()
+        for rk in self.ranks:  # per-step maxima are atomicMax targets: a rerun starts from scratch
+            rk.m_key.fill_(INT32_MIN)
         for rk in self.ranks:
             N.check(L.cuppl_smc_init(C.byref(self.cm), rk.n, rk.lo, self.key, float(self.ys[0]),
                                      N.ptr(rk.x[0]), N.ptr(rk.m_key[0:1]), N.ptr(rk.ws), rk.ws.numel(), st),
@@ -371,6 +375,7 @@ class SmcRunner:
         if self.record_ancestors:
             self._pending_anc = nxt  # complete only after the next collective (peer stores)
         self.cur = nxt
+        self.t_next = t + 1
 
     def log_weights(self, rk):
         """Per-particle log-weights of the current population (tabulated per state)."""
@@ -423,6 +428,62 @@ class SmcRunner:
             self._capturing = False
         self._graph = g
         self._graph_cur = self.cur
+
+    # ------------------------------------------------------------------ checkpoint -------
+    def advance(self, until: int):
+        """Eager run of populations [t_next, until) (init first when nothing ran yet)."""
+        if self.use_graph:
+            raise InferRuntimeError("advance/snapshot need an eager runner (graph=False)")
+        if self.t_next == 0:
+            self.init()
+        for t in range(self.t_next, min(until, self.T)):
+            self.step(t)
+        if until >= self.T:
+            self.t_next = self.T
+            self._snapshot_ancestors()
+
+    def snapshot(self) -> dict:
+        """Host copy of the run state between steps: the current population, the per-step
+        records / maxima / statistics / histograms so far and the scan workspace. Philox is
+        counter-based, so (key, t_next) is the whole generator state."""
+        import torch
+
+        if self.use_graph or self.multiprocess:
+            raise InferRuntimeError("snapshots are taken from eager single-process runners")
+        torch.cuda.synchronize(self.device)
+        self._snapshot_ancestors()
+        return {"n": self.N, "T": self.T, "world": self.world, "key": self.key, "seed": self.seed,
+                "t_next": self.t_next, "x": [rk.x[self.cur].cpu() for rk in self.ranks],
+                "m_key": [rk.m_key.cpu() for rk in self.ranks], "rec": [rk.rec.cpu() for rk in self.ranks],
+                "stats": [rk.stats.cpu() for rk in self.ranks], "ws": [rk.ws.cpu() for rk in self.ranks],
+                "gathered": self.gathered.cpu(), "hist": {t: h.cpu() for t, h in self.hist.items()},
+                "ancestors": [[a.cpu() for a in step] for step in self.ancestors]}
+
+    def restore(self, snap: dict):
+        """Load a snapshot into this runner (same model, population size, steps and ranks);
+        resume() then continues exactly where the snapshot was taken."""
+        if (snap["n"], snap["T"], snap["world"]) != (self.N, self.T, self.world) or self.use_graph:
+            raise InferRuntimeError("snapshot does not match this runner (n, steps, ranks, eager)")
+        if set(snap["hist"]) != set(self.hist):
+            raise InferRuntimeError("snapshot histogram steps differ from this runner's")
+        self.key, self.seed, self.t_next = snap["key"], snap["seed"], snap["t_next"]
+        self.cur = 0
+        self._pending_anc = None
+        for i, rk in enumerate(self.ranks):
+            rk.x[0].copy_(snap["x"][i])
+            rk.m_key.copy_(snap["m_key"][i])
+            rk.rec.copy_(snap["rec"][i])
+            rk.stats.copy_(snap["stats"][i])
+            rk.ws.copy_(snap["ws"][i])
+        self.gathered.copy_(snap["gathered"])
+        for t, h in snap["hist"].items():
+            self.hist[t].copy_(h)
+        self.ancestors = [[a.to(self.device) for a in step] for step in snap["ancestors"]]
+
+    def resume(self) -> SmcResult:
+        """Run the remaining steps and return the result of the whole run."""
+        self.advance(self.T)
+        return self.result()
 
     def k6_ms(self) -> float:
         """Sum of the recorded K6 launch durations (after a synchronize)."""

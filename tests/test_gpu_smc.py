@@ -119,6 +119,55 @@ def test_smc_graph_replay_matches_eager(cuda, R):
     assert len(g.k6_events) == steps - 1 and g.k6_ms() > 0  # one pair per time step
 
 
+@pytest.mark.parametrize("graph", [False, True])
+def test_smc_reseeded_runner_matches_fresh(cuda, oracle_lib, graph):
+    """A runner reused under other keys (reseed) equals fresh runs and the oracle: per-step state
+    (maxima, histograms) is reset by init. Small populations make the per-step maximum depend
+    on the key, so stale maxima would show."""
+    from paper_2010_08454_b200 import models, smc
+
+    steps, n = 10, 64
+    m = models.HiddenMarkovModel.synthetic(S=50, T=steps, seed=8)
+    r = smc.SmcRunner(m, n, KEY, steps=steps, graph=graph, hist_steps=[steps - 1])
+    for key in (KEY, KEY + 1, KEY + 2, KEY + 3):
+        r.reseed(key)
+        got = _snapshot(r.run())
+        ref = oracle_lib.smc_run(m, n, key, record_ancestors=False, hist_steps=[steps - 1])
+        assert np.array_equal(got[2], ref["T"]), key
+        assert np.array_equal(got[0].astype(np.int32), ref["x"]) and np.array_equal(got[1], ref["lw"].view(np.uint32))
+        assert np.array_equal(got[4][steps - 1], ref["hist"][steps - 1])
+
+
+@pytest.mark.parametrize("R", [None, 3])
+def test_smc_snapshot_resume_bit_identical(cuda, tmp_path, R):
+    """Checkpoint / resume: stop after 5 of 12 steps, save the snapshot to disk,
+    restore it into a fresh runner and finish — bit-identical to the uninterrupted run."""
+    import torch
+
+    from paper_2010_08454_b200 import models, smc
+
+    steps, n = 12, 50_000
+    m = models.HiddenMarkovModel.synthetic(S=20, T=steps, seed=9)
+    kw = dict(steps=steps, hist_steps=[3, steps - 1], record_ancestors=True, local_world=R)
+    full_res = smc.SmcRunner(m, n, KEY, **kw).run()
+    full = _snapshot(full_res)
+    full_anc = [[a.cpu().numpy() for a in step] for step in full_res.ancestors]
+    a = smc.SmcRunner(m, n, KEY, **kw)
+    a.advance(5)
+    torch.save(a.snapshot(), tmp_path / "smc.pt")
+    del a
+    b = smc.SmcRunner(m, n, 12345, **kw)  # another key: restore brings the snapshot's
+    b.restore(torch.load(tmp_path / "smc.pt"))
+    res = b.resume()
+    got = _snapshot(res)
+    for x, y in zip(got[:4], full[:4]):
+        assert np.array_equal(x, y)
+    assert all(np.array_equal(got[4][t], full[4][t]) for t in (3, steps - 1))
+    anc = [[a.cpu().numpy() for a in step] for step in res.ancestors]
+    assert len(anc) == len(full_anc) == steps - 1
+    assert all(np.array_equal(p, q) for s1, s2 in zip(anc, full_anc) for p, q in zip(s1, s2))
+
+
 def test_smc_degenerate_weights(cuda, oracle_lib):
     """An observation only one state explains: a few particles get all the offspring."""
     from paper_2010_08454_b200 import models

@@ -4,10 +4,8 @@ OUT=gpurun_out/sanitize
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()"
 SM="python -c 'import __graft_entry__ as g; g.smoke()'"
-for tool in memcheck racecheck synccheck initcheck; do
+for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
   extra=""
-  [ $tool = initcheck ] && extra="--track-unused-memory no"
-  [ $tool = memcheck ] && extra="--leak-check no"
   timeout 1500 compute-sanitizer --tool $tool $extra --print-limit 30 bash -c "$SM" > $OUT/$tool.log 2>&1
   echo "$tool exit=$?"
   grep -E "ERROR SUMMARY|RACECHECK SUMMARY|smoke " $OUT/$tool.log | tail -8
