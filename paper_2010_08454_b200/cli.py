@@ -57,7 +57,7 @@ class _Summary:
 
 
 def infer_once(model_name: str, inference: str, samples: int, seed: int, *, burn_in: int = 0, thin: int = 1,
-               chains: int = 4096, points: int | None = None):
+               chains: int = 4096, points: int | None = None, smc_steps: int | None = None):
     """Run one inference; returns a posterior with .support / .log_z (and summaries)."""
     from . import infer
     from .rng import Rng
@@ -71,7 +71,7 @@ def infer_once(model_name: str, inference: str, samples: int, seed: int, *, burn
         return _Summary([], None, n=r.n_chains * r.n_steps, mean={"sorted_mu": r.mean.tolist()},
                         var=r.var.tolist(), acceptance=r.acceptance)
     if inference == "smc":
-        r = infer.run_smc(model, samples, rng)
+        r = infer.run_smc(model, samples, rng, steps=smc_steps)
         t = max(r.filtering)
         f = r.filtering[t]
         return _Summary([(int(s), float(p)) for s, p in enumerate(f) if p > 0], r.log_z, n=r.n_particles,
@@ -126,10 +126,56 @@ def _run_file(args) -> int:
     return 0
 
 
-def cmd_run(args) -> int:
+def relaunch_command(argv: list, gpus: int) -> list:
+    """`run --gpus N` outside a launcher: the same command, one process per GPU, under
+    torch.distributed.run (rendezvous on 127.0.0.1)."""
+    rest = []
+    skip = False
+    for a in argv:
+        if skip:
+            skip = False
+            continue
+        if a == "--gpus":
+            skip = True
+            continue
+        if a.startswith("--gpus="):
+            continue
+        rest.append(a)
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", "-m", "paper_2010_08454_b200"] + rest
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _join_world():
+    """Under torch.distributed.run: one process per GPU, NCCL; only rank 0 prints. The engines
+    shard particles / chains over the default group."""
+    import torch
+    import torch.distributed as dist
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dist.get_rank()
+
+
+def cmd_run(args, argv=None) -> int:
     from .errors import CupError
     from .posterior import serialize_posterior
 
+    if args.gpus > 1 and int(os.environ.get("WORLD_SIZE", "1")) == 1:
+        import subprocess
+
+        return subprocess.call(relaunch_command(list(argv if argv is not None else sys.argv[1:]), args.gpus))
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and _join_world() != 0:
+        sys.stdout = open(os.devnull, "w")  # ranks > 0 run their shard and stay silent
     if args.file:
         return _run_file(args)
     if not args.model:
@@ -142,7 +188,7 @@ def cmd_run(args) -> int:
         return 1
     try:
         post = infer_once(args.model, inference, samples, _seed(args), burn_in=args.burn_in, thin=args.thin,
-                          chains=args.chains, points=args.points)
+                          chains=args.chains, points=args.points, smc_steps=args.smc_steps)
         text = serialize_posterior(post, args.format)
     except ValueError as e:
         print(f"error: {e}", file=sys.stderr)
@@ -247,7 +293,11 @@ def main(argv=None) -> int:
     r.add_argument("--model", choices=tuple(DEFAULT_INFERENCE))
     r.add_argument("--inference", choices=("importance", "mcmc", "smc", "enumerate"))
     r.add_argument("--max-executions", type=int, default=0, help="enumeration: bound on the path space")
-    r.add_argument("--samples", type=int, default=0, help="particles (importance, smc) or steps per chain (mcmc)")
+    r.add_argument("--samples", "--particles", type=int, default=0,
+                   help="particles (importance, smc) or steps per chain (mcmc)")
+    r.add_argument("--smc-steps", type=int, default=None, help="smc: time steps to filter (default: all)")
+    r.add_argument("--gpus", type=int, default=1, help="one process per GPU (NCCL; relaunched under "
+                   "torch.distributed.run unless already inside it)")
     r.add_argument("--seed", type=int, default=None)
     r.add_argument("--burn-in", type=int, default=0)
     r.add_argument("--thin", type=int, default=1)
@@ -262,7 +312,7 @@ def main(argv=None) -> int:
         args = ap.parse_args(argv)
     except SystemExit as e:
         return 1 if e.code else 0
-    return cmd_run(args) if args.cmd == "run" else cmd_bench(args)
+    return cmd_run(args, argv) if args.cmd == "run" else cmd_bench(args)
 
 
 if __name__ == "__main__":

@@ -22,6 +22,7 @@ from typing import Any
 import numpy as np
 
 from . import _native as N
+from . import _nvtx
 from .errors import AllZeroWeightError, InferRuntimeError
 from .models import LinearRegression, PolyRegression
 from .rng import key_of, seed_of
@@ -239,6 +240,7 @@ def normalize_tensors(lw, bins=None, n_bins: int = 1) -> dict:
             "argmax_lw": float(o[2]), "n_finite": nf, "scale_bits": sb.value}
 
 
+@_nvtx.traced("cuppl.normalize")
 def normalize(samples, *, device=None) -> EmpiricalDistribution:
     """normalize(samples): WeightedSample list (or (value, log_weight) pairs)
     -> EmpiricalDistribution. Support is merged by structural equality (value_key,
@@ -270,6 +272,7 @@ def normalize(samples, *, device=None) -> EmpiricalDistribution:
                                  mode_log_weight=r["argmax_lw"], mode_index=r["argmax"], record=r)
 
 
+@_nvtx.traced("cuppl.run_lmh")
 def run_lmh(model, n_samples: int, rng, *, chains: int = 4096, burn_in: int = 0, thin: int = 1,
             return_trace: bool = False, group=None, device=None):
     """Lightweight Metropolis-Hastings as `chains` independent GPU chains of
@@ -285,6 +288,7 @@ def run_lmh(model, n_samples: int, rng, *, chains: int = 4096, burn_in: int = 0,
                 return_trace=return_trace, group=group, device=device)
 
 
+@_nvtx.traced("cuppl.run_smc")
 def run_smc(model, n_particles: int, rng, *, steps: int | None = None, record_ancestors: bool = False,
             hist_steps=None, group=None, device=None):
     """Bootstrap particle filter with systematic resampling every step (smc.py, K4-K6)."""
@@ -294,6 +298,7 @@ def run_smc(model, n_particles: int, rng, *, steps: int | None = None, record_an
                 hist_steps=hist_steps, group=group, device=device)
 
 
+@_nvtx.traced("cuppl.run_importance")
 def run_importance(model, n_samples: int, rng, *, return_traces: bool = False, group=None,
                    device=None) -> EmpiricalDistribution:
     """Likelihood-weighting importance sampling on the GPU.
@@ -368,6 +373,7 @@ def _run_compiled(model, n_samples: int, rng, *, return_traces: bool, group, dev
     return out
 
 
+@_nvtx.traced("cuppl.run_enumeration")
 def run_enumeration(model, max_executions: int | None = None, max_depth: int | None = None, *, group=None,
                     device=None) -> EmpiricalDistribution:
     """run_enumeration of a compiled program `enumerate(model, n)` on the GPU.

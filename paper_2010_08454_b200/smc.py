@@ -25,6 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
+from . import _nvtx
 from .dists import alias_table
 from .errors import AllZeroWeightError, InferRuntimeError
 from .models import HiddenMarkovModel
@@ -341,17 +342,27 @@ class SmcRunner:
         self._allreduce_max(t)  # also the barrier after every rank's K6(t - 1) peer stores
         self._snapshot_ancestors()
         h = self.hist.get(t)
+        with _nvtx.phase("smc.scan"):
+            self._scan(t, h, L, st)
+        with _nvtx.phase("smc.allgather"):
+            self._allgather(t)
+        if t + 1 >= self.T:
+            with _nvtx.phase("smc.fold"):
+                for rk in self.ranks:
+                    N.check(L.cuppl_smc_fold(rk.n, N.ptr(rk.stats[t]), N.ptr(rk.ws), rk.ws.numel(), st),
+                            "smc_fold", seed=self.seed, step=t)
+            return
+        with _nvtx.phase("smc.resample"):
+            self._resample(t, L, st)
+
+    def _scan(self, t, h, L, st):
         for i, rk in enumerate(self.ranks):
             N.check(L.cuppl_smc_scan(C.byref(self.cm), rk.n, float(self.ys[t]), N.ptr(rk.x[self.cur]),
                                      N.ptr(rk.m_key[t:t + 1]), None if h is None else N.ptr(h[i]),
                                      N.ptr(rk.rec[t]), N.ptr(rk.ws), rk.ws.numel(), st),
                     "smc_scan", seed=self.seed, step=t)
-        self._allgather(t)
-        if t + 1 >= self.T:
-            for rk in self.ranks:
-                N.check(L.cuppl_smc_fold(rk.n, N.ptr(rk.stats[t]), N.ptr(rk.ws), rk.ws.numel(), st),
-                        "smc_fold", seed=self.seed, step=t)
-            return
+
+    def _resample(self, t, L, st):
         nxt = 1 - self.cur
         xt, at = self._tables[nxt]
         ev = None
@@ -410,7 +421,8 @@ class SmcRunner:
         self.key_dev.fill_(int(np.uint64(self.key).view(np.int64)))
         if self._graph is None:
             self._capture()
-        self._graph.replay()
+        with _nvtx.phase("smc.graph_replay"):
+            self._graph.replay()
         self.cur = self._graph_cur
 
     def _capture(self):

@@ -96,3 +96,19 @@ def test_cli_run_program_file(cuda, capsys, tmp_path):
     probs = {e["value"]: e["prob"] for e in obj["support"]}
     # posterior Beta(9, 3): P(p > 0.5) = 1 - I_0.5(9, 3) = 0.96728515625
     assert abs(probs[True] - 0.96728515625) < 0.01
+
+
+def test_cli_flags_and_multi_gpu_relaunch():
+    """--particles (alias of --samples), --smc-steps, --chains and
+    --gpus N, which re-runs the same command one process per GPU under torch.distributed.run."""
+    from paper_2010_08454_b200 import cli
+
+    cmd = cli.relaunch_command(["run", "--model", "hmm", "--gpus", "8", "--particles", "1000000",
+                                "--smc-steps", "50"], 8)
+    i = cmd.index("-m")
+    assert cmd[i:i + 2] == ["-m", "torch.distributed.run"] and "--nproc-per-node=8" in cmd
+    assert "--master-addr=127.0.0.1" in cmd
+    tail = cmd[cmd.index("paper_2010_08454_b200"):]
+    assert tail == ["paper_2010_08454_b200", "run", "--model", "hmm", "--particles", "1000000", "--smc-steps", "50"]
+    assert "--gpus" not in " ".join(tail)
+    assert cli.relaunch_command(["run", "x.cup", "--gpus=2"], 2)[-2:] == ["run", "x.cup"]
