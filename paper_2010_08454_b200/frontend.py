@@ -34,6 +34,18 @@ of bounded length, no recursion, no unit-returning user functions as values.
 The kernel fuses the model with the importance-sampling record (log-sum-exp, ESS, mode,
 moments of the returned components, histogram of a discrete return or of a returned vector's
 length) exactly like the hand-written kernels (csrc/is_accum.cuh).
+
+Engines: a program's result selects the kernel — `importance(model, n)` (above),
+`enumerate(model, n)` (forced choices: thread p runs the path given by the base-R digits of p,
+SPEC.md:438) and `mcmc(model, n)` (many single-site LMH chains with a per-thread trace
+database).
+
+Lanes (csrc/dsl_lanes.cuh): the body is emitted once in lane-polymorphic C++ (VF / VI / VB,
+sel, to_f, lifted math, mask-aware draws). Importance kernels are built with several particles
+per thread when that compiles without spills and the program has no particle-dependent
+control flow; otherwise with one. Peepholes: Gaussian-likelihood reduces (and map / repeat of
+observe) become packed FFMA2 loops over pairs of data points; literal-init reduces are peeled
+with exact constant folds.
 """
 
 from __future__ import annotations
