@@ -233,8 +233,13 @@ __device__ __forceinline__ void masked_add(T& var, const M& m, const X& x) {
 // ------------------------------------------------------------------ draws --------------
 // uniform-discrete(lo, hi): support [lo, hi); an empty range raises
 // InvalidDistParamError on the host (err word) and draws from [lo, lo + 1)
-__device__ __forceinline__ unsigned ud_check(bool valid, int lo, int hi) {
-  return valid && !(hi > lo) ? 1u : 0u;
+// parameter checks: flag bit of the error word; the smallest failing particle id is kept in
+// first_bad (reported with InvalidDistParamError)
+__device__ __forceinline__ unsigned ud_check(bool valid, int lo, int hi, unsigned long long pid,
+                                             unsigned long long& first_bad) {
+  const bool bad = valid && !(hi > lo);
+  if (bad && pid < first_bad) first_bad = pid;
+  return bad ? 1u : 0u;
 }
 __device__ __forceinline__ int ud_draw1(WordStream& ws, int lo, int hi) {
   return lo + static_cast<int>(ws.randint(static_cast<unsigned>(hi > lo ? hi - lo : 1)));
@@ -255,8 +260,11 @@ __device__ __forceinline__ float draw_gamma(WordStream& ws, float a, const M&) {
 template <class M>
 __device__ __forceinline__ int draw_poisson(WordStream& ws, float lam, const M&) { return ws.poisson(lam); }
 // categorical(w): P(k) = w_k / sum w; weights must be >= 0 and not all 0
-__device__ __forceinline__ unsigned cat_check(bool valid, float tot, float wmin) {
-  return valid && !(tot > 0.f && wmin >= 0.f) ? 2u : 0u;
+__device__ __forceinline__ unsigned cat_check(bool valid, float tot, float wmin, unsigned long long pid,
+                                              unsigned long long& first_bad) {
+  const bool bad = valid && !(tot > 0.f && wmin >= 0.f);
+  if (bad && pid < first_bad) first_bad = pid;
+  return bad ? 2u : 0u;
 }
 __device__ __forceinline__ float score_categorical(int k, int n, float wk, float tot) {
   return (k >= 0 && k < n && wk > 0.f) ? logf(wk / tot) : neg_inf_f();
@@ -305,17 +313,23 @@ CUPPL_LANE_DRAW1(int, draw_poisson, poisson)
 #undef CUPPL_LANE_DRAW0
 #undef CUPPL_LANE_DRAW1
 template <class A, class B>
-__device__ __forceinline__ unsigned ud_check(const Lane<bool>& valid, const A& lo, const B& hi) {
+__device__ __forceinline__ unsigned ud_check(const Lane<bool>& valid, const A& lo, const B& hi,
+                                             const Lane<unsigned long long>& pid,
+                                             unsigned long long& first_bad) {
   unsigned e = 0u;
 #pragma unroll
-  for (int p = 0; p < LANES; ++p) e |= ud_check(valid.v[p], lane_at(lo, p), lane_at(hi, p));
+  for (int p = 0; p < LANES; ++p)
+    e |= ud_check(valid.v[p], lane_at(lo, p), lane_at(hi, p), pid.v[p], first_bad);
   return e;
 }
 template <class T, class W>
-__device__ __forceinline__ unsigned cat_check(const Lane<bool>& valid, const T& tot, const W& wmin) {
+__device__ __forceinline__ unsigned cat_check(const Lane<bool>& valid, const T& tot, const W& wmin,
+                                              const Lane<unsigned long long>& pid,
+                                              unsigned long long& first_bad) {
   unsigned e = 0u;
 #pragma unroll
-  for (int p = 0; p < LANES; ++p) e |= cat_check(valid.v[p], lane_at(tot, p), lane_at(wmin, p));
+  for (int p = 0; p < LANES; ++p)
+    e |= cat_check(valid.v[p], lane_at(tot, p), lane_at(wmin, p), pid.v[p], first_bad);
   return e;
 }
 template <class A, class B, class M>

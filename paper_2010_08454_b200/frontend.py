@@ -600,7 +600,7 @@ class _Compiler:
         elif k == "uniform-continuous":
             g.emit(f"{lhs} = fmaf({_real(a[1])} - {_real(a[0])}, draw_uniform(ws, {m}), {_real(a[0])});")
         elif k == "uniform-discrete":
-            g.emit(f"err |= ud_check({g.valid_m()}, {a[0].code}, {a[1].code});")
+            g.emit(f"err |= ud_check({g.valid_m()}, {a[0].code}, {a[1].code}, pid, first_bad);")
             g.emit(f"{lhs} = ud_draw(ws, {a[0].code}, {a[1].code}, {m});")
         elif k == "bernoulli":
             g.emit(f"{lhs} = draw_uniform(ws, {m}) < {_real(a[0])};")
@@ -617,7 +617,7 @@ class _Compiler:
             w = a[0]
             tot, wmin = self._cat_total(w), g.fresh("cmin")
             g.emit(f"const auto {wmin} = {self._fold('fminf', w)};")
-            g.emit(f"err |= cat_check({g.valid_m()}, {tot}, {wmin});")
+            g.emit(f"err |= cat_check({g.valid_m()}, {tot}, {wmin}, pid, first_bad);")
             u = g.fresh("cu")
             g.emit(f"const auto {u} = draw_uniform(ws, {m}) * {tot};")
             terms, cum = [], None
@@ -1106,6 +1106,7 @@ cuppl_dsl_model(const float* __restrict__ D, unsigned long long pid_begin, unsig
   acc.init();
   const PhiloxKey key{{k0, k1}};
   unsigned int err = 0u;
+  unsigned long long first_bad = ~0ull;  // smallest particle id with invalid parameters
   // block-uniform chunk loop (lanes past the end run masked): the model body stays in
   // uniform control flow, so warp-uniform data indices use the uniform datapath
   for (unsigned long long base = blockIdx.x * (256ull * LANES); base < n;
@@ -1140,7 +1141,10 @@ cuppl_dsl_model(const float* __restrict__ D, unsigned long long pid_begin, unsig
     }}
     (void)nd;
   }}
-  if (err) atomicOr(err_out, err);
+  if (err) {{
+    atomicOr(err_out, err);
+    atomicMin(reinterpret_cast<unsigned long long*>(err_out + 2), first_bad);
+  }}
   is_epilogue(acc, block_recs, counter, rec_out);
 }}
 '''
@@ -1159,9 +1163,11 @@ cuppl_dsl_mcmc(const float* __restrict__ D, unsigned int n_chains, unsigned int 
                unsigned int k1, double* stats_out, unsigned int* err_out) {{
   const PhiloxKey key{{k0, k1}};
   unsigned int err = 0u;
+  unsigned long long first_bad = ~0ull;  // smallest chain id with invalid parameters
   const bool valid = true;
   for (unsigned int c = blockIdx.x * blockDim.x + threadIdx.x; c < n_chains; c += gridDim.x * blockDim.x) {{
     const unsigned int chain = chain_begin + c;
+    const unsigned long long pid = chain;
     float oldVal[MAXD], newVal[MAXD], oldScore[MAXD], newScore[MAXD];
     unsigned char oldKind[MAXD], newKind[MAXD];
     int oldLen = 0;
@@ -1216,7 +1222,10 @@ cuppl_dsl_mcmc(const float* __restrict__ D, unsigned int n_chains, unsigned int 
     out[{ns_arr} + {nb_arr}] = nrec;
     out[{ns_arr} + {nb_arr} + 1] = nacc;
   }}
-  if (err) atomicOr(err_out, err);
+  if (err) {{
+    atomicOr(err_out, err);
+    atomicMin(reinterpret_cast<unsigned long long*>(err_out + 2), first_bad);
+  }}
 }}
 """
 
@@ -1390,6 +1399,21 @@ def _function(model: CompiledModel):
     return _MODULES[h][1], _MODULES[h][2]
 
 
+def _raise_param_error(err, what: str):
+    """Map a kernel error word [flags, 0, first failing id (u64)] to InvalidDistParamError and
+    reset it."""
+    w = err.cpu().numpy()
+    if not w[0]:
+        return
+    first = int(w[2:4].view(np.uint64)[0])
+    err.copy_(err.new_tensor([0, 0, -1, -1]))
+    if w[0] & 1:
+        msg = "uniform-discrete(a, b) needs b > a (SPEC.md:347)"
+    else:
+        msg = "categorical(w): weights must be >= 0 and not all 0 (SURVEY.md D5)"
+    raise InvalidDistParamError(f"{msg}; first failing {what}: {first}")
+
+
 class DslLauncher:
     """Launcher of a compiled model with the IsLauncher interface (launch(lo, hi, key, ...),
     .rec): infer.run_importance shards and merges it like the hand-written kernels."""
@@ -1407,7 +1431,8 @@ class DslLauncher:
         self.data = torch.from_numpy(model.data).to(self.device)
         self.ws = torch.zeros(256 + self.max_grid * N.REC_BYTES, dtype=torch.uint8, device=self.device)
         self.rec = torch.empty(N.REC_BYTES, dtype=torch.uint8, device=self.device)
-        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        # error word: [flags, 0, first failing particle id (u64, all ones when none)]
+        self.err = torch.tensor([0, 0, -1, -1], dtype=torch.int32, device=self.device)
         self.fn, self.lanes = _function(model)
 
     def launch(self, pid_begin: int, pid_end: int, key: int, lw_out=None, draws_out=None, ret_out=None,
@@ -1436,12 +1461,7 @@ class DslLauncher:
             raise InferRuntimeError(f"cuLaunchKernel failed: {err}")
 
     def check_errors(self):
-        e = int(self.err.item())
-        if e:
-            self.err.zero_()
-            if e & 1:
-                raise InvalidDistParamError("uniform-discrete(a, b) needs b > a (SPEC.md:347)")
-            raise InvalidDistParamError("categorical(w): weights must be >= 0 and not all 0 (SURVEY.md D5)")
+        _raise_param_error(self.err, "particle")
 
     def trace_of(self, pid: int, key: int):
         """Return value of one particle (re-executed: the streams are counter-based)."""
@@ -1503,7 +1523,7 @@ def run_mcmc(model: CompiledModel, n_steps: int, rng, *, chains: int = 4096, bur
     fn, _ = _function(model)
     width = max(model.n_stats, 1) + max(model.n_bins, 1) + 2
     stats = torch.zeros((chains, width), dtype=torch.float64, device=dev)
-    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    err = torch.tensor([0, 0, -1, -1], dtype=torch.int32, device=dev)
     key = key_of(rng)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     grid = int(min((chains + 127) // 128, sms * 16))
@@ -1515,6 +1535,5 @@ def run_mcmc(model: CompiledModel, n_steps: int, rng, *, chains: int = 4096, bur
     e, = cu.cuLaunchKernel(fn, grid, 1, 1, 128, 1, 1, 0, st, C.addressof(ptrs), 0)
     if e != cu.CUresult.CUDA_SUCCESS:
         raise InferRuntimeError(f"cuLaunchKernel failed: {e}")
-    if int(err.item()):
-        raise InvalidDistParamError("uniform-discrete(a, b) needs b > a (SPEC.md:347)")
+    _raise_param_error(err, "chain")
     return stats.cpu().numpy()

@@ -459,8 +459,30 @@ def test_gpu_categorical_lmh_and_invalid_weights(cuda):
     tv = 0.5 * sum(abs(got.get(k, 0.0) - p) for k, p in ex.items())
     assert tv < 0.03, (got, ex)
     bad = frontend.compile_program("model <- function() { sample(categorical([0.0, 0.0])) }; importance(model, 10)")
-    with pytest.raises(InvalidDistParamError):
+    with pytest.raises(InvalidDistParamError, match="first failing particle: 0"):
         infer.run_importance(bad, 1000, Rng(1))
+
+
+@pytest.mark.gpu
+def test_gpu_error_word_names_the_first_failing_particle(cuda):
+    """the device error word keeps the first failing particle id — here
+    uniform-discrete(k, 2) is invalid exactly for the particles whose first draw k is 2."""
+    import torch
+
+    from paper_2010_08454_b200.errors import InvalidDistParamError
+
+    m = frontend.compile_program("model <- function() { k <- sample(uniform-discrete(0, 3)); "
+                                 "sample(uniform-discrete(k, 2)) }; importance(model, 10)")
+    la = frontend.DslLauncher(m)
+    first, n = 10**10, 5000
+    draws = torch.zeros((n, m.max_draws), dtype=torch.float32, device=la.device)
+    la.launch(first, first + n, 0xABCDEF, draws_out=draws)
+    k = draws[:, 0].cpu().numpy()
+    expect = first + int(np.argmax(k == 2))
+    assert (k == 2).any()
+    with pytest.raises(InvalidDistParamError, match=f"first failing particle: {expect}$"):
+        la.check_errors()
+    la.check_errors()  # the word was reset
 
 
 @pytest.mark.gpu
