@@ -523,3 +523,29 @@ def test_gpu_compiled_lmh_spec_rows(cuda):
     assert 0.0 < post.stats["acceptance"] < 1.0
     one = infer.run_lmh(prior, 1, Rng(4), chains=1)
     assert len(one.support) == 1 and one.support[0][1] == 1.0
+
+
+REFERENCE_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not __import__("os").path.isdir(REFERENCE_SRC),
+                    reason="the reference package is only present in the build container")
+def test_reference_parser_accepts_every_compiled_program():
+    """Drop-in surface syntax: every CuPPL program the GPU compiler is tested on parses with
+    the reference's own parser (cuppl/parser.py:68-451) to the same top-level bindings and a
+    result application (importance / enumerate / mcmc)."""
+    import importlib
+    import sys
+
+    sys.path.insert(0, REFERENCE_SRC)
+    try:
+        ref_parser = importlib.import_module("cuppl.parser")
+    finally:
+        sys.path.remove(REFERENCE_SRC)
+    progs = [LINREG, FIG1, COIN, MIXTURE, BRANCHY, UNBOUNDED, OBS_REPEAT, OBS_MAP, OBS_VARSD, FACTOR_REPEAT,
+             CAT_MIX, CAT_ENUM, ENUM_TWO, ENUM_BINOMIAL, LINREG_EXT]
+    for src in progs:
+        ref = ref_parser.parse(src)
+        ours = lang.parse(src)
+        assert [b.name for b in ref.bindings] == [name for name, _ in ours.bindings]
+        assert type(ref.result).__name__ == "Apply" and isinstance(ours.result, lang.Call)
