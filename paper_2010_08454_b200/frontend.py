@@ -1505,7 +1505,37 @@ def distribution_from_record(model: CompiledModel, rec, n: int, launcher: DslLau
         bins = np.array(rec.bin_w[:model.n_bins]) / S_
         conv = bool if model.return_kind == "bool" else int
         out.support = [(conv(k), float(p)) for k, p in enumerate(bins) if p > 0]
+        out.support_truncated = False
+        if model.return_kind == "int" and bins.sum() < 1.0 - 1e-6:
+            full = _full_int_support(model, n, launcher, key)
+            if full is not None:
+                out.support = full
+            else:
+                out.support_truncated = True
     return out
+
+
+def _full_int_support(model: CompiledModel, n: int, launcher: DslLauncher, key: int):
+    """The record histograms returned values 0..MAX_BINS-1; when weight falls outside, re-run
+    the (counter-based, hence identical) particles with their log-weights and returned values
+    materialised and histogram the whole support with K3 (exact fixed-point bins). One process
+    and n <= 2^30 only; None otherwise."""
+    import torch
+
+    from .infer import _world, normalize_tensors
+
+    if n > 1 << 30 or _world(None)[1] > 1:
+        return None
+    lw = torch.empty(n, dtype=torch.float32, device=launcher.device)
+    ret = torch.empty(n, dtype=torch.float32, device=launcher.device)
+    rec = torch.empty_like(launcher.rec)
+    launcher.launch(0, n, key, lw_out=lw, ret_out=ret, rec_out=rec)
+    v = ret.to(torch.int64)
+    lo, hi = int(v.min()), int(v.max())
+    if hi - lo >= 1 << 20:
+        return None
+    res = normalize_tensors(lw, (v - lo).to(torch.int32), hi - lo + 1)
+    return [(lo + k, float(p)) for k, p in enumerate(res["probs"]) if p > 0]
 
 
 def run_mcmc(model: CompiledModel, n_steps: int, rng, *, chains: int = 4096, burn_in: int = 0, thin: int = 1,

@@ -60,8 +60,9 @@ def test_binomial(cuda):
     post = infer.run_importance(frontend.compile_program(_src("binomial")), 2_000_000, Rng(3))
     pmf = [math.comb(10, k) * 0.3 ** k * 0.7 ** (10 - k) for k in range(11)]
     got = dict(post.support)
-    for k in range(8):  # the compact record histograms returned values 0..7 (MAX_BINS)
+    for k in range(11):  # beyond the record's 8 bins: the K3 second pass (full support)
         assert abs(got.get(k, 0.0) - pmf[k]) < 2e-3, (k, got.get(k), pmf[k])
+    assert 8 in got and abs(sum(got.values()) - 1.0) < 1e-9
     assert abs(post.mean["value"] - 3.0) < 0.01
 
 
@@ -139,8 +140,9 @@ def test_enumerate_geometric_and_cli(cuda, capsys):
 
     post = infer.run_enumeration(frontend.compile_program(_src("enumerate_geometric")))
     got = dict(post.support)
-    for k in range(8):
+    for k in range(20):  # the whole support: 0..19 and -1 (all tails)
         assert abs(got[k] - 0.5 ** (k + 1)) < 1e-6
+    assert abs(got[-1] - 0.5 ** 20) < 1e-9
     assert cli.main(["run", str(EX / "enumerate_geometric.cup"), "--format", "tsv"]) == 0
     lines = capsys.readouterr().out.splitlines()
     assert lines[0].split("\t")[0] == "0" and abs(float(lines[0].split("\t")[1]) - 0.5) < 1e-6
