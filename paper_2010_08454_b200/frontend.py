@@ -202,6 +202,7 @@ class _Gen:
         self.depth = 0
         self.bounds: dict = {}  # C variable of a uniform-discrete draw -> largest value
         self.masks: list = []  # (indent, C name) of the open particle masks, innermost last
+        self.calls: list = []  # user functions being inlined (recursion depth per function)
         self.masked = False  # some control flow depends on particle values
 
     def fresh(self, p="t"):
@@ -312,7 +313,7 @@ def _scalar(v, what) -> S:
 
 
 class _Compiler:
-    def __init__(self, prog: lang.Program, data: dict | None):
+    def __init__(self, prog: lang.Program, data: dict | None, max_depth: int = 20):
         self.prog = prog
         self.g = _Gen([])
         self.globals: dict = {}
@@ -321,6 +322,7 @@ class _Compiler:
         self.default_n = None
         self.engine = "importance"
         self.radix = 1  # enumeration: largest support size of a choice point
+        self.max_depth = max_depth  # enumeration: recursion bound per function
 
     # -------------------------------------------------------------- top level ----
     def _data_vec(self, values) -> DataVec:
@@ -484,13 +486,16 @@ class _Compiler:
         g = self.g
         c = _scalar(self.ev(e.cond, env), "if condition")
         mark, b0 = len(g.lines), g.draw_bound
-        t = self.ev(e.then, dict(env))
-        f = self.ev(e.orelse, dict(env))
-        g.draw_bound = b0
-        if len(g.lines) == mark and isinstance(t, S) and isinstance(f, S) and t.pure and f.pure:
-            ty = "real" if "real" in (t.ty, f.ty) else t.ty
-            tc, fc = (_real(t), _real(f)) if ty == "real" else (t.code, f.code)
-            return S(f"sel({c.code}, {tc}, {fc})", ty, c.pure)
+        if not (self._effects(e.then, env) or self._effects(e.orelse, env)):
+            # pure branches: both evaluated, one select (no probe of effectful branches: with
+            # recursion that would evaluate every level twice)
+            t = self.ev(e.then, dict(env))
+            f = self.ev(e.orelse, dict(env))
+            g.draw_bound = b0
+            if len(g.lines) == mark and isinstance(t, S) and isinstance(f, S) and t.pure and f.pure:
+                ty = "real" if "real" in (t.ty, f.ty) else t.ty
+                tc, fc = (_real(t), _real(f)) if ty == "real" else (t.code, f.code)
+                return S(f"sel({c.code}, {tc}, {fc})", ty, c.pure)
         # side effects in a branch: emit real control flow (draws happen on the taken path only)
         del g.lines[mark:]
         res = g.fresh("r")
@@ -577,9 +582,15 @@ class _Compiler:
     def _apply(self, f: Fn, args):
         if len(args) != len(f.params):
             raise CompileError(f"{f.name} takes {len(f.params)} argument(s)")
+        if self.engine == "enumerate" and self.g.calls.count(id(f.body)) >= self.max_depth:
+            # bounded recursion (geometric with max_depth 20): a path that would
+            # recurse deeper is cut — zero mass; the enumeration posterior renormalises the rest
+            self.g.emit(f"dead = true;  // recursion deeper than max_depth = {self.max_depth}")
+            return S("0", "int")
         self.g.depth += 1
-        if self.g.depth > 64:
-            raise CompileError("recursion is not supported in GPU models")
+        if self.g.depth > 64 + (self.max_depth if self.engine == "enumerate" else 0):
+            raise CompileError("recursion is not supported in GPU models (enumeration bounds it by max_depth)")
+        self.g.calls.append(id(f.body))
         env = dict(f.env)
         for p, a in zip(f.params, args):
             env[p] = self.g.let(a, "a") if isinstance(a, S) else a
@@ -587,6 +598,7 @@ class _Compiler:
             return self.ev(f.body, env)
         finally:
             self.g.depth -= 1
+            self.g.calls.pop()
 
     def _emit_draw(self, k: str, a, v: str, decl: bool = True):
         """Draw from the particle's / step's word stream into `v` (the reference algorithms,
@@ -1030,10 +1042,10 @@ class _Compiler:
         """A throwaway copy for type probes: nothing it emits or binds reaches this compiler."""
         c = _Compiler.__new__(_Compiler)
         c.prog, c.model, c.default_n = self.prog, self.model, self.default_n
-        c.engine, c.radix = self.engine, self.radix
+        c.engine, c.radix, c.max_depth = self.engine, self.radix, self.max_depth
         c.globals, c.external = dict(self.globals), dict(self.external)
         c.g = _Gen(list(self.g.data))
-        c.g.n, c.g.bounds = self.g.n, dict(self.g.bounds)
+        c.g.n, c.g.bounds, c.g.calls = self.g.n, dict(self.g.bounds), list(self.g.calls)
         return c
 
     def _effects(self, node, env, seen=None) -> bool:
@@ -1260,10 +1272,11 @@ def _return_parts(ret, g: _Gen):
     raise CompileError(f"unsupported return value {type(ret).__name__}")
 
 
-def compile_program(source: str, data: dict | None = None) -> CompiledModel:
-    """Parse and compile a CuPPL program whose result is importance(model, n)."""
+def compile_program(source: str, data: dict | None = None, max_depth: int = 20) -> CompiledModel:
+    """Parse and compile a CuPPL program whose result is importance(model, n), enumerate(model,
+    n) or mcmc(model, n). max_depth bounds recursion in enumerated programs."""
     prog = lang.parse(source)
-    comp = _Compiler(prog, data)
+    comp = _Compiler(prog, data, max_depth)
     ret = comp.compile()
     g = comp.g
     stats, names, bin_expr, nb, kind, width, store = _return_parts(ret, g)

@@ -409,6 +409,15 @@ enumerate(model, 100000)
 """
 
 
+def test_recursion_is_bounded_in_enumeration_only():
+    src = ("geom <- function() { if (sample(bernoulli(0.5))) { 0 } else { 1 + geom() } }; "
+           "model <- function() { geom() }; enumerate(model, 2000000)")
+    m = frontend.compile_program(src, max_depth=12)
+    assert m.max_draws == 12 and m.cuda.count("dead = true;  // recursion") == 1
+    with pytest.raises(frontend.CompileError, match="recursion"):
+        frontend.compile_program(src.replace("enumerate(model, 2000000)", "importance(model, 10)"))
+
+
 def test_enumeration_compile_and_reject():
     from paper_2010_08454_b200.errors import ContinuousDistError
 
