@@ -45,7 +45,7 @@ def test_smc_bit_exact_single_rank(cuda, oracle_lib, n, S, steps):
     assert np.allclose(res.log_z_steps, ref["log_z_steps"], rtol=1e-7, atol=1e-7)
 
 
-@pytest.mark.parametrize("R", [2, 3, 8])
+@pytest.mark.parametrize("R", [2, 3, 4, 8])
 def test_smc_rank_partition_invariance(cuda, oracle_lib, R):
     """Virtual ranks on one GPU: identical bits for every partition of the particles."""
     from paper_2010_08454_b200 import models
