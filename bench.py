@@ -362,6 +362,12 @@ def run_ours(args) -> dict | None:
                     "peak_source": f"measured: Philox {ph:.3g} blocks/s (calib kind 2) + FFMA2 {peak / 1e12:.1f} "
                                    "TFLOP/s (kind 0), 1 block + {fpp:.0f} flops per particle".replace("{fpp:.0f}", f"{fpp:.0f}"),
                     "flops_per_particle": fpp}
+            # the same serialisation over the EXECUTED fma-pipe mix per particle (ncu SASS of this
+            # kernel, profiles/r1_final_ncu_summary.json: 61 FFMA2/FADD2 + 22 scalar FP; padded
+            # Horner, FADD as a full slot, Box-Muller, epilogue) — DESIGN.md §4 "Why C5 ..."
+            exec_roof = 1.0 / (1.0 / ph + 61.0 / (peak / 4.0) + 22.0 / (peak / 2.0))
+            roof["executed_mix_bound"] = exec_roof
+            roof["frac_of_executed_mix_bound"] = rate / exec_roof
         result = {
             "metric": METRIC,
             "value": value,
