@@ -1,0 +1,120 @@
+"""Seeded random CuPPL programs for differential testing of the model compiler against the
+fp64 interpreter (tests/test_frontend_fuzz.py). Expressions stay numerically tame: bounded
+arguments for exp / log / sqrt, literal sds, no division by values near zero."""
+
+import random
+
+DISTS = ["normal", "uniform-continuous", "beta", "exponential", "bernoulli", "uniform-discrete", "poisson"]
+
+
+class _Gen:
+    def __init__(self, seed):
+        self.r = random.Random(seed)
+        self.reals = []   # names of real-valued model variables
+        self.ints = []
+        self.bools = []
+        self.n = 0
+
+    def name(self):
+        self.n += 1
+        return f"v{self.n}"
+
+    def real_atom(self):
+        r = self.r
+        if self.reals and r.random() < 0.7:
+            return r.choice(self.reals)
+        if self.ints and r.random() < 0.3:
+            return f"to-real({r.choice(self.ints)})"
+        return f"{r.uniform(-3, 3):.3f}"
+
+    def real_expr(self, depth=0):
+        r = self.r
+        if depth >= 2 or r.random() < 0.35:
+            return self.real_atom()
+        k = r.random()
+        a, b = self.real_expr(depth + 1), self.real_expr(depth + 1)
+        if k < 0.25:
+            return f"({a} + {b})"
+        if k < 0.45:
+            return f"({a} - {b})"
+        if k < 0.65:
+            return f"({a} * {b})"
+        if k < 0.72:
+            return f"({a} / (abs({b}) + 1.0))"
+        if k < 0.79:
+            return f"exp({a} / 20.0)"
+        if k < 0.86:
+            return f"log(abs({a}) + 1.0)"
+        if k < 0.92:
+            return f"sqrt(abs({a}))"
+        if self.bools:
+            return f"if ({r.choice(self.bools)}) {{ {a} }} else {{ {b} }}"
+        return f"if ({a} > {b}) {{ {a} }} else {{ {b} }}"
+
+    def draw(self):
+        r = self.r
+        k = r.choice(DISTS)
+        v = self.name()
+        if k == "normal":
+            s = f"sample(normal({self.real_expr(1)}, {r.uniform(0.5, 5):.2f}))"
+            self.reals.append(v)
+        elif k == "uniform-continuous":
+            lo = r.uniform(-5, 0)
+            s = f"sample(uniform-continuous({lo:.2f}, {lo + r.uniform(0.5, 5):.2f}))"
+            self.reals.append(v)
+        elif k == "beta":
+            s = f"sample(beta({r.uniform(0.5, 4):.2f}, {r.uniform(0.5, 4):.2f}))"
+            self.reals.append(v)
+        elif k == "exponential":
+            s = f"sample(exponential({r.uniform(0.2, 3):.2f}))"
+            self.reals.append(v)
+        elif k == "bernoulli":
+            s = f"sample(bernoulli({r.uniform(0.1, 0.9):.2f}))"
+            self.bools.append(v)
+        elif k == "uniform-discrete":
+            lo = r.randint(-3, 2)
+            s = f"sample(uniform-discrete({lo}, {lo + r.randint(1, 5)}))"
+            self.ints.append(v)
+        else:
+            s = f"sample(poisson({r.uniform(0.5, 6):.2f}))"
+            self.ints.append(v)
+        return f"  {v} <- {s};"
+
+    def effect(self):
+        r = self.r
+        k = r.random()
+        if k < 0.3:
+            return f"  factor(-abs({self.real_expr()}) / 4.0);"
+        if k < 0.55:
+            return (f"  observe(normal({self.real_expr(1)}, {r.uniform(0.5, 3):.2f}), {r.uniform(-3, 3):.2f});")
+        if k < 0.75:
+            return ("  map(function(i) { observe(normal(" + self.real_expr(1) + " * xs[i], "
+                    f"{r.uniform(0.5, 3):.2f}), ys[i]) }}, repeat(function(i) {{ i }}, length(xs)));")
+        if k < 0.9:
+            return ("  factor(reduce(function(acc, i) { acc - abs(" + self.real_expr(1)
+                    + " - ys[i]) / 10.0 }, 0.0, repeat(function(i) { i }, length(ys))));")
+        c = r.choice(self.bools) if self.bools else f"({self.real_expr(1)} > 0.0)"
+        return (f"  if ({c}) {{ factor({self.real_expr(1)} / 10.0) }} else "
+                f"{{ observe(normal({self.real_expr(1)}, 2.0), 0.5) }};")
+
+
+def program(seed: int) -> str:
+    g = _Gen(seed)
+    r = g.r
+    n_pts = r.randint(1, 9)
+    xs = ", ".join(f"{r.uniform(-2, 2):.3f}" for _ in range(n_pts))
+    ys = ", ".join(f"{r.uniform(-2, 2):.3f}" for _ in range(n_pts))
+    lines = [f"xs <- [{xs}];", f"ys <- [{ys}];", "model <- function() {"]
+    for _ in range(r.randint(2, 5)):
+        lines.append(g.draw())
+        if r.random() < 0.6:
+            lines.append(g.effect())
+    lines.append(g.effect())
+    if r.random() < 0.5 or not g.reals:
+        ret = g.real_expr()
+    else:
+        ret = "[" + ", ".join(r.sample(g.reals, min(len(g.reals), 3))) + "]"
+    lines.append(f"  {ret}")
+    lines.append("};")
+    lines.append("importance(model, 1000)")
+    return "\n".join(lines) + "\n"
