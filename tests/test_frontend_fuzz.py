@@ -40,3 +40,12 @@ def test_gpu_fuzz_program_matches_interpreter(cuda, seed):
             assert not np.isfinite(lw[i]) or math.isinf(ref), (seed, i, lw[i], ref)
             continue
         assert abs(lw[i] - ref) <= 1e-4 * abs(ref) + 1e-4, (seed, i, lw[i], ref, draws[i], src)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", SEEDS[:12])
+def test_gpu_fuzz_program_masked_lanes(cuda, seed, monkeypatch):
+    """The same programs built with 8 particles per thread even where control flow depends on
+    particle values (masked lane form, dsl_lanes.cuh)."""
+    monkeypatch.setenv("CUPPL_DSL_LANES", "8")
+    test_gpu_fuzz_program_matches_interpreter(cuda, seed)
