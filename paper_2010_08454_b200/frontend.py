@@ -413,6 +413,8 @@ class _Compiler:
                 if e.op != "-" or a.ty == "int2":
                     raise _PairUnsupported(e.op)
                 return S(f"mul2({a.code}, pack2(-1.f, -1.f))", "real2", a.pure)
+            if e.op == "-" and a.ty in ("int", "real") and _is_literal(a.code):
+                return _lit(-int(a.code) if a.ty == "int" else -float(a.code.rstrip("f")))  # a constant
             if e.op == "-":
                 return S(f"(-{a.code})", a.ty if a.ty != "bool" else "int", a.pure)
             return S(f"(!{a.code})", "bool", a.pure)

@@ -118,3 +118,46 @@ def program(seed: int) -> str:
     lines.append("};")
     lines.append("importance(model, 1000)")
     return "\n".join(lines) + "\n"
+
+
+def discrete_program(seed: int) -> str:
+    """A random finite-support program for enumerate(model, n): bernoulli / uniform-discrete /
+    categorical choice points (at most 5), factors and observes of real expressions of them, an
+    integer return."""
+    r = random.Random(10_000 + seed)
+    ints, bools, lines = [], [], ["model <- function() {"]
+    n = 0
+    for _ in range(r.randint(2, 5)):
+        n += 1
+        v = f"d{n}"
+        k = r.random()
+        if k < 0.35:
+            lines.append(f"  {v} <- sample(bernoulli({r.uniform(0.1, 0.9):.2f}));")
+            bools.append(v)
+        elif k < 0.7:
+            lo = r.randint(-2, 2)
+            lines.append(f"  {v} <- sample(uniform-discrete({lo}, {lo + r.randint(2, 4)}));")
+            ints.append(v)
+        else:
+            w = ", ".join(f"{r.uniform(0.1, 2):.2f}" for _ in range(r.randint(2, 4)))
+            lines.append(f"  {v} <- sample(categorical([{w}]));")
+            ints.append(v)
+        if (ints or bools) and r.random() < 0.7:
+            def term():
+                if ints and (not bools or r.random() < 0.6):
+                    return f"to-real({r.choice(ints)})"
+                b = r.choice(bools)
+                return f"if ({b}) {{ {r.uniform(-2, 2):.2f} }} else {{ {r.uniform(-2, 2):.2f} }}"
+            e = term() if r.random() < 0.5 else f"({term()} * {r.uniform(-1.5, 1.5):.2f} + {term()})"
+            if r.random() < 0.5:
+                lines.append(f"  factor(-abs({e}) / 2.0);")
+            else:
+                lines.append(f"  observe(normal({e}, {r.uniform(0.5, 2):.2f}), {r.uniform(-2, 2):.2f});")
+    if ints:
+        ret = " + ".join(r.sample(ints, min(len(ints), 2)))
+    else:
+        ret = f"if ({bools[0]}) {{ 1 }} else {{ 0 }}"
+    if bools and r.random() < 0.5:
+        ret = f"if ({r.choice(bools)}) {{ {ret} }} else {{ 7 }}"
+    lines += [f"  {ret}", "};", "enumerate(model, 100000)"]
+    return "\n".join(lines) + "\n"

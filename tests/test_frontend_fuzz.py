@@ -49,3 +49,20 @@ def test_gpu_fuzz_program_masked_lanes(cuda, seed, monkeypatch):
     particle values (masked lane form, dsl_lanes.cuh)."""
     monkeypatch.setenv("CUPPL_DSL_LANES", "8")
     test_gpu_fuzz_program_matches_interpreter(cuda, seed)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", list(range(16)))
+def test_gpu_fuzz_enumeration_matches_forced_choice_oracle(cuda, seed):
+    from fuzz_programs import discrete_program
+    from oracle.dsl_eval import Enumerator
+    from paper_2010_08454_b200 import infer
+
+    src = discrete_program(seed)
+    post = infer.run_enumeration(frontend.compile_program(src))
+    ref, log_z = Enumerator(src).posterior()
+    got = dict(post.support)
+    assert set(got) == {k for k, p in ref.items() if p > 0}, (seed, src)
+    for k, p in ref.items():
+        assert abs(got.get(k, 0.0) - p) < 1e-5, (seed, k, got.get(k), p, src)
+    assert abs(post.log_z - log_z) < 1e-4, (seed, post.log_z, log_z)
