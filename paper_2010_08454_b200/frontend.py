@@ -68,6 +68,7 @@ TAG_DSL = 8  # CUPPL_TAG_DSL
 TAG_DSL_MH = 9  # CUPPL_TAG_DSL_MH: LMH step streams, id = step << 32 | chain
 MAX_STATS = 16  # cuppl_is_record.stat_w
 MAX_BINS = 8   # cuppl_is_record.bin_w
+MCMC_BINS, MCMC_BIN_LO = 128, -32  # chain histograms of integer returns: values [-32, 96)
 MAX_TRACE_DRAWS = 256
 MAX_CONST_DATA = 16_000  # floats kept in the module's __constant__ bank (64 KB); larger: __ldg
 DATA_SYM = "DATA"        # resolved by the kernel prelude to the constant bank or the buffer
@@ -1100,6 +1101,7 @@ class CompiledModel:
     engine: str = "importance"
     radix: int = 1
     masked: bool = False  # particle-dependent control flow (lane builds are opt-in)
+    bin_lo: int = 0  # histogram bin k holds the integer return value bin_lo + k
     kind: str = "dsl"
     _fn: object = field(default=None, repr=False)
 
@@ -1244,17 +1246,19 @@ cuppl_dsl_mcmc(const float* __restrict__ D, unsigned int n_chains, unsigned int 
 """
 
 
-def _return_parts(ret, g: _Gen):
+def _return_parts(ret, g: _Gen, int_bins: tuple = (0, MAX_BINS)):
     """(stat expressions, stat names, bin expression, n_bins, kind, width, stores); a store is
-    (component index, value expression) of ret_out[idx * width + k]."""
+    (component index, value expression) of ret_out[idx * width + k]. An integer return is
+    histogrammed over values [lo, lo + n) of int_bins = (lo, n)."""
     if ret is None:
         return [], [], "0", 0, "none", 0, []
     if isinstance(ret, S):
         v = g.let(ret, "ret")
         st = [_real(v), f"{_real(v)} * {_real(v)}"]
         if ret.ty in ("int", "bool"):
-            b = f"sel(({v.code}) >= 0 && ({v.code}) < {MAX_BINS}, to_i({v.code}), -1)"
-            return st, ["value", "value^2"], b, MAX_BINS, ret.ty, 1, [(0, _real(v))]
+            lo, nb = int_bins if ret.ty == "int" else (0, MAX_BINS)
+            b = f"sel(({v.code}) >= {lo} && ({v.code}) < {lo + nb}, to_i({v.code}) - ({lo}), -1)"
+            return st, ["value", "value^2"], b, nb, ret.ty, 1, [(0, _real(v))]
         return st, ["value", "value^2"], "0", 0, "real", 1, [(0, _real(v))]
     if isinstance(ret, ConstVec):
         items = [g.let(x, "ret") for x in ret.items]
@@ -1281,7 +1285,9 @@ def compile_program(source: str, data: dict | None = None, max_depth: int = 20) 
     comp = _Compiler(prog, data, max_depth)
     ret = comp.compile()
     g = comp.g
-    stats, names, bin_expr, nb, kind, width, store = _return_parts(ret, g)
+    int_bins = (MCMC_BIN_LO, MCMC_BINS) if comp.engine == "mcmc" else (0, MAX_BINS)
+    stats, names, bin_expr, nb, kind, width, store = _return_parts(ret, g, int_bins)
+    bin_lo = int_bins[0] if kind == "int" else 0
     lane_stats = [f"lane_at({x}, p_)" for x in stats]
     maxd = g.draw_bound if 0 < g.draw_bound <= MAX_TRACE_DRAWS else 1
     body = "\n".join("  " + line for line in g.lines)
@@ -1314,7 +1320,8 @@ def compile_program(source: str, data: dict | None = None, max_depth: int = 20) 
                                    body="\n".join("    " + line for line in g.lines))
         return CompiledModel(source=source, cuda=cuda, data=data_arr, n_stats=len(stats), n_bins=nb,
                              stat_names=names, return_kind=kind, return_width=width,
-                             max_draws=g.draw_bound, default_n=comp.default_n, engine="mcmc")
+                             max_draws=g.draw_bound, default_n=comp.default_n, engine="mcmc",
+                             bin_lo=bin_lo)
     cuda = _KERNEL.format(maxd=maxd, data_decl=data_decl, enum_init=enum_init, enum_final=enum_final,
                           ns=len(stats), nb=nb, ns_arr=max(len(stats), 1),
                           stats=", ".join(lane_stats) if stats else "0.f", bin=bin_expr, tag=TAG_DSL,

@@ -443,7 +443,9 @@ def _run_compiled_lmh(model, n_samples: int, rng, *, chains: int, burn_in: int, 
     if model.n_bins:
         probs = st[:, ns:ns + nb].sum(axis=0) / nrec
         conv = bool if model.return_kind == "bool" else int
-        out.support = [(conv(k), float(p)) for k, p in enumerate(probs) if p > 0]
+        lo = getattr(model, "bin_lo", 0)
+        out.support = [(conv(lo + k), float(p)) for k, p in enumerate(probs) if p > 0]
+        out.support_truncated = bool(probs.sum() < 1.0 - 1e-9)  # values outside the chain histogram
     steps = max(n_samples - 1, 1)
     out.stats["acceptance"] = float(st[:, ns + nb + 1].sum() / (len(st) * steps))
     out.stats["chains"] = chains

@@ -66,3 +66,21 @@ def test_gpu_fuzz_enumeration_matches_forced_choice_oracle(cuda, seed):
     for k, p in ref.items():
         assert abs(got.get(k, 0.0) - p) < 1e-5, (seed, k, got.get(k), p, src)
     assert abs(post.log_z - log_z) < 1e-4, (seed, post.log_z, log_z)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", list(range(12)))
+def test_gpu_fuzz_lmh_matches_enumeration(cuda, seed):
+    """LMH on random finite-support programs (mcmc) against their exact enumeration: total
+    variation of the return value's distribution (negative values included)."""
+    from fuzz_programs import discrete_program
+    from paper_2010_08454_b200 import Rng, infer
+
+    src = discrete_program(seed)
+    ex = dict(infer.run_enumeration(frontend.compile_program(src)).support)
+    mc = infer.run_lmh(frontend.compile_program(src.replace("enumerate(model, 100000)", "mcmc(model, 10)")),
+                       3000, Rng(seed), chains=512, burn_in=300)
+    got = dict(mc.support)
+    assert not mc.support_truncated
+    tv = 0.5 * sum(abs(got.get(k, 0.0) - ex.get(k, 0.0)) for k in set(ex) | set(got))
+    assert tv < 0.04, (seed, tv, got, ex, src)
