@@ -84,3 +84,22 @@ def test_gpu_fuzz_lmh_matches_enumeration(cuda, seed):
     assert not mc.support_truncated
     tv = 0.5 * sum(abs(got.get(k, 0.0) - ex.get(k, 0.0)) for k in set(ex) | set(got))
     assert tv < 0.04, (seed, tv, got, ex, src)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", list(range(8)))
+def test_gpu_fuzz_importance_matches_enumeration(cuda, seed):
+    """Importance sampling of the same random finite-support programs against their exact
+    enumeration (negative and > 7 returns go through the full-support second pass)."""
+    from fuzz_programs import discrete_program
+    from paper_2010_08454_b200 import Rng, infer
+
+    src = discrete_program(seed)
+    ex = infer.run_enumeration(frontend.compile_program(src))
+    post = infer.run_importance(frontend.compile_program(src.replace("enumerate(model, 100000)",
+                                                                     "importance(model, 1000)")),
+                                1_000_000, Rng(seed))
+    got, exd = dict(post.support), dict(ex.support)
+    tv = 0.5 * sum(abs(got.get(k, 0.0) - exd.get(k, 0.0)) for k in set(exd) | set(got))
+    assert tv < 0.01 and not post.support_truncated, (seed, tv, got, exd)
+    assert abs(post.log_z - ex.log_z) < 0.01
