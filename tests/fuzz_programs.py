@@ -161,3 +161,36 @@ def discrete_program(seed: int) -> str:
         ret = f"if ({r.choice(bools)}) {{ {ret} }} else {{ 7 }}"
     lines += [f"  {ret}", "};", "enumerate(model, 100000)"]
     return "\n".join(lines) + "\n"
+
+
+def vector_program(seed: int) -> str:
+    """Random programs over drawn vectors: repeat of draws (literal or uniform-discrete length),
+    reduce / map over them and over data, indexing by drawn integers, vector returns."""
+    r = random.Random(20_000 + seed)
+    n_pts = r.randint(1, 7)
+    xs = ", ".join(f"{r.uniform(-2, 2):.3f}" for _ in range(n_pts))
+    ys = ", ".join(f"{r.uniform(-2, 2):.3f}" for _ in range(n_pts))
+    lines = [f"xs <- [{xs}];", f"ys <- [{ys}];", "model <- function() {"]
+    length = str(r.randint(1, 5)) if r.random() < 0.5 else "k"
+    if length == "k":
+        lines.append(f"  k <- sample(uniform-discrete(1, {r.randint(2, 6)}));")
+    lines.append(f"  c <- repeat(function(i) {{ sample(normal({r.uniform(-1, 1):.2f}, {r.uniform(0.5, 3):.2f})) }}, {length});")
+    choice = r.random()
+    if choice < 0.3:  # sum of squares of the vector as a factor
+        lines.append("  factor(-reduce(function(acc, v) { acc + v * v }, 0.0, c) / 4.0);")
+    elif choice < 0.6:  # a polynomial over the data (Horner over the drawn coefficients)
+        lines.append("  factor(-reduce(function(acc, i) { acc + pow(ys[i] - reduce(function(p, j) { "
+                     "p * xs[i] + c[length(c) - 1 - j] }, 0.0, repeat(function(j) { j }, length(c))), 2) }, "
+                     "0.0, repeat(function(i) { i }, length(xs))) / 8.0);")
+    else:  # an element picked by a drawn index
+        lines.append("  j <- sample(uniform-discrete(0, length(c)));")
+        lines.append(f"  observe(normal(c[j], {r.uniform(0.5, 2):.2f}), {r.uniform(-1, 1):.2f});")
+    if r.random() < 0.5:  # per-datum draws inside map
+        lines.append(f"  map(function(y) {{ e <- sample(normal(0.0, {r.uniform(0.5, 2):.2f})); "
+                     f"observe(normal(e, 1.0), y) }}, ys);")
+    if r.random() < 0.5:
+        lines.append("  c")
+    else:
+        lines.append("  reduce(function(acc, v) { acc + v }, 0.0, c)")
+    lines += ["};", "importance(model, 1000)"]
+    return "\n".join(lines) + "\n"

@@ -103,3 +103,22 @@ def test_gpu_fuzz_importance_matches_enumeration(cuda, seed):
     tv = 0.5 * sum(abs(got.get(k, 0.0) - exd.get(k, 0.0)) for k in set(exd) | set(got))
     assert tv < 0.01 and not post.support_truncated, (seed, tv, got, exd)
     assert abs(post.log_z - ex.log_z) < 0.01
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", list(range(12)))
+def test_gpu_fuzz_vector_program_matches_interpreter(cuda, seed):
+    """Random programs over drawn vectors (repeat of draws with literal or drawn length, reduces,
+    Horner over data, indexing by a drawn integer, per-datum draws in map, vector returns)."""
+    from fuzz_programs import vector_program
+    from oracle.dsl_eval import Interpreter
+    from paper_2010_08454_b200 import Rng, infer
+
+    src = vector_program(seed)
+    post = infer.run_importance(frontend.compile_program(src), 2048, Rng(seed), return_traces=True)
+    lw = post.traces["log_weight"].cpu().numpy().astype(float)
+    draws = post.traces["draws"].cpu().numpy().astype(float)
+    it = Interpreter(src)
+    for i in range(0, 2048, 61):
+        ref, _ = it.run(draws[i])
+        assert abs(lw[i] - ref) <= 1e-4 * abs(ref) + 1e-4, (seed, i, lw[i], ref, src)

@@ -9,13 +9,16 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 import numpy as np  # noqa: E402
 
-from fuzz_programs import program  # noqa: E402
+from fuzz_programs import program, vector_program  # noqa: E402
 from oracle.dsl_eval import Interpreter  # noqa: E402
 from paper_2010_08454_b200 import Rng, frontend, infer  # noqa: E402
 
 
-def check(seed):
-    src = program(seed)
+GEN = {"scalar": program, "vector": vector_program}
+
+
+def check(seed, gen="scalar"):
+    src = GEN[gen](seed)
     m = frontend.compile_program(src)
     post = infer.run_importance(m, 1024, Rng(seed), return_traces=True)
     lw = post.traces["log_weight"].cpu().numpy().astype(float)
@@ -35,11 +38,11 @@ def check(seed):
     return None
 
 
-def main(a, b):
+def main(a, b, gen="scalar"):
     fails = 0
     for seed in range(a, b):
         try:
-            msg = check(seed)
+            msg = check(seed, gen)
         except Exception as e:  # noqa: BLE001
             msg = f"{type(e).__name__}: {str(e)[:300]}"
         if msg:
@@ -49,4 +52,4 @@ def main(a, b):
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]), int(sys.argv[2]))
+    main(int(sys.argv[1]), int(sys.argv[2]), sys.argv[3] if len(sys.argv) > 3 else "scalar")
