@@ -122,3 +122,20 @@ def test_gpu_fuzz_vector_program_matches_interpreter(cuda, seed):
     for i in range(0, 2048, 61):
         ref, _ = it.run(draws[i])
         assert abs(lw[i] - ref) <= 1e-4 * abs(ref) + 1e-4, (seed, i, lw[i], ref, src)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [0, 1, 3, 4, 9, 13])
+def test_gpu_fuzz_lmh_matches_importance_on_vector_programs(cuda, seed):
+    """LMH on programs whose trace dimension changes (a drawn vector length: the trace database
+    reuses sites by position and kind) against importance sampling of the same
+    program: posterior means within a tenth of a posterior sd."""
+    from fuzz_programs import vector_program
+    from paper_2010_08454_b200 import Rng, infer
+
+    src = vector_program(seed)
+    isd = infer.run_importance(frontend.compile_program(src), 4_000_000, Rng(seed))
+    mc = infer.run_lmh(frontend.compile_program(src.replace("importance(model, 1000)", "mcmc(model, 10)")),
+                       4000, Rng(seed), chains=1024, burn_in=1000)
+    sd = max(isd.stats["var_value"], 1e-12) ** 0.5
+    assert abs(isd.mean["value"] - mc.mean["value"]) < 0.1 * sd, (seed, isd.mean, mc.mean, sd)
