@@ -395,6 +395,8 @@ def run_ours(args) -> dict | None:
             "gpu_launches": args.steps,
             "clocks": clk,
         }
+        if args.workload == "dsl-linreg":
+            result["config"]["particles_per_thread"] = launcher.lanes  # dsl_lanes.cuh build chosen
         if world == 1 and not args.no_cpu_baseline:
             result["cpu_baseline"] = cpu_baseline("linreg" if args.workload == "dsl-linreg" else args.workload,
                                                   src_model)
