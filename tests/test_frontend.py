@@ -558,3 +558,39 @@ def test_reference_parser_accepts_every_compiled_program():
         ours = lang.parse(src)
         assert [b.name for b in ref.bindings] == [name for name, _ in ours.bindings]
         assert type(ref.result).__name__ == "Apply" and isinstance(ours.result, lang.Call)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dist,mean,var", [
+    ("normal(1.5, 2.0)", 1.5, 4.0),
+    ("uniform-continuous(-1.0, 3.0)", 1.0, 16.0 / 12.0),
+    ("beta(2.0, 5.0)", 2.0 / 7.0, 10.0 / (49.0 * 8.0)),
+    ("beta(0.5, 0.7)", 0.5 / 1.2, 0.35 / (1.44 * 2.2)),
+    ("exponential(2.5)", 0.4, 0.16),
+    ("poisson(3.5)", 3.5, 3.5),
+    ("poisson(40.0)", 40.0, 40.0),
+    ("uniform-discrete(-3, 4)", 0.0, 4.0),
+    ("categorical([1.0, 2.0, 3.0, 4.0])", 2.0, 1.0),
+])
+def test_gpu_compiled_draw_moments(cuda, dist, mean, var):
+    """The compiled word-stream draws (csrc/draws.cuh, the reference algorithms rng.py:43-117)
+    have the right distributions: prior means and variances within 5 standard errors."""
+    from paper_2010_08454_b200 import Rng, infer
+
+    n = 1_000_000
+    post = infer.run_importance(frontend.compile_program(f"model <- function() {{ sample({dist}) }}; "
+                                                         f"importance(model, 10)"), n, Rng(13))
+    v = post.stats["var_value"]
+    assert abs(post.mean["value"] - mean) < 5 * math.sqrt(var / n), (dist, post.mean["value"], mean)
+    assert abs(v - var) < 0.02 * var + 1e-6, (dist, v, var)
+
+
+@pytest.mark.gpu
+def test_gpu_compiled_bernoulli_frequency(cuda):
+    from paper_2010_08454_b200 import Rng, infer
+
+    n = 1_000_000
+    post = infer.run_importance(frontend.compile_program("model <- function() { sample(bernoulli(0.3)) }; "
+                                                         "importance(model, 10)"), n, Rng(14))
+    got = dict(post.support)
+    assert abs(got[True] - 0.3) < 5 * math.sqrt(0.21 / n)
