@@ -3,10 +3,10 @@
 OUT=gpurun_out/sanitize
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()"
-SM="python -c 'import __graft_entry__ as g; g.smoke()'"
+SM="${SANITIZE_CMD:-python -c 'import __graft_entry__ as g; g.smoke()'}"
 for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
   extra=""
   timeout 1500 compute-sanitizer --tool $tool $extra --print-limit 30 bash -c "$SM" > $OUT/$tool.log 2>&1
   echo "$tool exit=$?"
-  grep -E "ERROR SUMMARY|RACECHECK SUMMARY|smoke " $OUT/$tool.log | tail -8
+  grep -E "ERROR SUMMARY|RACECHECK SUMMARY|smoke |sanitize_extra" $OUT/$tool.log | tail -8
 done
