@@ -194,3 +194,30 @@ def vector_program(seed: int) -> str:
         lines.append("  reduce(function(acc, v) { acc + v }, 0.0, c)")
     lines += ["};", "importance(model, 1000)"]
     return "\n".join(lines) + "\n"
+
+
+def misc_program(seed: int) -> str:
+    """Operators the other generators do not reach: integer % and /, floor, to-int, pow with
+    non-2 exponents, && || !, int-valued ifs, closures over drawn values, a discrete return."""
+    r = random.Random(30_000 + seed)
+    lines = ["model <- function() {"]
+    lines.append(f"  a <- sample(uniform-discrete({r.randint(-4, 0)}, {r.randint(2, 7)}));")
+    lines.append(f"  b <- sample(uniform-discrete(1, {r.randint(3, 6)}));")
+    lines.append(f"  x <- sample(normal({r.uniform(-1, 1):.2f}, {r.uniform(0.5, 2):.2f}));")
+    lines.append(f"  t <- sample(bernoulli({r.uniform(0.2, 0.8):.2f}));")
+    lines.append(f"  scale <- function(v) {{ v * x + {r.uniform(-1, 1):.2f} }};")  # closure over x
+    ops = [
+        "to-real(a % b)", "to-real(a / b)", "floor(x * 1.7)", "to-real(to-int(x * 2.3))",
+        f"pow(abs(x) + 0.5, {r.choice([0.5, 1.5, 3.0])})", "scale(to-real(b))",
+        "if (t && a > 0) { 1.5 } else { -0.5 }", "if (t || !(b > 2)) { x } else { -x }",
+        "to-real(if (a >= b) { a - b } else { b - a })",
+    ]
+    for _ in range(r.randint(2, 4)):
+        e = r.choice(ops)
+        if r.random() < 0.5:
+            lines.append(f"  factor(-abs({e}) / 3.0);")
+        else:
+            lines.append(f"  observe(normal({e}, {r.uniform(0.7, 2):.2f}), {r.uniform(-1, 1):.2f});")
+    ret = r.choice(["a % b + 3", "if (t) { a } else { b }", "to-int(floor(x)) + 5", "a * b"])
+    lines += [f"  {ret}", "};", "importance(model, 1000)"]
+    return "\n".join(lines) + "\n"

@@ -139,3 +139,21 @@ def test_gpu_fuzz_lmh_matches_importance_on_vector_programs(cuda, seed):
                        4000, Rng(seed), chains=1024, burn_in=1000)
     sd = max(isd.stats["var_value"], 1e-12) ** 0.5
     assert abs(isd.mean["value"] - mc.mean["value"]) < 0.1 * sd, (seed, isd.mean, mc.mean, sd)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", list(range(8)))
+def test_gpu_fuzz_misc_operators(cuda, seed):
+    """Integer % and /, floor, to-int, pow, && || !, int-valued ifs, closures over draws."""
+    from fuzz_programs import misc_program
+    from oracle.dsl_eval import Interpreter
+    from paper_2010_08454_b200 import Rng, infer
+
+    src = misc_program(seed)
+    post = infer.run_importance(frontend.compile_program(src), 2048, Rng(seed), return_traces=True)
+    lw = post.traces["log_weight"].cpu().numpy().astype(float)
+    draws = post.traces["draws"].cpu().numpy().astype(float)
+    it = Interpreter(src)
+    for i in range(0, 2048, 61):
+        ref, _ = it.run(draws[i])
+        assert abs(lw[i] - ref) <= 1e-4 * abs(ref) + 1e-4, (seed, i, lw[i], ref, src)

@@ -9,12 +9,12 @@ sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 import numpy as np  # noqa: E402
 
-from fuzz_programs import program, vector_program  # noqa: E402
+from fuzz_programs import misc_program, program, vector_program  # noqa: E402
 from oracle.dsl_eval import Interpreter  # noqa: E402
 from paper_2010_08454_b200 import Rng, frontend, infer  # noqa: E402
 
 
-GEN = {"scalar": program, "vector": vector_program}
+GEN = {"scalar": program, "vector": vector_program, "misc": misc_program}
 
 
 def check(seed, gen="scalar"):
