@@ -148,3 +148,23 @@ def test_enumerate_geometric_and_cli(cuda, capsys):
     lines = capsys.readouterr().out.splitlines()
     assert lines[0].split("\t")[0] == "0" and abs(float(lines[0].split("\t")[1]) - 0.5) < 1e-6
     assert lines[1].split("\t")[0] == "1" and abs(float(lines[1].split("\t")[1]) - 0.25) < 1e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", NAMES)
+def test_example_through_the_cli(cuda, capsys, name):
+    """`run FILE.cup --format json` for every corpus program: exit code 0 and a posterior that
+    parses back."""
+    from paper_2010_08454_b200 import cli
+    from paper_2010_08454_b200.posterior import parse_posterior
+
+    args = ["run", str(EX / f"{name}.cup"), "--format", "json", "--seed", "3"]
+    if name in ("linear_regression", "logistic_regression"):
+        args += ["--samples", "200", "--chains", "256"]
+    elif name != "enumerate_geometric":
+        args += ["--particles", "200000"]
+    assert cli.main(args) == 0
+    out = parse_posterior(capsys.readouterr().out, "json")
+    assert "support" in out
+    if name in ("binomial", "enumerate_geometric", "linefitting"):
+        assert abs(sum(p for _, p in out["support"]) - 1.0) < 1e-6
