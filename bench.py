@@ -2,10 +2,17 @@
 """Benchmark: weighted particles/s of GPU importance sampling (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload linreg|poly|smc|mh]
+                    [--workload linreg|poly|smc|mh|dsl-linreg] [--dry-run]
+
+`--gpus N` outside a launcher re-executes the same command under torch.distributed.run, one
+process per GPU (NCCL, rendezvous on 127.0.0.1, NCCL_DEBUG=INFO init lines on stderr); under a
+launcher the world comes from WORLD_SIZE / RANK / LOCAL_RANK. `--dry-run` runs the multi-rank
+orchestration (sharding, record all-gather, max-over-ranks timing) over gloo on CPU without
+launching a kernel, for the CPU test suite.
 
 Default workload (BASELINE.json configs[1]): Bayesian linear regression,
-1e9 particles per GPU (weak scaling), 1,000 synthetic points, prior normal(0,10) on (a, b).
+1e9 particles in total, strong-scaled (1e9/N per GPU), 1,000 synthetic points, prior
+normal(0,10) on (a, b).
 A step is one full importance-sampling pass over those particles: Philox draws, the model's
 1,000 observe() terms, the fused log-sum-exp / ESS / moment / mode reduction, and (N > 1) the
 per-rank record all-gather over NCCL. `--workload poly` runs the Fig.1 polynomial model
@@ -51,31 +58,37 @@ UNIT = "particles/s"
 
 WORKLOADS = {
     "linreg": {
-        "name": "C2: Bayesian linear regression IS, 1e9 particles/GPU, 1k points (BASELINE configs[1])",
-        "particles_per_gpu": 10**9,
+        "name": "C2: Bayesian linear regression IS, 1e9 particles in total (strong scaling over 1-8 GPUs), "
+                "1k points (BASELINE configs[1])",
+        "particles": 10**9,
+        "scaling": "strong",
         "n_points": 1000,
     },
     "poly": {
         "name": "C5: Fig.1 polynomial regression IS, 1.25e10 particles/GPU (1e11 on 8 GPUs), 20 points "
                 "(BASELINE configs[4])",
-        "particles_per_gpu": 12_500_000_000,
+        "particles": 12_500_000_000,
+        "scaling": "weak",
         "n_points": 20,
     },
     "smc": {
         "name": "C4: HMM S=50 bootstrap particle filter, 1e8 particles, T=1000, systematic resampling "
                 "every step (BASELINE configs[3], single GPU)",
-        "particles_per_gpu": 100_000_000,
+        "particles": 100_000_000,
+        "scaling": "strong",
         "n_points": 1000,
     },
     "dsl-linreg": {
         "name": "C2 written in CuPPL and compiled (frontend.py -> NVRTC sm_100a): Bayesian linear regression IS, "
-                "1e9 particles/GPU, 1k points",
-        "particles_per_gpu": 10**9,
+                "1e9 particles in total (strong scaling), 1k points",
+        "particles": 10**9,
+        "scaling": "strong",
         "n_points": 1000,
     },
     "mh": {
         "name": "C3: GMM K=5, 10k points, 4096 LMH chains x 10k steps (BASELINE configs[2])",
-        "particles_per_gpu": 4096,
+        "particles": 4096,
+        "scaling": "weak",
         "n_points": 10_000,
     },
 }
@@ -166,6 +179,66 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def shard(args, wl: dict, rank: int, world: int) -> tuple[int, int, int]:
+    """(lo, hi, total): this rank's global particle ids [lo, hi) and the whole job's count.
+
+    Strong-scaled workloads fix the total (C2: 1e9 over 1-8 GPUs, BASELINE configs[1]); weak-
+    scaled ones fix the per-GPU share (C5: 1.25e10 per GPU, 1e11 on 8). Ranks own
+    [floor(rN/R), floor((r+1)N/R)) like infer.shard_range."""
+    n = args.particles or wl["particles"]
+    total = n if wl["scaling"] == "strong" else n * world
+    return total * rank // world, total * (rank + 1) // world, total
+
+
+def relaunch(argv: list, gpus: int) -> int:
+    """`--gpus N` without a launcher: the same command under torch.distributed.run, one process
+    per GPU, rendezvous on 127.0.0.1; NCCL communicator init lines go to stderr."""
+    from paper_2010_08454_b200.cli import relaunch_command
+
+    cmd = relaunch_command(argv, gpus)
+    i = cmd.index("-m", cmd.index("torch.distributed.run") + 1)
+    cmd[i:i + 2] = [str(Path(__file__).resolve())]  # run bench.py, not the package CLI
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd + [f"--gpus={gpus}"], env=env)
+
+
+def run_dry(args) -> dict | None:
+    """Multi-rank orchestration without a GPU (gloo on CPU): the same sharding, the same 256-B
+    rank-record all-gather and max-over-ranks timing as run_ours, no kernel launched."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world, _ = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+    wl = WORKLOADS[args.workload]
+    lo, hi, total = shard(args, wl, rank, world)
+    rec = torch.zeros(256, dtype=torch.uint8)
+    rec[:8] = torch.tensor(list((hi - lo).to_bytes(8, "little")), dtype=torch.uint8)
+    gathered = torch.empty(world * 256, dtype=torch.uint8)
+    t0 = time.perf_counter()
+    if world > 1:
+        dist.all_gather_into_tensor(gathered, rec)
+    else:
+        gathered.copy_(rec)
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    counts = [int.from_bytes(bytes(gathered[r * 256:r * 256 + 8].tolist()), "little") for r in range(world)]
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return None
+    assert sum(counts) == total, (counts, total)
+    return {"metric": METRICS[args.workload][0], "value": None, "unit": METRICS[args.workload][1],
+            "n_gpus": world, "steps": 0, "warmup": 0, "dry_run": True, "scaling": wl["scaling"],
+            "config": {"workload": wl["name"], "particles": total, "rank_shares": counts,
+                       "parallelism": f"particle-sharded dp{world} (gloo dry run, no kernels)"},
+            "max_rank_s": dt.item()}
 
 
 def cpu_baseline(workload: str, model, target_s: float = 12.0, threads: int | None = None) -> dict:
@@ -259,7 +332,8 @@ def run_ours(args) -> dict | None:
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
     wl = WORKLOADS[args.workload]
-    per_gpu = args.particles or wl["particles_per_gpu"]
+    lo, hi, total = shard(args, wl, rank, world)
+    per_gpu = hi - lo
     model = make_model(args.workload)
     if args.workload == "dsl-linreg":  # the same model and data, from CuPPL source
         from paper_2010_08454_b200 import frontend
@@ -270,8 +344,6 @@ def run_ours(args) -> dict | None:
         src_model = model
         launcher = infer.IsLauncher(model, device)
     base = Rng(1)
-    lo = rank * per_gpu
-    hi = lo + per_gpu
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
     gathered = torch.empty(world * 256, dtype=torch.uint8, device=device)
 
@@ -304,12 +376,12 @@ def run_ours(args) -> dict | None:
     if world > 1:
         dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
     t_ms = total_ms.item()
-    value = world * per_gpu * args.steps / (t_ms / 1e3)
+    value = total * args.steps / (t_ms / 1e3)
 
     # e2e: the public API from host data (model arrays in host memory -> kernel parameter
     # block; record + mode trace back to the host), same particle count and GPUs.
     e2e_steps = max(1, min(args.steps, 3))
-    infer.run_importance(model, world * per_gpu, Rng(777))  # warm
+    infer.run_importance(model, total, Rng(777))  # warm
     torch.cuda.synchronize()
     e2e_t = []
     for k in range(e2e_steps):
@@ -317,14 +389,14 @@ def run_ours(args) -> dict | None:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        post = infer.run_importance(model, world * per_gpu, base.split(500 + k))
+        post = infer.run_importance(model, total, base.split(500 + k))
         e1.record()
         torch.cuda.synchronize()
         e2e_t.append(e0.elapsed_time(e1))
     e2e_ms = torch.tensor([sum(e2e_t)], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = world * per_gpu * e2e_steps / (e2e_ms.item() / 1e3)
+    e2e_value = total * e2e_steps / (e2e_ms.item() / 1e3)
     h2d = src_model.xs.nbytes + src_model.ys.nbytes
     d2h = 256 * world + (16 if args.workload == "poly" else 8) + (4 if args.workload == "poly" else 0)
 
@@ -377,13 +449,14 @@ def run_ours(args) -> dict | None:
             "warmup": args.warmup,
             "ms_per_step": t_ms / args.steps,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": wl["scaling"],
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic (numpy seed 0, fp64 -> fp32; SURVEY.md §8(d)); Philox draws keyed by Rng(1).split(step)",
             "config": {
                 "workload": wl["name"],
-                "particles_per_gpu": per_gpu,
+                "particles": total,
+                "particles_rank0": per_gpu,
                 "n_points": wl["n_points"],
                 "parallelism": f"particle-sharded dp{world} (NCCL all-gather of 256 B rank records)",
                 "l2": "flushed between timed steps (256 MiB write, excluded by per-step CUDA events)",
@@ -437,7 +510,7 @@ def run_ours_engine(args) -> dict | None:
     metric, unit = METRICS[args.workload]
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
     if args.workload == "smc":
-        n = args.particles or wl["particles_per_gpu"]
+        n = args.particles or wl["particles"]
         T = model.T
         # buffers built once; one process per GPU: the whole T-step run is one captured CUDA graph
         # (device-resident key), replayed per step; N > 1 launches step by step around NCCL
@@ -452,7 +525,7 @@ def run_ours_engine(args) -> dict | None:
             return runner
         units_per_step = T  # time steps of the whole (strong-scaled) population
     else:
-        chains = args.particles or wl["particles_per_gpu"]
+        chains = args.particles or wl["particles"]
         n_steps = args.mh_steps
 
         def step(k):  # weak scaling: `chains` chains per GPU, sharded by rank inside run_lmh
@@ -575,7 +648,7 @@ def cpu_baseline_engine(args, model) -> dict:
     core.build()
     threads = os.cpu_count() or 1
     if args.workload == "smc":
-        n_full = args.particles or WORKLOADS["smc"]["particles_per_gpu"]
+        n_full = args.particles or WORKLOADS["smc"]["particles"]
         n, T = 1_000_000, 50
         t0 = time.perf_counter()
         core.smc_run(model, n, 0x9E0160293A33AAF7, steps=T)
@@ -606,7 +679,7 @@ def run_reference(args) -> dict | None:
     key = 0x9E0160293A33AAF7
     if args.workload == "smc":
         per_step, cores = 1_000_000, threads
-        n_full = args.particles or wl["particles_per_gpu"]
+        n_full = args.particles or wl["particles"]
         sample = (f"{per_step} particles x 20 time steps per step (or_smc_step, OpenMP {threads}), rate quoted "
                   f"per time step of the {n_full}-particle filter (linear in particles)")
 
@@ -639,9 +712,9 @@ def run_reference(args) -> dict | None:
     dt = time.perf_counter() - t0
     value = units * args.steps / dt
     return {
-        "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+        "metric": metric, "value": value, "unit": unit, "n_gpus": max(world, args.gpus), "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
-        "scaling": "strong" if args.workload == "smc" else "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "impl": "reference",
         "config": {"workload": wl["name"], "units_per_step": units, "n_points": wl["n_points"]},
@@ -660,10 +733,15 @@ def main():
     ap.add_argument("--particles", type=int, default=0, help="override particles per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mh-steps", type=int, default=10_000, help="MH steps per chain (workload mh)")
+    ap.add_argument("--dry-run", action="store_true", help="gloo on CPU, no kernels (orchestration only)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return relaunch(sys.argv[1:], args.gpus)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
-    if args.impl == "reference":
+    if args.dry_run:
+        res = run_dry(args)
+    elif args.impl == "reference":
         res = run_reference(args)
     elif args.workload in ("smc", "mh"):
         res = run_ours_engine(args)
@@ -671,7 +749,8 @@ def main():
         res = run_ours(args)
     if res is not None:
         print(json.dumps(res), flush=True)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())
