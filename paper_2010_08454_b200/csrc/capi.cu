@@ -95,8 +95,9 @@ int check_dist(const cuppl_dist* d, DistArgs* a) {
         return set_error(CUPPL_E_INVALID_PARAM, "bernoulli(%g): p must be in [0, 1]", d->p0);
       break;
     case CUPPL_DIST_POISSON:
-      if (!(d->p0 >= 0.0) || !std::isfinite(d->p0))
-        return set_error(CUPPL_E_INVALID_PARAM, "poisson(%g): rate must be >= 0", d->p0);
+      // rate < 2^31: the count is an int32 (and the halving tree stays <= 27 levels deep)
+      if (!(d->p0 >= 0.0 && d->p0 < 2147483648.0))
+        return set_error(CUPPL_E_INVALID_PARAM, "poisson(%g): rate must be >= 0 and < 2^31", d->p0);
       break;
     case CUPPL_DIST_UNIFORM_DISCRETE: {
       const double lo = d->p0, hi = d->p1;

@@ -136,7 +136,9 @@ int cuppl_smc_resample(const cuppl_smc_model* m, uint64_t n_local, uint64_t n_to
   if (int s = check_ws(n_local, workspace, workspace_bytes, &w)) return s;
   if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
     return set_error(CUPPL_E_ARGUMENT, "rank %d / world %d", rank, world);
-  if (n_total < n_local || n_total >= (1ull << 32)) return set_error(CUPPL_E_CAPACITY, "n_total");
+  // the comb arithmetic needs N < 2^31 (j*R0 + Ra ~ N^2 in signed 64 bits, T <= N*2^31 in the
+  // 62-bit look-back flag words), as SmcRunner and check_ws already enforce
+  if (n_total < n_local || n_total >= (1ull << 31)) return set_error(CUPPL_E_CAPACITY, "n_total >= 2^31");
   if (!x || !m_key || !rank_recs || !rank_begin || !x_out || !m_key_next || !stats_out)
     return set_error(CUPPL_E_ARGUMENT, "NULL buffer");
   int sms = 0;

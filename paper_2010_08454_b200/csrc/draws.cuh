@@ -97,7 +97,7 @@ struct WordStream {
           p *= uniform();
         }
         total += k;
-      } else {
+      } else if (sp < 62) {  // rates are checked < 2^31 (<= 27 levels); never overflow the stack
         const float half = floorf(l / 2.0f);
         stack[sp++] = l - half;  // processed second
         stack[sp++] = half;      // processed first

@@ -257,8 +257,16 @@ template <class M>
 __device__ __forceinline__ float draw_uniform_pos(WordStream& ws, const M&) { return ws.uniform_pos(); }
 template <class M>
 __device__ __forceinline__ float draw_gamma(WordStream& ws, float a, const M&) { return ws.gamma(a); }
+// poisson(rate): rate must be finite, >= 0 and < 2^31 (int count); a bad lane draws with rate 0
+__device__ __forceinline__ float pois_rate(float lam) { return (lam >= 0.f && lam < 2147483648.f) ? lam : 0.f; }
+__device__ __forceinline__ unsigned pois_check(bool valid, float lam, unsigned long long pid,
+                                               unsigned long long& first_bad) {
+  const bool bad = valid && !(lam >= 0.f && lam < 2147483648.f);
+  if (bad && pid < first_bad) first_bad = pid;
+  return bad ? 4u : 0u;
+}
 template <class M>
-__device__ __forceinline__ int draw_poisson(WordStream& ws, float lam, const M&) { return ws.poisson(lam); }
+__device__ __forceinline__ int draw_poisson(WordStream& ws, float lam, const M&) { return ws.poisson(pois_rate(lam)); }
 // categorical(w): P(k) = w_k / sum w; weights must be >= 0 and not all 0
 __device__ __forceinline__ unsigned cat_check(bool valid, float tot, float wmin, unsigned long long pid,
                                               unsigned long long& first_bad) {
@@ -309,7 +317,9 @@ CUPPL_LANE_DRAW0(float, draw_normal, normal)
 CUPPL_LANE_DRAW0(float, draw_uniform, uniform)
 CUPPL_LANE_DRAW0(float, draw_uniform_pos, uniform_pos)
 CUPPL_LANE_DRAW1(float, draw_gamma, gamma)
-CUPPL_LANE_DRAW1(int, draw_poisson, poisson)
+#define poisson_checked(lam) poisson(pois_rate(lam))
+CUPPL_LANE_DRAW1(int, draw_poisson, poisson_checked)
+#undef poisson_checked
 #undef CUPPL_LANE_DRAW0
 #undef CUPPL_LANE_DRAW1
 template <class A, class B>
@@ -320,6 +330,15 @@ __device__ __forceinline__ unsigned ud_check(const Lane<bool>& valid, const A& l
 #pragma unroll
   for (int p = 0; p < LANES; ++p)
     e |= ud_check(valid.v[p], lane_at(lo, p), lane_at(hi, p), pid.v[p], first_bad);
+  return e;
+}
+template <class T>
+__device__ __forceinline__ unsigned pois_check(const Lane<bool>& valid, const T& lam,
+                                               const Lane<unsigned long long>& pid,
+                                               unsigned long long& first_bad) {
+  unsigned e = 0u;
+#pragma unroll
+  for (int p = 0; p < LANES; ++p) e |= pois_check(valid.v[p], lane_at(lam, p), pid.v[p], first_bad);
   return e;
 }
 template <class T, class W>

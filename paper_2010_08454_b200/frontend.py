@@ -627,6 +627,7 @@ class _Compiler:
         elif k == "exponential":
             g.emit(f"{lhs} = -logf(draw_uniform_pos(ws, {m})) / {_real(a[0])};")
         elif k == "poisson":
+            g.emit(f"err |= pois_check({g.valid_m()}, {_real(a[0])}, pid, first_bad);")
             g.emit(f"{lhs} = draw_poisson(ws, {_real(a[0])}, {m});")
         elif k == "categorical":  # k = #{j < n-1 : w_0 + .. + w_j <= u * sum w}
             w = a[0]
@@ -1431,8 +1432,10 @@ def _raise_param_error(err, what: str):
     err.copy_(err.new_tensor([0, 0, -1, -1]))
     if w[0] & 1:
         msg = "uniform-discrete(a, b) needs b > a (SPEC.md:347)"
-    else:
+    elif w[0] & 2:
         msg = "categorical(w): weights must be >= 0 and not all 0 (SURVEY.md D5)"
+    else:
+        msg = "poisson(rate): rate must be finite, >= 0 and < 2^31"
     raise InvalidDistParamError(f"{msg}; first failing {what}: {first}")
 
 

@@ -50,8 +50,16 @@ def test_record_layout_matches_header():
     assert fields == [f for f, _ in _native.IsRecord._fields_]
     assert C.sizeof(_native.IsRecord) == 256
     body = re.search(r"typedef struct cuppl_dist \{(.*?)\} cuppl_dist;", text, re.S).group(1)
-    fields = re.findall(r"(\w+);", body)
-    assert fields == [f for f, _ in _native.Dist._fields_][:2] + ["p2"] + ["table"] or True
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = []
+    for decl in body.split(";"):  # every declarator: "double p0, p1, p2" -> p0, p1, p2
+        decl = decl.strip()
+        if not decl:
+            continue
+        head, *rest = decl.split(",")
+        fields.append(re.search(r"(\w+)\s*$", head).group(1))
+        fields += [r.strip().lstrip("*").strip() for r in rest]
+    assert fields == [f for f, _ in _native.Dist._fields_]
     assert C.sizeof(_native.Dist) == 40
 
 
@@ -96,6 +104,11 @@ def test_smc_arguments_rejected_before_cuda(native_lib):
                               ws.ctypes.data, ws.ctypes.data, ws.ctypes.data, None, mk.ctypes.data,
                               ws.ctypes.data, ws.ctypes.data, wsb, None)
     assert rc == _native.E_ARGUMENT and b"world" in L.cuppl_last_error()
+    # populations of 2^31 or more: the comb's 64-bit arithmetic would overflow
+    rc = L.cuppl_smc_resample(C.byref(m), n, 1 << 31, 1, 0, 0, 1, 0.0, 0.0, x.ctypes.data, mk.ctypes.data,
+                              ws.ctypes.data, ws.ctypes.data, ws.ctypes.data, None, mk.ctypes.data,
+                              ws.ctypes.data, ws.ctypes.data, wsb, None)
+    assert rc == _native.E_CAPACITY and b"2^31" in L.cuppl_last_error()
     # too many states for the one-byte population
     m.n_states = 300
     rc = L.cuppl_smc_init(C.byref(m), n, 0, 1, 0.0, x.ctypes.data, mk.ctypes.data, ws.ctypes.data, wsb, None)

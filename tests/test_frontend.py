@@ -495,6 +495,26 @@ def test_gpu_error_word_names_the_first_failing_particle(cuda):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("lanes", ["1", "8"])
+def test_gpu_poisson_bad_rate_raises(cuda, monkeypatch, lanes):
+    """poisson with a data-dependent rate that is inf (r > 1.22) or beyond an int count raises
+    InvalidDistParamError (the reference fails on floor(inf)) instead of looping forever or
+    overflowing the halving stack; also through the masked lane form."""
+    from paper_2010_08454_b200 import Rng, infer
+    from paper_2010_08454_b200.errors import InvalidDistParamError
+
+    monkeypatch.setenv("CUPPL_DSL_LANES", lanes)
+    src = ("model <- function() { r <- sample(normal(0, 1)); k <- sample(poisson(exp(r) * 1e38)); k }; "
+           "importance(model, 10)")
+    m = frontend.compile_program(src)
+    with pytest.raises(InvalidDistParamError, match="poisson"):
+        infer.run_importance(m, 20_000, Rng(3))
+    ok = frontend.compile_program(src.replace("1e38", "3.0"))
+    post = infer.run_importance(ok, 20_000, Rng(3))
+    assert np.isfinite(post.log_z)
+
+
+@pytest.mark.gpu
 def test_gpu_enumeration_spec_example(cuda):
     from paper_2010_08454_b200 import infer
 
