@@ -297,3 +297,23 @@ def mh_gmm_init(ys, K, prior_sd, sigma, chain, key):
     L.or_mh_gmm_chain(_ptr(y, C.c_float), len(y), K, prior_sd, sigma, chain, 0, 0, 1, key, _ptr(mu, C.c_double),
                       _ptr(st, C.c_double), None, 0, _ptr(z, C.c_int32), C.byref(ll0))
     return z, mu, ll0.value
+
+
+def rec_from_dict(d: dict) -> OrRecord:
+    r = OrRecord()
+    for k, v in d.items():
+        if k in ("stat_w", "bin_w"):
+            getattr(r, k)[:] = [float(x) for x in v]
+        else:
+            setattr(r, k, v)
+    return r
+
+
+def merge_records(recs: list) -> dict:
+    """or_rec_merge over window records (dicts) in window order: the record of their union."""
+    L = lib()
+    out = rec_from_dict(recs[0])
+    for d in recs[1:]:
+        b = rec_from_dict(d)
+        L.or_rec_merge(C.byref(out), C.byref(b))
+    return out.as_dict()
