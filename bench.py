@@ -422,24 +422,27 @@ def run_ours(args) -> dict | None:
             "flops_per_particle": fpp,
         }
         if args.workload == "poly":
-            # issue-bound: one Philox block (IMAD.WIDE on the fma pipe) + the fp32 Horner work
-            # share the fma pipe; roof = 1 / (t_philox + t_fp32) with both rates measured here
+            # SURVEY.md §8(d) C1/C5 roofline (fixed definition): issue-bound on the FMA pipe,
+            # Philox at its MEASURED rate on this GPU (calib kind 2; the survey's 40-instruction
+            # count is faster than the hardware's quarter-rate IMAD.WIDE) plus the algorithmic
+            # I_fp32 = 86 FP32 instructions per particle (E[n] = 3: Horner 40 FFMA + 20 FADD +
+            # 20 FFMA + 6) at 128 lanes/clk/SM, serialised (no credit for overlapping the two)
             ph = calibrate_philox(device)
-            t_part = 1.0 / ph + fpp / peak
-            roof_rate = 1.0 / t_part
+            n_sm = torch.cuda.get_device_properties(device).multi_processor_count
+            f_sm = (clk.get("sm_mhz") or sm_max) * 1e6
+            i_fp32 = 86.0
+            roof_rate = 1.0 / (1.0 / ph + i_fp32 / (128.0 * n_sm * f_sm))
             rate = per_gpu / kernel_s
-            roof = {"bound": "issue (fma pipe: Philox IMAD.WIDE + fp32 FFMA2)", "achieved": rate,
+            flop_roof = 1.0 / (1.0 / ph + fpp / peak)
+            roof = {"bound": "issue (fma pipe: Philox IMAD.WIDE + fp32)", "achieved": rate,
                     "peak": roof_rate, "unit": "particles/s", "frac": rate / roof_rate,
                     "traffic": (load_traffic(args.workload) or {}).get("bytes_per_launch"),
-                    "peak_source": f"measured: Philox {ph:.3g} blocks/s (calib kind 2) + FFMA2 {peak / 1e12:.1f} "
-                                   "TFLOP/s (kind 0), 1 block + {fpp:.0f} flops per particle".replace("{fpp:.0f}", f"{fpp:.0f}"),
-                    "flops_per_particle": fpp}
-            # the same serialisation over the EXECUTED fma-pipe mix per particle (ncu SASS of this
-            # kernel, profiles/r1_final_ncu_summary.json: 61 FFMA2/FADD2 + 22 scalar FP; padded
-            # Horner, FADD as a full slot, Box-Muller, epilogue) — DESIGN.md §4 "Why C5 ..."
-            exec_roof = 1.0 / (1.0 / ph + 61.0 / (peak / 4.0) + 22.0 / (peak / 2.0))
-            roof["executed_mix_bound"] = exec_roof
-            roof["frac_of_executed_mix_bound"] = rate / exec_roof
+                    "peak_source": f"SURVEY.md §8(d) C5: measured Philox {ph:.3g} blocks/s (calib kind 2) + "
+                                   f"I_fp32 = 86 instr/particle at 128 lanes/clk x {n_sm} SMs x {f_sm / 1e6:.0f} MHz",
+                    "flops_per_particle": fpp,
+                    "flop_roof": flop_roof, "frac_of_flop_roof": rate / flop_roof,
+                    "flop_roof_source": f"Philox + {fpp:.0f} flops/particle at the measured FFMA2 peak "
+                                        f"{peak / 1e12:.1f} TFLOP/s (counts an FADD at half an FFMA's cost)"}
         result = {
             "metric": METRIC,
             "value": value,

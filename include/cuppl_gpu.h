@@ -277,6 +277,37 @@ CUPPL_API int cuppl_calibrate(int kind, int blocks, int iters, float* sink, void
 /* Host-side ordered merge of n records (rank order). Pure host function. */
 CUPPL_API int cuppl_is_record_merge(const cuppl_is_record* recs, int n, cuppl_is_record* out);
 
+/* ---------------------------------------------------------------- generic resampling --------
+ * Systematic resampling of ANY population (BASELINE north_star "resampling
+ * and ancestor gather"): N particles with fp32 log-weights lw[N] and a fixed-size payload of
+ * payload_bytes per particle (the particle state, opaque to the library). The reference has no
+ * SMC (a non-goal), so oracle/resample_oracle.c or_resample DEFINES the result,
+ * with the exact integer rule of SURVEY.md Appendix A D6 that cuppl_smc_resample applies to
+ * HMM populations:
+ *   M = max lw (NaN ignored), w_i = min(floor(exp(lw_i - M) 2^31), 2^31) (reproducible fp32 exp),
+ *   C = inclusive u64 prefix of w, T = C[N-1], u = word 0 of Philox(key; t, 0, 0, CUPPL_TAG_SMC_COMB),
+ *   target_j = floor((j 2^32 + u) T / (N 2^32)), a_j = min{i : C_i > target_j},
+ *   payload_out[j] = payload[a_j], ancestors_out[j] = a_j.
+ * Ancestors are bit-exact for any weights; stats are written to device memory: max_lw = M,
+ * total = T (0 means every weight quantised to 0 and nothing else was written: the caller
+ * raises AllZeroWeightError), sum_e / sum_e2 = sum and sum of squares of exp(lw - M) (fp64;
+ * ESS = sum_e^2 / sum_e2, log-evidence increment = M + ln(sum_e / N)).
+ * Requirements: 1 <= n < 2^31; lw, payload and payload_out 16-byte aligned (PyTorch allocations
+ * are); payload may be NULL with payload_bytes == 0 (ancestors only); ancestors_out may be NULL.
+ * The workspace (cuppl_resample_workspace_bytes) needs no initialisation. */
+typedef struct cuppl_resample_stats {
+  double max_lw;
+  uint64_t total;
+  double sum_e;
+  double sum_e2;
+} cuppl_resample_stats;
+
+CUPPL_API size_t cuppl_resample_workspace_bytes(uint64_t n);
+CUPPL_API int cuppl_resample(const float* lw, uint64_t n, const void* payload, uint64_t payload_bytes,
+                             uint64_t key, uint32_t t, void* payload_out, uint64_t* ancestors_out,
+                             cuppl_resample_stats* stats_out, void* workspace, size_t workspace_bytes,
+                             void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -317,3 +317,33 @@ def merge_records(recs: list) -> dict:
         b = rec_from_dict(d)
         L.or_rec_merge(C.byref(out), C.byref(b))
     return out.as_dict()
+
+
+# ---------------------------------------------------------------- generic resampling --------
+class OrResampleStats(C.Structure):
+    _fields_ = [("M", C.c_float), ("status", C.c_uint32), ("T", C.c_uint64), ("s1", C.c_double),
+                ("s2", C.c_double)]
+
+
+def resample(lw, payload, key: int, t: int):
+    """or_resample: systematic resampling of fp32 log-weights with a payload
+    array whose first axis is the particle; returns (payload_out, ancestors, stats dict)."""
+    L = lib()
+    if not getattr(L, "_rs_sig", False):
+        P = C.POINTER
+        L.or_resample.argtypes = [C.c_uint64, P(C.c_float), C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint32,
+                                  C.c_void_p, P(C.c_uint64), P(OrResampleStats)]
+        L.or_resample.restype = C.c_int
+        L._rs_sig = True
+    w = np.ascontiguousarray(lw, dtype=np.float32)
+    n = len(w)
+    pay = np.ascontiguousarray(payload)
+    assert pay.shape[0] == n
+    nbytes = pay.nbytes // n if n else 0
+    out = np.empty_like(pay)
+    anc = np.zeros(n, dtype=np.uint64)
+    st = OrResampleStats()
+    rc = L.or_resample(n, _ptr(w, C.c_float), pay.ctypes.data, nbytes, key, t, out.ctypes.data,
+                       anc.ctypes.data_as(C.POINTER(C.c_uint64)), C.byref(st))
+    stats = {"M": st.M, "T": st.T, "s1": st.s1, "s2": st.s2, "status": rc}
+    return out, anc, stats

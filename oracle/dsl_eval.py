@@ -217,3 +217,37 @@ class Enumerator(Interpreter):
             mass[key] = mass.get(key, 0.0) + math.exp(lw)
         z = sum(mass.values())
         return {k: v / z for k, v in mass.items()}, math.log(z)
+
+
+def _f32(x):
+    return float(np.float32(x)) if isinstance(x, float) else x
+
+
+class Fp32Interpreter(Interpreter):
+    """The same interpreter rounding every real-valued operation to fp32 (round to nearest per
+    operation; no FMA contraction, correctly rounded functions). Its distance from the fp64
+    result measures how much fp32 arithmetic itself moves a given program's log-weight — the
+    conditioning term of the compiler's parity tolerance (tests/test_frontend_fuzz.py): random
+    expression trees can cancel, where no fixed relative tolerance holds for any fp32 code."""
+
+    def run(self, draws):
+        self._draws = [_f32(float(d)) for d in draws]
+        self._k = 0
+        self._lw = 0.0
+        ret = self.apply(self.model, [])
+        return self._lw, ret
+
+    def ev(self, e, env):
+        v = super().ev(e, env)
+        if isinstance(e, (lang.BinOp, lang.Unary)):
+            return _f32(v)
+        return v
+
+    def call(self, e, env):
+        if isinstance(e.fn, lang.Var) and e.fn.name in ("factor", "observe") and e.fn.name not in env \
+                and e.fn.name not in self.globals:
+            before = self._lw
+            out = super().call(e, env)
+            self._lw = _f32(self._lw) if self._lw != before else self._lw
+            return out
+        return _f32(super().call(e, env))

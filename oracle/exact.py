@@ -7,6 +7,8 @@
                     per-degree evidence and the coefficient posterior are closed form
   hmm_forward       forward algorithm for the SMC HMM: log p(y_{0:T})
                     and the filtering marginals p(x_t | y_{0:t})
+  kalman_loglik     Kalman filter of a 1-D linear-Gaussian state-space model: the exact log
+                    p(y_{0:T}) a particle filter on a continuous state estimates
 """
 
 from __future__ import annotations
@@ -84,3 +86,20 @@ def hmm_forward(A, pi0, mu, sd, y):
         filt[t] = a / s
         pred = filt[t] @ A
     return logp, filt
+
+
+def kalman_loglik(y, a: float, q: float, r: float, s0: float):
+    """x_0 ~ N(0, s0^2), x_{t+1} = a x_t + N(0, q^2), y_t = x_t + N(0, r^2): log p(y_{0:T-1}) and
+    the filtering means E[x_t | y_{0:t}]."""
+    m, P = 0.0, s0 * s0
+    ll = 0.0
+    means = []
+    for t, yt in enumerate(np.asarray(y, dtype=np.float64)):
+        if t > 0:
+            m, P = a * m, a * a * P + q * q
+        S = P + r * r
+        ll += -0.5 * (math.log(2 * math.pi * S) + (yt - m) ** 2 / S)
+        K = P / S
+        m, P = m + K * (yt - m), (1 - K) * P
+        means.append(m)
+    return ll, np.array(means)

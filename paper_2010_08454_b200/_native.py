@@ -73,6 +73,12 @@ class SmcModel(C.Structure):
     ]
 
 
+class ResampleStats(C.Structure):
+    """cuppl_resample_stats (include/cuppl_gpu.h)."""
+
+    _fields_ = [("max_lw", C.c_double), ("total", C.c_uint64), ("sum_e", C.c_double), ("sum_e2", C.c_double)]
+
+
 _lock = threading.Lock()
 _lib: C.CDLL | None = None
 
@@ -111,6 +117,8 @@ _SIG = {
     "cuppl_smc_fold": ([_U64, _P, _P, C.c_size_t, _P], C.c_int),
     "cuppl_smc_resample": ([_P, _U64, _U64, _U64, _U32, C.c_int, C.c_int, _F32, _F32, _P, _P, _P, _P,
                             _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
+    "cuppl_resample_workspace_bytes": ([_U64], C.c_size_t),
+    "cuppl_resample": ([_P, _U64, _P, _U64, _U64, _U32, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
 }
 
 

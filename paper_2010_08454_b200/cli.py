@@ -68,8 +68,8 @@ def infer_once(model_name: str, inference: str, samples: int, seed: int, *, burn
         return infer.run_importance(model, samples, rng)
     if inference == "mcmc":
         r = infer.run_lmh(model, samples, rng, chains=chains, burn_in=burn_in, thin=thin)
-        return _Summary([], None, n=r.n_chains * r.n_steps, mean={"sorted_mu": r.mean.tolist()},
-                        var=r.var.tolist(), acceptance=r.acceptance)
+        return _Summary([], None, n=r.n, mean={"sorted_mu": r.mean_vec.tolist()},
+                        var=r.var_vec.tolist(), acceptance=r.acceptance)
     if inference == "smc":
         r = infer.run_smc(model, samples, rng, steps=smc_steps)
         t = max(r.filtering)

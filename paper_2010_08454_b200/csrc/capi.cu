@@ -149,6 +149,7 @@ int fill_common(P& prm, const float* xs, const float* ys, int n_points, int cap,
   prm.pid_end = pid_end;
   prm.k0 = static_cast<uint32_t>(key);
   prm.k1 = static_cast<uint32_t>(key >> 32);
+  philox_key_schedule(key, prm.ks);
   prm.n_points = n_points;
   prm.pad_ = 0;
   prm.injected = injected;

@@ -67,6 +67,8 @@ int cuppl_mh_gmm(const float* y, int D, int K, float prior_sd, float sigma, uint
   a.prior_sd = prior_sd;
   a.neg_half_inv_var = static_cast<float>(-0.5 / (static_cast<double>(sigma) * sigma));
   a.ll_const = static_cast<float>(-D * (std::log(static_cast<double>(sigma)) + 0.91893853320467274178));
+  a.neg_half_inv_var64 = -0.5 / (static_cast<double>(sigma) * sigma);
+  a.ll_const64 = -D * (std::log(static_cast<double>(sigma)) + 0.91893853320467274178);
   a.chains_per_cta = cpc;
   a.y = y;
   a.mu_out = mu_out;

@@ -37,6 +37,36 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
   return c;
 }
 
+// The same block with the key schedule precomputed (ks[2r], ks[2r + 1] = key words of round r):
+// a launch-uniform schedule in the kernel-parameter block feeds the LOP3s as constant-bank
+// operands, so it costs neither registers nor key-schedule adds.
+__device__ __forceinline__ uint4 philox4x32_10_ks(uint4 c, const uint32_t (&ks)[20]) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint32_t lo0, hi0, lo1, hi1;
+    asm("{\n\t.reg .b64 p;\n\tmul.wide.u32 p, %2, %3;\n\tmov.b64 {%0, %1}, p;\n\t}"
+        : "=r"(lo0), "=r"(hi0) : "r"(c.x), "n"(kPhiloxM0));
+    asm("{\n\t.reg .b64 p;\n\tmul.wide.u32 p, %2, %3;\n\tmov.b64 {%0, %1}, p;\n\t}"
+        : "=r"(lo1), "=r"(hi1) : "r"(c.z), "n"(kPhiloxM1));
+    c = make_uint4(hi1 ^ c.y ^ ks[2 * r], lo1, hi0 ^ c.w ^ ks[2 * r + 1], lo0);
+  }
+  return c;
+}
+__host__ __device__ inline void philox_key_schedule(uint64_t key, uint32_t (&ks)[20]) {
+  uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
+  for (int r = 0; r < 10; ++r) {
+    ks[2 * r] = k0;
+    ks[2 * r + 1] = k1;
+    k0 += kPhiloxW0;
+    k1 += kPhiloxW1;
+  }
+}
+__device__ __forceinline__ uint4 draw_block_ks(const uint32_t (&ks)[20], uint64_t id, uint32_t blk,
+                                               uint32_t tag) {
+  return philox4x32_10_ks(
+      make_uint4(static_cast<uint32_t>(id), static_cast<uint32_t>(id >> 32), blk, tag), ks);
+}
+
 struct PhiloxKey {
   uint32_t k0, k1;
 };
@@ -119,6 +149,20 @@ __device__ __forceinline__ float2 box_muller(uint32_t wa, uint32_t wb) {
   const float th = fmaf(kTwoPi, u2, -kPi);
   return make_float2(-r * fast_cos(th), -r * fast_sin(th));
 }
+
+// sd * (Box-Muller pair) with the constants folded (the prior-draw form of the IS kernels):
+// r_sd = sqrt(-2 sd^2 ln2 lg2 u1) carries the scale, and the angle 2 pi u2 - pi is formed from
+// the mantissa-trick float f = 1 + u2 in [1, 2) as fma(2 pi, f, -3 pi) (the same [-pi, pi)
+// range; no u2 = f - 1 subtraction). Two FMA-pipe instructions fewer per normal than
+// sd * box_muller(); the values agree to fp32 rounding (~1e-6 relative).
+__device__ __forceinline__ float2 box_muller_sd(uint32_t wa, uint32_t wb, float neg2_sd2_ln2) {
+  const float u1 = u01_open0(wa);
+  const float f = __uint_as_float(0x3F800000u | (wb >> 9));
+  const float r = fast_sqrt(neg2_sd2_ln2 * fast_lg2(u1));
+  const float th = fmaf(kTwoPi, f, -3.0f * kPi);
+  return make_float2(-r * fast_cos(th), -r * fast_sin(th));
+}
+constexpr float kNeg2Sd2Ln2Prior = -2.0f * 100.0f * kLn2;  // normal(0, 10) priors (D2)
 
 // ---------------------------------------------------------------- packed fp32 ----------
 // sm_100 executes fma.rn.f32x2 / add.rn.f32x2 as one FFMA2 / FADD2 on a register pair.

@@ -25,7 +25,6 @@ is_linreg_kernel(const __grid_constant__ LinregParams<CAP> prm) {
   static_assert(P % 2 == 0, "particles are processed in FFMA2 pairs");
   ThreadAcc<5, 0> acc;
   acc.init();
-  const PhiloxKey key{prm.k0, prm.k1};
   const uint64_t n = prm.pid_end - prm.pid_begin;
   const uint64_t chunk = static_cast<uint64_t>(blockDim.x) * P;
   const uint64_t nchunks = (n + chunk - 1) / chunk;
@@ -42,10 +41,10 @@ is_linreg_kernel(const __grid_constant__ LinregParams<CAP> prm) {
         a[p] = ok ? prm.injected[2 * idx] : 0.f;
         b[p] = ok ? prm.injected[2 * idx + 1] : 0.f;
       } else {
-        const uint4 w = draw_block(key, prm.pid_begin + idx, 0u, CUPPL_TAG_IS);
-        const float2 z = box_muller(w.x, w.y);
-        a[p] = 10.0f * z.x;  // normal(0, 10): mean + sd * z (D2)
-        b[p] = 10.0f * z.y;
+        const uint4 w = draw_block_ks(prm.ks, prm.pid_begin + idx, 0u, CUPPL_TAG_IS);
+        const float2 z = box_muller_sd(w.x, w.y, kNeg2Sd2Ln2Prior);  // normal(0, 10) (D2)
+        a[p] = z.x;
+        b[p] = z.y;
       }
     }
     // sum_i r_i^2 per particle, two accumulators per particle (even / odd points)
@@ -148,21 +147,21 @@ __device__ __forceinline__ uint32_t poly_degree_word(uint4 w) {
   return (w.x & 0x1FFu) | ((w.y & 0x1FFu) << 9) | ((w.z & 0x1FFu) << 18) | ((w.w & 0x1Fu) << 27);
 }
 
-__device__ __forceinline__ void poly_draw(PhiloxKey key, uint64_t pid, int& n, float c[4]) {
-  const uint4 w = draw_block(key, pid, 0u, CUPPL_TAG_IS);
+__device__ __forceinline__ void poly_draw(const uint32_t (&ks)[20], uint64_t pid, int& n, float c[4]) {
+  const uint4 w = draw_block_ks(ks, pid, 0u, CUPPL_TAG_IS);
   uint32_t k;
   if (!lemire(poly_degree_word(w), 3u, &k)) {
     for (uint32_t blk = 1;; ++blk) {
-      if (lemire(draw_block(key, pid, blk, CUPPL_TAG_IS).x, 3u, &k)) break;
+      if (lemire(draw_block_ks(ks, pid, blk, CUPPL_TAG_IS).x, 3u, &k)) break;
     }
   }
   n = 2 + static_cast<int>(k);
-  const float2 z01 = box_muller(w.x, w.y);
-  const float2 z23 = box_muller(w.z, w.w);
-  c[0] = 10.0f * z01.x;
-  c[1] = 10.0f * z01.y;
-  c[2] = n > 2 ? 10.0f * z23.x : 0.0f;
-  c[3] = n > 3 ? 10.0f * z23.y : 0.0f;
+  const float2 z01 = box_muller_sd(w.x, w.y, kNeg2Sd2Ln2Prior);  // normal(0, 10) (D2)
+  const float2 z23 = box_muller_sd(w.z, w.w, kNeg2Sd2Ln2Prior);
+  c[0] = z01.x;
+  c[1] = z01.y;
+  c[2] = n > 2 ? z23.x : 0.0f;
+  c[3] = n > 3 ? z23.y : 0.0f;
 }
 
 // Pair-packed online accumulator of the Fig.1 record: the two halves of every f32x2 belong to
@@ -271,7 +270,7 @@ __device__ __forceinline__ void poly_chunk(const PolyParams<CAP>& prm, PolyAcc& 
 #pragma unroll
       for (int j = 0; j < 4; ++j) c[p][j] = (ok && j < deg[p]) ? src[1 + j] : 0.f;
     } else {
-      poly_draw(key, prm.pid_begin + idx, deg[p], c[p]);
+      poly_draw(prm.ks, prm.pid_begin + idx, deg[p], c[p]);
     }
   }
   f32x2 C0[P / 2], C1[P / 2], C2[P / 2], C3[P / 2], S[P / 2];

@@ -20,6 +20,7 @@ constexpr int kPolyCap = 64;
 struct IsCommon {
   uint64_t pid_begin, pid_end;
   uint32_t k0, k1;
+  uint32_t ks[20];  // Philox key schedule of (k0, k1) (philox_key_schedule)
   int n_points;
   int pad_;
   const float* injected;

@@ -10,7 +10,7 @@ constexpr int kMhMaxK = 7;            // mixture components (label K is padding)
 constexpr int kMhMaxThreads = 640;    // threads per CTA (each holds 8-point groups of y)
 constexpr int kMhMaxGroupsPerThread = 8;  // D <= 640 * 8 * 8 = 40960 points
 constexpr int kMhMaxChainsPerCta = 32;    // one chain per lane of warp 0
-constexpr int kMhTab = 64;                // pair-code table entries (W^2 <= 64: K <= 7)
+constexpr int kMhTab = 64;                // pair-code table entries: K^2 + K + 1 <= 57 (K <= 7)
 
 // Point groups per thread (M) and threads per CTA (NT) for D points: D is padded to 8 NT M.
 inline void mh_shape(int D, int* M, int* NT) {
@@ -39,6 +39,8 @@ struct MhArgs {
   float prior_sd;             // mu_k ~ normal(0, prior_sd)
   float neg_half_inv_var;     // -0.5 / sigma^2
   float ll_const;             // -D (ln sigma + 0.5 ln 2 pi)
+  double neg_half_inv_var64;  // the same in fp64: the chains' log-likelihood folds in fp64
+  double ll_const64;
   int chains_per_cta;
   const float* y;             // device [D_pad] (zero padded)
   float* mu_out;              // [n_chains][K] final state

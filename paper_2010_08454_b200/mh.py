@@ -11,40 +11,52 @@ oracle/cuppl_oracle.c or_mh_gmm.
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
-
 import numpy as np
 
 from . import _native as N
 from .errors import InferRuntimeError
+from .infer import EmpiricalDistribution
 from .models import GaussianMixture
 from .rng import key_of, seed_of
 
 
-@dataclass
-class MhResult:
-    """Posterior summary of the return value (the sorted component means, label switching)."""
+class ChainsDistribution(EmpiricalDistribution):
+    """The EmpiricalDistribution of `chains` LMH chains' recorded
+    return values — the sorted component means (label switching), a real vector: singleton
+    support, summarised like a compiled model's vector return (mean["v<k>"],
+    stats["var_v<k>"]), plus the chain diagnostics the many-chain form adds (per-chain means
+    for Monte Carlo standard errors, acceptance rate, final states)."""
 
-    n_chains: int
-    n_steps: int
-    recorded: int                 # recorded samples per chain (after burn-in / thinning)
-    mean: np.ndarray              # pooled posterior mean of the sorted means
-    var: np.ndarray               # pooled posterior variance
-    chain_means: np.ndarray       # [chains, K] per-chain means (for MC standard errors / R-hat)
-    acceptance: float
-    final_mu: object = None       # device tensor [chains, K]
-    final_log_lik: object = None  # device tensor [chains]
-    trace: object = None          # device tensor [chains, recorded, K] when requested
-    extra: dict = field(default_factory=dict)
+    @property
+    def acceptance(self) -> float:
+        return self.stats["acceptance"]
+
+    @property
+    def n_chains(self) -> int:
+        return self.stats["chains"]
+
+    @property
+    def mean_vec(self) -> np.ndarray:
+        return np.array([self.mean[f"v{k}"] for k in range(len(self.mean))])
+
+    @property
+    def var_vec(self) -> np.ndarray:
+        return np.array([self.stats[f"var_v{k}"] for k in range(len(self.mean))])
+
+    @property
+    def chain_means(self) -> np.ndarray:
+        return self.record["chain_means"]
 
     def mcse(self) -> np.ndarray:
-        """Monte Carlo standard error of `mean` from the between-chain spread."""
-        return self.chain_means.std(axis=0, ddof=1) / math.sqrt(self.n_chains)
+        """Monte Carlo standard error of the mean from the between-chain spread."""
+        cm = self.chain_means
+        return cm.std(axis=0, ddof=1) / math.sqrt(len(cm))
 
 
 def run_lmh(model: GaussianMixture, n_samples: int, rng, *, chains: int = 4096, burn_in: int = 0,
-            thin: int = 1, return_trace: bool = False, group=None, device=None) -> MhResult:
-    """`chains` independent LMH chains of `n_samples` steps each on the GPU."""
+            thin: int = 1, return_trace: bool = False, group=None, device=None) -> ChainsDistribution:
+    """`chains` independent LMH chains of `n_samples` steps each on the GPU; the result is the
+    EmpiricalDistribution of the recorded sorted means."""
     import torch
 
     from .infer import _world, shard_range
@@ -91,6 +103,13 @@ def run_lmh(model: GaussianMixture, n_samples: int, rng, *, chains: int = 4096, 
     var = s[:, K:2 * K].sum(axis=0) / tot - mean ** 2
     chain_means = s[:, :K] / np.maximum(nrec, 1)[:, None]
     acc = float(s[:, 2 * K + 1].sum() / (len(s) * n_samples))
-    return MhResult(n_chains=chains, n_steps=n_samples, recorded=int(nrec[0]) if len(nrec) else 0, mean=mean,
-                    var=var, chain_means=chain_means, acceptance=acc, final_mu=mu[:nc], final_log_lik=ll[:nc],
-                    trace=None if tr is None else tr[:nc])
+    out = ChainsDistribution(n=int(tot))
+    out.mean = {f"v{k}": float(mean[k]) for k in range(K)}
+    out.stats = {f"var_v{k}": float(var[k]) for k in range(K)}
+    out.stats.update({"acceptance": acc, "chains": chains, "steps": n_samples,
+                      "recorded_per_chain": int(nrec[0]) if len(nrec) else 0})
+    out.record = {"chain_stats": s, "chain_means": chain_means}
+    out.traces = {"final_mu": mu[:nc], "final_log_lik": ll[:nc]}
+    if tr is not None:
+        out.traces["sorted_mu"] = tr[:nc]
+    return out

@@ -1,11 +1,21 @@
 """Differential testing of the model compiler: seeded random CuPPL programs (tests/fuzz_programs.py
 — every draw kind, arithmetic, pure and effectful ifs, factors, observe loops over data, scalar
 and tuple returns) compiled for the GPU, their log-weights compared with the fp64 interpreter on
-the GPU's recorded draws. fp32 evaluation of random expression trees: 1e-4 relative."""
+the GPU's recorded draws. Tolerance: SURVEY.md D11 (1e-5 relative + 1e-6) plus the program's
+own fp32 conditioning — ten times the distance between the fp64 interpreter and the same
+interpreter rounding every operation to fp32 (oracle/dsl_eval.Fp32Interpreter). Random
+expression trees cancel (x - y with x ~ y, pow of large arguments), where no fixed relative
+tolerance holds for any fp32 evaluation; for well-conditioned programs the extra term is ~0."""
 
 import math
 
 import numpy as np
+
+
+def tol_ok(got: float, ref: float, ref32: float) -> bool:
+    """D11 plus the program's fp32 conditioning (module docstring)."""
+    cond = abs(ref32 - ref) if math.isfinite(ref32) else 0.0
+    return abs(got - ref) <= 1e-5 * abs(ref) + 1e-6 + 10.0 * cond
 import pytest
 
 from fuzz_programs import program
@@ -24,7 +34,7 @@ def test_fuzz_programs_compile():
 @pytest.mark.gpu
 @pytest.mark.parametrize("seed", SEEDS)
 def test_gpu_fuzz_program_matches_interpreter(cuda, seed):
-    from oracle.dsl_eval import Interpreter
+    from oracle.dsl_eval import Fp32Interpreter, Interpreter
     from paper_2010_08454_b200 import Rng, infer
 
     src = program(seed)
@@ -33,13 +43,13 @@ def test_gpu_fuzz_program_matches_interpreter(cuda, seed):
     post = infer.run_importance(m, n, Rng(seed), return_traces=True)
     lw = post.traces["log_weight"].cpu().numpy().astype(float)
     draws = post.traces["draws"].cpu().numpy().astype(float)
-    it = Interpreter(src)
+    it, it32 = Interpreter(src), Fp32Interpreter(src)
     for i in range(0, n, 67):
         ref, _ = it.run(draws[i])
         if math.isinf(ref) or math.isnan(ref):
             assert not np.isfinite(lw[i]) or math.isinf(ref), (seed, i, lw[i], ref)
             continue
-        assert abs(lw[i] - ref) <= 1e-4 * abs(ref) + 1e-4, (seed, i, lw[i], ref, draws[i], src)
+        assert tol_ok(lw[i], ref, it32.run(draws[i])[0]), (seed, i, lw[i], ref, draws[i], src)
 
 
 @pytest.mark.gpu
@@ -111,17 +121,17 @@ def test_gpu_fuzz_vector_program_matches_interpreter(cuda, seed):
     """Random programs over drawn vectors (repeat of draws with literal or drawn length, reduces,
     Horner over data, indexing by a drawn integer, per-datum draws in map, vector returns)."""
     from fuzz_programs import vector_program
-    from oracle.dsl_eval import Interpreter
+    from oracle.dsl_eval import Fp32Interpreter, Interpreter
     from paper_2010_08454_b200 import Rng, infer
 
     src = vector_program(seed)
     post = infer.run_importance(frontend.compile_program(src), 2048, Rng(seed), return_traces=True)
     lw = post.traces["log_weight"].cpu().numpy().astype(float)
     draws = post.traces["draws"].cpu().numpy().astype(float)
-    it = Interpreter(src)
+    it, it32 = Interpreter(src), Fp32Interpreter(src)
     for i in range(0, 2048, 61):
         ref, _ = it.run(draws[i])
-        assert abs(lw[i] - ref) <= 1e-4 * abs(ref) + 1e-4, (seed, i, lw[i], ref, src)
+        assert tol_ok(lw[i], ref, it32.run(draws[i])[0]), (seed, i, lw[i], ref, src)
 
 
 @pytest.mark.gpu
@@ -146,14 +156,14 @@ def test_gpu_fuzz_lmh_matches_importance_on_vector_programs(cuda, seed):
 def test_gpu_fuzz_misc_operators(cuda, seed):
     """Integer % and /, floor, to-int, pow, && || !, int-valued ifs, closures over draws."""
     from fuzz_programs import misc_program
-    from oracle.dsl_eval import Interpreter
+    from oracle.dsl_eval import Fp32Interpreter, Interpreter
     from paper_2010_08454_b200 import Rng, infer
 
     src = misc_program(seed)
     post = infer.run_importance(frontend.compile_program(src), 2048, Rng(seed), return_traces=True)
     lw = post.traces["log_weight"].cpu().numpy().astype(float)
     draws = post.traces["draws"].cpu().numpy().astype(float)
-    it = Interpreter(src)
+    it, it32 = Interpreter(src), Fp32Interpreter(src)
     for i in range(0, 2048, 61):
         ref, _ = it.run(draws[i])
-        assert abs(lw[i] - ref) <= 1e-4 * abs(ref) + 1e-4, (seed, i, lw[i], ref, src)
+        assert tol_ok(lw[i], ref, it32.run(draws[i])[0]), (seed, i, lw[i], ref, src)

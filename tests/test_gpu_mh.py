@@ -31,17 +31,23 @@ def test_mh_initial_trace_and_short_chain_match_oracle(cuda, oracle_lib):
     N.check(L.cuppl_mh_gmm(N.ptr(y), D, K, 10.0, 1.0, nc, 0, 0, 0, 1, KEY, N.ptr(mu), N.ptr(ll), N.ptr(st),
                            None, 0, N.stream_ptr()))
     mu0, ll0 = mu.cpu().numpy(), ll.cpu().numpy()
+    y64 = np.asarray(m.ys, dtype=np.float32).astype(np.float64)
     for c in range(nc):
         z, mref, lref = core.mh_gmm_init(m.ys, K, 10.0, 1.0, c, KEY)
+        # means: fp32 SFU Box-Muller against fp64 (the D11 note of test_gpu_is.py)
         assert np.allclose(mu0[c], mref, rtol=1e-5, atol=1e-4)
-        assert abs(ll0[c] - lref) <= 1e-4 * abs(lref) + 1e-2
+        # log-likelihood: D11 against the fp64 re-evaluation of the GPU's own trace (labels are
+        # integer draws, bit-exact; means the GPU's)
+        r = y64 - mu0[c].astype(np.float64)[z]
+        l64 = -0.5 * float(np.dot(r, r)) - D * 0.5 * math.log(2 * math.pi)
+        assert abs(ll0[c] - l64) <= 1e-5 * abs(l64) + 1e-6, (c, ll0[c], l64)
     steps = 200
     N.check(L.cuppl_mh_gmm(N.ptr(y), D, K, 10.0, 1.0, nc, 0, steps, 0, 1, KEY, N.ptr(mu), N.ptr(ll), N.ptr(st),
                            None, 0, N.stream_ptr()))
     mref, lref, sref = core.mh_gmm(m.ys, K, 10.0, 1.0, nc, steps, KEY)
     got = st.cpu().numpy()
     same = np.all(np.isclose(mu.cpu().numpy(), mref, rtol=1e-4, atol=1e-3), axis=1)
-    assert same.mean() > 0.9, same.mean()  # chains whose decisions never straddled
+    assert same.mean() >= 0.98, same.mean()  # chains whose decisions never straddled
     assert np.array_equal(got[same, 2 * K + 1], sref[same, 2 * K + 1])
 
 
@@ -56,8 +62,8 @@ def test_mh_single_component_matches_conjugate_posterior(cuda):
     prec = 1 / 4 + len(y)
     mean = y.astype(np.float32).astype(float).sum() / prec
     post = infer.run_lmh(m, 40_000, Rng(5), chains=256, burn_in=10_000)
-    assert abs(post.mean[0] - mean) < 5 * post.mcse()[0] + 1e-3
-    assert abs(post.var[0] - 1 / prec) < 0.2 / prec
+    assert abs(post.mean_vec[0] - mean) < 5 * post.mcse()[0] + 1e-3
+    assert abs(post.var_vec[0] - 1 / prec) < 0.2 / prec
     assert 0.0 < post.acceptance < 1.0
 
 
@@ -82,6 +88,8 @@ def test_mh_statistics_match_oracle_chains(cuda, oracle_lib):
     m = models.GaussianMixture.synthetic(n_points=300, K=3)
     rng = Rng(11)
     post = infer.run_lmh(m, 3000, rng, chains=128, burn_in=1000)
+    assert isinstance(post, infer.EmpiricalDistribution)  # SPEC.md:408-413's result type
+    assert post.n == 128 * 2000 and set(post.mean) == {"v0", "v1", "v2"}
     mref, lref, sref = core.mh_gmm(m.ys, 3, 10.0, 1.0, 128, 3000, rng.key, burn_in=1000)
     ref_chain = sref[:, :3] / sref[:, [6]]
     se = np.sqrt(post.chain_means.var(axis=0, ddof=1) / 128 + ref_chain.var(axis=0, ddof=1) / 128)
@@ -112,7 +120,13 @@ def test_mh_data_shapes_match_oracle_initial_trace(cuda, oracle_lib, D):
     N.check(L.cuppl_mh_gmm(N.ptr(y), D, K, 10.0, 1.0, nc, 0, 0, 0, 1, KEY, N.ptr(mu), N.ptr(ll), N.ptr(st),
                            None, 0, N.stream_ptr()))
     mu0, ll0 = mu.cpu().numpy(), ll.cpu().numpy()
+    y64 = np.asarray(m.ys, dtype=np.float32).astype(np.float64)
     for c in range(nc):
         z, mref, lref = core.mh_gmm_init(m.ys, K, 10.0, 1.0, c, KEY)
+        # means: fp32 SFU Box-Muller against fp64 (the D11 note of test_gpu_is.py)
         assert np.allclose(mu0[c], mref, rtol=1e-5, atol=1e-4)
-        assert abs(ll0[c] - lref) <= 1e-4 * abs(lref) + 1e-2
+        # log-likelihood: D11 against the fp64 re-evaluation of the GPU's own trace (labels are
+        # integer draws, bit-exact; means the GPU's)
+        r = y64 - mu0[c].astype(np.float64)[z]
+        l64 = -0.5 * float(np.dot(r, r)) - D * 0.5 * math.log(2 * math.pi)
+        assert abs(ll0[c] - l64) <= 1e-5 * abs(l64) + 1e-6, (c, ll0[c], l64)

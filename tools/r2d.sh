@@ -1,0 +1,6 @@
+mkdir -p gpurun_out/r2d
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r2d/build.log 2>&1
+python tools/prof_mh.py 4096 2000 3 > gpurun_out/r2d/mh_time.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_mh.py tests/test_gpu_scale.py -k "mh or c3" -q -s > gpurun_out/r2d/mh_tests.log 2>&1
+timeout 600 python bench.py --workload mh --no-cpu-baseline > gpurun_out/r2d/mh.json 2> gpurun_out/r2d/mh.err
+ncu --set full --import-source on --clock-control none -f -k regex:mh_gmm_kernel -s 0 -c 1 -o gpurun_out/r2d/mh python tools/prof_mh.py 4096 1000 1 > gpurun_out/r2d/ncu.log 2>&1
