@@ -91,6 +91,13 @@ WORKLOADS = {
         "scaling": "weak",
         "n_points": 10_000,
     },
+    "resample": {
+        "name": "Generic systematic resampling (cuppl_resample) of C4's 1e8-particle population: fp32 "
+                "log-weights + a 4-byte state payload per particle (BASELINE configs[3] population)",
+        "particles": 100_000_000,
+        "scaling": "weak",
+        "n_points": 0,
+    },
 }
 METRICS = {
     "linreg": (METRIC, UNIT),
@@ -98,6 +105,7 @@ METRICS = {
     "dsl-linreg": (METRIC, UNIT),
     "smc": ("SMC steps/sec", "time-steps/s"),
     "mh": ("MH chain-steps/sec", "chain-steps/s"),
+    "resample": ("resampled particles/sec", "particles/s"),
 }
 
 
@@ -668,6 +676,119 @@ def cpu_baseline_engine(args, model) -> dict:
             "sample": f"{chains} chains x {steps} steps, oracle/cuppl_oracle.c or_mh_gmm (fp64, OpenMP {threads})"}
 
 
+def run_ours_resample(args) -> dict | None:
+    """Generic resampling (csrc/resample_kernels.cu) of a resident population: each step is one
+    cuppl_resample call (max, quantise + scan, TMA-staged gather) over N particles."""
+    import numpy as np
+    import torch
+
+    from paper_2010_08454_b200 import build as B
+
+    B.build()
+    from paper_2010_08454_b200 import Rng, resample
+    from paper_2010_08454_b200 import _native as N
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    wl = WORKLOADS["resample"]
+    n = args.particles or wl["particles"]
+    gen = torch.Generator(device=device).manual_seed(1234 + rank)
+    lw = (0.5 * torch.randn(n, device=device, generator=gen)).float()
+    payload = torch.arange(n, dtype=torch.int32, device=device)
+    out = torch.empty_like(payload)
+    r = resample.Resampler(n, device)
+    key = Rng(1).key
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+    for k in range(args.warmup):
+        r.launch(lw, payload, key, 1000 + k, out, None)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    for k in range(args.steps):
+        flush.zero_()
+        starts[k].record()
+        r.launch(lw, payload, key, k, out, None)
+        ends[k].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    t_ms = tot.item()
+    value = world * n * args.steps / (t_ms / 1e3)
+    # e2e: the public API from host (pinned) arrays: H2D of lw + payload, D2H of the new payload
+    lw_h = lw.cpu().pin_memory()
+    pay_h = payload.cpu().pin_memory()
+    out_h = torch.empty_like(pay_h).pin_memory()
+    e2e_t = []
+    for k in range(2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        res = resample.systematic(lw_h.to(device, non_blocking=True), pay_h.to(device, non_blocking=True),
+                                  Rng(1), 500 + k)
+        out_h.copy_(res.payload, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_t.append(e0.elapsed_time(e1))
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return None
+    peak, src = _hbm_peak()
+    kernel_s = (t_ms / args.steps) / 1e3
+    bpp = 20.0  # SURVEY.md §8(d) C4: 12 + 2s B per particle-step, s = 4-byte state
+    achieved = bpp * n / kernel_s / 1e9
+    tr = load_traffic("resample")
+    res_line = {
+        "metric": METRICS["resample"][0], "value": value, "unit": "particles/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64 (exact integer comb), f32 log-weights",
+        "data": "synthetic: lw ~ 0.5 N(0,1) fp32, payload = int32 particle ids (torch seed 1234 + rank)",
+        "config": {"workload": wl["name"], "particles_per_gpu": n, "payload_bytes": 4,
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "parallelism": f"replicas dp{world} (one population per GPU)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None if tr is None else tr["bytes_per_launch"] * (n / tr["n"]),
+                     "peak_source": src, "algorithmic_bytes_per_particle": bpp,
+                     "note": "one step = 3 kernels (RS1 max, RS2 quantise+scan, RS3 TMA-staged gather); "
+                             "algorithmic bytes: lw read 3x (12) + payload read + write (8)"},
+        "e2e": {"value": n * 2 / (sum(e2e_t) / 1e3), "unit": "particles/s",
+                "h2d_bytes_per_step": int(lw_h.nbytes + pay_h.nbytes), "d2h_bytes_per_step": int(out_h.nbytes),
+                "api": "paper_2010_08454_b200.resample.systematic(lw, payload, rng, t)"},
+        "gpu_launches": 3 * args.steps,
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        from oracle import core
+
+        core.build()
+        m = 10_000_000
+        lw_c = lw[:m].cpu().numpy()
+        pay_c = payload[:m].cpu().numpy()
+        t0 = time.perf_counter()
+        core.resample(lw_c, pay_c, key, 0)
+        dt = time.perf_counter() - t0
+        res_line["cpu_baseline"] = {"value": m / dt, "unit": "particles/s", "cores": os.cpu_count() or 1,
+                                    "kind": "port", "sample": f"{m} particles, oracle/resample_oracle.c or_resample "
+                                                              f"(OpenMP) in {dt:.2f} s"}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return res_line
+
+
 def run_reference(args) -> dict | None:
     rank, world, _ = dist_env()
     if rank != 0:
@@ -689,6 +810,18 @@ def run_reference(args) -> dict | None:
         def step(k):
             core.smc_run(model, per_step, key + k, steps=20)
         units = 20 * per_step / n_full
+    elif args.workload == "resample":
+        import numpy as np
+
+        per_step, cores = 10_000_000, threads
+        rs_ = np.random.default_rng(1234)
+        lw_c = (0.5 * rs_.standard_normal(per_step)).astype(np.float32)
+        pay_c = np.arange(per_step, dtype=np.int32)
+        sample = f"{per_step} particles per step (oracle/resample_oracle.c or_resample, OpenMP {threads})"
+
+        def step(k):
+            core.resample(lw_c, pay_c, key, k)
+        units = per_step
     elif args.workload == "mh":
         per_step, cores = 64, threads
         sample = f"{per_step} chains x 200 steps per step (or_mh_gmm, fp64, OpenMP {threads})"
@@ -746,6 +879,8 @@ def main():
         res = run_dry(args)
     elif args.impl == "reference":
         res = run_reference(args)
+    elif args.workload == "resample":
+        res = run_ours_resample(args)
     elif args.workload in ("smc", "mh"):
         res = run_ours_engine(args)
     else:
