@@ -136,6 +136,10 @@ CUPPL_API int cuppl_dist_score(const cuppl_dist* d, const void* x, uint64_t coun
 /* ---- K1 + K2: importance sampling (replaces run_importance) -------- */
 /* Workspace bytes for an importance-sampling launch on the current device. */
 CUPPL_API size_t cuppl_is_workspace_bytes(void);
+/* The same for a data set of n_points: data sets larger than the kernel-parameter block
+ * (> 3968 points for linear regression, > 64 for the polynomial model) are copied into the
+ * workspace tail and read from device memory (up to 2^24 points). */
+CUPPL_API size_t cuppl_is_workspace_bytes_n(int n_points);
 
 /* Fig.1 polynomial model:
  *   n ~ uniform-discrete(2, 5); c_j ~ normal(0, 10), j < n; factor(-sum_i (y_i - sum_j c_j x_i^j)^2)

@@ -95,6 +95,7 @@ _SIG = {
     "cuppl_dist_sample": ([_P, _U64, _U32, _U64, _U64, _P, _P], C.c_int),
     "cuppl_dist_score": ([_P, _P, _U64, _P, _P], C.c_int),
     "cuppl_is_workspace_bytes": ([], C.c_size_t),
+    "cuppl_is_workspace_bytes_n": ([C.c_int], C.c_size_t),
     "cuppl_is_poly": ([_P, _P, C.c_int, _U64, _U64, _U64, _P, _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
     "cuppl_is_linreg": ([_P, _P, C.c_int, _F32, _U64, _U64, _U64, _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
     "cuppl_is_record_merge": ([_P, C.c_int, _P], C.c_int),

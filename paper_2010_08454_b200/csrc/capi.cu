@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 #include <mutex>
 #include <string>
 
@@ -77,6 +78,11 @@ int poly_variant() {
 size_t is_ws_bytes(int sm) {
   return 256 + static_cast<size_t>(sm) * kMaxBlocksPerSm * sizeof(cuppl_is_record);
 }
+// ... plus the device copy of data sets too large for the kernel-parameter block
+constexpr int kMaxDataPoints = 1 << 24;
+size_t is_ws_bytes_data(int sm, int n_points) {
+  return ((is_ws_bytes(sm) + 255) & ~static_cast<size_t>(255)) + static_cast<size_t>(n_points) * sizeof(float2);
+}
 
 int check_dist(const cuppl_dist* d, DistArgs* a) {
   if (!d) return set_error(CUPPL_E_ARGUMENT, "dist is NULL");
@@ -137,14 +143,17 @@ template <typename P>
 int fill_common(P& prm, const float* xs, const float* ys, int n_points, int cap,
                 uint64_t pid_begin, uint64_t pid_end, uint64_t key, const float* injected,
                 float* lw_out, float* coef_out, cuppl_is_record* rec_out, void* ws,
-                size_t ws_bytes, int sm) {
+                size_t ws_bytes, int sm, cudaStream_t stream) {
   if (!xs || !ys) return set_error(CUPPL_E_ARGUMENT, "xs/ys are NULL");
-  if (n_points < 1 || n_points > cap)
+  if (n_points < 1 || (cap > 0 && n_points > cap))
     return set_error(CUPPL_E_CAPACITY, "n_points=%d outside [1, %d]", n_points, cap);
+  if (n_points > kMaxDataPoints)
+    return set_error(CUPPL_E_CAPACITY, "n_points=%d > %d", n_points, kMaxDataPoints);
   if (pid_end < pid_begin) return set_error(CUPPL_E_ARGUMENT, "pid_end < pid_begin");
   if (!rec_out) return set_error(CUPPL_E_ARGUMENT, "rec_out is NULL");
-  if (!ws || ws_bytes < is_ws_bytes(sm))
-    return set_error(CUPPL_E_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, is_ws_bytes(sm));
+  const size_t need = cap > 0 ? is_ws_bytes(sm) : is_ws_bytes_data(sm, n_points);
+  if (!ws || ws_bytes < need)
+    return set_error(CUPPL_E_CAPACITY, "workspace %zu < %zu bytes", ws_bytes, need);
   prm.pid_begin = pid_begin;
   prm.pid_end = pid_end;
   prm.k0 = static_cast<uint32_t>(key);
@@ -158,8 +167,21 @@ int fill_common(P& prm, const float* xs, const float* ys, int n_points, int cap,
   prm.counter = static_cast<unsigned int*>(ws);
   prm.block_recs = reinterpret_cast<cuppl_is_record*>(static_cast<char*>(ws) + 256);
   prm.rec_out = rec_out;
-  for (int i = 0; i < n_points; ++i) prm.xy[i] = make_float2(xs[i], ys[i]);
-  for (int i = n_points; i < cap; ++i) prm.xy[i] = make_float2(0.f, 0.f);
+  prm.xy_g = nullptr;
+  if (cap > 0) {
+    for (int i = 0; i < n_points; ++i) prm.xy[i] = make_float2(xs[i], ys[i]);
+    for (int i = n_points; i < cap; ++i) prm.xy[i] = make_float2(0.f, 0.f);
+    return CUPPL_OK;
+  }
+  // large data: interleaved (x, y) pairs in the workspace tail (pageable H2D copy: the host
+  // staging vector may be released as soon as cudaMemcpyAsync returns)
+  prm.xy[0] = make_float2(0.f, 0.f);
+  std::vector<float2> host(static_cast<size_t>(n_points));
+  for (int i = 0; i < n_points; ++i) host[i] = make_float2(xs[i], ys[i]);
+  float2* dev = reinterpret_cast<float2*>(static_cast<char*>(ws) + is_ws_bytes(sm));
+  cudaError_t e = cudaMemcpyAsync(dev, host.data(), host.size() * sizeof(float2), cudaMemcpyHostToDevice, stream);
+  if (e != cudaSuccess) return cuda_status(e, "cudaMemcpyAsync");
+  prm.xy_g = dev;
   return CUPPL_OK;
 }
 }  // namespace
@@ -228,6 +250,12 @@ size_t cuppl_is_workspace_bytes(void) {
   return is_ws_bytes(sm);
 }
 
+size_t cuppl_is_workspace_bytes_n(int n_points) {
+  int sm = 0;
+  if (device_sm_count(&sm)) sm = 256;
+  return n_points > kPolyCap ? is_ws_bytes_data(sm, n_points) : is_ws_bytes(sm);
+}
+
 int cuppl_is_linreg(const float* xs, const float* ys, int n_points, float sigma,
                     uint64_t pid_begin, uint64_t pid_end, uint64_t key, const float* injected,
                     float* lw_out, float* coef_out, cuppl_is_record* rec_out, void* workspace,
@@ -245,7 +273,20 @@ int cuppl_is_linreg(const float* xs, const float* ys, int n_points, float sigma,
   if (n_points <= kLinregCapSmall) {
     LinregParams<kLinregCapSmall> prm;
     if (int s = fill_common(prm, xs, ys, n_points, kLinregCapSmall, pid_begin, pid_end, key,
-                            injected, lw_out, coef_out, rec_out, workspace, workspace_bytes, sm))
+                            injected, lw_out, coef_out, rec_out, workspace, workspace_bytes, sm, st))
+      return s;
+    prm.neg_half_inv_var = nhiv;
+    prm.lw_const = lwc;
+    prm.one = 1.0f;
+    prm.pad1_ = 0.f;
+    return cuda_status(
+        launch_linreg(prm, injected != nullptr, sm, sm * kMaxBlocksPerSm, st, linreg_variant()),
+        "is_linreg");
+  }
+  if (n_points > kLinregCapLarge) {  // data in device memory (workspace tail)
+    LinregParams<kIsCapGlobal> prm;
+    if (int s = fill_common(prm, xs, ys, n_points, kIsCapGlobal, pid_begin, pid_end, key, injected, lw_out,
+                            coef_out, rec_out, workspace, workspace_bytes, sm, st))
       return s;
     prm.neg_half_inv_var = nhiv;
     prm.lw_const = lwc;
@@ -257,7 +298,7 @@ int cuppl_is_linreg(const float* xs, const float* ys, int n_points, float sigma,
   }
   LinregParams<kLinregCapLarge> prm;
   if (int s = fill_common(prm, xs, ys, n_points, kLinregCapLarge, pid_begin, pid_end, key,
-                          injected, lw_out, coef_out, rec_out, workspace, workspace_bytes, sm))
+                          injected, lw_out, coef_out, rec_out, workspace, workspace_bytes, sm, st))
     return s;
   prm.neg_half_inv_var = nhiv;
   prm.lw_const = lwc;
@@ -275,13 +316,22 @@ int cuppl_is_poly(const float* xs, const float* ys, int n_points, uint64_t pid_b
   int sm = 0;
   if (int s = device_sm_count(&sm)) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  PolyParams<kPolyCap> prm;
-  if (int s = fill_common(prm, xs, ys, n_points, kPolyCap, pid_begin, pid_end, key, injected,
-                          lw_out, coef_out, rec_out, workspace, workspace_bytes, sm))
-    return s;
-  prm.deg_out = deg_out;
   cudaError_t e = cudaMemsetAsync(workspace, 0, 256, st);
   if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync");
+  if (n_points > kPolyCap) {  // data in device memory (workspace tail)
+    PolyParams<kIsCapGlobal> prm;
+    if (int s = fill_common(prm, xs, ys, n_points, kIsCapGlobal, pid_begin, pid_end, key, injected, lw_out,
+                            coef_out, rec_out, workspace, workspace_bytes, sm, st))
+      return s;
+    prm.deg_out = deg_out;
+    return cuda_status(launch_poly(prm, injected != nullptr, sm, sm * kMaxBlocksPerSm, st, poly_variant()),
+                       "is_poly");
+  }
+  PolyParams<kPolyCap> prm;
+  if (int s = fill_common(prm, xs, ys, n_points, kPolyCap, pid_begin, pid_end, key, injected,
+                          lw_out, coef_out, rec_out, workspace, workspace_bytes, sm, st))
+    return s;
+  prm.deg_out = deg_out;
   return cuda_status(launch_poly(prm, injected != nullptr, sm, sm * kMaxBlocksPerSm, st, poly_variant()),
                      "is_poly");
 }

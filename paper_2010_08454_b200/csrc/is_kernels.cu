@@ -58,7 +58,7 @@ is_linreg_kernel(const __grid_constant__ LinregParams<CAP> prm) {
       int i = 0;
 #pragma unroll 2
       for (; i + 1 < D; i += 2) {
-        const float2 p0 = prm.xy[i], p1 = prm.xy[i + 1];
+        const float2 p0 = xy_at(prm, i), p1 = xy_at(prm, i + 1);
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           const float r0 = fmaf(-a[p], p0.x, p0.y - b[p]);
@@ -68,7 +68,7 @@ is_linreg_kernel(const __grid_constant__ LinregParams<CAP> prm) {
         }
       }
       if (i < D) {
-        const float2 p0 = prm.xy[i];
+        const float2 p0 = xy_at(prm, i);
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           const float r0 = fmaf(-a[p], p0.x, p0.y - b[p]);
@@ -89,24 +89,42 @@ is_linreg_kernel(const __grid_constant__ LinregParams<CAP> prm) {
         S0[q] = pack2(0.f, 0.f);
         S1[q] = pack2(0.f, 0.f);
       }
-      int i = 0;
-#pragma unroll 2
-      for (; i + 1 < D; i += 2) {
-        const float2 p0 = prm.xy[i], p1 = prm.xy[i + 1];
-        const f32x2 X0 = pack2(p0.x, p0.x), Y0 = pack2(p0.y, p0.y);
-        const f32x2 X1 = pack2(p1.x, p1.x), Y1 = pack2(p1.y, p1.y);
+      // large data sets (device-memory path): fp32 sums over 512-point chunks, folded in fp64
+      // (D10), so the absolute error of lw stays ~1e-3 at 1e4..1e5 points
+      constexpr bool kChunked = LinregParams<CAP>::kCap == 0;
+      constexpr int kChunk = kChunked ? 512 : (1 << 30);
+      double T64[kChunked ? P : 1];
 #pragma unroll
-        for (int q = 0; q < P / 2; ++q) {
-          const f32x2 c0 = V == 1 ? fma2(NB[q], ONE, Y0) : add2(Y0, NB[q]);
-          const f32x2 c1 = V == 1 ? fma2(NB[q], ONE, Y1) : add2(Y1, NB[q]);
-          const f32x2 r0 = fma2(NA[q], X0, c0);
-          const f32x2 r1 = fma2(NA[q], X1, c1);
-          S0[q] = fma2(r0, r0, S0[q]);
-          S1[q] = fma2(r1, r1, S1[q]);
+      for (int p = 0; p < (kChunked ? P : 1); ++p) T64[p] = 0.0;
+      int i = 0;
+      for (int cend = min(D, kChunk); ; cend = min(D, cend + kChunk)) {
+#pragma unroll 2
+        for (; i + 1 < cend; i += 2) {
+          const float2 p0 = xy_at(prm, i), p1 = xy_at(prm, i + 1);
+          const f32x2 X0 = pack2(p0.x, p0.x), Y0 = pack2(p0.y, p0.y);
+          const f32x2 X1 = pack2(p1.x, p1.x), Y1 = pack2(p1.y, p1.y);
+#pragma unroll
+          for (int q = 0; q < P / 2; ++q) {
+            const f32x2 c0 = V == 1 ? fma2(NB[q], ONE, Y0) : add2(Y0, NB[q]);
+            const f32x2 c1 = V == 1 ? fma2(NB[q], ONE, Y1) : add2(Y1, NB[q]);
+            const f32x2 r0 = fma2(NA[q], X0, c0);
+            const f32x2 r1 = fma2(NA[q], X1, c1);
+            S0[q] = fma2(r0, r0, S0[q]);
+            S1[q] = fma2(r1, r1, S1[q]);
+          }
+        }
+        if (!kChunked || cend >= D) break;
+#pragma unroll
+        for (int q = 0; q < P / 2; ++q) {  // fold the chunk (even chunk sizes: i == cend here)
+          const float2 t = unpack2(add2(S0[q], S1[q]));
+          T64[(2 * q) % (kChunked ? P : 1)] += t.x;
+          T64[(2 * q + 1) % (kChunked ? P : 1)] += t.y;
+          S0[q] = pack2(0.f, 0.f);
+          S1[q] = pack2(0.f, 0.f);
         }
       }
       if (i < D) {
-        const float2 p0 = prm.xy[i];
+        const float2 p0 = xy_at(prm, i);
         const f32x2 X0 = pack2(p0.x, p0.x), Y0 = pack2(p0.y, p0.y);
 #pragma unroll
         for (int q = 0; q < P / 2; ++q) {
@@ -118,8 +136,13 @@ is_linreg_kernel(const __grid_constant__ LinregParams<CAP> prm) {
 #pragma unroll
       for (int q = 0; q < P / 2; ++q) {
         const float2 t = unpack2(add2(S0[q], S1[q]));
-        ssum[2 * q] = t.x;
-        ssum[2 * q + 1] = t.y;
+        if constexpr (kChunked) {
+          ssum[2 * q] = static_cast<float>(T64[(2 * q) % (kChunked ? P : 1)] + t.x);
+          ssum[2 * q + 1] = static_cast<float>(T64[(2 * q + 1) % (kChunked ? P : 1)] + t.y);
+        } else {
+          ssum[2 * q] = t.x;
+          ssum[2 * q + 1] = t.y;
+        }
       }
     }
 #pragma unroll
@@ -284,7 +307,7 @@ __device__ __forceinline__ void poly_chunk(const PolyParams<CAP>& prm, PolyAcc& 
   }
 #pragma unroll(DC > 0 ? DC : 4)
   for (int i = 0; i < D; ++i) {
-    const float2 xy = prm.xy[i];  // warp-uniform constant-bank load (LDCU)
+    const float2 xy = xy_at(prm, i);  // warp-uniform constant-bank load (LDCU)
     const f32x2 X = pack2(xy.x, xy.x), NY = pack2(-xy.y, -xy.y);
 #pragma unroll
     for (int q = 0; q < P / 2; ++q) {
@@ -401,5 +424,7 @@ cudaError_t launch_poly(const PolyParams<CAP>& prm, bool injected, int sm_count,
 template cudaError_t launch_linreg<kLinregCapSmall>(const LinregParams<kLinregCapSmall>&, bool, int, int, cudaStream_t, int);
 template cudaError_t launch_linreg<kLinregCapLarge>(const LinregParams<kLinregCapLarge>&, bool, int, int, cudaStream_t, int);
 template cudaError_t launch_poly<kPolyCap>(const PolyParams<kPolyCap>&, bool, int, int, cudaStream_t, int);
+template cudaError_t launch_linreg<kIsCapGlobal>(const LinregParams<kIsCapGlobal>&, bool, int, int, cudaStream_t, int);
+template cudaError_t launch_poly<kIsCapGlobal>(const PolyParams<kIsCapGlobal>&, bool, int, int, cudaStream_t, int);
 
 }  // namespace cuppl

@@ -29,22 +29,37 @@ struct IsCommon {
   cuppl_is_record* block_recs;
   unsigned int* counter;
   cuppl_is_record* rec_out;
+  const float2* xy_g;  // CAP == 0: the (x_i, y_i) pairs in device memory (the workspace tail)
 };
 
 template <int CAP>
 struct LinregParams : IsCommon {
+  static constexpr int kCap = CAP;
   float neg_half_inv_var;  // -0.5 / sigma^2
   float lw_const;          // -D (ln sigma + 0.5 ln 2 pi)
   float one;               // 1.0f at run time (operand of the FFMA2 form of the add, V == 1)
   float pad1_;
-  float2 xy[CAP];
+  float2 xy[CAP > 0 ? CAP : 1];
 };
 
 template <int CAP>
 struct PolyParams : IsCommon {
+  static constexpr int kCap = CAP;
   int32_t* deg_out;
-  float2 xy[CAP];
+  float2 xy[CAP > 0 ? CAP : 1];
 };
+
+// Point i of the data: the kernel-parameter block (constant bank) up to CAP points; larger
+// data sets (CAP == 0) are read from device memory with warp-uniform __ldg (L1 broadcasts).
+template <typename P>
+__device__ __forceinline__ float2 xy_at(const P& prm, int i) {
+  if constexpr (P::kCap > 0) {
+    return prm.xy[i];
+  } else {
+    return __ldg(prm.xy_g + i);
+  }
+}
+constexpr int kIsCapGlobal = 0;
 
 template <int CAP>
 cudaError_t launch_linreg(const LinregParams<CAP>& prm, bool injected, int sm_count,

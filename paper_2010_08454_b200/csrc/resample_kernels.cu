@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(kRsThreads) rs_scan_kernel(RsArgs a) {
 
 // ------------------------------------------------------------------ RS3: gather ---------
 template <bool STAGE_PAY>
-__global__ void __launch_bounds__(kRsThreads) rs_gather_kernel(RsArgs a) {
+__global__ void __launch_bounds__(kRsThreads, 3) rs_gather_kernel(RsArgs a) {
   extern __shared__ __align__(128) uint8_t pay_s[];  // [kRsTile][P] staged payload (STAGE_PAY)
   __shared__ __align__(128) float lws[kRsTile];     // staged log-weights
   __shared__ __align__(16) uint16_t marks[kRsWin];  // tile index + 1 of a first child
@@ -303,11 +303,16 @@ __global__ void __launch_bounds__(kRsThreads) rs_gather_kernel(RsArgs a) {
     // ---- my sources [8 tid, +8): exact integer weights, block exclusive scan
     double wd[kRsSeg];
     unsigned long long tw = 0;
+    {
+      const float4 l0 = reinterpret_cast<const float4*>(lws)[2 * tid];  // two LDS.128
+      const float4 l1 = reinterpret_cast<const float4*>(lws)[2 * tid + 1];
+      const float lv[kRsSeg] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
 #pragma unroll
-    for (int k = 0; k < kRsSeg; ++k) {
-      const uint32_t w = any ? smc_w(smc_e(lws[kRsSeg * tid + k], M)) : 0u;
-      tw += w;
-      wd[k] = static_cast<double>(w);
+      for (int k = 0; k < kRsSeg; ++k) {
+        const uint32_t w = any ? smc_w(smc_e(lv[k], M)) : 0u;
+        tw += w;
+        wd[k] = static_cast<double>(w);
+      }
     }
     unsigned long long incl = tw;
 #pragma unroll

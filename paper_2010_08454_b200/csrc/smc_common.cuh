@@ -9,9 +9,14 @@
 namespace cuppl {
 
 // ------------------------------------------------------------------ exact helpers -------
+// k = rint(t) by the 1.5 * 2^23 magic addition (round-half-even, exact for |t| < 2^22; here
+// |t| <= 126): the same value as the oracle's rintf, and its integer is read from the sum's
+// low bits — no FRND / F2I conversion-pipe instructions.
 __device__ __forceinline__ float exp_repro(float d) {
   const float t = __fmul_rn(d, 1.44269504f);
-  const float k = rintf(t);
+  const float kb = __fadd_rn(t, 12582912.0f);
+  const float k = __fsub_rn(kb, 12582912.0f);
+  const int ki = __float_as_int(kb) - 0x4B400000;
   float r = __fmaf_rn(k, -0.693145752f, d);
   r = __fmaf_rn(k, -1.42860677e-06f, r);
   float p = 1.38888893e-03f;
@@ -21,7 +26,7 @@ __device__ __forceinline__ float exp_repro(float d) {
   p = __fmaf_rn(p, r, 0.5f);
   p = __fmaf_rn(p, r, 1.0f);
   p = __fmaf_rn(p, r, 1.0f);
-  return __fmul_rn(p, __int_as_float((static_cast<int>(k) + 127) << 23));
+  return __fmul_rn(p, __int_as_float((ki + 127) << 23));
 }
 
 __device__ __forceinline__ float smc_e(float lw, float M) {

@@ -1281,8 +1281,14 @@ def _return_parts(ret, g: _Gen, int_bins: tuple = (0, MAX_BINS)):
 
 def compile_program(source: str, data: dict | None = None, max_depth: int = 20) -> CompiledModel:
     """Parse and compile a CuPPL program whose result is importance(model, n), enumerate(model,
-    n) or mcmc(model, n). max_depth bounds recursion in enumerated programs."""
-    prog = lang.parse(source)
+    n) or mcmc(model, n). max_depth bounds recursion in enumerated programs.
+    Programs that bind engine results and compute with them (dist-var of a posterior,
+    SPEC.md:432) run through program.run_program."""
+    return compile_parsed(lang.parse(source), source, data, max_depth)
+
+
+def compile_parsed(prog, source: str, data: dict | None = None, max_depth: int = 20) -> CompiledModel:
+    """compile_program of an already parsed lang.Program."""
     comp = _Compiler(prog, data, max_depth)
     ret = comp.compile()
     g = comp.g

@@ -134,7 +134,7 @@ class IsLauncher:
         self.model = model
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         L = N.lib()
-        ws = L.cuppl_is_workspace_bytes()
+        ws = L.cuppl_is_workspace_bytes_n(len(model.xs))
         self.ws = torch.empty(int(ws), dtype=torch.uint8, device=self.device)
         self.rec = torch.empty(N.REC_BYTES, dtype=torch.uint8, device=self.device)
         self._xs = np.ascontiguousarray(model.xs, dtype=np.float32)
