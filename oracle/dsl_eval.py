@@ -37,14 +37,19 @@ class _Dist:
 
 
 class Interpreter:
+    F32_LITERALS = True  # literals and data as the fp32 GPU kernels see them
+
+    def _rl(self, v):
+        return float(np.float32(v)) if self.F32_LITERALS else float(v)
+
     def __init__(self, source: str, data: dict | None = None):
         self.prog = lang.parse(source)
         self.globals = {}
         for name, arr in (data or {}).items():
-            self.globals[name] = [float(np.float32(v)) for v in np.asarray(arr).reshape(-1)]
+            self.globals[name] = [self._rl(v) for v in np.asarray(arr).reshape(-1)]
         for name, e in self.prog.bindings:
             if isinstance(e, lang.VecLit):
-                self.globals[name] = [float(np.float32(self._const(x))) for x in e.elems]
+                self.globals[name] = [self._rl(self._const(x)) for x in e.elems]
             else:
                 self.globals[name] = self.ev(e, {})
         res = self.prog.result
@@ -73,7 +78,7 @@ class Interpreter:
 
     def ev(self, e, env):
         if isinstance(e, lang.Num):
-            return float(np.float32(e.value)) if isinstance(e.value, float) else e.value
+            return self._rl(e.value) if isinstance(e.value, float) else e.value
         if isinstance(e, lang.Bool):
             return e.value
         if isinstance(e, lang.Var):
@@ -175,7 +180,10 @@ class _NeedChoice(Exception):
 class Enumerator(Interpreter):
     """Exact enumeration by re-execution (SPEC.md:438's brute-force forced-choice oracle):
     a run with a choice prefix either completes or asks for the next choice point's support;
-    every completed path contributes exp(sum of choice log-masses + factors)."""
+    every completed path contributes exp(sum of choice log-masses + factors). Literals and data
+    stay fp64, as in the GPU's fp64 enumeration kernels (frontend.py)."""
+
+    F32_LITERALS = False
 
     def run_forced(self, prefix):
         self._prefix = prefix

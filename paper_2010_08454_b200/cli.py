@@ -99,7 +99,7 @@ def _run_file(args) -> int:
         print(f"error: file not found: {args.file}", file=sys.stderr)
         return 1
     try:
-        model = frontend.compile_program(src)
+        model = frontend.compile_program(src, max_depth=args.max_depth or 20)
     except CupError as e:
         print(e.render() if hasattr(e, "render") else f"error: {e}", file=sys.stderr)
         return 1
@@ -108,7 +108,9 @@ def _run_file(args) -> int:
         return 1
     try:
         if model.engine == "enumerate":
-            post = infer.run_enumeration(model, args.max_executions or None)
+            # the program's own enumerate(model, n) bound unless --max-executions overrides it
+            post = infer.run_enumeration(model, args.max_executions or model.default_n,
+                                         args.max_depth or None)
         elif model.engine == "mcmc":
             post = infer.run_lmh(model, args.samples or model.default_n, Rng(_seed(args)), chains=args.chains,
                                  burn_in=args.burn_in, thin=args.thin)
@@ -292,7 +294,10 @@ def main(argv=None) -> int:
                    "the GPU by frontend.py)")
     r.add_argument("--model", choices=tuple(DEFAULT_INFERENCE))
     r.add_argument("--inference", choices=("importance", "mcmc", "smc", "enumerate"))
-    r.add_argument("--max-executions", type=int, default=0, help="enumeration: bound on the path space")
+    r.add_argument("--max-executions", type=int, default=0,
+                   help="enumeration: bound on the path index space (default: the program's enumerate(model, n))")
+    r.add_argument("--max-depth", type=int, default=0,
+                   help="enumeration: recursion / choice-point depth bound (SPEC.md RunConfig; default 20)")
     r.add_argument("--samples", "--particles", type=int, default=0,
                    help="particles (importance, smc) or steps per chain (mcmc)")
     r.add_argument("--smc-steps", type=int, default=None, help="smc: time steps to filter (default: all)")

@@ -143,10 +143,17 @@ __device__ __forceinline__ float hsum2(f32x2 v) {
   const float2 t = unpack2(v);
   return t.x + t.y;
 }
+#ifdef CUPPL_F64
+template <class A, class B>  // fp64 models: the common type, so a double branch is never narrowed
+__device__ __forceinline__ auto sel_(bool c, const A& a, const B& b) -> decltype(true ? a : b) {
+  return c ? a : b;
+}
+#else
 template <class A, class B>
 __device__ __forceinline__ A sel_(bool c, const A& a, const B& b) {
   return c ? a : static_cast<A>(b);
 }
+#endif
 
 // pure select: both operands are already evaluated (they are side-effect free)
 template <class C, class A, class B>
@@ -372,12 +379,68 @@ typedef Lane<f32x2> VF2;
 typedef Lane<unsigned long long> VU64;
 typedef LaneStream VStream;
 #else
+#ifdef CUPPL_F64
+typedef double VF;
+#else
 typedef float VF;
+#endif
 typedef int VI;
 typedef bool VB;
 typedef f32x2 VF2;
 typedef unsigned long long VU64;
 typedef WordStream VStream;
+#endif
+
+
+#ifdef CUPPL_F64
+// ------------------------------------------------------------------ fp64 models ---------
+// Enumeration (frontend.py): path log-masses, factors and the record are fp64, and the body's
+// real-valued helpers resolve to these forms (the generated source also maps the C math names
+// logf, log1pf, fmaf, ... to their double functions). One path per thread.
+#if LANES != 1
+#error "fp64 models run one path per thread"
+#endif
+__device__ __forceinline__ double to_d(double x) { return x; }
+__device__ __forceinline__ double to_d(float x) { return static_cast<double>(x); }
+__device__ __forceinline__ double to_d(int x) { return static_cast<double>(x); }
+__device__ __forceinline__ double to_d(bool x) { return x ? 1.0 : 0.0; }
+__device__ __forceinline__ int to_i(double x) { return static_cast<int>(x); }
+__device__ __forceinline__ bool to_b(double x) { return x != 0.0; }
+__device__ __forceinline__ double neg_inf_d_() { return -__longlong_as_double(0x7FF0000000000000ll); }
+__device__ __forceinline__ double score_normal_d(double x, double m, double sd) {
+  const double z = (x - m) / sd;
+  return -0.5 * z * z - log(sd) - 0.91893853320467274178032973640562;
+}
+__device__ __forceinline__ double score_bernoulli_d(bool v, double p) { return v ? log(p) : log1p(-p); }
+__device__ __forceinline__ double score_poisson_d(int k, double lam) {
+  return k < 0 ? neg_inf_d_() : (k == 0 ? 0.0 : k * log(lam)) - lam - lgamma(k + 1.0);
+}
+__device__ __forceinline__ double score_uniform_discrete_d(int k, int a, int b) {
+  return (k >= a && k < b) ? -log(static_cast<double>(b - a)) : neg_inf_d_();
+}
+__device__ __forceinline__ double score_uniform_continuous_d(double x, double a, double b) {
+  return (x >= a && x <= b) ? -log(b - a) : neg_inf_d_();
+}
+__device__ __forceinline__ double score_beta_d(double x, double a, double b) {
+  return (x >= 0.0 && x <= 1.0)
+             ? (a - 1.0) * log(x) + (b - 1.0) * log1p(-x) - (lgamma(a) + lgamma(b) - lgamma(a + b))
+             : neg_inf_d_();
+}
+__device__ __forceinline__ double score_exponential_d(double x, double r) {
+  return x >= 0.0 ? log(r) - r * x : neg_inf_d_();
+}
+__device__ __forceinline__ double score_categorical_d(int k, int n, double wk, double tot) {
+  return (k >= 0 && k < n && wk > 0.0) ? log(wk / tot) : neg_inf_d_();
+}
+#define to_f to_d
+#define score_normal score_normal_d
+#define score_bernoulli score_bernoulli_d
+#define score_poisson score_poisson_d
+#define score_uniform_discrete score_uniform_discrete_d
+#define score_uniform_continuous score_uniform_continuous_d
+#define score_beta score_beta_d
+#define score_exponential score_exponential_d
+#define score_categorical score_categorical_d
 #endif
 
 }  // namespace cuppl

@@ -288,11 +288,25 @@ def _is_literal(code: str) -> bool:
         return code in ("true", "false")
 
 
+# Real arithmetic of the model being compiled: fp32 (importance / mcmc kernels)
+# or fp64 (enumerate: path probabilities are exact to ~1e-15, SPEC.md:438 asks 1e-12); set by
+# compile_parsed for the duration of one compilation.
+_F64 = False
+_COMPILE_LOCK = __import__("threading").Lock()
+
+
+def _fconst(x: float) -> str:
+    """A real constant folded at compile time, in the model's real type."""
+    return repr(float(x)) if _F64 else repr(float(np.float32(x))) + "f"
+
+
 def _lit(v) -> S:
     if isinstance(v, bool):
         return S("true" if v else "false", "bool")
     if isinstance(v, int):
         return S(str(v), "int", finite=True)
+    if _F64:
+        return S(repr(float(v)), "real", finite=math.isfinite(v))
     f = float(np.float32(v))
     return S(repr(f) + "f", "real", finite=math.isfinite(f))
 
@@ -331,8 +345,9 @@ class _Compiler:
         if len(self.g.data) % 2:  # even offsets: pairs of elements load as one f32x2
             self.g.data.append(0.0)
         off = len(self.g.data)
-        self.g.data.extend(np.float32(arr).tolist())
-        return DataVec(off, len(arr), bool(np.isfinite(np.float32(arr)).all()))
+        vals = arr if _F64 else np.float32(arr)
+        self.g.data.extend(vals.tolist())
+        return DataVec(off, len(arr), bool(np.isfinite(vals).all()))
 
     def top(self):
         for name, e in self.prog.bindings:
@@ -715,7 +730,7 @@ class _Compiler:
             g.bounds[v] = hi - 1
             g.emit("{ const unsigned dg = static_cast<unsigned>(rem % ENUM_R); rem /= ENUM_R; ++nd;")
             g.emit(f"  if (dg >= {hi - lo}u) dead = true;")
-            g.emit(f"  lw += {repr(float(np.float32(-math.log(hi - lo))))}f;")
+            g.emit(f"  lw += {_fconst(-math.log(hi - lo))};")
             g.emit(f"  chosen_i = {lo} + static_cast<int>(dg); }}")
             g.emit(f"const int {v} = chosen_i;")
             return S(v, "int", False)
@@ -747,8 +762,8 @@ class _Compiler:
                 sdv = float(sd.code.rstrip("f"))
                 if not sdv > 0:
                     raise CompileError("normal(mean, sd): sd must be > 0")
-                inv = repr(float(np.float32(1.0 / sdv))) + "f"
-                c = repr(float(np.float32(-math.log(sdv) - 0.5 * math.log(2 * math.pi)))) + "f"
+                inv = _fconst(1.0 / sdv)
+                c = _fconst(-math.log(sdv) - 0.5 * math.log(2 * math.pi))
                 z = self.g.fresh("z")
                 self.g.emit(f"const auto {z} = ({_real(v)} - {_real(a[0])}) * {inv};")
                 return f"fmaf(-0.5f * {z}, {z}, {c})"
@@ -902,15 +917,17 @@ class _Compiler:
         g.assign(acc, f"fmaf({z}, {z}, {acc})")
         for _ in range(depth):
             g.close()
-        k = repr(float(np.float32(-0.5 / (sdv * sdv)))) + "f"
-        c = repr(float(np.float32(-math.log(sdv) - 0.5 * math.log(2 * math.pi)))) + "f"
+        k = _fconst(-0.5 / (sdv * sdv))
+        c = _fconst(-math.log(sdv) - 0.5 * math.log(2 * math.pi))
         return S(f"({_real(init)} + fmaf({k}, {acc}, to_f({n.code}) * {c}))", "real", False)
 
     def _gaussian_reduce_packed(self, f: Fn, body, v, n: int, init: S, sdv: float):
         """The Gaussian-likelihood reduce over pairs of elements: elements (i, i + 1) of the
         data as one f32x2, the particle's scalars broadcast, so each FFMA2 / FADD2 covers two
         data points (the hand-written kernels pack two particles instead). None if some
-        operation has no packed form."""
+        operation has no packed form (or the model computes in fp64)."""
+        if _F64:
+            return None
         sb = self._sandbox()
         try:  # dry run: every operation of m and y must have a packed form
             envp = dict(f.env)
@@ -946,9 +963,9 @@ class _Compiler:
             z = g.fresh("z")
             g.emit(f"const auto {z} = {_real(y)} - {_real(m)};")
             g.emit(f"{tot} = fmaf({z}, {z}, {tot});")
-        k = repr(float(np.float32(-0.5 / (sdv * sdv)))) + "f"
-        c = repr(float(np.float32(-math.log(sdv) - 0.5 * math.log(2 * math.pi)))) + "f"
-        return S(f"({_real(init)} + fmaf({k}, {tot}, {float(n)}f * {c}))", "real", False)
+        k = _fconst(-0.5 / (sdv * sdv))
+        c = _fconst(-math.log(sdv) - 0.5 * math.log(2 * math.pi))
+        return S(f"({_real(init)} + fmaf({k}, {tot}, {_fconst(n)} * {c}))", "real", False)
 
     def _loop(self, i: str, n: S, bound, start: int = 0):
         """Open `for i < n`: small known bounds are unrolled with a guard (static indices keep
@@ -1102,6 +1119,7 @@ class CompiledModel:
     engine: str = "importance"
     radix: int = 1
     masked: bool = False  # particle-dependent control flow (lane builds are opt-in)
+    f64: bool = False  # fp64 model arithmetic and record (enumerate)
     bin_lo: int = 0  # histogram bin k holds the integer return value bin_lo + k
     kind: str = "dsl"
     _fn: object = field(default=None, repr=False)
@@ -1109,17 +1127,19 @@ class CompiledModel:
 
 _KERNEL = r'''
 #define MAXD {maxd}
+{f64_define}
 #include "dsl_lanes.cuh"
 #include "is_accum.cuh"
 using namespace cuppl;
+{f64_prelude}
 {data_decl}
 // LANES particles per thread (dsl_lanes.cuh): particle (base + p * 256 + threadIdx.x) is lane p
 extern "C" __global__ void __launch_bounds__(256)
 cuppl_dsl_model(const float* __restrict__ D, unsigned long long pid_begin, unsigned long long n,
                 unsigned int k0, unsigned int k1, cuppl_is_record* block_recs, unsigned int* counter,
-                cuppl_is_record* rec_out, float* lw_out, float* draws_out, float* ret_out,
+                cuppl_is_record* rec_out, {real_t}* lw_out, float* draws_out, float* ret_out,
                 unsigned int* err_out) {{
-  ThreadAcc<{ns}, {nb}> acc;
+  {acc_t}<{ns}, {nb}> acc;
   acc.init();
   const PhiloxKey key{{k0, k1}};
   unsigned int err = 0u;
@@ -1147,8 +1167,8 @@ cuppl_dsl_model(const float* __restrict__ D, unsigned long long pid_begin, unsig
     for (int p_ = 0; p_ < LANES; ++p_) {{
       const unsigned long long idx_ = lane_at(idx, p_);
       if (lane_at(valid, p_)) {{
-        const float lw_ = lane_at(lw, p_);
-        float f[{ns_arr}] = {{{stats}}};
+        const {real_t} lw_ = lane_at(lw, p_);
+        {real_t} f[{ns_arr}] = {{{stats}}};
         acc.add(lw_, pid_begin + idx_, f, lane_at({bin}, p_));
         if (lw_out) lw_out[idx_] = lw_;
         if (ret_out) {{
@@ -1289,6 +1309,18 @@ def compile_program(source: str, data: dict | None = None, max_depth: int = 20) 
 
 def compile_parsed(prog, source: str, data: dict | None = None, max_depth: int = 20) -> CompiledModel:
     """compile_program of an already parsed lang.Program."""
+    global _F64
+    res = prog.result
+    f64 = isinstance(res, lang.Call) and isinstance(res.fn, lang.Var) and res.fn.name == "enumerate"
+    with _COMPILE_LOCK:
+        _F64 = f64
+        try:
+            return _compile_parsed(prog, source, data, max_depth)
+        finally:
+            _F64 = False
+
+
+def _compile_parsed(prog, source: str, data: dict | None, max_depth: int) -> CompiledModel:
     comp = _Compiler(prog, data, max_depth)
     ret = comp.compile()
     g = comp.g
@@ -1298,10 +1330,13 @@ def compile_parsed(prog, source: str, data: dict | None = None, max_depth: int =
     lane_stats = [f"lane_at({x}, p_)" for x in stats]
     maxd = g.draw_bound if 0 < g.draw_bound <= MAX_TRACE_DRAWS else 1
     body = "\n".join("  " + line for line in g.lines)
-    data_arr = np.asarray(g.data if g.data else [0.0], dtype=np.float32)
+    data_arr = np.asarray(g.data if g.data else [0.0], dtype=np.float64 if _F64 else np.float32)
+    rt = "double" if _F64 else "float"
+    if _F64 and len(data_arr) > MAX_CONST_DATA // 2:
+        raise CompileError(f"enumerate programs hold up to {MAX_CONST_DATA // 2} data values (fp64 constant bank)")
     if len(data_arr) <= MAX_CONST_DATA:  # warp-uniform indices: constant-cache broadcasts
-        data_decl = (f"__constant__ __align__(8) float DC[{len(data_arr)}];\n"
-                     "__device__ __forceinline__ float dat(int i) { return DC[i]; }\n"
+        data_decl = (f"__constant__ __align__(8) {rt} DC[{len(data_arr)}];\n"
+                     f"__device__ __forceinline__ {rt} dat(int i) {{ return DC[i]; }}\n"
                      "CUPPL_LIFT(dat)  // a per-particle index: one constant-bank read per lane\n"
                      f"#define {DATA_SYM}(i) dat(i)\n"
                      f"#define {DATA_SYM}2(i) (*reinterpret_cast<const f32x2*>(&DC[i]))")
@@ -1317,7 +1352,7 @@ def compile_parsed(prog, source: str, data: dict | None = None, max_depth: int =
                      "    bool dead = false, chosen = false;\n    int chosen_i = 0;\n    (void)chosen; (void)chosen_i;")
         # a path that made nd < MAXD choices stands for R^(MAXD - nd) indices: divide them out
         enum_final = (f"    if (dead) lw = neg_inf_f();\n"
-                      f"    lw -= static_cast<float>(MAXD - nd) * {repr(float(np.float32(math.log(radix))))}f;")
+                      f"    lw -= static_cast<double>(MAXD - nd) * {repr(math.log(radix))};")
     if comp.engine == "mcmc":
         if g.draw_bound > 64:
             raise CompileError("mcmc supports up to 64 sample calls per execution")
@@ -1329,7 +1364,15 @@ def compile_parsed(prog, source: str, data: dict | None = None, max_depth: int =
                              stat_names=names, return_kind=kind, return_width=width,
                              max_draws=g.draw_bound, default_n=comp.default_n, engine="mcmc",
                              bin_lo=bin_lo)
+    f64_define = "#define CUPPL_F64 1" if _F64 else ""
+    # fp64 models: the body's float math names resolve to the double functions (dsl_lanes.cuh
+    # CUPPL_F64 keeps VF = double and the score functions' fp64 forms)
+    f64_prelude = ("#define expf exp\n#define logf log\n#define log1pf log1p\n#define sqrtf sqrt\n"
+                   "#define fabsf fabs\n#define floorf floor\n#define fmodf fmod\n#define powf pow\n"
+                   "#define fmaf fma\n#define fminf fmin\n#define fmaxf fmax") if _F64 else ""
     cuda = _KERNEL.format(maxd=maxd, data_decl=data_decl, enum_init=enum_init, enum_final=enum_final,
+                          f64_define=f64_define, f64_prelude=f64_prelude,
+                          acc_t="ThreadAccF64" if _F64 else "ThreadAcc", real_t=rt,
                           ns=len(stats), nb=nb, ns_arr=max(len(stats), 1),
                           stats=", ".join(lane_stats) if stats else "0.f", bin=bin_expr, tag=TAG_DSL,
                           body=body, ret_store="\n".join(f"          ret_out[idx_ * {width} + {k}] = lane_at({x}, p_);"
@@ -1337,7 +1380,8 @@ def compile_parsed(prog, source: str, data: dict | None = None, max_depth: int =
     return CompiledModel(source=source, cuda=cuda, data=data_arr, n_stats=len(stats), n_bins=nb,
                          stat_names=names, return_kind=kind, return_width=width,
                          max_draws=g.draw_bound, default_n=comp.default_n, engine=comp.engine,
-                         radix=max(comp.radix, 2) if comp.engine == "enumerate" else 1, masked=g.masked)
+                         radix=max(comp.radix, 2) if comp.engine == "enumerate" else 1, masked=g.masked,
+                         f64=_F64)
 
 
 # ----------------------------------------------------------------------------- JIT -------
@@ -1417,7 +1461,7 @@ def _function(model: CompiledModel):
                 cu.cuModuleUnload(mod)
                 continue
             break
-        if " float DC[" in model.cuda:  # the data live in this module's constant bank
+        if " float DC[" in model.cuda or " double DC[" in model.cuda:  # data in the module's constant bank
             err, dptr, size = cu.cuModuleGetGlobal(mod, b"DC")
             if err != cu.CUresult.CUDA_SUCCESS or size != model.data.nbytes:
                 raise InferRuntimeError(f"cuModuleGetGlobal(DC) failed: {err}")
@@ -1557,7 +1601,7 @@ def _full_int_support(model: CompiledModel, n: int, launcher: DslLauncher, key: 
 
     if n > 1 << 30 or _world(None)[1] > 1:
         return None
-    lw = torch.empty(n, dtype=torch.float32, device=launcher.device)
+    lw = torch.empty(n, dtype=torch.float64 if model.f64 else torch.float32, device=launcher.device)
     ret = torch.empty(n, dtype=torch.float32, device=launcher.device)
     rec = torch.empty_like(launcher.rec)
     launcher.launch(0, n, key, lw_out=lw, ret_out=ret, rec_out=rec)

@@ -430,8 +430,8 @@ def test_enumeration_compile_and_reject():
 @pytest.mark.gpu
 @pytest.mark.parametrize("src", [ENUM_TWO, ENUM_BINOMIAL, CAT_ENUM], ids=["two-choice", "binomial", "categorical"])
 def test_gpu_enumeration_matches_forced_choice_oracle(cuda, src):
-    """enumeration equals the brute-force forced-choice evaluation (fp32 device
-    arithmetic: 1e-6 per probability instead of the fp64 reference's 1e-12)."""
+    """enumeration equals the brute-force forced-choice evaluation to 1e-12 per
+    probability (the enumeration kernels compute paths and records in fp64)."""
     from oracle.dsl_eval import Enumerator
     from paper_2010_08454_b200 import infer
 
@@ -440,8 +440,8 @@ def test_gpu_enumeration_matches_forced_choice_oracle(cuda, src):
     got = dict(post.support)
     assert set(got) == set(ref)
     for k, p in ref.items():
-        assert abs(got[k] - p) < 1e-6, (k, got[k], p)
-    assert abs(post.log_z - log_z) < 1e-5
+        assert abs(got[k] - p) < 1e-12, (k, got[k], p)  # SPEC.md:438 (fp64 enumeration)
+    assert abs(post.log_z - log_z) < 1e-12
 
 
 def test_categorical_compile_checks():
@@ -521,7 +521,7 @@ def test_gpu_enumeration_spec_example(cuda):
     post = infer.run_enumeration(frontend.compile_program(
         "model <- function() { sample(bernoulli(0.3)) }; enumerate(model, 100)"))
     got = dict(post.support)
-    assert abs(got[True] - 0.3) < 1e-7 and abs(got[False] - 0.7) < 1e-7
+    assert abs(got[True] - 0.3) < 1e-14 and abs(got[False] - 0.7) < 1e-14
 
 
 @pytest.mark.gpu

@@ -74,8 +74,8 @@ def test_gpu_fuzz_enumeration_matches_forced_choice_oracle(cuda, seed):
     got = dict(post.support)
     assert set(got) == {k for k, p in ref.items() if p > 0}, (seed, src)
     for k, p in ref.items():
-        assert abs(got.get(k, 0.0) - p) < 1e-5, (seed, k, got.get(k), p, src)
-    assert abs(post.log_z - log_z) < 1e-4, (seed, post.log_z, log_z)
+        assert abs(got.get(k, 0.0) - p) < 1e-12, (seed, k, got.get(k), p, src)
+    assert abs(post.log_z - log_z) < 1e-10 * max(1.0, abs(log_z)), (seed, post.log_z, log_z)
 
 
 @pytest.mark.gpu
