@@ -78,6 +78,15 @@ double or_u01_open0(uint32_t w) { return 2.0 - (double)bits_f(0x3F800000u | (w >
 double or_u01_closed0(uint32_t w) { return (double)bits_f(0x3F800000u | (w >> 9)) - 1.0; }
 
 /* Lemire multiply-shift with exact rejection; returns 0 if w must be rejected */
+/* the same on a b-bit word v < 2^b */
+int or_lemire_bits(uint32_t v, uint32_t range, int bits, uint32_t* out) {
+  const uint32_t m = v * range, mask = (1u << bits) - 1u;
+  *out = m >> bits;
+  const uint32_t lo = m & mask;
+  if (lo < range) return lo >= ((1u << bits) % range);
+  return 1;
+}
+
 int or_lemire(uint32_t w, uint32_t range, uint32_t* out) {
   const uint64_t m = (uint64_t)w * range;
   const uint32_t lo = (uint32_t)m;
@@ -89,8 +98,12 @@ int or_lemire(uint32_t w, uint32_t range, uint32_t* out) {
   return 1;
 }
 
+/* u1 in (0, 1] from all 32 bits of wa: (wa + 1) 2^-32 (normals up to 6.66 sd); u2 in [0, 1)
+ * from the top 23 bits of wb */
+double or_u01_open0_32(uint32_t w) { return ((double)w + 1.0) * (1.0 / 4294967296.0); }
+
 void or_box_muller(uint32_t wa, uint32_t wb, double* z0, double* z1) {
-  const double u1 = or_u01_open0(wa), u2 = or_u01_closed0(wb);
+  const double u1 = or_u01_open0_32(wa), u2 = or_u01_closed0(wb);
   const double r = sqrt(-2.0 * log(u1));
   const double th = 2.0 * M_PI * u2;
   *z0 = r * cos(th);
@@ -164,17 +177,18 @@ void or_rec_merge(or_record* a, const or_record* b) {
 
 /* ---------------------------------------------------------------- Fig.1 polynomial ---- */
 /* One Philox block per particle (csrc/is_kernels.cu poly_draw): (c0, c1) = 10 BM(w0, w1),
- * (c2, c3) = 10 BM(w2, w3) (normal(0, 10), D2); n ~ uniform-discrete(2,5) (support [2,5), D1)
- * by Lemire on u = w0[8:0] | w1[8:0] << 9 | w2[8:0] << 18 | w3[4:0] << 27 (the bits the 23-bit
- * Box-Muller uniforms do not use); a rejected u is redrawn from word 0 of blocks 1, 2, ... */
+ * (c2, c3) = 10 BM(w2, w3) (normal(0, 10), D2; radius uniforms from all 32 bits of w0 / w2,
+ * angles from the top 23 bits of w1 / w3); n ~ uniform-discrete(2,5) (support [2,5), D1) by
+ * Lemire on the 18-bit v = w1[8:0] | w3[8:0] << 9 (the bits the angle uniforms do not use); a
+ * rejected v is redrawn from word 0 of blocks 1, 2, ... (32-bit Lemire) */
 uint32_t or_poly_degree_word(const uint32_t w[4]) {
-  return (w[0] & 0x1FFu) | ((w[1] & 0x1FFu) << 9) | ((w[2] & 0x1FFu) << 18) | ((w[3] & 0x1Fu) << 27);
+  return (w[1] & 0x1FFu) | ((w[3] & 0x1FFu) << 9);
 }
 
 void or_poly_draw(uint64_t key, uint64_t pid, int* n, double c[4]) {
   uint32_t b0[4], k;
   block_of(key, pid, 0, TAG_IS, b0);
-  if (!or_lemire(or_poly_degree_word(b0), 3u, &k)) {
+  if (!or_lemire_bits(or_poly_degree_word(b0), 3u, 18, &k)) {
     for (uint32_t blk = 1;; ++blk) {
       uint32_t bb[4];
       block_of(key, pid, blk, TAG_IS, bb);
@@ -345,21 +359,33 @@ static uint32_t ws_next(wstream* s) {
   }
   return s->buf[s->pos++];
 }
-static double ws_uniform(wstream* s) { return or_u01_closed0(ws_next(s)); }
-static double ws_uniform_pos(wstream* s) { return or_u01_open0(ws_next(s)); }
+/* the reference's u64 generator (rng.py:39-41): two consecutive Philox words, first word high,
+ * and its algorithms verbatim on that stream (rng.py:43-71) */
+static uint64_t ws_next_u64(wstream* s) {
+  const uint64_t hi = ws_next(s);
+  return (hi << 32) | ws_next(s);
+}
+static double ws_uniform(wstream* s) { return (double)(ws_next_u64(s) >> 11) * (1.0 / 9007199254740992.0); }
+static double ws_uniform_pos(wstream* s) {
+  double u;
+  do { u = ws_uniform(s); } while (!(u > 0.0));
+  return u;
+}
 static double ws_normal(wstream* s) {
   if (s->has_spare) { s->has_spare = 0; return s->spare; }
-  const uint32_t wa = ws_next(s), wb = ws_next(s);
-  double z0, z1;
-  or_box_muller(wa, wb, &z0, &z1);
-  s->spare = z1;
+  const double u1 = ws_uniform_pos(s);
+  const double u2 = ws_uniform(s);
+  const double r = sqrt(-2.0 * log(u1));
+  s->spare = r * sin(2.0 * M_PI * u2);
   s->has_spare = 1;
-  return z0;
+  return r * cos(2.0 * M_PI * u2);
 }
 static uint32_t ws_randint(wstream* s, uint32_t range) {
-  uint32_t k;
-  while (!or_lemire(ws_next(s), range, &k)) {}
-  return k;
+  const uint64_t n = range, limit = UINT64_MAX - (UINT64_MAX % n);
+  for (;;) {
+    const uint64_t r = ws_next_u64(s);
+    if (r < limit) return (uint32_t)(r % n);
+  }
 }
 static double ws_gamma(wstream* s, double shape) {
   double boost = 1.0;

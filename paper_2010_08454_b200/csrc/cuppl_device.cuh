@@ -92,6 +92,17 @@ __device__ __forceinline__ float u01_closed0(uint32_t w) {  // [0, 1)
   return __uint_as_float(0x3F800000u | (w >> 9)) - 1.0f;
 }
 
+// Lemire's multiply-shift on a b-bit word v < 2^b (range * 2^b < 2^32): exact uniform integer
+// in [0, range); false when v must be rejected.
+__device__ __forceinline__ bool lemire_bits(uint32_t v, uint32_t range, int bits, uint32_t* out) {
+  const uint32_t m = v * range;
+  const uint32_t mask = (1u << bits) - 1u;
+  *out = m >> bits;
+  const uint32_t lo = m & mask;
+  if (lo < range) return lo >= ((1u << bits) % range);
+  return true;
+}
+
 // Lemire's multiply-shift: uniform integer in [0, range) for range >= 1. Returns false when
 // the word must be rejected for exact uniformity (cuppl/rng.py:47-56 rejects too).
 __device__ __forceinline__ bool lemire(uint32_t w, uint32_t range, uint32_t* out) {
@@ -137,13 +148,20 @@ constexpr float kTwoPi = 6.28318530717958647692f;
 constexpr float kPi = 3.14159265358979323846f;
 constexpr float kHalfLog2Pi = 0.91893853320467274178f;
 
+// u1 in (0, 1] from all 32 bits of a word: (w + 1) 2^-32 (the I2F rounds w above 2^24 to 24
+// bits; the tail region u1 -> 0 is exact). A 32-bit u1 caps Box-Muller normals at
+// sqrt(64 ln 2) = 6.66 sd (a 23-bit one would cap them at 5.65 sd).
+__device__ __forceinline__ float u01_open0_32(uint32_t w) {
+  return fmaf(__uint2float_rn(w), 0x1p-32f, 0x1p-32f);
+}
+
 // Box-Muller pair (cuppl/rng.py:58-71 without the cached spare: both normals are used).
-// u1 in (0,1] from wa, u2 in [0,1) from wb; r = sqrt(-2 ln u1); (r cos 2pi u2, r sin 2pi u2).
-// The angle is taken as 2pi u2 - pi in [-pi, pi) — sin.approx / cos.approx meet their 2^-20.5
-// absolute-error bound only there (2pi u2 up to 2pi measured ~1.6e-5) — and the signs flipped:
-// cos(t + pi) = -cos t, sin(t + pi) = -sin t.
+// u1 = u01_open0_32(wa); u2 in [0,1) from the top 23 bits of wb; r = sqrt(-2 ln u1);
+// (r cos 2pi u2, r sin 2pi u2). The angle is taken as 2pi u2 - pi in [-pi, pi) — sin.approx /
+// cos.approx meet their 2^-20.5 absolute-error bound only there (2pi u2 up to 2pi measured
+// ~1.6e-5) — and the signs flipped: cos(t + pi) = -cos t, sin(t + pi) = -sin t.
 __device__ __forceinline__ float2 box_muller(uint32_t wa, uint32_t wb) {
-  const float u1 = u01_open0(wa);
+  const float u1 = u01_open0_32(wa);
   const float u2 = u01_closed0(wb);
   const float r = fast_sqrt(-2.0f * kLn2 * fast_lg2(u1));
   const float th = fmaf(kTwoPi, u2, -kPi);
@@ -156,7 +174,7 @@ __device__ __forceinline__ float2 box_muller(uint32_t wa, uint32_t wb) {
 // range; no u2 = f - 1 subtraction). Two FMA-pipe instructions fewer per normal than
 // sd * box_muller(); the values agree to fp32 rounding (~1e-6 relative).
 __device__ __forceinline__ float2 box_muller_sd(uint32_t wa, uint32_t wb, float neg2_sd2_ln2) {
-  const float u1 = u01_open0(wa);
+  const float u1 = u01_open0_32(wa);
   const float f = __uint_as_float(0x3F800000u | (wb >> 9));
   const float r = fast_sqrt(neg2_sd2_ln2 * fast_lg2(u1));
   const float th = fmaf(kTwoPi, f, -3.0f * kPi);

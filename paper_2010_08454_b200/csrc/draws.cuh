@@ -3,7 +3,14 @@
 //
 // A WordStream replays the reference draw algorithms (pkg/src/cuppl/rng.py:43-117) on the
 // Philox words of blocks (id, 0..), tag: one stream per particle plays the role of
-// Rng.split(i) (rng.py:31-37), and successive sample sites consume it in program order.
+// Rng.split(i) (rng.py:31-37), and successive sample sites consume it in program order. The
+// reference's generator yields u64 words (rng.py:39-41); here next_u64() is two consecutive
+// Philox words (first word high), and every algorithm is the reference's on that u64 stream:
+// uniform = (x >> 11) 2^-53 (rng.py:43-45), randint = rejection below MASK - MASK % n then
+// x % n (rng.py:47-56), normal = Box-Muller with u1 redrawn while 0 and the cached spare
+// (rng.py:58-71), exponential / gamma / beta / poisson as rng.py:73-117. The integer decisions
+// are exact; the real-valued transforms run in fp32 (the oracle restates them in fp64 and
+// equals oracle/refstream.Algorithms bit for bit on the same u64 stream, tests/test_oracle.py).
 #pragma once
 #include "cuppl_device.cuh"
 
@@ -40,25 +47,40 @@ struct WordStream {
     ++pos;
     return w;
   }
-  __device__ __forceinline__ float uniform() { return u01_closed0(next()); }
-  __device__ __forceinline__ float uniform_pos() { return u01_open0(next()); }
-  __device__ __forceinline__ float normal() {
+  __device__ __forceinline__ unsigned long long next_u64() {
+    const unsigned long long hi = next();
+    return (hi << 32) | next();
+  }
+  // (x >> 11) 2^-53, rounded toward zero to fp32: in [0, 1) like the reference's double
+  __device__ __forceinline__ float uniform() { return __ull2float_rz(next_u64() >> 11) * 0x1p-53f; }
+  // the reference's `while u <= 0: u = uniform()` (rng.py:73-77, 79-85): in (0, 1)
+  __device__ __forceinline__ float uniform_pos() {
+    unsigned long long m;
+    do {
+      m = next_u64() >> 11;
+    } while (m == 0ull);
+    return __ull2float_rz(m) * 0x1p-53f;
+  }
+  __device__ __forceinline__ float normal() {  // rng.py:58-71
     if (has_spare) {
       has_spare = false;
       return spare;
     }
-    const uint32_t wa = next();
-    const uint32_t wb = next();
-    const float2 z = box_muller(wa, wb);
-    spare = z.y;
+    const float u1 = uniform_pos();
+    const float u2 = uniform();
+    const float r = fast_sqrt(-2.0f * kLn2 * fast_lg2(u1));
+    const float th = fmaf(kTwoPi, u2, -kPi);  // 2 pi u2 - pi in [-pi, pi): signs flipped below
+    spare = -r * fast_sin(th);
     has_spare = true;
-    return z.x;
+    return -r * fast_cos(th);
   }
-  __device__ __forceinline__ uint32_t randint(uint32_t range) {
-    uint32_t k;
-    while (!lemire(next(), range, &k)) {
+  __device__ __forceinline__ uint32_t randint(uint32_t range) {  // rng.py:47-56
+    const unsigned long long n = range;
+    const unsigned long long limit = ~0ull - (~0ull % n);
+    for (;;) {
+      const unsigned long long r = next_u64();
+      if (r < limit) return static_cast<uint32_t>(r % n);
     }
-    return k;
   }
   // Marsaglia-Tsang (cuppl/rng.py:79-98); accurate logf for the acceptance test.
   __device__ float gamma(float shape) {

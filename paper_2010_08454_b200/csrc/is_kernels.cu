@@ -161,19 +161,20 @@ is_linreg_kernel(const __grid_constant__ LinregParams<CAP> prm) {
 }
 
 // ------------------------------------------------------------------ Fig.1 polynomial ----
-// One Philox block per particle: (c0, c1) = 10 BM(w0, w1), (c2, c3) = 10 BM(w2, w3); the
-// Box-Muller uniforms use the top 23 bits of each word, and n ~ uniform-discrete(2,5) (D1)
-// uses the otherwise unused low bits: u = w0[8:0] | w1[8:0] << 9 | w2[8:0] << 18 |
-// w3[4:0] << 27, Lemire on 3; a rejected u (u == 0) is redrawn from word 0 of blocks 1, 2, ...
-// c_j = 0 for j >= n (exact: Horner with zero leading terms). lw = -sum_i (y_i - p(x_i))^2 (D3).
+// One Philox block per particle: (c0, c1) = 10 BM(w0, w1), (c2, c3) = 10 BM(w2, w3); each
+// Box-Muller pair takes its radius uniform from all 32 bits of w0 / w2 and its angle from the
+// top 23 bits of w1 / w3, and n ~ uniform-discrete(2,5) (D1) uses the angle words' otherwise
+// unused low bits: v = w1[8:0] | w3[8:0] << 9, Lemire on 18 bits; a rejected v (3 / 2^18) is
+// redrawn from word 0 of blocks 1, 2, ... (32-bit Lemire). c_j = 0 for j >= n (exact: Horner
+// with zero leading terms). lw = -sum_i (y_i - p(x_i))^2 (D3).
 __device__ __forceinline__ uint32_t poly_degree_word(uint4 w) {
-  return (w.x & 0x1FFu) | ((w.y & 0x1FFu) << 9) | ((w.z & 0x1FFu) << 18) | ((w.w & 0x1Fu) << 27);
+  return (w.y & 0x1FFu) | ((w.w & 0x1FFu) << 9);
 }
 
 __device__ __forceinline__ void poly_draw(const uint32_t (&ks)[20], uint64_t pid, int& n, float c[4]) {
   const uint4 w = draw_block_ks(ks, pid, 0u, CUPPL_TAG_IS);
   uint32_t k;
-  if (!lemire(poly_degree_word(w), 3u, &k)) {
+  if (!lemire_bits(poly_degree_word(w), 3u, 18, &k)) {
     for (uint32_t blk = 1;; ++blk) {
       if (lemire(draw_block_ks(ks, pid, blk, CUPPL_TAG_IS).x, 3u, &k)) break;
     }

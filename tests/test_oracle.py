@@ -96,6 +96,59 @@ def test_refstream_algorithms_match_reference():
         assert [s.exponential(2.0) for _ in range(3)] == rec["exponential_2"]
 
 
+class _PhiloxU64Stream(refstream.Algorithms):
+    """The reference's draw algorithms (refstream.Algorithms, pinned to the reference's own
+    outputs above) on the GPU's word stream: u64 = two consecutive Philox words of blocks
+    (id, 0..), tag, first word high (csrc/draws.cuh WordStream::next_u64)."""
+
+    def __init__(self, key, pid, tag):
+        super().__init__()
+        self.key, self.pid, self.tag, self.blk, self.buf = key, pid, tag, 0, []
+
+    def _next32(self):
+        from oracle import core
+
+        if not self.buf:
+            self.buf = [int(w) for w in core.philox_blocks(self.key, self.pid, self.blk, self.tag, 1)[0]]
+            self.blk += 1
+        return self.buf.pop(0)
+
+    def next_u64(self):
+        hi = self._next32()
+        return (hi << 32) | self._next32()
+
+
+@pytest.mark.parametrize("kind,p0,p1", [("normal", 1.5, 2.0), ("bernoulli", 0.3, 0.0), ("poisson", 3.5, 0.0),
+                                        ("poisson", 75.0, 0.0), ("uniform-discrete", -3, 7),
+                                        ("uniform-continuous", -1.0, 2.0), ("beta", 0.5, 2.5), ("beta", 2.0, 3.0),
+                                        ("exponential", 1.7, 0.0)])
+def test_word_stream_oracle_is_the_reference_algorithm(oracle_lib, kind, p0, p1):
+    """The C oracle's word-stream draws (or_dist_sample, restated by csrc/draws.cuh on the GPU)
+    equal the reference algorithms run on the same u64 stream, bit for bit (fp64)."""
+    tags = {"normal": 0, "bernoulli": 1, "poisson": 2, "uniform-discrete": 3, "uniform-continuous": 4,
+            "beta": 5, "exponential": 6}
+    key, tag, n = refstream.key_of(3), 7, 300
+    got = oracle_lib.dist_sample(tags[kind], p0, p1, key, tag, 0, n)
+    want = []
+    for i in range(n):
+        a = _PhiloxU64Stream(key, i, tag)
+        if kind == "normal":
+            want.append(a.normal(p0, p1))
+        elif kind == "bernoulli":
+            want.append(1 if a.uniform() < p0 else 0)
+        elif kind == "poisson":
+            want.append(a.poisson(p0))
+        elif kind == "uniform-discrete":
+            want.append(p0 + a.randint(p1 - p0))
+        elif kind == "uniform-continuous":
+            want.append(p0 + (p1 - p0) * a.uniform())
+        elif kind == "beta":
+            want.append(a.beta(p0, p1))
+        else:
+            want.append(a.exponential(p0))
+    assert [float(x) for x in got] == [float(x) for x in want]
+
+
 def test_value_key_matches_reference():
     from paper_2010_08454_b200 import values
 

@@ -1,6 +1,7 @@
 """Small runs of the paths smoke() does not cover, for compute-sanitizer: SMC graph replay and
-snapshot/restore, compiled categorical / enumeration (recursive) / LMH programs, masked lanes,
-the full-support second pass."""
+snapshot/restore, compiled categorical / enumeration (recursive, fp64) / LMH programs, masked
+lanes, the full-support second pass, the generic resampler (every payload path, partial tiles),
+programs over engine results, importance sampling with device-memory data."""
 import os
 import sys
 from pathlib import Path
@@ -36,6 +37,21 @@ def main():
     os.environ["CUPPL_DSL_LANES"] = "8"  # masked lane form
     cm = frontend.compile_program((ex / "linefitting.cup").read_text())
     infer.run_importance(cm, 50_000, Rng(7), return_traces=True)
+    del os.environ["CUPPL_DSL_LANES"]
+    from paper_2010_08454_b200 import program, resample
+
+    g = torch.Generator(device="cuda").manual_seed(0)
+    for n in (1, 2049, 70_001):
+        lw = torch.randn(n, device="cuda", generator=g)
+        for pay in (None, torch.arange(n, dtype=torch.int32, device="cuda"),
+                    torch.randn((n, 3), device="cuda", generator=g),
+                    torch.zeros((n, 5), dtype=torch.uint8, device="cuda"),
+                    torch.randn((n, 16), device="cuda", generator=g)):
+            resample.systematic(lw, pay, Rng(8), 1, ancestors=True)
+    program.run_program("m <- function() { k <- sample(uniform-discrete(0, 3)); k }; p <- enumerate(m, 10); "
+                        "dist-var(p)", Rng(9))
+    big = models.LinearRegression.synthetic(n_points=5000)
+    infer.run_importance(big, 100_000, Rng(10))
     torch.cuda.synchronize()
     print("sanitize_extra done")
 
