@@ -331,6 +331,28 @@ __global__ void __launch_bounds__(kRsThreads, 3) rs_gather_kernel(RsArgs a) {
     const unsigned long long c0 = c_base + ex;
     const double est0 = __fma_rn(__ull2double_rn(c0), n_over_t, -cb.a_over_t);
     const unsigned int f0 = c0 == 0 ? 0u : comb_rank(est0, c0, cb);
+    // F(C_k) of my 8 sources, once per tile: fp64 estimates, then the rare exact fix-ups in one
+    // batch (no per-source branch)
+    unsigned int fr[kRsSeg];
+    {
+      uint32_t need = 0;
+      double cd = 0.0;
+#pragma unroll
+      for (int k = 0; k < kRsSeg; ++k) {
+        cd += wd[k];
+        bool ex;
+        fr[k] = comb_rank_fast(__fma_rn(cd, n_over_t, est0), &ex);
+        need |= static_cast<uint32_t>(ex) << k;
+      }
+      if (need) {
+        double cd2 = 0.0;
+#pragma unroll
+        for (int k = 0; k < kRsSeg; ++k) {
+          cd2 += wd[k];
+          if ((need >> k) & 1u) fr[k] = comb_rank_exact2(__fma_rn(cd2, n_over_t, est0), c0, cd2, cb);
+        }
+      }
+    }
 
     unsigned long long o0 = j_cur;
     while (true) {
@@ -339,11 +361,9 @@ __global__ void __launch_bounds__(kRsThreads, 3) rs_gather_kernel(RsArgs a) {
       {
         const unsigned int wb32 = static_cast<unsigned int>(wb);
         unsigned int fp = f0;
-        double cd = 0.0;
 #pragma unroll
         for (int k = 0; k < kRsSeg; ++k) {
-          cd += wd[k];
-          const unsigned int fn = comb_rank(__fma_rn(cd, n_over_t, est0), c0, cd, cb);
+          const unsigned int fn = fr[k];
           if (fp < fn && fn > wb32 && fp < wb32 + static_cast<unsigned int>(kRsWin))
             marks[(fp > wb32 ? fp : wb32) - wb32] = static_cast<uint16_t>(kRsSeg * tid + k + 1);
           fp = fn;

@@ -170,6 +170,15 @@ __device__ __forceinline__ unsigned int comb_rank(double est, unsigned long long
   if (!(frac > 0x1p-14 && frac < 1.0 - 0x1p-14)) j = comb_rank_exact(est, c, cb);
   return j;
 }
+// The fast path alone: ceil(est), and whether the exact path must decide (callers batch the rare
+// fix-ups after a loop instead of branching per source).
+__device__ __forceinline__ unsigned int comb_rank_fast(double est, bool* exact) {
+  constexpr double kMagic = 6755399441055744.0;
+  const double t = __dadd_ru(est, kMagic);
+  const double frac = __dsub_rn(__dsub_rn(t, kMagic), est);
+  *exact = !(frac > 0x1p-14 && frac < 1.0 - 0x1p-14);
+  return static_cast<unsigned int>(__double2loint(t));
+}
 __device__ __forceinline__ unsigned int comb_rank(unsigned long long c, const Comb& cb) {
   if (c == 0) return 0u;
   return comb_rank(__fma_rn(__ull2double_rn(c), cb.n_over_t, -cb.a_over_t), c, cb);
