@@ -249,6 +249,42 @@ def run_dry(args) -> dict | None:
             "max_rank_s": dt.item()}
 
 
+def python_scalar_rate(workload: str, model, seconds: float = 3.0) -> dict:
+    """SURVEY.md §8(d) CPU protocol item (i): the reference-arithmetic scalar Python rate on one
+    core — per particle the reference's keyed split stream (rng.py:31-41) and draw algorithms
+    (rng.py:43-117, restated in oracle/refstream.py) and the model's log-weight in Python floats,
+    as the reference's (absent) VM would compute it."""
+    from oracle import refstream
+
+    xs = [float(x) for x in model.xs]
+    ys = [float(y) for y in model.ys]
+    base = refstream.key_of(1)
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < seconds:
+        s = refstream.SplitMixStream(key=refstream.split_key(base, n))
+        if workload in ("linreg", "dsl-linreg"):
+            a, b = s.normal(0.0, 10.0), s.normal(0.0, 10.0)
+            lw = 0.0
+            for x, y in zip(xs, ys):
+                z = (y - (a * x + b)) / model.sigma
+                lw += -0.5 * z * z - math.log(model.sigma) - 0.5 * math.log(2 * math.pi)
+        else:
+            k = 2 + s.randint(3)
+            c = [s.normal(0.0, 10.0) for _ in range(k)]
+            lw = 0.0
+            for x, y in zip(xs, ys):
+                p = 0.0
+                for cj in reversed(c):
+                    p = p * x + cj
+                lw -= (y - p) ** 2
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{n} particles in {dt:.1f} s: scalar Python, reference arithmetic (refstream SplitMix "
+                      "streams and draw algorithms, fp64 log-weights)"}
+
+
 def cpu_baseline(workload: str, model, target_s: float = 12.0, threads: int | None = None) -> dict:
     """Oracle (C port of the reference semantics) on the host cores, bounded sample."""
     from oracle import core
@@ -268,7 +304,8 @@ def cpu_baseline(workload: str, model, target_s: float = 12.0, threads: int | No
     dt = time.perf_counter() - t0
     return {"value": n2 / dt, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{n2} particles of the same model/data in {dt:.1f} s "
-                      f"(oracle/cuppl_oracle.c, fp64, OpenMP {threads} threads)"}
+                      f"(oracle/cuppl_oracle.c, fp64, OpenMP {threads} threads)",
+            "python_scalar_1core": python_scalar_rate(workload, model)}
 
 
 def calibrate_philox(device) -> float:
