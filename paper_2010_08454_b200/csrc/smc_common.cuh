@@ -29,11 +29,13 @@ __device__ __forceinline__ float exp_repro(float d) {
   return __fmul_rn(p, __int_as_float((ki + 127) << 23));
 }
 
+// e = exp(lw - M) for lw - M >= -87, else 0 (and 0 for lw = -inf / NaN): branch-free, the
+// polynomial evaluated on the clamped difference and discarded outside the range (the same
+// values as the oracle's or_smc_e)
 __device__ __forceinline__ float smc_e(float lw, float M) {
-  if (!(lw > neg_inf_f())) return 0.0f;
   const float d = __fsub_rn(lw, M);
-  if (!(d >= -87.0f)) return 0.0f;
-  return exp_repro(d);
+  const float e = exp_repro(fmaxf(d, -87.0f));
+  return (lw > neg_inf_f() && d >= -87.0f) ? e : 0.0f;
 }
 
 __device__ __forceinline__ uint32_t smc_w(float e) {
