@@ -432,39 +432,14 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
         unsigned int fp = f0;
         double cd = 0.0;  // exact prefix of my sources (integer sums < 2^53)
         const uint16_t mark0 = static_cast<uint16_t>(kSegment * tid + 1);
-        // two halves of 8 sources: fp64 rank estimates first, the rare exact fix-ups batched
-        // after (no per-source branch or call), then the marks
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          unsigned int fr[8];
-          uint32_t need = 0;
-          const double cd_start = cd;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int kk = 8 * hh + k;
-            const uint32_t st = (xw[kk >> 2] >> (8 * (kk & 3))) & 0xFFu;
-            cd += (nv == kSegment || kk < nv) ? wdS[st] : 0.0;
-            bool ex;
-            fr[k] = comb_rank_fast(__fma_rn(cd, n_over_t, est0), &ex);
-            need |= static_cast<uint32_t>(ex) << k;
-          }
-          if (need) {
-            double c2 = cd_start;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const int kk = 8 * hh + k;
-              const uint32_t st = (xw[kk >> 2] >> (8 * (kk & 3))) & 0xFFu;
-              c2 += (nv == kSegment || kk < nv) ? wdS[st] : 0.0;
-              if ((need >> k) & 1u) fr[k] = comb_rank_exact2(__fma_rn(c2, n_over_t, est0), c0, c2, cb);
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const unsigned int fn = fr[k];
-            if (fp < fn && fn > wb32 && fp < wb32 + static_cast<unsigned int>(kWindow))
-              marks[(fp > wb32 ? fp : wb32) - wb32] = static_cast<uint16_t>(mark0 + 8 * hh + k);
-            fp = fn;
-          }
+        for (int k = 0; k < kSegment; ++k) {
+          const uint32_t st = (xw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+          cd += (nv == kSegment || k < nv) ? wdS[st] : 0.0;
+          const unsigned int fn = comb_rank(__fma_rn(cd, n_over_t, est0), c0, cd, cb);
+          if (fp < fn && fn > wb32 && fp < wb32 + static_cast<unsigned int>(kWindow))
+            marks[(fp > wb32 ? fp : wb32) - wb32] = static_cast<uint16_t>(mark0 + k);
+          fp = fn;
         }
         if (tid == kSmcThreads - 1) s_jn = fp;  // F(end of batch): first output of the next batch
       }
