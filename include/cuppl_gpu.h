@@ -312,6 +312,22 @@ CUPPL_API int cuppl_resample(const float* lw, uint64_t n, const void* payload, u
                              cuppl_resample_stats* stats_out, void* workspace, size_t workspace_bytes,
                              void* stream);
 
+/* ---------------------------------------------------------------- peer exchange -------------
+ * The multi-rank SMC filter's two per-step collectives (all-reduce MAX of the
+ * stabiliser, all-gather of the 32-byte rank records) over peer memory, in one kernel and
+ * without the host: every rank's arena (cuppl_arena_alloc, CUDA-IPC mapped by the others)
+ * holds a mailbox of `world` 64-byte slots at mbox_off and `world` u64 flags at flags_off (zero
+ * on first use); peer_bases[q] is rank q's arena base as mapped here (device array). The call
+ * writes this rank's payload (nbytes <= 64) into slot `rank` of every peer, releases flag
+ * `rank` there with the next value of *epoch (a device counter per phase), waits for every
+ * peer's flag, then writes the MAX of the int32 payloads to max_out and/or copies the world
+ * payloads to gather_out [world][nbytes]. Stream-ordered and graph-capturable (the epoch lives
+ * in device memory). A wait beyond timeout_ns sets *status to 1. Replaces the NCCL
+ * all_reduce / all_gather of a multi-process run (smc.SmcRunner(exchange="peer")). */
+CUPPL_API int cuppl_peer_exchange(const void* src, uint32_t nbytes, const uint64_t* peer_bases, uint64_t mbox_off,
+                                  uint64_t flags_off, int rank, int world, uint64_t* epoch, int32_t* max_out,
+                                  void* gather_out, uint32_t* status, uint64_t timeout_ns, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

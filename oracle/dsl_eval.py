@@ -211,6 +211,26 @@ class Enumerator(Interpreter):
             return v
         return super().call(e, env)
 
+    def posterior_bfs(self, max_executions: int):
+        """The reference's breadth-first traversal: a FIFO frontier of choice
+        prefixes, children in support order; stops after max_executions completed paths and
+        normalises over them."""
+        from collections import deque
+
+        mass, done, q = {}, 0, deque([[]])
+        while q and done < max_executions:
+            prefix = q.popleft()
+            try:
+                lw, ret = self.run_forced(prefix)
+            except _NeedChoice as need:
+                q.extend(prefix + [v] for v in need.support)
+                continue
+            key = tuple(ret) if isinstance(ret, list) else ret
+            mass[key] = mass.get(key, 0.0) + math.exp(lw)
+            done += 1
+        z = sum(mass.values())
+        return {k: v / z for k, v in mass.items()}, math.log(z)
+
     def posterior(self):
         """{return value: probability}, log evidence (fp64)."""
         mass, stack = {}, [[]]

@@ -119,6 +119,7 @@ _SIG = {
     "cuppl_smc_resample": ([_P, _U64, _U64, _U64, _U32, C.c_int, C.c_int, _F32, _F32, _P, _P, _P, _P,
                             _P, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
     "cuppl_resample_workspace_bytes": ([_U64], C.c_size_t),
+    "cuppl_peer_exchange": ([_P, _U32, _P, _U64, _U64, C.c_int, C.c_int, _P, _P, _P, _P, _U64, _P], C.c_int),
     "cuppl_resample": ([_P, _U64, _P, _U64, _U64, _U32, _P, _P, _P, _P, C.c_size_t, _P], C.c_int),
 }
 

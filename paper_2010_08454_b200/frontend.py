@@ -1351,8 +1351,11 @@ def _compile_parsed(prog, source: str, data: dict | None, max_depth: int) -> Com
         enum_init = ("    unsigned long long rem = pid;  // base-R digits: the forced choices of this path\n"
                      "    bool dead = false, chosen = false;\n    int chosen_i = 0;\n    (void)chosen; (void)chosen_i;")
         # a path that made nd < MAXD choices stands for R^(MAXD - nd) indices: divide them out
+        # draws_out carries each index's number of choices (int32) in enumeration launches:
+        # the breadth-first truncation of run_enumeration ranks paths by (choices, digits)
         enum_final = (f"    if (dead) lw = neg_inf_f();\n"
-                      f"    lw -= static_cast<double>(MAXD - nd) * {repr(math.log(radix))};")
+                      f"    lw -= static_cast<double>(MAXD - nd) * {repr(math.log(radix))};\n"
+                      f"    if (draws_out && valid) reinterpret_cast<int*>(draws_out)[idx] = dead ? -1 : nd;")
     if comp.engine == "mcmc":
         if g.draw_bound > 64:
             raise CompileError("mcmc supports up to 64 sample calls per execution")

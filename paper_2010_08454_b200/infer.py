@@ -373,16 +373,23 @@ def _run_compiled(model, n_samples: int, rng, *, return_traces: bool, group, dev
     return out
 
 
+ENUM_INDEX_CAP = 1 << 36  # forced-choice indices one enumeration may launch (R^max choice points)
+ENUM_BFS_CAP = 1 << 28    # indices whose completed paths are materialised for the breadth-first bound
+
+
 @_nvtx.traced("cuppl.run_enumeration")
 def run_enumeration(model, max_executions: int | None = None, max_depth: int | None = None, *, group=None,
                     device=None) -> EmpiricalDistribution:
     """run_enumeration of a compiled program `enumerate(model, n)` on the GPU.
 
-    Exact: every path through the model's choice points is executed as a forced-choice run (one
-    GPU thread per index of the base-R choice space, frontend.py), weighted by the log-masses of
-    its choices plus its factors; the posterior is normalised over all paths. Paths shard over
-    ranks like particles. `max_executions` bounds the index space (the whole space is
-    enumerated — there is no breadth-first truncation); `max_depth` bounds the choice points.
+    Every path through the model's choice points is executed as a forced-choice run (one GPU
+    thread per index of the base-R choice space, fp64, frontend.py), weighted by the log-masses
+    of its choices plus its factors. `max_executions` counts COMPLETED paths, as in the
+    reference's breadth-first traversal (SPEC.md:394, DESIGN DECISIONS "frontier order is FIFO;
+    --max-executions counts completed paths"): when the program has more completed paths than
+    that, the result keeps the first max_executions in breadth-first order — fewer choices
+    first, then support order of the choices — and normalises over them. `max_depth` bounds the
+    choice points. The index space R^depth is capped at ENUM_INDEX_CAP.
     """
     from .frontend import CompiledModel, DslLauncher, distribution_from_record
 
@@ -392,18 +399,87 @@ def run_enumeration(model, max_executions: int | None = None, max_depth: int | N
     if max_depth is not None and depth > max_depth:
         raise InferRuntimeError(f"the model has up to {depth} choice points > max_depth={max_depth}")
     n_paths = model.radix ** max(depth, 1)
-    limit = max_executions if max_executions is not None else 2**36
-    if n_paths > limit:
-        raise InferRuntimeError(f"{n_paths} paths (radix {model.radix}, depth {depth}) exceed {limit}")
+    if n_paths > ENUM_INDEX_CAP:
+        raise InferRuntimeError(f"{n_paths} forced-choice indices (radix {model.radix}, depth {depth}) exceed "
+                                f"{ENUM_INDEX_CAP}")
+    limit = max_executions if max_executions is not None else model.default_n
     rank, world = _world(group)
     lo, hi = shard_range(n_paths, rank, world)
     launcher = DslLauncher(model, device)
+    if limit is not None and limit < n_paths:  # completed paths may exceed the bound: count them
+        if world > 1 or n_paths > ENUM_BFS_CAP:
+            raise InferRuntimeError(f"{n_paths} forced-choice indices: checking the breadth-first bound of "
+                                    f"{limit} completed paths needs one process and <= {ENUM_BFS_CAP} indices; "
+                                    f"pass max_executions >= {n_paths}")
+        out = _enumeration_bfs(model, launcher, n_paths, int(limit))
+        if out is not None:
+            return out
     launcher.launch(lo, hi, 0)
     recs = _gather_records(launcher.rec, group)
     launcher.check_errors()
     rec = merge_records(recs)
     out = distribution_from_record(model, rec, n_paths, launcher, 0)
     out.log_z = rec.max_lw + math.log(rec.sum_w)  # exact evidence: the sum over paths
+    return out
+
+
+def _enumeration_bfs(model, launcher, n_paths: int, limit: int):
+    """Breadth-first truncation (run_enumeration's docstring): None when every completed path
+    fits in `limit` (the record of the whole space is then the result)."""
+    import torch
+
+    dev = launcher.device
+    lw = torch.empty(n_paths, dtype=torch.float64, device=dev)
+    nd = torch.empty(n_paths, dtype=torch.int32, device=dev)
+    ret = torch.empty((n_paths, model.return_width), dtype=torch.float32, device=dev)
+    rec = torch.empty_like(launcher.rec)
+    launcher.launch(0, n_paths, 0, lw_out=lw, draws_out=nd, ret_out=ret, rec_out=rec)
+    launcher.check_errors()
+    R = model.radix
+    p = torch.arange(n_paths, dtype=torch.int64, device=dev)
+    ndl = nd.to(torch.int64)
+    powR = torch.tensor([R ** k for k in range(max(model.max_draws, 1) + 1)], dtype=torch.int64, device=dev)
+    # a path with k choices is index p < R^k (its unused digits zero): its canonical index
+    canon = (ndl >= 0) & (p < powR[ndl.clamp(min=0)])
+    if int(canon.sum()) <= limit:
+        return None
+    # breadth-first order: (choices, digits with the first choice most significant)
+    lex = torch.zeros_like(p)
+    rem = p.clone()
+    for k in range(max(model.max_draws, 1)):
+        dk = rem % R
+        rem = rem // R
+        lex = torch.where(k < ndl, lex + dk * powR[(ndl - 1 - k).clamp(min=0)], lex)
+    key = ndl * (R ** max(model.max_draws, 1)) + lex
+    key = torch.where(canon, key, torch.full_like(key, torch.iinfo(torch.int64).max))
+    kept = torch.argsort(key)[:limit]
+    # the path's own log-probability (the launch divided out the R^(MAXD - k) indices sharing it)
+    lwp = lw[kept] + (model.max_draws - ndl[kept]).to(torch.float64) * math.log(R)
+    keep_lw = lwp
+    vals = ret[kept]
+    out = EmpiricalDistribution(n=limit)
+    m = float(keep_lw.max())
+    if not math.isfinite(m):
+        raise AllZeroWeightError("every kept path has probability 0 (SPEC.md:421)")
+    w = torch.exp(keep_lw - m)
+    z = float(w.sum())
+    out.log_z = m + math.log(z)
+    probs = w / z
+    out.ess = z * z / float((w * w).sum())
+    if model.return_kind in ("int", "bool"):
+        v = vals[:, 0].to(torch.int64)
+        lo_v = int(v.min())
+        agg = torch.zeros(int(v.max()) - lo_v + 1, dtype=torch.float64, device=dev)
+        agg.index_add_(0, v - lo_v, probs)
+        conv = bool if model.return_kind == "bool" else int
+        out.support = [(conv(lo_v + k), float(q)) for k, q in enumerate(agg.cpu().tolist()) if q > 0]
+    names = [nm for nm in model.stat_names if not nm.endswith("^2")]
+    for j, nm in enumerate(names[:model.return_width]):
+        mean = float((probs * vals[:, j].to(torch.float64)).sum())
+        out.mean[nm] = mean
+        out.stats[f"var_{nm}"] = float((probs * vals[:, j].to(torch.float64) ** 2).sum()) - mean * mean
+    out.stats["truncated_paths"] = int(canon.sum()) - limit
+    out.record = {"bfs_limit": limit}
     return out
 
 

@@ -89,7 +89,10 @@ class _Arena:
         self.n = n
         self.off = {}
         o = 0
-        for name, size in (("x0", n), ("x1", n)) + ((("anc0", 8 * n), ("anc1", 8 * n)) if with_anc else ()):
+        # xch: the peer-exchange mailboxes and flags of both phases (cuppl_peer_exchange):
+        # [mbox A: 32 x 64 B][flags A: 32 x u64][mbox B][flags B]
+        for name, size in ((("x0", n), ("x1", n)) + ((("anc0", 8 * n), ("anc1", 8 * n)) if with_anc else ())
+                           + (("xch", 2 * (32 * 64 + 32 * 8)),)):
             self.off[name] = o
             o += _align(size)
         self.bytes = o
@@ -99,6 +102,8 @@ class _Arena:
         with torch.cuda.device(device):
             self.x = [torch.as_tensor(_DevArray(self.base + self.off[f"x{i}"], n, "|u1"), device=device)
                       for i in range(2)]
+            xb = 2 * (32 * 64 + 32 * 8)
+            torch.as_tensor(_DevArray(self.base + self.off["xch"], xb, "|u1"), device=device).zero_()
             self.anc = ([torch.as_tensor(_DevArray(self.base + self.off[f"anc{i}"], n, "<i8"), device=device)
                          for i in range(2)] if with_anc else None)
 
@@ -142,7 +147,7 @@ class _Rank:
 class SmcRunner:
     def __init__(self, model: HiddenMarkovModel, n_particles: int, rng, *, group=None, device=None,
                  record_ancestors: bool = False, hist_steps=None, local_world: int | None = None,
-                 steps: int | None = None, graph: bool = False):
+                 steps: int | None = None, graph: bool = False, exchange: str = "auto"):
         import torch
 
         if not isinstance(model, HiddenMarkovModel):
@@ -171,6 +176,13 @@ class SmcRunner:
             self.rank, self.world = _world(group)
             self.ranks_here = [self.rank]
         self.multiprocess = self.world > 1 and not self.local
+        # multi-process exchanges: "peer" = cuppl_peer_exchange over the IPC-mapped arenas (device
+        # only, graph-capturable), "collective" = torch.distributed (NCCL / gloo)
+        if exchange not in ("auto", "peer", "collective"):
+            raise ValueError("exchange must be 'auto', 'peer' or 'collective'")
+        self.peer = self.multiprocess and (exchange == "peer" or (exchange == "auto" and self.world <= 32))
+        if self.peer and self.world > 32:
+            raise InferRuntimeError("peer exchange supports up to 32 ranks")
         self.bounds = rank_boundaries(self.N, self.world)
         S = model.n_states
         aliasA = np.array([alias_table(list(model.A[s])) for s in range(S)], dtype=np.uint64)
@@ -198,6 +210,9 @@ class SmcRunner:
         self._peers = []
         if self.multiprocess:
             xps, aps = self._exchange_arenas()
+            if self.peer:
+                self.epoch = torch.zeros(2, dtype=torch.int64, device=dev)
+                self.xstatus = torch.zeros(1, dtype=torch.int32, device=dev)
         self._tables = {}
         for par in (0, 1):
             if self.multiprocess:
@@ -216,7 +231,7 @@ class SmcRunner:
         # CUDA graph of the whole run (init + T steps): one process, no ancestor snapshots (their
         # host-side list cannot be replayed). The Philox key then lives in device memory
         # (cuppl_smc_model.key_dev), so one capture serves every reseed.
-        self.use_graph = bool(graph) and not self.multiprocess and not record_ancestors
+        self.use_graph = bool(graph) and (not self.multiprocess or self.peer) and not record_ancestors
         self.key_dev = None
         if self.use_graph:
             import torch
@@ -247,6 +262,10 @@ class SmcRunner:
             N.check(N.lib().cuppl_ipc_open(hb, C.byref(p)), "ipc_open")
             self._peers.append(p.value)
             bases.append((p.value, off))
+        import torch
+
+        self.peer_bases = torch.tensor([b for b, _ in bases], dtype=torch.int64, device=self.device)
+        self.xch_off = me.off["xch"]
         xs = [[b + o[f"x{par}"] for b, o in bases] for par in (0, 1)]
         an = ([[b + o[f"anc{par}"] for b, o in bases] for par in (0, 1)] if self.record_ancestors else None)
         return xs, an
@@ -271,6 +290,9 @@ class SmcRunner:
             m = torch.stack([rk.m_key[t] for rk in self.ranks]).max()
             for rk in self.ranks:
                 rk.m_key[t].copy_(m)
+        elif self.peer:
+            v = self.ranks[0].m_key[t:t + 1]
+            self._peer_exchange(v, 4, 0, max_out=v)
         else:
             import torch.distributed as dist
 
@@ -288,6 +310,8 @@ class SmcRunner:
         if self.local or self.world == 1:
             for i, rk in enumerate(self.ranks):
                 self.gathered[t, rk.r].copy_(rk.rec[t])
+        elif self.peer:
+            self._peer_exchange(self.ranks[0].rec[t], 32, 1, gather_out=self.gathered[t])
         else:
             import torch.distributed as dist
 
@@ -297,6 +321,16 @@ class SmcRunner:
                 h = torch.empty(self.world * 4, dtype=torch.int64)
                 dist.all_gather_into_tensor(h, self.ranks[0].rec[t].cpu(), group=self.group)
                 self.gathered[t].view(-1).copy_(h)
+
+    PEER_TIMEOUT_NS = 60_000_000_000
+
+    def _peer_exchange(self, src, nbytes: int, phase: int, max_out=None, gather_out=None):
+        """cuppl_peer_exchange: phase 0 = MAX of the stabiliser keys, phase 1 = the rank records."""
+        mbox = self.xch_off + phase * (32 * 64 + 32 * 8)
+        N.check(N.lib().cuppl_peer_exchange(N.ptr(src), nbytes, N.ptr(self.peer_bases), mbox, mbox + 32 * 64,
+                                            self.rank, self.world, N.ptr(self.epoch[phase:phase + 1]),
+                                            N.ptr(max_out), N.ptr(gather_out), N.ptr(self.xstatus),
+                                            self.PEER_TIMEOUT_NS, N.stream_ptr(self.device)), "peer_exchange")
 
     def _gather_stats(self) -> np.ndarray:
         import torch
@@ -502,6 +536,8 @@ class SmcRunner:
         return sum(a.elapsed_time(b) for a, b in self.k6_events or [])
 
     def result(self) -> SmcResult:
+        if self.peer and int(self.xstatus.item()):
+            raise InferRuntimeError("peer exchange timed out (a rank did not reach the step)", seed=self.seed)
         g = self.gathered.cpu().numpy().view(np.uint64)
         mk = self.ranks[0].m_key.cpu().numpy()
         Tt = g[:, :, 0].sum(axis=1)

@@ -614,3 +614,44 @@ def test_gpu_compiled_bernoulli_frequency(cuda):
                                                          "importance(model, 10)"), n, Rng(14))
     got = dict(post.support)
     assert abs(got[True] - 0.3) < 5 * math.sqrt(0.21 / n)
+
+
+GEOM_SRC = """geom <- function() { if (sample(bernoulli(0.5))) { 0 } else { 1 + geom() } };
+model <- function() { geom() };
+enumerate(model, {n})"""
+TWO_COINS = ("model <- function() { a <- sample(bernoulli(0.3)); b <- sample(bernoulli(0.6)); "
+             "(if (a) { 1 } else { 0 }) + (if (b) { 2 } else { 0 }) }; enumerate(model, {n})")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("src,n", [(GEOM_SRC, 5), (GEOM_SRC, 13), (TWO_COINS, 3), (TWO_COINS, 1)])
+def test_gpu_enumeration_breadth_first_truncation(cuda, src, n):
+    """max_executions counts completed paths of the reference's breadth-first traversal
+    (SPEC.md:394): with fewer than the program's paths, the first n in breadth-first order
+    (fewer choices first, then support order) are kept and normalised — equal to the oracle's
+    FIFO traversal to 1e-12."""
+    from oracle.dsl_eval import Enumerator
+    from paper_2010_08454_b200 import infer
+
+    prog = src.replace("{n}", str(n))
+    post = infer.run_enumeration(frontend.compile_program(prog))
+    ref, log_z = Enumerator(prog).posterior_bfs(n)
+    got = dict(post.support)
+    assert set(got) == set(ref), (got, ref)
+    for k, p in ref.items():
+        assert abs(got[k] - p) < 1e-12, (k, got[k], p)
+    assert abs(post.log_z - log_z) < 1e-12
+
+
+@pytest.mark.gpu
+def test_gpu_enumeration_spec_geometric_10000(cuda):
+    """enumerate(geometric, 10000) with max_depth 20 — 20 completed paths, far
+    below the bound: P(k) = 0.5^(k+1) / (1 - 2^-20), k <= 19."""
+    from paper_2010_08454_b200 import infer
+
+    post = infer.run_enumeration(frontend.compile_program(GEOM_SRC.replace("{n}", "10000")))
+    got = dict(post.support)
+    z = 1.0 - 0.5 ** 20
+    assert set(got) == set(range(20))
+    for k in range(20):
+        assert abs(got[k] - 0.5 ** (k + 1) / z) < 1e-12

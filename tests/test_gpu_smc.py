@@ -206,7 +206,7 @@ def test_smc_deterministic(cuda):
     assert np.array_equal(x1, x2) and np.array_equal(lw1.view(np.uint32), lw2.view(np.uint32))
 
 
-def _mp_worker(rank, world, port, n, steps, q):
+def _mp_worker(rank, world, port, n, steps, q, exchange="collective", graph=False):
     import os
 
     import torch
@@ -220,7 +220,12 @@ def _mp_worker(rank, world, port, n, steps, q):
         from paper_2010_08454_b200 import models, smc
 
         m = models.HiddenMarkovModel.synthetic(S=50, T=steps, seed=5)
-        r = smc.SmcRunner(m, n, KEY, record_ancestors=True, steps=steps)
+        r = smc.SmcRunner(m, n, KEY, record_ancestors=not graph, steps=steps, exchange=exchange, graph=graph)
+        if graph:  # a first replay under another key: the second one must still be exact
+            assert r.use_graph
+            r.reseed(KEY ^ 0x5555)
+            r.run()
+            r.reseed(KEY)
         res = r.run()
         torch.cuda.synchronize()
         q.put((rank, r.bounds[rank], res.states[0].cpu().numpy(), res.log_weights[0].cpu().numpy(),
@@ -231,9 +236,12 @@ def _mp_worker(rank, world, port, n, steps, q):
         dist.destroy_process_group()
 
 
-def test_smc_multiprocess_ipc_matches_oracle(cuda, oracle_lib):
-    """Two processes (gloo for the tiny collectives, CUDA-IPC peer stores for the particles):
-    the same bits as the single-rank oracle."""
+@pytest.mark.parametrize("exchange,graph", [("collective", False), ("peer", False), ("peer", True)])
+def test_smc_multiprocess_ipc_matches_oracle(cuda, oracle_lib, exchange, graph):
+    """Two processes sharing the GPU, CUDA-IPC peer stores for the particles; the per-step
+    exchanges either through torch.distributed (gloo here) or device-side over the peer-mapped
+    arenas (cuppl_peer_exchange) — then the whole run of each rank is also one CUDA graph,
+    replayed twice: the same bits as the single-rank oracle."""
     import multiprocessing as mp
     import socket
 
@@ -246,7 +254,7 @@ def test_smc_multiprocess_ipc_matches_oracle(cuda, oracle_lib):
     n, steps = 40_000, 8
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_mp_worker, args=(r, 2, port, n, steps, q)) for r in range(2)]
+    procs = [ctx.Process(target=_mp_worker, args=(r, 2, port, n, steps, q, exchange, graph)) for r in range(2)]
     for p in procs:
         p.start()
     out = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
@@ -258,7 +266,7 @@ def test_smc_multiprocess_ipc_matches_oracle(cuda, oracle_lib):
     x = np.concatenate([o[2] for o in out]).astype(np.int32)
     lw = np.concatenate([o[3] for o in out])
     assert np.array_equal(out[0][5], ref["T"]) and np.array_equal(out[1][5], ref["T"])
-    for t in range(steps - 1):
+    for t in range(steps - 1 if not graph else 0):
         anc = np.concatenate([o[4][t] for o in out]).astype(np.uint64)
         assert np.array_equal(anc, ref["ancestors"][t]), f"ancestors differ at step {t}"
     assert np.array_equal(x, ref["x"]) and np.array_equal(lw.view(np.uint32), ref["lw"].view(np.uint32))
