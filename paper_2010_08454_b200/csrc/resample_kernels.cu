@@ -195,8 +195,8 @@ __global__ void __launch_bounds__(kRsThreads) rs_scan_kernel(RsArgs a) {
 // ------------------------------------------------------------------ RS3: gather ---------
 template <bool STAGE_PAY>
 __global__ void __launch_bounds__(kRsThreads, 3) rs_gather_kernel(RsArgs a) {
-  extern __shared__ __align__(128) uint8_t pay_s[];  // [kRsTile][P] staged payload (STAGE_PAY)
-  __shared__ __align__(128) float lws[kRsTile];     // staged log-weights
+  extern __shared__ __align__(128) uint8_t pay_s2[];  // [2][kRsTile][P] staged payloads (STAGE_PAY)
+  __shared__ __align__(128) float lws2[2][kRsTile];   // staged log-weights, double-buffered
   __shared__ __align__(16) uint16_t marks[kRsWin];  // tile index + 1 of a first child
   __shared__ __align__(16) uint16_t ancs[kRsWin];   // resolved ancestor (tile index + 1)
   __shared__ unsigned long long wsum[kRsThreads / 32];
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kRsThreads, 3) rs_gather_kernel(RsArgs a) {
   __shared__ unsigned long long s_u64[3];
   __shared__ unsigned int s_jn;
   __shared__ Comb s_cb;
-  __shared__ __align__(8) unsigned long long mbar;
+  __shared__ __align__(8) unsigned long long mbar[2];
   __shared__ BlockScratch sc;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long n = a.n;
@@ -242,7 +242,8 @@ __global__ void __launch_bounds__(kRsThreads, 3) rs_gather_kernel(RsArgs a) {
     c.n_over_t = static_cast<double>(c.N) / static_cast<double>(T);
     c.a_over_t = static_cast<double>(c.A) / static_cast<double>(T);
     s_cb = c;
-    mbar_init(&mbar, 1);
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = tid; i < kRsWin / 8; i += kRsThreads) reinterpret_cast<uint4*>(marks)[i] = make_uint4(0, 0, 0, 0);
@@ -277,28 +278,44 @@ __global__ void __launch_bounds__(kRsThreads, 3) rs_gather_kernel(RsArgs a) {
   unsigned long long tile = s_u64[0];
   unsigned long long c_base = __ldg(a.tile_prefix + tile);
   unsigned long long j_cur = jb_lo;
-  unsigned int phase = 0;
   const bool tma_ok = a.tma;
+  // double-buffered TMA staging: tile t + 1 is fetched while tile t is processed
+  unsigned int ph[2] = {0u, 0u};
+  bool pending[2] = {false, false};  // a bulk copy into buffer b is in flight (same in all threads)
+  const unsigned int pay_bytes = STAGE_PAY ? static_cast<unsigned int>(kRsTile * P) : 0u;
+  auto full_tile = [&](unsigned long long t) { return tma_ok && t < a.n_tiles && (t + 1) * kRsTile <= n; };
+  auto issue = [&](int b, unsigned long long t) {  // thread 0
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of buffer b
+    mbar_expect_tx(&mbar[b], kRsTile * 4u + pay_bytes);
+    tma_load_1d(lws2[b], a.lw + t * kRsTile, kRsTile * 4u, &mbar[b]);
+    if (STAGE_PAY) tma_load_1d(pay_s2 + static_cast<size_t>(b) * kRsTile * P, a.payload + t * kRsTile * P, pay_bytes,
+                               &mbar[b]);
+  };
+  int bf = 0;
+  if (full_tile(tile)) {
+    if (tid == 0) issue(0, tile);
+    pending[0] = true;
+  }
 
   while (j_cur < jb_hi && tile < a.n_tiles) {
     const unsigned long long base = tile * kRsTile;
     const unsigned long long nv_tile = n - base < static_cast<unsigned long long>(kRsTile) ? n - base : kRsTile;
-    // ---- stage the tile's log-weights (and payload) in shared memory
-    if (tma_ok && nv_tile == kRsTile) {
-      if (tid == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads
-        const unsigned int pay_bytes = STAGE_PAY ? static_cast<unsigned int>(kRsTile * P) : 0u;
-        mbar_expect_tx(&mbar, kRsTile * 4u + pay_bytes);
-        tma_load_1d(lws, a.lw + base, kRsTile * 4u, &mbar);
-        if (STAGE_PAY) tma_load_1d(pay_s, a.payload + base * P, pay_bytes, &mbar);
-      }
-      mbar_wait(&mbar, phase);
-      phase ^= 1u;
+    float* lws = lws2[bf];
+    uint8_t* pay_s = pay_s2 + static_cast<size_t>(bf) * kRsTile * P;
+    // ---- the tile's log-weights (and payload) in shared memory
+    if (pending[bf]) {
+      mbar_wait(&mbar[bf], ph[bf]);
+      ph[bf] ^= 1u;
+      pending[bf] = false;
     } else {
       for (int i = tid; i < kRsTile; i += kRsThreads) lws[i] = i < static_cast<int>(nv_tile) ? a.lw[base + i] : neg_inf_f();
       if (STAGE_PAY)
         for (unsigned long long i = tid; i < nv_tile * P; i += kRsThreads) pay_s[i] = a.payload[base * P + i];
       __syncthreads();
+    }
+    if (full_tile(tile + 1)) {  // buffer 1 - bf was released by the previous tile's final barrier
+      if (tid == 0) issue(1 - bf, tile + 1);
+      pending[1 - bf] = true;
     }
     // ---- my sources [8 tid, +8): exact integer weights, block exclusive scan
     double wd[kRsSeg];
@@ -457,8 +474,12 @@ __global__ void __launch_bounds__(kRsThreads, 3) rs_gather_kernel(RsArgs a) {
     j_cur = s_jn < jb_hi ? s_jn : jb_hi;
     c_base += btot;
     ++tile;
+    bf ^= 1;
     __syncthreads();  // lws / pay_s / wsum / s_jn / ancs reuse
   }
+  // a prefetch the CTA did not need must land before it exits
+  if (pending[0]) mbar_wait(&mbar[0], ph[0]);
+  if (pending[1]) mbar_wait(&mbar[1], ph[1]);
 }
 
 // ------------------------------------------------------------------ launch --------------
@@ -470,7 +491,7 @@ cudaError_t launch_resample(const RsArgs& a, int sm_count, cudaStream_t st) {
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const bool stage = a.P > 0 && a.P <= static_cast<unsigned long long>(kRsStageMaxP) && a.tma;
-  const int smem = stage ? static_cast<int>(kRsTile * a.P) : 0;
+  const int smem = stage ? static_cast<int>(2 * kRsTile * a.P) : 0;
   int per_sm = 0;
   if (stage) {
     e = cudaFuncSetAttribute(rs_gather_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

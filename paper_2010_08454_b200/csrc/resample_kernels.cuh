@@ -12,7 +12,7 @@ constexpr int kRsSeg = 8;                       // sources per thread per tile
 constexpr int kRsTile = kRsThreads * kRsSeg;    // 2048 particles: RS2 tile == RS3 staged source tile
 constexpr int kRsScanTiles = 4;                 // RS2 tiles per CTA (one look-back per 8192 particles)
 constexpr int kRsWin = 16 * kRsThreads;         // RS3 output window: 16 consecutive outputs per thread
-constexpr int kRsStageMaxP = 32;                // payloads up to 32 B/particle are TMA-staged (64 KB tile)
+constexpr int kRsStageMaxP = 16;                // payloads up to 16 B/particle are TMA-staged (2 x 32 KB)
 constexpr int kRsMaxG1 = 1024;                  // RS1 CTAs
 
 struct RsArgs {
