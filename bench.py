@@ -769,6 +769,8 @@ def run_ours_resample(args) -> dict | None:
     lw_h = lw.cpu().pin_memory()
     pay_h = payload.cpu().pin_memory()
     out_h = torch.empty_like(pay_h).pin_memory()
+    resample.systematic(lw_h.to(device), pay_h.to(device), Rng(1), 499)  # warm (allocator, first touch)
+    torch.cuda.synchronize()
     e2e_t = []
     for k in range(2):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
