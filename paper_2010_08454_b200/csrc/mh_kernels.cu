@@ -10,7 +10,7 @@
 // oracle/cuppl_oracle.c (same Philox words; fp64).
 //
 // Decomposition: a CTA runs C <= 32 chains in lockstep. The data never move: thread t holds
-// the y values of its 8-point groups g = t + NT m (m < M) in REGISTERS, for every chain of the
+// the y values of its 8-point groups g = t M + m (m < M) in REGISTERS, for every chain of the
 // CTA. Per chain the labels are one byte per pair of points (even, odd), four pair bytes per
 // u32 (one LDS.32 per group). A pair byte is the BYTE OFFSET 4e of the pair's entry e in the
 // chain's split tables TA[e] = -mu_a, TB[e] = -mu_b, with e = a K + b for two data points,
@@ -117,9 +117,12 @@ __device__ __forceinline__ void labels4(const MhArgs& a, PhiloxKey key, unsigned
 
 }  // namespace
 
+// A chain's code words sit at a fixed stride of kMhMaxThreads * M words (>= G = NT * M): the
+// chain offset of every code-word load is then a compile-time immediate.
 size_t mh_smem_bytes(int G, int K, int chains_per_cta, int threads) {
   (void)K;
-  return mh_layout(G, chains_per_cta, threads).total;
+  const int M = (G + threads - 1) / threads;
+  return mh_layout(kMhMaxThreads * M, chains_per_cta, threads).total;
 }
 
 // (21 warps: one SMSP holds 6, so <= 80 registers per thread.)
@@ -136,7 +139,8 @@ __global__ void __launch_bounds__(kMhMaxThreads + 32, 1) mh_gmm_kernel(const MhA
   const bool control = tid >= NT;
   const int NW = NT / 32;
   const int K = a.K, G = a.G, C = a.chains_per_cta;
-  const MhLayout Ly = mh_layout(G, C, NT);
+  constexpr int CS = kMhMaxThreads * M;  // code-word stride per chain (words)
+  const MhLayout Ly = mh_layout(CS, C, NT);
   uint32_t* codes = reinterpret_cast<uint32_t*>(smem + Ly.codes);
   float* tabs = reinterpret_cast<float*>(smem + Ly.tabs);
   float* mus = reinterpret_cast<float*>(smem + Ly.mus);
@@ -149,11 +153,11 @@ __global__ void __launch_bounds__(kMhMaxThreads + 32, 1) mh_gmm_kernel(const MhA
   const unsigned int n_sites = static_cast<unsigned int>(K + a.D);
   const uint32_t uK = static_cast<uint32_t>(K);
 
-  // ---- my data (evaluation threads): groups g = tid + NT m, points 8g .. 8g + 7 as 4 pairs
+  // ---- my data (evaluation threads): groups g = tid M + m, points 8g .. 8g + 7 as 4 pairs
   f32x2 Y[M][4];
 #pragma unroll
   for (int m = 0; m < M; ++m) {
-    const int g = control ? 0 : tid + NT * m;
+    const int g = control ? 0 : tid * M + m;  // a thread's groups are contiguous
     const float4 y0 = reinterpret_cast<const float4*>(a.y)[2 * g];
     const float4 y1 = reinterpret_cast<const float4*>(a.y)[2 * g + 1];
     Y[m][0] = pack2(y0.x, y0.y);
@@ -168,11 +172,11 @@ __global__ void __launch_bounds__(kMhMaxThreads + 32, 1) mh_gmm_kernel(const MhA
       const unsigned int chain = a.chain_begin + local0 + c;
 #pragma unroll
       for (int m = 0; m < M; ++m) {
-        const int g = tid + NT * m;
+        const int g = tid * M + m;
         uint32_t l0[4], l1[4];
         labels4(a, key, chain, 8 * g, l0);
         labels4(a, key, chain, 8 * g + 4, l1);
-        codes[c * G + g] = (4u * pair_entry(l0[0], l0[1], uK)) | ((4u * pair_entry(l0[2], l0[3], uK)) << 8) |
+        codes[c * CS + g] = (4u * pair_entry(l0[0], l0[1], uK)) | ((4u * pair_entry(l0[2], l0[3], uK)) << 8) |
                            ((4u * pair_entry(l1[0], l1[1], uK)) << 16) |
                            ((4u * pair_entry(l1[2], l1[3], uK)) << 24);
       }
@@ -220,17 +224,18 @@ __global__ void __launch_bounds__(kMhMaxThreads + 32, 1) mh_gmm_kernel(const MhA
   // of warp w ends with the warp's partial of the group's chain l in parts[q][w][l]
   auto evaluate = [&](int q) {
     const int cb = q ? c0 : 0, ncq = q ? nc - c0 : c0;
+    const uint32_t* cwq = codes + cb * CS + tid * M;  // this thread's M code words (contiguous)
     float v[16];
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
       v[c] = 0.f;
       if (c < ncq) {
-        const uint32_t* cw = codes + (cb + c) * G;
+        const uint32_t* cw = cwq + c * CS;
         const uint8_t* tab = smem + (cb + c) * kMhTabBytes;  // + byte offset: LDS [R + imm]
         f32x2 acc = pack2(0.f, 0.f);
 #pragma unroll
         for (int m = 0; m < M; ++m) {
-          const uint32_t word = cw[tid + NT * m];
+          const uint32_t word = cw[m];
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             const uint32_t off = __byte_perm(word, 0u, 0x4440u | static_cast<uint32_t>(b));
@@ -288,7 +293,7 @@ __global__ void __launch_bounds__(kMhMaxThreads + 32, 1) mh_gmm_kernel(const MhA
           if (lemire(mh_block(key, chain, s, r, CUPPL_TAG_MH).y, uK, &zprop)) break;
       }
       const int i = static_cast<int>(site) - K;  // point index
-      gidx = lane * G + (i >> 3);
+      gidx = lane * CS + (i >> 3);
       const int sh = 8 * ((i & 7) >> 1);
       old_word = codes[gidx];
       uint32_t ca, cb;
