@@ -141,11 +141,15 @@ __global__ void __launch_bounds__(kRsThreads) rs_scan_kernel(RsArgs a) {
     unsigned long long ws = 0;
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-    for (int k = 0; k < kRsSeg; ++k) {
-      const float e = any ? smc_e(v[u][k], M) : 0.f;
-      ws += smc_w(e);
-      s1 += e;
-      s2 = fmaf(e, e, s2);
+    for (int k = 0; k < kRsSeg; k += 2) {
+      const float2 ee = smc_e2(v[u][k], v[u][k + 1], M);
+      const float e0 = any ? ee.x : 0.f, e1 = any ? ee.y : 0.f;
+      ws += smc_w(e0);
+      s1 += e0;
+      s2 = fmaf(e0, e0, s2);
+      ws += smc_w(e1);
+      s1 += e1;
+      s2 = fmaf(e1, e1, s2);
     }
     d1 += s1;
     d2 += s2;
@@ -325,10 +329,13 @@ __global__ void __launch_bounds__(kRsThreads, 3) rs_gather_kernel(RsArgs a) {
       const float4 l1 = reinterpret_cast<const float4*>(lws)[2 * tid + 1];
       const float lv[kRsSeg] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
 #pragma unroll
-      for (int k = 0; k < kRsSeg; ++k) {
-        const uint32_t w = any ? smc_w(smc_e(lv[k], M)) : 0u;
-        tw += w;
-        wd[k] = static_cast<double>(w);
+      for (int k = 0; k < kRsSeg; k += 2) {
+        const float2 ee = smc_e2(lv[k], lv[k + 1], M);
+        const uint32_t w0 = any ? smc_w(ee.x) : 0u, w1 = any ? smc_w(ee.y) : 0u;
+        tw += w0;
+        tw += w1;
+        wd[k] = static_cast<double>(w0);
+        wd[k + 1] = static_cast<double>(w1);
       }
     }
     unsigned long long incl = tw;

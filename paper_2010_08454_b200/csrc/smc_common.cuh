@@ -29,6 +29,25 @@ __device__ __forceinline__ float exp_repro(float d) {
   return __fmul_rn(p, __int_as_float((ki + 127) << 23));
 }
 
+// The same sequence on two values at once (fma.rn / add.rn / mul.rn .f32x2 round each lane as
+// the scalar instructions do: bit-identical results, half the FMA-pipe instructions).
+__device__ __forceinline__ f32x2 exp_repro2(f32x2 d) {
+  const f32x2 t = mul2(d, pack2(1.44269504f, 1.44269504f));
+  const f32x2 kb = add2(t, pack2(12582912.0f, 12582912.0f));
+  const f32x2 k = add2(kb, pack2(-12582912.0f, -12582912.0f));
+  const float2 kbs = unpack2(kb);
+  const int k0 = __float_as_int(kbs.x) - 0x4B400000, k1 = __float_as_int(kbs.y) - 0x4B400000;
+  f32x2 r = fma2(k, pack2(-0.693145752f, -0.693145752f), d);
+  r = fma2(k, pack2(-1.42860677e-06f, -1.42860677e-06f), r);
+  f32x2 p = fma2(pack2(1.38888893e-03f, 1.38888893e-03f), r, pack2(8.33333377e-03f, 8.33333377e-03f));
+  p = fma2(p, r, pack2(4.16666679e-02f, 4.16666679e-02f));
+  p = fma2(p, r, pack2(1.66666672e-01f, 1.66666672e-01f));
+  p = fma2(p, r, pack2(0.5f, 0.5f));
+  p = fma2(p, r, pack2(1.0f, 1.0f));
+  p = fma2(p, r, pack2(1.0f, 1.0f));
+  return mul2(p, pack2(__int_as_float((k0 + 127) << 23), __int_as_float((k1 + 127) << 23)));
+}
+
 // e = exp(lw - M) for lw - M >= -87, else 0 (and 0 for lw = -inf / NaN): branch-free, the
 // polynomial evaluated on the clamped difference and discarded outside the range (the same
 // values as the oracle's or_smc_e)
@@ -36,6 +55,13 @@ __device__ __forceinline__ float smc_e(float lw, float M) {
   const float d = __fsub_rn(lw, M);
   const float e = exp_repro(fmaxf(d, -87.0f));
   return (lw > neg_inf_f() && d >= -87.0f) ? e : 0.0f;
+}
+
+// smc_e of two log-weights (exp_repro2)
+__device__ __forceinline__ float2 smc_e2(float la, float lb, float M) {
+  const float da = __fsub_rn(la, M), db = __fsub_rn(lb, M);
+  const float2 e = unpack2(exp_repro2(pack2(fmaxf(da, -87.0f), fmaxf(db, -87.0f))));
+  return make_float2((la > neg_inf_f() && da >= -87.0f) ? e.x : 0.0f, (lb > neg_inf_f() && db >= -87.0f) ? e.y : 0.0f);
 }
 
 __device__ __forceinline__ uint32_t smc_w(float e) {
