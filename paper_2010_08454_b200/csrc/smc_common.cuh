@@ -31,12 +31,14 @@ __device__ __forceinline__ float exp_repro(float d) {
 
 // The same sequence on two values at once (fma.rn / add.rn / mul.rn .f32x2 round each lane as
 // the scalar instructions do: bit-identical results, half the FMA-pipe instructions).
-__device__ __forceinline__ f32x2 exp_repro2(f32x2 d) {
-  const f32x2 t = mul2(d, pack2(1.44269504f, 1.44269504f));
-  const f32x2 kb = add2(t, pack2(12582912.0f, 12582912.0f));
-  const f32x2 k = add2(kb, pack2(-12582912.0f, -12582912.0f));
-  const float2 kbs = unpack2(kb);
-  const int k0 = __float_as_int(kbs.x) - 0x4B400000, k1 = __float_as_int(kbs.y) - 0x4B400000;
+__device__ __forceinline__ f32x2 exp_repro2(float d0, float d1) {
+  // the range reduction stays scalar: the packed add does not reproduce the scalar
+  // round-half-even of the 1.5 * 2^23 magic addition at exact ties (measured)
+  const float t0 = __fmul_rn(d0, 1.44269504f), t1 = __fmul_rn(d1, 1.44269504f);
+  const float kb0 = __fadd_rn(t0, 12582912.0f), kb1 = __fadd_rn(t1, 12582912.0f);
+  const f32x2 k = pack2(__fsub_rn(kb0, 12582912.0f), __fsub_rn(kb1, 12582912.0f));
+  const int k0 = __float_as_int(kb0) - 0x4B400000, k1 = __float_as_int(kb1) - 0x4B400000;
+  const f32x2 d = pack2(d0, d1);
   f32x2 r = fma2(k, pack2(-0.693145752f, -0.693145752f), d);
   r = fma2(k, pack2(-1.42860677e-06f, -1.42860677e-06f), r);
   f32x2 p = fma2(pack2(1.38888893e-03f, 1.38888893e-03f), r, pack2(8.33333377e-03f, 8.33333377e-03f));
@@ -60,7 +62,7 @@ __device__ __forceinline__ float smc_e(float lw, float M) {
 // smc_e of two log-weights (exp_repro2)
 __device__ __forceinline__ float2 smc_e2(float la, float lb, float M) {
   const float da = __fsub_rn(la, M), db = __fsub_rn(lb, M);
-  const float2 e = unpack2(exp_repro2(pack2(fmaxf(da, -87.0f), fmaxf(db, -87.0f))));
+  const float2 e = unpack2(exp_repro2(fmaxf(da, -87.0f), fmaxf(db, -87.0f)));
   return make_float2((la > neg_inf_f() && da >= -87.0f) ? e.x : 0.0f, (lb > neg_inf_f() && db >= -87.0f) ? e.y : 0.0f);
 }
 
