@@ -113,14 +113,18 @@ is_linreg_kernel(const __grid_constant__ LinregParams<CAP> prm) {
             S1[q] = fma2(r1, r1, S1[q]);
           }
         }
-        if (!kChunked || cend >= D) break;
+        if constexpr (!kChunked) {
+          break;
+        } else {
+          if (cend >= D) break;
 #pragma unroll
-        for (int q = 0; q < P / 2; ++q) {  // fold the chunk (even chunk sizes: i == cend here)
-          const float2 t = unpack2(add2(S0[q], S1[q]));
-          T64[(2 * q) % (kChunked ? P : 1)] += t.x;
-          T64[(2 * q + 1) % (kChunked ? P : 1)] += t.y;
-          S0[q] = pack2(0.f, 0.f);
-          S1[q] = pack2(0.f, 0.f);
+          for (int q = 0; q < P / 2; ++q) {  // fold the chunk (even chunk sizes: i == cend here)
+            const float2 t = unpack2(add2(S0[q], S1[q]));
+            T64[2 * q] += t.x;
+            T64[2 * q + 1] += t.y;
+            S0[q] = pack2(0.f, 0.f);
+            S1[q] = pack2(0.f, 0.f);
+          }
         }
       }
       if (i < D) {
@@ -421,6 +425,16 @@ cudaError_t launch_poly(const PolyParams<CAP>& prm, bool injected, int sm_count,
     return launch_persistent(is_poly_kernel<P, false, 0, false, CAP>, prm, sm_count, chunks(P), max_blocks, stream, &grid);
   return launch_persistent(is_poly_kernel<P, false, 0, true, CAP>, prm, sm_count, chunks(P), max_blocks, stream, &grid);
 }
+
+// the measured point-array placement (is_kernels.cuh kXyOffset)
+#pragma nv_diag_suppress 1427
+#pragma GCC diagnostic push
+#pragma GCC diagnostic ignored "-Winvalid-offsetof"
+static_assert(offsetof(LinregParams<kLinregCapSmall>, xy) == kXyOffset, "linreg xy offset");
+static_assert(offsetof(LinregParams<kLinregCapLarge>, xy) == kXyOffset, "linreg xy offset");
+static_assert(offsetof(PolyParams<kPolyCap>, xy) == kXyOffset, "poly xy offset");
+#pragma GCC diagnostic pop
+#pragma nv_diag_default 1427
 
 template cudaError_t launch_linreg<kLinregCapSmall>(const LinregParams<kLinregCapSmall>&, bool, int, int, cudaStream_t, int);
 template cudaError_t launch_linreg<kLinregCapLarge>(const LinregParams<kLinregCapLarge>&, bool, int, int, cudaStream_t, int);

@@ -29,7 +29,6 @@ struct IsCommon {
   cuppl_is_record* block_recs;
   unsigned int* counter;
   cuppl_is_record* rec_out;
-  const float2* xy_g;  // CAP == 0: the (x_i, y_i) pairs in device memory (the workspace tail)
 };
 
 template <int CAP>
@@ -39,15 +38,26 @@ struct LinregParams : IsCommon {
   float lw_const;          // -D (ln sigma + 0.5 ln 2 pi)
   float one;               // 1.0f at run time (operand of the FFMA2 form of the add, V == 1)
   float pad1_;
-  float2 xy[CAP > 0 ? CAP : 1];
+  float2 xy[CAP > 0 ? CAP : 1];  // at kXyOffset (below)
+  const float2* xy_g;  // CAP == 0: the (x_i, y_i) pairs in device memory (the workspace tail)
 };
 
 template <int CAP>
 struct PolyParams : IsCommon {
   static constexpr int kCap = CAP;
   int32_t* deg_out;
-  float2 xy[CAP > 0 ? CAP : 1];
+  uint64_t pad2_;
+  float2 xy[CAP > 0 ? CAP : 1];  // at kXyOffset (below)
+  const float2* xy_g;  // CAP == 0: the (x_i, y_i) pairs in device memory (the workspace tail)
 };
+
+// Offset of the point array in both parameter blocks. Measured on B200 (xy offsets 168..256
+// swept): the linreg loop runs 3% faster when the array starts 16 bytes past a 32-byte
+// boundary of the constant bank (offsets 176 / 208 / 240: 89.1-89.5 ms per 1e9 particles; 184 /
+// 192 / 224 / 256: 91.5-92.2 ms) and the poly kernel's LDCU.128 point loads want 16-byte
+// alignment (176 / 192: 92.85 ms per 1.25e10 particles; 168 / 184 / 200: 93.5-93.7 ms). The
+// kernel parameters start at a 32-byte-aligned bank address (c[0x0][0x380]).
+constexpr size_t kXyOffset = 176;
 
 // Point i of the data: the kernel-parameter block (constant bank) up to CAP points; larger
 // data sets (CAP == 0) are read from device memory with warp-uniform __ldg (L1 broadcasts).
