@@ -71,6 +71,12 @@ MAX_BINS = 8   # cuppl_is_record.bin_w
 MCMC_BINS, MCMC_BIN_LO = 128, -32  # chain histograms of integer returns: values [-32, 96)
 MAX_TRACE_DRAWS = 256
 MAX_CONST_DATA = 16_000  # floats kept in the module's __constant__ bank (64 KB); larger: __ldg
+# Bytes of padding before the constant-bank data (multiple of 8): where the data starts
+# relative to 32-byte bank boundaries changes the speed of the point loops (is_kernels.cuh
+# kXyOffset). Measured on the dsl-linreg bench: 16 bytes past a 32-byte boundary 103.2 ms per
+# 1e9 particles, offsets 0 / 8 / 24 bytes 104.4-104.9 ms. CUPPL_DC_PAD_BYTES overrides it
+# (tuning only).
+_DC_PAD = int(os.environ.get("CUPPL_DC_PAD_BYTES", "16")) // 8
 DATA_SYM = "DATA"        # resolved by the kernel prelude to the constant bank or the buffer
 DSL_LANES = 8            # particles per thread of an importance kernel (CUPPL_DSL_LANES overrides)
 
@@ -1335,7 +1341,9 @@ def _compile_parsed(prog, source: str, data: dict | None, max_depth: int) -> Com
     if _F64 and len(data_arr) > MAX_CONST_DATA // 2:
         raise CompileError(f"enumerate programs hold up to {MAX_CONST_DATA // 2} data values (fp64 constant bank)")
     if len(data_arr) <= MAX_CONST_DATA:  # warp-uniform indices: constant-cache broadcasts
-        data_decl = (f"__constant__ __align__(8) {rt} DC[{len(data_arr)}];\n"
+        pad = _DC_PAD * (1 if _F64 else 2)  # elements before the data (DC_PAD_BYTES)
+        data_decl = (f"__constant__ __align__(32) {rt} DCP[{pad + len(data_arr)}];\n"
+                     f"#define DC (DCP + {pad})\n"
                      f"__device__ __forceinline__ {rt} dat(int i) {{ return DC[i]; }}\n"
                      "CUPPL_LIFT(dat)  // a per-particle index: one constant-bank read per lane\n"
                      f"#define {DATA_SYM}(i) dat(i)\n"
@@ -1464,11 +1472,12 @@ def _function(model: CompiledModel):
                 cu.cuModuleUnload(mod)
                 continue
             break
-        if " float DC[" in model.cuda or " double DC[" in model.cuda:  # data in the module's constant bank
-            err, dptr, size = cu.cuModuleGetGlobal(mod, b"DC")
-            if err != cu.CUresult.CUDA_SUCCESS or size != model.data.nbytes:
-                raise InferRuntimeError(f"cuModuleGetGlobal(DC) failed: {err}")
-            err, = cu.cuMemcpyHtoD(dptr, model.data.ctypes.data, model.data.nbytes)
+        if " float DCP[" in model.cuda or " double DCP[" in model.cuda:  # data in the module's constant bank
+            err, dptr, size = cu.cuModuleGetGlobal(mod, b"DCP")
+            pad_bytes = size - model.data.nbytes
+            if err != cu.CUresult.CUDA_SUCCESS or pad_bytes not in (0, _DC_PAD * 8):
+                raise InferRuntimeError(f"cuModuleGetGlobal(DCP) failed: {err}")
+            err, = cu.cuMemcpyHtoD(int(dptr) + pad_bytes, model.data.ctypes.data, model.data.nbytes)
             if err != cu.CUresult.CUDA_SUCCESS:
                 raise InferRuntimeError(f"cuMemcpyHtoD(DC) failed: {err}")
         _MODULES[h] = (mod, fn, lanes)

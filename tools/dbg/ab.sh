@@ -1,6 +1,6 @@
 #!/bin/bash
-# linreg + poly bench lines of the working tree
-O=gpurun_out/ab7; mkdir -p $O
-for k in 1 2; do for w in linreg poly; do
-  timeout 300 python bench.py --workload $w --steps 8 --warmup 3 --no-cpu-baseline > $O/$w$k.json 2> $O/$w$k.err
-done; done
+# dsl-linreg: constant-bank data offset sweep (CUPPL_DC_PAD_BYTES)
+O=gpurun_out/ab8; mkdir -p $O
+for pad in 0 8 16 24 0 16; do
+  CUPPL_DC_PAD_BYTES=$pad timeout 300 python bench.py --workload dsl-linreg --steps 8 --warmup 3 --no-cpu-baseline > $O/pad$pad.$RANDOM.json 2> $O/pad$pad.err
+done
