@@ -229,14 +229,6 @@ __global__ void __launch_bounds__(kSmcThreads) smc_scan_kernel(const __grid_cons
 }
 
 // ------------------------------------------------------------------ K6: resample --------
-// Alias draw from a shared-memory copy of the transition tables (entry layout as alias_draw).
-__device__ __forceinline__ int alias_draw_s(const unsigned long long* row, unsigned int K, uint32_t w) {
-  const unsigned long long p = static_cast<unsigned long long>(w) * K;
-  const unsigned int col = static_cast<unsigned int>(p >> 32);
-  const unsigned long long e = row[col];
-  return static_cast<uint32_t>(p) < (e & 0x1FFFFFFFFull) ? static_cast<int>(col) : static_cast<int>(e >> 40);
-}
-
 // K6: CTA b owns an even share [jb_lo, jb_hi) of this rank's outputs. It stages its sources
 // tile by tile (the 4096-particle K5 tiles: states in shared memory, batch-relative integer
 // weight prefix in registers) and RANKS EVERY SOURCE INTO THE COMB: the comb targets are an
@@ -257,6 +249,7 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
   extern __shared__ __align__(16) unsigned long long alias_s[];  // [S][S] (SMEM_ALIAS)
   __shared__ __align__(16) uint8_t xs[kBatch];         // staged source states
   __shared__ __align__(16) uint16_t marks[kWindow];    // batch index + 1 of a first child
+  __shared__ uint8_t present[kMaxStates];              // states drawn into population t + 1
   __shared__ unsigned long long wsum[kSmcThreads / 32];
   __shared__ unsigned int wmax[2 * (kSmcThreads / 32)];  // warp totals of both window halves
   __shared__ unsigned long long s_u64[4];
@@ -307,9 +300,18 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
     build_tables(m, a.y_next, neg_inf_f(), lwS1, nullptr, nullptr);
   }
   for (int i = tid; i < kWindow / 8; i += kSmcThreads) reinterpret_cast<uint4*>(marks)[i] = make_uint4(0, 0, 0, 0);
+  for (int s = tid; s < kMaxStates; s += kSmcThreads) present[s] = 0;
   if (SMEM_ALIAS) {
+    // compact entries: low word thr - 1, high word (kept state) | (alias << 16), where the kept
+    // state is the column, or the alias when thr == 0 (never kept): coin < thr <=> coin <= thr - 1
     const unsigned int nA = S * S;
-    for (unsigned int i = tid; i < nA; i += kSmcThreads) alias_s[i] = __ldg(m.alias_trans + i);
+    for (unsigned int i = tid; i < nA; i += kSmcThreads) {
+      const unsigned long long e = __ldg(m.alias_trans + i);
+      const unsigned long long thr = e & 0x1FFFFFFFFull;
+      const unsigned int al = static_cast<unsigned int>(e >> 40), col = i % S;
+      const unsigned int keep = thr == 0 ? al : col;
+      alias_s[i] = (thr == 0 ? 0ull : thr - 1) | (static_cast<unsigned long long>(keep | (al << 16)) << 32);
+    }
   }
   __syncthreads();
   for (int s = tid; s < m.S; s += kSmcThreads) wdS[s] = static_cast<double>(wS[s]);
@@ -522,11 +524,18 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
             const int i = 4 * g + h;
             run = max(run, (mw[i >> 1] >> (16 * (i & 1))) & 0xFFFFu);
             const unsigned int anc = (run - 1u) & (kBatch - 1);  // run >= 1 at every output
-            const int xa = xs[anc];
-            const int st = SMEM_ALIAS ? alias_draw_s(alias_s + xa * S, S, wv[h])
-                                      : alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[h]);
-            packed |= static_cast<uint32_t>(st) << (8 * h);
-            if (full) bmax = fmaxf(bmax, lwS1[st]);
+            const unsigned int xa = xs[anc];
+            uint32_t st;
+            if (SMEM_ALIAS) {
+              const unsigned long long pp = static_cast<unsigned long long>(wv[h]) * S;
+              const unsigned long long e = alias_s[xa * S + static_cast<unsigned int>(pp >> 32)];
+              const bool keep = static_cast<uint32_t>(pp) <= static_cast<uint32_t>(e);
+              st = __byte_perm(static_cast<uint32_t>(e >> 32), 0u, keep ? 0x4410u : 0x4432u);
+            } else {
+              st = static_cast<uint32_t>(alias_draw(m.alias_trans + static_cast<size_t>(xa) * S, m.S, wv[h]));
+            }
+            packed = h == 0 ? st : __byte_perm(packed, st, h == 1 ? 0x3240u : h == 2 ? 0x3410u : 0x4210u);
+            if (full) present[st] = 1;
             if (DEBUG) {
               const unsigned long long j = jc + i;
               if (j >= o0 && j < o1) {
@@ -571,6 +580,9 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
     __syncthreads();  // xs / wsum / s_jn reuse
   }
   if (MULTI) __threadfence_system();  // peer stores performed before the next collective
+  __syncthreads();  // present[] complete
+  for (int s = tid; s < m.S; s += kSmcThreads)
+    if (present[s]) bmax = fmaxf(bmax, lwS1[s]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) bmax = fmaxf(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
   if (lane == 0 && bmax > neg_inf_f()) atomicMax(a.m_key_next, f2key(bmax));
