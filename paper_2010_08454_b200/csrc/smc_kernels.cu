@@ -434,14 +434,26 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
         unsigned int fp = f0;
         double cd = 0.0;  // exact prefix of my sources (integer sums < 2^53)
         const uint16_t mark0 = static_cast<uint16_t>(kSegment * tid + 1);
+        if (f0 >= wb32) {  // my first child is in the window: fp - wb32 is the position
 #pragma unroll
-        for (int k = 0; k < kSegment; ++k) {
-          const uint32_t st = (xw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-          cd += (nv == kSegment || k < nv) ? wdS[st] : 0.0;
-          const unsigned int fn = comb_rank(__fma_rn(cd, n_over_t, est0), c0, cd, cb);
-          if (fp < fn && fn > wb32 && fp < wb32 + static_cast<unsigned int>(kWindow))
-            marks[(fp > wb32 ? fp : wb32) - wb32] = static_cast<uint16_t>(mark0 + k);
-          fp = fn;
+          for (int k = 0; k < kSegment; ++k) {
+            const uint32_t st = (xw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+            cd += (nv == kSegment || k < nv) ? wdS[st] : 0.0;
+            const unsigned int fn = comb_rank(__fma_rn(cd, n_over_t, est0), c0, cd, cb);
+            if (fp < fn && fp - wb32 < static_cast<unsigned int>(kWindow))
+              marks[fp - wb32] = static_cast<uint16_t>(mark0 + k);
+            fp = fn;
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < kSegment; ++k) {
+            const uint32_t st = (xw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+            cd += (nv == kSegment || k < nv) ? wdS[st] : 0.0;
+            const unsigned int fn = comb_rank(__fma_rn(cd, n_over_t, est0), c0, cd, cb);
+            if (fp < fn && fn > wb32 && fp < wb32 + static_cast<unsigned int>(kWindow))
+              marks[(fp > wb32 ? fp : wb32) - wb32] = static_cast<uint16_t>(mark0 + k);
+            fp = fn;
+          }
         }
         if (tid == kSmcThreads - 1) s_jn = fp;  // F(end of batch): first output of the next batch
       }
@@ -450,9 +462,12 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
       if (o0 >= j_next) break;  // no outputs (no marks were written either)
       const unsigned long long o1 = we < j_next ? we : j_next;
       // chunk c of this thread covers positions wb + 16 (tid + 256 c) + [0, 16)
-      unsigned int cm[2];
+      // the second half of the window holds outputs only when the batch's outputs reach it
+      const bool two = o1 > wb + kWindow / 2;
+      unsigned int cm[2] = {0u, 0u};
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
+        if (c == 1 && !two) break;
         const uint4* mp = reinterpret_cast<const uint4*>(marks) + 2 * (tid + kSmcThreads * c);
         const uint4 a0 = mp[0], a1 = mp[1];
         const unsigned int m8 = __vmaxu2(__vmaxu2(__vmaxu2(a0.x, a0.y), __vmaxu2(a0.z, a0.w)),
@@ -461,13 +476,21 @@ __global__ void __launch_bounds__(kSmcThreads, CUPPL_SMC_MINBLOCKS) smc_resample
       }
       // inclusive max-scans over the threads (position order), both halves of the window
       unsigned int pm0 = cm[0], pm1 = cm[1];
+      if (two) {
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned int t0 = __shfl_up_sync(0xffffffffu, pm0, o);
-        const unsigned int t1 = __shfl_up_sync(0xffffffffu, pm1, o);
-        if (lane >= o) {
-          pm0 = max(pm0, t0);
-          pm1 = max(pm1, t1);
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned int t0 = __shfl_up_sync(0xffffffffu, pm0, o);
+          const unsigned int t1 = __shfl_up_sync(0xffffffffu, pm1, o);
+          if (lane >= o) {
+            pm0 = max(pm0, t0);
+            pm1 = max(pm1, t1);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned int t0 = __shfl_up_sync(0xffffffffu, pm0, o);
+          if (lane >= o) pm0 = max(pm0, t0);
         }
       }
       if (lane == 31) {
