@@ -500,7 +500,7 @@ def _run_compiled_lmh(model, n_samples: int, rng, *, chains: int, burn_in: int, 
     c0, c1 = shard_range(chains, rank, world)
     st = run_mcmc(model, n_samples, rng, chains=c1 - c0, burn_in=burn_in, thin=thin, chain_begin=c0,
                   device=device) if c1 > c0 else np.zeros((0, 1))
-    if world > 1:  # pragma: no cover - multi-GPU
+    if world > 1:  # replicas: per-chain statistics gathered in rank (= chain) order
         import torch.distributed as dist
 
         parts = [None] * world

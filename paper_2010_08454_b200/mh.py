@@ -85,15 +85,16 @@ def run_lmh(model: GaussianMixture, n_samples: int, rng, *, chains: int = 4096, 
                             n_rec, N.stream_ptr(dev))
         N.check(rc, "mh_gmm", seed=seed_of(rng))
     stats = st[:nc]
-    if world > 1:  # pragma: no cover - multi-GPU
+    if world > 1:  # replicas: gather the per-chain statistics in rank (= chain) order
         import torch.distributed as dist
 
         sizes = [shard_range(chains, q, world)[1] - shard_range(chains, q, world)[0] for q in range(world)]
-        buf = torch.zeros((max(sizes) * world, 2 * K + 2), dtype=torch.float64, device=dev)
-        pad = torch.zeros((max(sizes), 2 * K + 2), dtype=torch.float64, device=dev)
-        pad[:nc] = stats
-        dist.all_gather_into_tensor(buf, pad, group=group)
-        stats = torch.cat([buf[q * max(sizes):q * max(sizes) + sizes[q]] for q in range(world)])
+        tdev = dev if dist.get_backend(group) == "nccl" else torch.device("cpu")  # gloo: host tensors
+        pad = torch.zeros((max(sizes), 2 * K + 2), dtype=torch.float64, device=tdev)
+        pad[:nc] = stats.to(tdev)
+        parts = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(parts, pad, group=group)
+        stats = torch.cat([parts[q][:sizes[q]] for q in range(world)])
     s = stats.cpu().numpy()
     nrec = s[:, 2 * K]
     tot = nrec.sum()

@@ -130,3 +130,70 @@ def test_mh_data_shapes_match_oracle_initial_trace(cuda, oracle_lib, D):
         r = y64 - mu0[c].astype(np.float64)[z]
         l64 = -0.5 * float(np.dot(r, r)) - D * 0.5 * math.log(2 * math.pi)
         assert abs(ll0[c] - l64) <= 1e-5 * abs(l64) + 1e-6, (c, ll0[c], l64)
+
+
+GMM_PROG = """
+ys <- [1.2, -0.7, 3.1, 2.2, -1.9, 0.4, 2.8, -0.3];
+model <- function() {
+  mu <- sample(normal(0, 3));
+  reduce(function(acc, y) { observe(normal(mu, 1), y); acc }, 0, ys);
+  mu
+};
+mcmc(model, 400)
+"""
+
+
+def _mh_ranks_worker(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)  # both ranks share the test box's GPU
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2010_08454_b200 import Rng, frontend, infer, models
+
+        m = models.GaussianMixture.synthetic(n_points=500, K=3)
+        post = infer.run_lmh(m, 300, Rng(11), chains=70, burn_in=100)
+        cm = frontend.compile_program(GMM_PROG)
+        post2 = infer.run_lmh(cm, 400, Rng(12), chains=50, burn_in=100)
+        q.put((rank, post.record["chain_stats"], dict(post.mean), post.stats["acceptance"],
+               post2.record["chain_stats"], dict(post2.mean)))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_mh_two_ranks_equal_one(cuda):
+    """MH is replicas: chains sharded over two processes (gloo, one GPU)
+    gather to exactly the per-chain statistics and posterior of a single-process run — the
+    hand-written K7 GMM chains and a compiled mcmc program."""
+    import multiprocessing as mp
+    import socket
+
+    from paper_2010_08454_b200 import Rng, frontend, infer, models
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_mh_ranks_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    m = models.GaussianMixture.synthetic(n_points=500, K=3)
+    one = infer.run_lmh(m, 300, Rng(11), chains=70, burn_in=100)
+    one2 = infer.run_lmh(frontend.compile_program(GMM_PROG), 400, Rng(12), chains=50, burn_in=100)
+    for o in out:
+        assert np.array_equal(o[1], one.record["chain_stats"])
+        assert o[2] == dict(one.mean) and o[3] == one.stats["acceptance"]
+        assert np.array_equal(o[4], one2.record["chain_stats"])
+        assert o[5] == dict(one2.mean)
