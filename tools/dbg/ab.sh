@@ -1,6 +1,11 @@
 #!/bin/bash
-# dsl-linreg: constant-bank data offset sweep (CUPPL_DC_PAD_BYTES)
-O=gpurun_out/ab8; mkdir -p $O
-for pad in 0 8 16 24 0 16; do
-  CUPPL_DC_PAD_BYTES=$pad timeout 300 python bench.py --workload dsl-linreg --steps 8 --warmup 3 --no-cpu-baseline > $O/pad$pad.$RANDOM.json 2> $O/pad$pad.err
+# smc bench: working tree vs repo copies under tools/dbg/ab_*, alternated on one box
+O=gpurun_out/ab9; mkdir -p $O
+R=$PWD
+for k in 1 2; do
+  for d in tools/dbg/ab_*/; do
+    n=$(basename $d)
+    (cd $d && timeout 300 python bench.py --workload smc --steps 10 --warmup 3 --no-cpu-baseline > $R/$O/$n.$k.json 2> $R/$O/$n.$k.err)
+  done
+  timeout 300 python bench.py --workload smc --steps 10 --warmup 3 --no-cpu-baseline > $O/main.$k.json 2> $O/main.$k.err
 done
