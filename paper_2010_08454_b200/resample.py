@@ -39,7 +39,10 @@ class Resampler:
         if not 1 <= n < 2**31:
             raise ValueError("n must be in [1, 2^31)")
         self.n = n
-        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        device = torch.device(device) if device is not None else torch.device("cuda")
+        if device.type == "cuda" and device.index is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = device
         L = N.lib()
         self.ws = torch.empty(L.cuppl_resample_workspace_bytes(n), dtype=torch.uint8, device=self.device)
         self.stats = torch.empty(4, dtype=torch.float64, device=self.device)  # cuppl_resample_stats
@@ -50,11 +53,20 @@ class Resampler:
 
         if lw.dtype != torch.float32 or lw.numel() != self.n or not lw.is_contiguous():
             raise ValueError("lw must be a contiguous float32 tensor of n elements")
+        bufs = [lw] + [b for b in (payload, payload_out, ancestors_out) if b is not None]
+        if any(b.device != self.device for b in bufs):
+            raise ValueError(f"every buffer must be on {self.device}")
         nbytes = 0
         if payload is not None:
             if payload.shape[0] != self.n or not payload.is_contiguous():
                 raise ValueError("payload must be contiguous with the particle as its first axis")
             nbytes = payload.element_size() * payload[0].numel()
+            if (payload_out is None or not payload_out.is_contiguous()
+                    or payload_out.numel() * payload_out.element_size() != self.n * nbytes):
+                raise ValueError("payload_out must be a contiguous buffer of the payload's size")
+        if ancestors_out is not None and (ancestors_out.dtype != torch.int64 or ancestors_out.numel() != self.n
+                                          or not ancestors_out.is_contiguous()):
+            raise ValueError("ancestors_out must be a contiguous int64 tensor of n elements")
         L = N.lib()
         rc = L.cuppl_resample(N.ptr(lw), self.n, N.ptr(payload), nbytes, key, t, N.ptr(payload_out),
                               N.ptr(ancestors_out), N.ptr(self.stats), N.ptr(self.ws), self.ws.numel(),

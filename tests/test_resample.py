@@ -185,3 +185,30 @@ def test_gpu_generic_smc_linear_gaussian_matches_kalman(cuda):
     runs = [make(9).run(T, Rng(3)) for _ in range(2)]
     assert runs[0].log_z == runs[1].log_z  # same seeds: the same bits
     assert abs(runs[0].log_z - ll_ref) < 0.05, (runs[0].log_z, ll_ref)
+
+
+@pytest.mark.gpu
+def test_gpu_resampler_rejects_mismatched_buffers(cuda):
+    """Buffer checks before the launch: a short output buffer, a wrong ancestor dtype or a
+    mismatched payload would otherwise be written out of bounds by the kernels."""
+    import torch
+
+    from paper_2010_08454_b200 import resample
+
+    n = 1000
+    r = resample.Resampler(n)
+    lw = torch.zeros(n, dtype=torch.float32, device="cuda")
+    pay = torch.zeros((n, 3), dtype=torch.float32, device="cuda")
+    with pytest.raises(ValueError):
+        r.launch(lw, pay, 1, 0, torch.empty((n - 1, 3), dtype=torch.float32, device="cuda"))
+    with pytest.raises(ValueError):
+        r.launch(lw, pay, 1, 0, None)
+    with pytest.raises(ValueError):
+        r.launch(lw, None, 1, 0, None, torch.empty(n, dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError):
+        r.launch(lw[:-1], None, 1, 0)
+    with pytest.raises(ValueError):
+        r.launch(lw, pay.cpu(), 1, 0, torch.empty_like(pay))
+    r.launch(lw, pay, 1, 0, torch.empty_like(pay), torch.empty(n, dtype=torch.int64, device="cuda"))
+    m, total, s1, s2 = r.read_stats()
+    assert total == n * 2**31 and s1 == n
