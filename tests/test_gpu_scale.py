@@ -186,6 +186,20 @@ def test_c4_smc_bit_exact_at_1e8(cuda, oracle_lib):
     for t in range(steps):
         assert np.array_equal(res.filtering_int[t], ref["hist"][t])
     assert np.allclose(res.log_z_steps, ref["log_z_steps"], rtol=1e-7, atol=1e-7)
+    del res, r
+    torch.cuda.empty_cache()
+    # the same run partitioned over 5 ranks (rank-local K5, exchanged records, K6 with stores
+    # into the other ranks' slots): bit-identical to the single-rank run
+    r5 = smc.SmcRunner(m, n, KEY, record_ancestors=True, steps=steps, local_world=5)
+    res5 = r5.run()
+    torch.cuda.synchronize()
+    assert np.array_equal(res5.total_weight, ref["T"])
+    for t in range(steps - 1):
+        anc = np.concatenate([a.cpu().numpy() for a in res5.ancestors[t]]).astype(np.uint64)
+        assert np.array_equal(anc, ref["ancestors"][t]), f"5 ranks: ancestors differ at step {t}"
+    x = np.concatenate([t.cpu().numpy() for t in res5.states]).astype(np.int32)
+    assert np.array_equal(x, ref["x"])
+    assert np.allclose(res5.log_z_steps, ref["log_z_steps"], rtol=1e-7, atol=1e-7)
 
 
 def test_c3_mh_initial_log_likelihood_and_statistics(cuda, oracle_lib):
