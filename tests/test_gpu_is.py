@@ -365,3 +365,63 @@ def test_philox_matches_curand(cuda):
     torch.cuda.synchronize()
     assert torch.equal(ours, theirs)
     cu.cuModuleUnload(mod)
+
+
+def _is_ranks_worker(rank, world, port, q):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)  # both ranks share the test box's GPU
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2010_08454_b200 import Rng, infer, models
+
+        out = []
+        for m in (models.LinearRegression.synthetic(n_points=200), models.PolyRegression.synthetic()):
+            post = infer.run_importance(m, 2_000_003, Rng(3))
+            out.append((post.log_z, post.ess, dict(post.mean), post.mode_index, post.mode_log_weight,
+                        list(post.support)))
+        q.put((rank, out))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_is_two_ranks_match_one(cuda):
+    """Particle sharding over two processes (gloo, one GPU): both ranks merge
+    the gathered records to the same posterior, whose mode is the single-process run's
+    particle (per-particle log-weights do not depend on the partition) and whose log Z, ESS,
+    moments and degree masses equal it to fp32-accumulation accuracy."""
+    import multiprocessing as mp
+    import socket
+
+    from paper_2010_08454_b200 import Rng, infer, models
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_is_ranks_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert res[0][1] == res[1][1]  # identical merges on every rank
+    for j, m in enumerate((models.LinearRegression.synthetic(n_points=200), models.PolyRegression.synthetic())):
+        one = infer.run_importance(m, 2_000_003, Rng(3))
+        lz, ess, mean, mi, mlw, sup = res[0][1][j]
+        assert mi == one.mode_index and mlw == one.mode_log_weight
+        assert abs(lz - one.log_z) <= 1e-6 * abs(one.log_z) + 1e-6
+        assert ess == pytest.approx(one.ess, rel=1e-5)
+        for k, v in one.mean.items():
+            assert mean[k] == pytest.approx(v, rel=1e-5, abs=1e-6)
+        for (v1, p1), (v2, p2) in zip(sup, one.support):
+            assert v1 == v2 and p1 == pytest.approx(p2, rel=1e-5, abs=1e-9)
