@@ -9,7 +9,8 @@
 // uniform = (x >> 11) 2^-53 (rng.py:43-45), randint = rejection below MASK - MASK % n then
 // x % n (rng.py:47-56), normal = Box-Muller with u1 redrawn while 0 and the cached spare
 // (rng.py:58-71), exponential / gamma / beta / poisson as rng.py:73-117. The integer decisions
-// are exact; the real-valued transforms run in fp32 (the oracle restates them in fp64 and
+// are exact (poisson's products of uniforms run in fp64, as in the reference); the other
+// real-valued transforms run in fp32 (the oracle restates them in fp64 and
 // equals oracle/refstream.Algorithms bit for bit on the same u64 stream, tests/test_oracle.py).
 #pragma once
 #include "cuppl_device.cuh"
@@ -102,25 +103,31 @@ struct WordStream {
       if (u > 0.0f && logf(u) < 0.5f * x * x + d * (1.0f - v + logf(v))) return d * v * boost;
     }
   }
+  // the reference's 53-bit uniform as the double it is (exact: (x >> 11) 2^-53)
+  __device__ __forceinline__ double uniform_d() {
+    return static_cast<double>(next_u64() >> 11) * 0x1p-53;
+  }
+  // rng.py:105-117 in fp64 like the reference (products of uniforms against exp(-lambda),
+  // halving above 30): the integer draws equal the oracle's, which is the reference algorithm
   __device__ int poisson(float lam) {
     // explicit DFS over the halving tree: same leaf order as the reference recursion
-    float stack[64];
+    double stack[64];
     int sp = 0;
-    stack[sp++] = lam;
+    stack[sp++] = static_cast<double>(lam);
     int total = 0;
     while (sp > 0) {
-      const float l = stack[--sp];
-      if (l < 30.0f) {
-        const float limit = expf(-l);
+      const double l = stack[--sp];
+      if (l < 30.0) {
+        const double limit = exp(-l);
         int k = 0;
-        float p = uniform();
+        double p = uniform_d();
         while (p > limit) {
           ++k;
-          p *= uniform();
+          p = __dmul_rn(p, uniform_d());
         }
         total += k;
       } else if (sp < 62) {  // rates are checked < 2^31 (<= 27 levels); never overflow the stack
-        const float half = floorf(l / 2.0f);
+        const double half = floor(l / 2.0);
         stack[sp++] = l - half;  // processed second
         stack[sp++] = half;      // processed first
       }
