@@ -46,13 +46,8 @@ __global__ void dist_sample_kernel(DistArgs a, uint64_t key, uint32_t tag, uint6
         io[i] = a.ia + static_cast<int32_t>(s.randint(static_cast<uint32_t>(a.ib - a.ia)));
         break;
       case CUPPL_DIST_UNIFORM_CONTINUOUS: fo[i] = a.p0 + (a.p1 - a.p0) * s.uniform(); break;
-      case CUPPL_DIST_BETA: {
-        const float x = s.gamma(a.p0);
-        const float y = s.gamma(a.p1);
-        fo[i] = x / (x + y);
-        break;
-      }
-      case CUPPL_DIST_EXPONENTIAL: fo[i] = -logf(s.uniform_pos()) / a.p0; break;
+      case CUPPL_DIST_BETA: fo[i] = s.beta(a.p0, a.p1); break;
+      case CUPPL_DIST_EXPONENTIAL: fo[i] = s.exponential(a.p0); break;
       case CUPPL_DIST_CATEGORICAL: io[i] = categorical_index(a.table, a.K, s.next()); break;
       default: break;
     }

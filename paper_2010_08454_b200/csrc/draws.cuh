@@ -9,8 +9,9 @@
 // uniform = (x >> 11) 2^-53 (rng.py:43-45), randint = rejection below MASK - MASK % n then
 // x % n (rng.py:47-56), normal = Box-Muller with u1 redrawn while 0 and the cached spare
 // (rng.py:58-71), exponential / gamma / beta / poisson as rng.py:73-117. The integer decisions
-// are exact (poisson's products of uniforms run in fp64, as in the reference); the other
-// real-valued transforms run in fp32 (the oracle restates them in fp64 and
+// are exact (poisson's products of uniforms run in fp64, as in the reference; so do the batch
+// path's gamma / beta / exponential); the other real-valued transforms run in fp32 (the oracle
+// restates them in fp64 and
 // equals oracle/refstream.Algorithms bit for bit on the same u64 stream, tests/test_oracle.py).
 #pragma once
 #include "cuppl_device.cuh"
@@ -23,7 +24,7 @@ struct WordStream {
   uint32_t tag, blk;
   uint32_t b0, b1, b2, b3;  // the current block, in registers (no dynamically indexed array)
   int pos;
-  float spare;
+  double spare;  // the reference's one cached Box-Muller spare, shared by the fp32 and fp64 paths
   bool has_spare;
 
   __device__ __forceinline__ void init(PhiloxKey k, uint64_t i, uint32_t t) {
@@ -33,7 +34,7 @@ struct WordStream {
     blk = 0;
     pos = 4;
     has_spare = false;
-    spare = 0.f;
+    spare = 0.0;
   }
   __device__ __forceinline__ uint32_t next() {
     if (pos == 4) {
@@ -65,15 +66,40 @@ struct WordStream {
   __device__ __forceinline__ float normal() {  // rng.py:58-71
     if (has_spare) {
       has_spare = false;
-      return spare;
+      return static_cast<float>(spare);
     }
     const float u1 = uniform_pos();
     const float u2 = uniform();
     const float r = fast_sqrt(-2.0f * kLn2 * fast_lg2(u1));
     const float th = fmaf(kTwoPi, u2, -kPi);  // 2 pi u2 - pi in [-pi, pi): signs flipped below
-    spare = -r * fast_sin(th);
+    spare = static_cast<double>(-r * fast_sin(th));
     has_spare = true;
     return -r * fast_cos(th);
+  }
+  // ---- fp64 paths, the reference's arithmetic op for op (the oracle is built with
+  // -ffp-contract=off: every product and sum below is rounded on its own, no FMA contraction)
+  __device__ __forceinline__ double uniform_pos_d() {  // rng.py:73-77: (0, 1)
+    double u;
+    do {
+      u = uniform_d();
+    } while (!(u > 0.0));
+    return u;
+  }
+  __device__ __forceinline__ double normal_d() {  // rng.py:58-71 in fp64
+    if (has_spare) {
+      has_spare = false;
+      return spare;
+    }
+    const double u1 = uniform_pos_d();
+    const double u2 = uniform_d();
+    const double r = sqrt(__dmul_rn(-2.0, log(u1)));
+    // sin / cos(2 pi u2) as sincospi(2 u2): exact argument reduction without the local-memory
+    // slow path (vs the reference's sin(fl(2 pi u2)): a relative difference ~1e-16)
+    double sn, cs;
+    sincospi(__dmul_rn(2.0, u2), &sn, &cs);
+    spare = __dmul_rn(r, sn);
+    has_spare = true;
+    return __dmul_rn(r, cs);
   }
   __device__ __forceinline__ uint32_t randint(uint32_t range) {  // rng.py:47-56
     const unsigned long long n = range;
@@ -83,7 +109,33 @@ struct WordStream {
       if (r < limit) return static_cast<uint32_t>(r % n);
     }
   }
-  // Marsaglia-Tsang (cuppl/rng.py:79-98); accurate logf for the acceptance test.
+  // Marsaglia-Tsang (cuppl/rng.py:79-98) in fp64 like the reference (the batch dist_sample
+  // path): the same acceptance decisions as the oracle (so the same words consumed), reals to
+  // double rounding
+  __device__ double gamma_d(double shape) {
+    double boost = 1.0;
+    if (shape < 1.0) {
+      const double u = uniform_pos_d();
+      boost = pow(u, __ddiv_rn(1.0, shape));
+      shape = __dadd_rn(shape, 1.0);
+    }
+    const double d = __dsub_rn(shape, 1.0 / 3.0);
+    const double c = __ddiv_rn(1.0, sqrt(__dmul_rn(9.0, d)));
+    for (;;) {
+      const double x = normal_d();
+      double v = __dadd_rn(1.0, __dmul_rn(c, x));
+      if (v <= 0.0) continue;
+      v = __dmul_rn(__dmul_rn(v, v), v);
+      const double u = uniform_d();
+      const double x2 = __dmul_rn(x, x);
+      if (u < __dsub_rn(1.0, __dmul_rn(__dmul_rn(0.0331, x2), x2))) return __dmul_rn(__dmul_rn(d, v), boost);
+      if (u > 0.0 &&
+          log(u) < __dadd_rn(__dmul_rn(__dmul_rn(0.5, x), x), __dmul_rn(d, __dadd_rn(__dsub_rn(1.0, v), log(v)))))
+        return __dmul_rn(__dmul_rn(d, v), boost);
+    }
+  }
+  // the fp32 version for compiled models (per-lane draws in registers; accurate logf for the
+  // acceptance test): the same algorithm, decisions equal to the fp64 ones except on rare draws
   __device__ float gamma(float shape) {
     float boost = 1.0f;
     if (shape < 1.0f) {
@@ -102,6 +154,15 @@ struct WordStream {
       if (u < 1.0f - 0.0331f * (x * x) * (x * x)) return d * v * boost;
       if (u > 0.0f && logf(u) < 0.5f * x * x + d * (1.0f - v + logf(v))) return d * v * boost;
     }
+  }
+  // beta = X / (X + Y) (rng.py:100-103) and exponential = -ln(u) / rate (rng.py:73-77), in fp64
+  __device__ float beta(float a, float b) {
+    const double x = gamma_d(static_cast<double>(a));
+    const double y = gamma_d(static_cast<double>(b));
+    return static_cast<float>(__ddiv_rn(x, __dadd_rn(x, y)));
+  }
+  __device__ float exponential(float rate) {
+    return static_cast<float>(__ddiv_rn(-log(uniform_pos_d()), static_cast<double>(rate)));
   }
   // the reference's 53-bit uniform as the double it is (exact: (x >> 11) 2^-53)
   __device__ __forceinline__ double uniform_d() {
