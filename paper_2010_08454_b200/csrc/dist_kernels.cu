@@ -39,13 +39,17 @@ __global__ void dist_sample_kernel(DistArgs a, uint64_t key, uint32_t tag, uint6
     float* fo = static_cast<float*>(out);
     int32_t* io = static_cast<int32_t*>(out);
     switch (a.tag) {
-      case CUPPL_DIST_NORMAL: fo[i] = a.p0 + a.p1 * s.normal(); break;
+      case CUPPL_DIST_NORMAL:  // fp64 like the reference, rounded once to the fp32 output
+        fo[i] = static_cast<float>(__dadd_rn(a.p0, __dmul_rn(a.p1, s.normal_d())));
+        break;
       case CUPPL_DIST_BERNOULLI: io[i] = s.uniform() < a.p0 ? 1 : 0; break;
       case CUPPL_DIST_POISSON: io[i] = s.poisson(a.p0); break;
       case CUPPL_DIST_UNIFORM_DISCRETE:
         io[i] = a.ia + static_cast<int32_t>(s.randint(static_cast<uint32_t>(a.ib - a.ia)));
         break;
-      case CUPPL_DIST_UNIFORM_CONTINUOUS: fo[i] = a.p0 + (a.p1 - a.p0) * s.uniform(); break;
+      case CUPPL_DIST_UNIFORM_CONTINUOUS:
+        fo[i] = static_cast<float>(__dadd_rn(a.p0, __dmul_rn(__dsub_rn(a.p1, a.p0), s.uniform_d())));
+        break;
       case CUPPL_DIST_BETA: fo[i] = s.beta(a.p0, a.p1); break;
       case CUPPL_DIST_EXPONENTIAL: fo[i] = s.exponential(a.p0); break;
       case CUPPL_DIST_CATEGORICAL: io[i] = categorical_index(a.table, a.K, s.next()); break;
